@@ -1,0 +1,164 @@
+"""Oracle-B — brute-force allocator over a unit bitmap.  TEST INFRASTRUCTURE ONLY.
+
+Structurally different from Oracle-L: it keeps no free list at all.  The state is
+one bit per unit of the arena (set = free), as in the paper's bitmask allocator
+(§3.2), plus the live map (start -> size) that a free needs.
+Free blocks are DERIVED on every call:
+
+* fits / SEGFIT / TLSF: the maximal runs of free units (coalescing is implicit in
+  the bitmap);
+* BUDDY: the maximal aligned free power-of-two blocks inside the root blocks of the
+  arena's greedy decomposition (binary buddies).
+
+An alloc enumerates every derived block and applies the policy key of DESIGN.md
+§5 directly (lowest key wins), then clears the bits it hands out.  The class
+mapping is written here from its *defining property* (search class = the smallest
+class whose lower bound is >= the request) rather than Oracle-L's formula, so the
+two oracles pin each other.  O(arena units) per op: tiny heaps and config 1 only.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+HEAP_NULL = (1 << 64) - 1
+FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY = 1, 2, 3, 4, 5
+
+
+def cls_of(u: int, L: int) -> int:
+    """Class of a block of u units: exact below 2^L, else (fl, sl) from the top L+1 bits."""
+    if u < (1 << L):
+        return u
+    m = u.bit_length() - 1
+    return (m - L + 1) * (1 << L) + ((u >> (m - L)) - (1 << L))
+
+
+def cls_lo(c: int, L: int) -> int:
+    """Smallest block size (units) of class c."""
+    fl, sl = divmod(c, 1 << L)
+    return sl if fl == 0 else ((1 << L) + sl) << (fl - 1)
+
+
+def search_cls(u: int, L: int) -> int:
+    """Smallest class all of whose blocks hold u units: min{c : lo(c) >= u}."""
+    c = cls_of(u, L)
+    while cls_lo(c, L) < u:
+        c += 1
+    return c
+
+
+class OracleB:
+    def __init__(self, arena_bytes: int, align: int, policy: int):
+        assert align > 0 and align & (align - 1) == 0 and arena_bytes % align == 0
+        self.align, self.policy = align, policy
+        self.A = arena_bytes // align
+        self.bits = np.ones(self.A, dtype=bool)
+        self.live: dict[int, int] = {}
+        self.L = 5 if policy == TLSF else 0
+        self.roots = []
+        if policy == BUDDY:
+            s, K = 0, self.A.bit_length() - 1
+            while s < self.A:
+                t = K
+                while t > 0 and (s % (1 << t) or s + (1 << t) > self.A):
+                    t -= 1
+                self.roots.append((s, t))
+                s += 1 << t
+        self.counts = dict(allocs_ok=0, allocs_failed=0, frees_ok=0, frees_invalid=0,
+                           frees_double=0, frees_null=0)
+
+    # ---- derived free blocks ----
+    def runs(self):
+        b = self.bits.astype(np.int8)
+        d = np.diff(np.concatenate(([0], b, [0])))
+        starts = np.flatnonzero(d == 1)
+        ends = np.flatnonzero(d == -1)
+        return [(int(s), int(e - s)) for s, e in zip(starts, ends)]
+
+    def buddy_blocks(self):
+        out = []
+
+        def rec(s, t):
+            if self.bits[s:s + (1 << t)].all():
+                out.append((s, 1 << t))
+            elif t > 0:
+                rec(s, t - 1)
+                rec(s + (1 << (t - 1)), t - 1)
+        for s, t in self.roots:
+            rec(s, t)
+        return out
+
+    def blocks(self):
+        return self.buddy_blocks() if self.policy == BUDDY else self.runs()
+
+    # ---- ops ----
+    def alloc_units(self, r: int):
+        blocks = self.blocks()
+        if self.policy == FIRST_FIT:
+            cand = [(s, s, z) for s, z in blocks if z >= r]
+        elif self.policy == BEST_FIT:
+            cand = [((z, s), s, z) for s, z in blocks if z >= r]
+        elif self.policy in (SEGFIT, TLSF):
+            c = search_cls(r, self.L)
+            cand = [((cls_of(z, self.L), s), s, z) for s, z in blocks if cls_of(z, self.L) >= c]
+        else:
+            cand = [((z, s), s, z) for s, z in blocks if z >= r]   # (order, start), z = 2^order
+        if not cand:
+            return None
+        _, s, _ = min(cand)
+        self.bits[s:s + r] = False
+        self.live[s] = r
+        return s
+
+    def alloc_batch(self, sizes):
+        out = np.empty(len(sizes), dtype=np.uint64)
+        for i, sz in enumerate(int(x) for x in sizes):
+            r = -(-sz // self.align)
+            u = None
+            if sz != 0 and r <= self.A:
+                if self.policy == BUDDY:
+                    p = 1
+                    while p < r:
+                        p <<= 1
+                    r = p
+                    u = self.alloc_units(r) if r <= self.A else None
+                else:
+                    u = self.alloc_units(r)
+            if u is None:
+                out[i] = HEAP_NULL
+                self.counts["allocs_failed"] += 1
+            else:
+                out[i] = u * self.align
+                self.counts["allocs_ok"] += 1
+        return out
+
+    def free_batch(self, offsets):
+        free_starts = {s for s, _ in self.blocks()}
+        seen = set()
+        to_free = []
+        for o in sorted(int(x) for x in offsets):
+            if o == HEAP_NULL:
+                self.counts["frees_null"] += 1
+            elif o % self.align or o // self.align >= self.A:
+                self.counts["frees_invalid"] += 1
+            else:
+                u = o // self.align
+                if u in self.live:
+                    if u in seen:
+                        self.counts["frees_double"] += 1
+                    else:
+                        seen.add(u)
+                        self.counts["frees_ok"] += 1
+                        to_free.append(u)
+                elif u in free_starts:
+                    self.counts["frees_double"] += 1
+                else:
+                    self.counts["frees_invalid"] += 1
+        for u in to_free:
+            self.bits[u:u + self.live.pop(u)] = True
+
+    def export(self):
+        fp = np.array([(s * self.align, z * self.align) for s, z in self.blocks()],
+                      dtype=np.uint64).reshape(-1, 2)
+        lp = np.array(sorted((s * self.align, z * self.align) for s, z in self.live.items()),
+                      dtype=np.uint64).reshape(-1, 2)
+        return fp, lp

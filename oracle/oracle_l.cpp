@@ -1,0 +1,312 @@
+/*
+ * oracle_l.cpp — Oracle-L: the plain, slow, single-threaded CPU reference for the
+ * batched device heap.  TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library.  The
+ * product path (paper_2405_07079_b200/) never links or calls it, and this file shares
+ * no code, header, table or constant with the CUDA path.
+ *
+ * What it computes (arXiv 2405.07079, "Host-Based Allocators for Device Memory"):
+ *   - the allocator never reads the memory it manages, so all metadata is out of band
+ *     (PAPER.md:39,55,61): here `live` plays the block table keyed by address
+ *     (§3.3) and `freeb` the address-sorted free list (§3.1 HAL role,
+ *     PAPER.md:166-168); the heap starts as one free block (Alg. 6 :617-618).
+ *   - alloc splits the chosen free block from its low end (Alg. 1).
+ *   - free coalesces with the free neighbour ending at the block and/or the one starting
+ *     right after it (Alg. 2; Alg. 5).
+ *   - policies (the candidate key; lowest key wins, readings C2-C13):
+ *       FIRST_FIT  first block with size >= r, by address
+ *       BEST_FIT   min (size, start) over size >= r               (Alg. 3 :298-317)
+ *       SEGFIT     TLSF mapping with SL_LOG2 = 0: search bin = ceil(log2 r), block bin =
+ *                  floor(log2 size) (+1 shift), address order within a bin
+ *                                                                 (Alg. 4 :332-351, :440)
+ *       TLSF       SL_LOG2 = 5 two-level classes, min (cls, start) with cls >= search class
+ *
+ *       BUDDY      binary buddy: smallest nonempty order >= k, lowest address, split keeping
+ *                  the low half, merge with a free buddy a XOR 2^k
+ *   - batch driver (canonical order, BASELINE.json north_star): a free batch classifies every
+ *     offset against the batch-start state, then frees the valid ones in ascending address
+ *     order; an alloc batch serves requests in request order, HEAP_NULL on failure.
+ * Everything is in units of `align` (reading C14).  Sizes of s bytes become
+ * r = ceil(s / align) units; s = 0 or r > A_u fails (C17).
+ */
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <set>
+#include <vector>
+#include <algorithm>
+#include <utility>
+
+namespace {
+
+const uint64_t HEAP_NULL = ~0ull;
+enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5 };
+
+/* floor(log2 u) for u >= 1, written as a plain loop */
+int floor_log2(uint64_t u) {
+    int m = -1;
+    while (u) { u >>= 1; m++; }
+    return m;
+}
+
+/* TLSF class of a free block of u units (insert mapping; Masmano's TLSF as read in
+ * DESIGN.md C10).  Classes below 2^L units are exact; above, first level fl = m - L + 1
+ * with m = floor(log2 u), second level = the next L bits below the leading one. */
+uint64_t insert_class(uint64_t u, int L) {
+    if (u < (1ull << L)) return u;                       /* fl = 0, sl = u */
+    int m = floor_log2(u);
+    uint64_t fl = (uint64_t)(m - L + 1);
+    uint64_t sl = (u >> (m - L)) - (1ull << L);
+    return fl * (1ull << L) + sl;
+}
+/* search class: round the request up to the next class boundary so that every block of
+ * that class or above fits (Alg. 4 "1 << ceil(log2(size))", generalised) */
+uint64_t search_class(uint64_t u, int L) {
+    if (u < (1ull << L)) return insert_class(u, L);
+    int m = floor_log2(u);
+    return insert_class(u + (1ull << (m - L)) - 1, L);
+}
+
+struct Counters {
+    uint64_t allocs_ok = 0, allocs_failed = 0, frees_ok = 0, frees_invalid = 0,
+             frees_double = 0, frees_null = 0, high_water_end = 0;
+};
+
+struct Heap {
+    int policy;
+    int L;
+    uint64_t align, A_u, arena_bytes;
+    std::map<uint64_t, uint64_t> live;    /* start -> size (units): the block table */
+    std::map<uint64_t, uint64_t> freeb;   /* start -> size (units): free list, address order */
+    std::set<std::pair<uint64_t, uint64_t>> cls_index;   /* (class, start): SEGFIT/TLSF bins */
+    std::vector<std::set<uint64_t>> bfree;                /* BUDDY: free starts per order */
+    int K = 0;                                            /* BUDDY: max order */
+    Counters c;
+
+    /* ---- free-list edits (keep the class index in step) ---- */
+    void free_insert(uint64_t s, uint64_t z) {
+        freeb[s] = z;
+        if (policy == SEGFIT || policy == TLSF) cls_index.insert({insert_class(z, L), s});
+    }
+    void free_erase(uint64_t s) {
+        auto it = freeb.find(s);
+        if (policy == SEGFIT || policy == TLSF) cls_index.erase({insert_class(it->second, L), s});
+        freeb.erase(it);
+    }
+
+    bool is_free_start(uint64_t u) const {
+        if (policy == BUDDY) {
+            for (const auto &st : bfree) if (st.count(u)) return true;
+            return false;
+        }
+        return freeb.count(u) != 0;
+    }
+
+    /* ---- Alg. 2 / Alg. 5: deallocate a live block with 3-way coalescing ---- */
+    void free_block(uint64_t o) {
+        uint64_t size = live[o];
+        live.erase(o);
+        if (policy == BUDDY) { buddy_free(o, size); return; }
+        uint64_t start = o, end = o + size;
+        /* left: the free block whose end is o */
+        auto it = freeb.lower_bound(o);
+        if (it != freeb.begin()) {
+            auto left = std::prev(it);
+            if (left->first + left->second == o) { start = left->first; free_erase(left->first); }
+        }
+        /* right: the free block starting at o + size */
+        auto right = freeb.find(end);
+        if (right != freeb.end()) { end = right->first + right->second; free_erase(right->first); }
+        free_insert(start, end - start);
+    }
+
+    /* buddy merge: while the buddy a XOR 2^k is a free block of order k, merge */
+    void buddy_free(uint64_t o, uint64_t size) {
+        int k = floor_log2(size);
+        while (k < K) {
+            uint64_t b = o ^ (1ull << k);
+            auto it = bfree[k].find(b);
+            if (it == bfree[k].end()) break;
+            bfree[k].erase(it);
+            o = std::min(o, b);
+            k++;
+        }
+        bfree[k].insert(o);
+    }
+
+    /* ---- Alg. 1: allocate r units from the chosen free block (low-end split) ---- */
+    uint64_t take(uint64_t s, uint64_t r) {
+        uint64_t z = freeb[s];
+        free_erase(s);
+        if (z > r) free_insert(s + r, z - r);   /* free_it.address += size; free_it.size -= size */
+        live[s] = r;                            /* record the rounded request (Alg. 4 :348) */
+        return s;
+    }
+
+    uint64_t alloc_units(uint64_t r) {
+        if (policy == FIRST_FIT) {
+            for (const auto &kv : freeb)
+                if (kv.second >= r) return take(kv.first, r);
+            return HEAP_NULL;
+        }
+        if (policy == BEST_FIT) {
+            /* Alg. 3: scan the whole free list, keep the smallest fitting block; exact match
+             * ends the scan.  Ties go to the lowest address (reading C3). */
+            bool found = false; uint64_t bs = 0, bz = 0;
+            for (const auto &kv : freeb) {
+                if (kv.second < r) continue;
+                if (!found || kv.second < bz) { found = true; bs = kv.first; bz = kv.second; }
+                if (kv.second == r) break;
+            }
+            return found ? take(bs, r) : HEAP_NULL;
+        }
+        if (policy == SEGFIT || policy == TLSF) {
+            /* Alg. 4 + availability bitmap/ffs fallback: the first
+             * nonempty bin at or above the search class, its lowest-address block (C9). */
+            uint64_t c = search_class(r, L);
+            auto it = cls_index.lower_bound({c, 0});
+            if (it == cls_index.end()) return HEAP_NULL;
+            return take(it->second, r);
+        }
+        /* BUDDY: r is already a power of two */
+        int k = floor_log2(r);
+        int j = k;
+        while (j <= K && bfree[j].empty()) j++;
+        if (j > K) return HEAP_NULL;
+        uint64_t a = *bfree[j].begin();
+        bfree[j].erase(bfree[j].begin());
+        for (int t = j - 1; t >= k; t--) bfree[t].insert(a + (1ull << t));  /* split, keep low half */
+        live[a] = r;
+        return a;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
+    if (align == 0 || (align & (align - 1)) || arena_bytes == 0 || arena_bytes % align) return nullptr;
+    if (policy < FIRST_FIT || policy > BUDDY) return nullptr;
+    Heap *h = new Heap();
+    h->policy = policy;
+    h->L = (policy == TLSF) ? 5 : 0;
+    h->align = align;
+    h->arena_bytes = arena_bytes;
+    h->A_u = arena_bytes / align;
+    if (policy == BUDDY) {
+        h->K = floor_log2(h->A_u);
+        h->bfree.assign(h->K + 1, std::set<uint64_t>());
+        /* greedy decomposition of [0, A_u) into maximal aligned power-of-two blocks (C13) */
+        uint64_t s = 0;
+        while (s < h->A_u) {
+            int t = h->K;
+            while (t > 0 && ((s & ((1ull << t) - 1)) || s + (1ull << t) > h->A_u)) t--;
+            h->bfree[t].insert(s);
+            s += 1ull << t;
+        }
+    } else {
+        h->free_insert(0, h->A_u);   /* "at least one entry: the heap itself" */
+    }
+    return h;
+}
+
+void oracle_destroy(void *p) { delete (Heap *)p; }
+
+/* frees: classify every copy against the batch-start state, then free the valid live starts
+ * in ascending address order.  Classification (reading C16):
+ *   HEAP_NULL -> null; unaligned / out of range / neither live nor free start -> invalid;
+ *   live start -> first copy frees, other copies double; start of a free block -> double. */
+void oracle_free_batch(void *p, const uint64_t *offsets, uint64_t n) {
+    Heap *h = (Heap *)p;
+    std::vector<uint64_t> v(offsets, offsets + n);
+    std::sort(v.begin(), v.end());
+    std::vector<uint64_t> to_free;
+    for (uint64_t i = 0; i < n; i++) {
+        uint64_t o = v[i];
+        bool dup = (i > 0 && v[i - 1] == o);
+        if (o == HEAP_NULL) { h->c.frees_null++; continue; }
+        if (o % h->align || o / h->align >= h->A_u) { h->c.frees_invalid++; continue; }
+        uint64_t u = o / h->align;
+        if (h->live.count(u)) {
+            if (dup) h->c.frees_double++;
+            else { h->c.frees_ok++; to_free.push_back(u); }
+        } else if (h->is_free_start(u)) {
+            h->c.frees_double++;
+        } else {
+            h->c.frees_invalid++;
+        }
+    }
+    for (uint64_t u : to_free) h->free_block(u);   /* ascending address order */
+}
+
+void oracle_alloc_batch(void *p, const uint64_t *sizes, uint64_t n, uint64_t *out) {
+    Heap *h = (Heap *)p;
+    for (uint64_t i = 0; i < n; i++) {
+        uint64_t s = sizes[i];
+        uint64_t r = s / h->align + (s % h->align != 0);     /* ceil(s / align) */
+        uint64_t u = HEAP_NULL;
+        if (s != 0 && r <= h->A_u) {
+            if (h->policy == BUDDY) {
+                uint64_t p2 = 1;
+                while (p2 < r) p2 <<= 1;                        /* round up to a power of two */
+                if (p2 <= h->A_u) u = h->alloc_units(p2);
+                if (u != HEAP_NULL) r = p2;
+            } else {
+                u = h->alloc_units(r);
+            }
+        }
+        if (u == HEAP_NULL) { out[i] = HEAP_NULL; h->c.allocs_failed++; }
+        else {
+            out[i] = u * h->align;
+            h->c.allocs_ok++;
+            h->c.high_water_end = std::max(h->c.high_water_end, (u + r) * h->align);
+        }
+    }
+}
+
+/* stats in the heap_stats_t field order (include/heap.h): 16 x u64, bytes */
+void oracle_stats(void *p, uint64_t *o) {
+    Heap *h = (Heap *)p;
+    uint64_t live_b = 0, free_b = 0, nfree = 0, largest = 0;
+    for (const auto &kv : h->live) live_b += kv.second;
+    if (h->policy == BUDDY) {
+        for (int k = 0; k <= h->K; k++) {
+            nfree += h->bfree[k].size();
+            free_b += (uint64_t)h->bfree[k].size() << k;
+            if (!h->bfree[k].empty()) largest = std::max<uint64_t>(largest, 1ull << k);
+        }
+    } else {
+        for (const auto &kv : h->freeb) { free_b += kv.second; nfree++; largest = std::max(largest, kv.second); }
+    }
+    uint64_t a = h->align;
+    uint64_t vals[16] = {h->arena_bytes, a, live_b * a, free_b * a, (uint64_t)h->live.size(), nfree,
+                         largest * a, h->c.high_water_end, h->c.allocs_ok, h->c.allocs_failed,
+                         h->c.frees_ok, h->c.frees_invalid, h->c.frees_double, h->c.frees_null, 0, 0};
+    memcpy(o, vals, sizeof(vals));
+}
+
+/* export: free (start,size) pairs in address order and live (start,size) pairs, bytes.
+ * counts[0] = #free, counts[1] = #live; pairs written only up to the capacities. */
+void oracle_export(void *p, uint64_t *free_pairs, uint64_t cap_free, uint64_t *live_pairs,
+                   uint64_t cap_live, uint64_t *counts) {
+    Heap *h = (Heap *)p;
+    uint64_t a = h->align, i = 0;
+    if (h->policy == BUDDY) {
+        std::map<uint64_t, uint64_t> all;
+        for (int k = 0; k <= h->K; k++) for (uint64_t s : h->bfree[k]) all[s] = 1ull << k;
+        for (const auto &kv : all) { if (i < cap_free) { free_pairs[2 * i] = kv.first * a; free_pairs[2 * i + 1] = kv.second * a; } i++; }
+    } else {
+        for (const auto &kv : h->freeb) { if (i < cap_free) { free_pairs[2 * i] = kv.first * a; free_pairs[2 * i + 1] = kv.second * a; } i++; }
+    }
+    counts[0] = i;
+    i = 0;
+    for (const auto &kv : h->live) { if (i < cap_live) { live_pairs[2 * i] = kv.first * a; live_pairs[2 * i + 1] = kv.second * a; } i++; }
+    counts[1] = i;
+}
+
+/* the TLSF mapping, exported so tests can pin it against the paper's log2 formulas */
+uint64_t oracle_insert_class(uint64_t u, int L) { return insert_class(u, L); }
+uint64_t oracle_search_class(uint64_t u, int L) { return search_class(u, L); }
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+"""Shared test helpers: trace replay, invariant checker, golden-file parser.
+
+Nothing here implements allocator arithmetic; the invariants are the paper's
+properties checked on exported state.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+HEAP_NULL = (1 << 64) - 1
+POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5}
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+class IdMap:
+    """id -> offset map of a trace (HEAP_NULL for failed or not-yet-made allocs)."""
+
+    def __init__(self, n: int):
+        self.a = np.full(max(n, 1), HEAP_NULL, dtype=np.uint64)
+
+    def ensure(self, n):
+        if n > self.a.size:
+            b = np.full(max(n, 2 * self.a.size), HEAP_NULL, dtype=np.uint64)
+            b[: self.a.size] = self.a
+            self.a = b
+
+    def offsets(self, ids: np.ndarray) -> np.ndarray:
+        return self.a[ids.astype(np.int64)] if ids.size else np.zeros(0, dtype=np.uint64)
+
+    def record(self, first: int, out: np.ndarray):
+        self.ensure(first + out.size)
+        self.a[first:first + out.size] = out
+
+
+def replay(heap, trace, idmap: IdMap | None = None, on_batch=None, max_batches=None):
+    """Drive ``heap`` (free_batch / alloc_batch) with a tracegen.Trace."""
+    idmap = idmap or IdMap(1 << 16)
+    for bi, (fids, sizes, first) in enumerate(trace):
+        if max_batches is not None and bi >= max_batches:
+            break
+        offs = idmap.offsets(fids)
+        heap.free_batch(offs)
+        out = heap.alloc_batch(sizes)
+        idmap.record(first, np.asarray(out, dtype=np.uint64))
+        if on_batch is not None:
+            on_batch(bi, offs, sizes, out)
+    return idmap
+
+
+def check_invariants(free_pairs, live_pairs, arena: int, align: int, buddy: bool):
+    """I1 no overlap, I2 tiling/conservation, I3 full coalescing, I4 alignment."""
+    fp = np.asarray(free_pairs, dtype=np.uint64).reshape(-1, 2)
+    lp = np.asarray(live_pairs, dtype=np.uint64).reshape(-1, 2)
+    allb = np.concatenate([np.c_[fp, np.zeros(len(fp), np.uint64)],
+                           np.c_[lp, np.ones(len(lp), np.uint64)]])
+    allb = allb[np.argsort(allb[:, 0], kind="stable")]
+    # I4 alignment and positive sizes
+    assert np.all(allb[:, 0] % align == 0) and np.all(allb[:, 1] % align == 0)
+    assert np.all(allb[:, 1] > 0)
+    # I1 + I2: sorted blocks tile [0, arena) exactly
+    if len(allb):
+        assert allb[0, 0] == 0
+        ends = allb[:, 0] + allb[:, 1]
+        assert np.all(ends[:-1] == allb[1:, 0]), "overlap or gap"
+        assert ends[-1] == arena
+    else:
+        assert arena == 0
+    assert int(fp[:, 1].sum()) + int(lp[:, 1].sum()) == arena
+    # I3 coalescing
+    if len(fp):
+        fps = fp[np.argsort(fp[:, 0])]
+        if not buddy:
+            assert np.all(fps[:-1, 0] + fps[:-1, 1] != fps[1:, 0]), "adjacent free blocks"
+        else:
+            sz = fps[:, 1]
+            assert np.all(sz & (sz - 1) == 0)
+            assert np.all(fps[:, 0] % sz == 0), "buddy block not aligned to its size"
+            s = set(map(tuple, fps.tolist()))
+            for a, z in s:
+                assert (a ^ z, z) not in s, "two free buddies not merged"
+
+
+def parse_golden(name: str):
+    cases = []
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            body, _, cite = line.partition("@")
+            head, ops, expect = [x.strip() for x in body.split("|")]
+            pol, arena, align = head.split()
+            batches = []
+            for b in ops.split("/"):
+                fr = [int(t[1:]) for t in b.split() if t.startswith("f")]
+                al = [int(t[1:]) for t in b.split() if t.startswith("a")]
+                batches.append((fr, al))
+            outs, _, frees = expect.partition("#")
+            outs = [int(x) for x in outs.split()]
+            frees = frees.strip()
+            if frees == "*":
+                fl = None
+            else:
+                fl = [tuple(int(v) for v in x.split(":")) for x in frees.split()]
+            cases.append(dict(policy=POLICY[pol], arena=int(arena), align=int(align),
+                              batches=batches, outs=outs, frees=fl, cite=cite.strip()))
+    return cases

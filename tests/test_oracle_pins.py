@@ -1,0 +1,336 @@
+"""Pins for the oracle (-m "not gpu").
+
+The oracle is only trusted because these tests tie it to something other than
+itself: the paper's formulas and worked examples (tests/golden/, each line cited),
+closed forms (fresh-heap prefix sums, buddy addresses), the paper's invariants,
+and a structurally different brute-force oracle (Oracle-B) including exhaustive
+enumeration on tiny heaps.  A plausible slip in Oracle-L (wrong split end, missing
+left/right merge, off-by-one class, wrong tie-break, LIFO instead of address order,
+wrong buddy half) fails at least one of them.
+"""
+from __future__ import annotations
+
+import itertools
+import random
+
+import numpy as np
+import pytest
+
+import tracegen as tg
+from oracle import OracleL, insert_class, search_class
+from oracle.oracle_b import OracleB, cls_lo, cls_of, search_cls
+from tests.helpers import HEAP_NULL, IdMap, check_invariants, parse_golden, replay
+
+FIT_POLICIES = [1, 2, 3, 4]
+ALL_POLICIES = [1, 2, 3, 4, 5]
+
+
+def run_case(H, case):
+    h = H(case["arena"], case["align"], case["policy"])
+    outs = []
+    for fr, al in case["batches"]:
+        h.free_batch(np.array(fr, dtype=np.uint64))
+        outs = [int(x) for x in h.alloc_batch(np.array(al, dtype=np.uint64))]
+    return h, outs
+
+
+@pytest.mark.parametrize("case", parse_golden("spec_examples.txt"), ids=lambda c: c["cite"][:40])
+def test_golden_examples(case):
+    impls = [OracleL]
+    if case["arena"] // case["align"] <= 1 << 16:
+        impls.append(OracleB)
+    for H in impls:
+        h, outs = run_case(H, case)
+        assert outs == case["outs"], (H.__name__, case["cite"])
+        if case["frees"] is not None:
+            fp, _ = h.export()
+            assert [tuple(int(v) for v in p) for p in fp] == case["frees"], (H.__name__, case["cite"])
+
+
+# ---------------- TLSF / segregated-fit class mapping ----------------
+
+def test_segfit_mapping_is_paper_log2():
+    """SL_LOG2 = 0: block bin = floor(log2 size), request bin = ceil(log2 size)
+    (Alg. 4 PAPER.md:332 '1 << ceil(log2(size))', :351/:429 'floor(log2(...))');
+    our class numbers carry a +1 shift (C7)."""
+    for u in list(range(1, 1 << 14)) + [2**31 - 1, 2**31, 2**31 + 1, 2**32 - 1, 2**32]:
+        fl = u.bit_length() - 1                  # floor(log2 u)
+        cl = (u - 1).bit_length()                # ceil(log2 u)
+        assert insert_class(u, 0) == fl + 1
+        assert search_class(u, 0) == cl + 1
+
+
+def test_mapping_spec_examples():
+    """SPEC.md:416-418,425-427 (derived from Alg. 4): bins 3000->11, 4096->12; requests
+    1000->10, 1024->10 (align 1, our classes shifted by +1); TLSF SLI=16: 2432 -> sl 3."""
+    assert insert_class(3000, 0) - 1 == 11
+    assert insert_class(4096, 0) - 1 == 12
+    assert search_class(1000, 0) - 1 == 10
+    assert search_class(1024, 0) - 1 == 10
+    assert insert_class(2432, 4) % 16 == 3
+
+
+@pytest.mark.parametrize("L", [0, 4, 5])
+def test_mapping_defining_properties(L):
+    """insert class brackets the size; search class is the smallest class whose every
+    block fits (lo >= u) — Oracle-B's definition, checked against Oracle-L's formula."""
+    us = list(range(1, 1 << 13)) + [random.Random(L).randrange(1, 1 << 32) for _ in range(3000)]
+    for u in us:
+        c = insert_class(u, L)
+        assert c == cls_of(u, L)
+        assert cls_lo(c, L) <= u < cls_lo(c + 1, L)
+        s = search_class(u, L)
+        assert s == search_cls(u, L)
+        assert cls_lo(s, L) >= u and (s == 0 or cls_lo(s - 1, L) < u)
+
+
+def test_tlsf_worked_values():
+    """Worked values at align 16, SL_LOG2=5 (C10 table)."""
+    L = 5
+    def fs(c):
+        return divmod(c, 32)
+    assert fs(insert_class(16 // 16, L)) == (0, 1)
+    assert fs(insert_class(496 // 16, L)) == (0, 31)
+    assert fs(insert_class(512 // 16, L)) == (1, 0)
+    assert fs(insert_class(-(-1000 // 16), L)) == (1, 31) and fs(search_class(63, L)) == (1, 31)
+    assert fs(insert_class(1024 // 16, L)) == (2, 0) and cls_lo(insert_class(64, L), L) == 64
+    assert fs(insert_class(-(-3000 // 16), L)) == (3, 15) and fs(search_class(188, L)) == (3, 15)
+    assert fs(insert_class(-(-3010 // 16), L)) == (3, 15) and fs(search_class(189, L)) == (3, 16)
+    assert cls_lo(search_class(189, L), L) == 192
+    assert fs(insert_class((4 << 30) // 16, L)) == (24, 0)
+    assert fs(insert_class((64 << 30) // 16, L)) == (28, 0)
+
+
+def test_segfit_nearly_4x_bound():
+    """a request served from its own (power-of-two) bin gets a block
+    'nearly 4x larger' at worst, i.e. strictly below 4x."""
+    worst = 0.0
+    for u in range(1, 8193):
+        c = search_class(u, 0)
+        biggest = cls_lo(c + 1, 0) - 1
+        assert biggest < 4 * u
+        worst = max(worst, biggest / u)
+    assert worst > 3.9
+
+
+def test_tlsf_good_fit_failure():
+    """I6: TLSF rounds the request up to its search class, so it can fail while a block
+    >= r exists one class below (Masmano's good fit).  65 units: block class (2,0), search
+    class (2,1) -> NULL; first fit takes it."""
+    for H in (OracleL, OracleB):
+        h = H(65, 1, tg.TLSF)
+        assert int(h.alloc_batch([65])[0]) == HEAP_NULL
+        h = H(65, 1, tg.FIRST_FIT)
+        assert int(h.alloc_batch([65])[0]) == 0
+
+
+# ---------------- closed forms ----------------
+
+@pytest.mark.parametrize("policy", FIT_POLICIES)
+def test_fresh_heap_prefix_sums(policy):
+    """L3: with no frees every fit policy bump-allocates: out[i] = sum_{j<i} r_j * align
+    (Alg. 1 split from the low end of the single free block)."""
+    rng = np.random.default_rng(policy)
+    align = 16
+    sizes = rng.integers(1, 5000, size=400).astype(np.uint64)
+    r = -(-sizes.astype(np.int64) // align)
+    arena = int(r.sum() * align * 4)
+    h = OracleL(arena, align, policy)
+    out = h.alloc_batch(sizes).astype(np.int64)
+    expect = np.concatenate([[0], np.cumsum(r)[:-1]]) * align
+    assert np.array_equal(out, expect)
+
+
+def test_buddy_closed_forms():
+    """Buddy: a fresh heap serving only order-k requests returns
+    i*2^k; non-increasing orders return prefix sums; buddy of a is a XOR 2^k."""
+    A = 1 << 12
+    for k in range(0, 6):
+        h = OracleL(A, 1, tg.BUDDY)
+        n = A >> k
+        out = h.alloc_batch(np.full(n, 1 << k, dtype=np.uint64)).astype(np.int64)
+        assert np.array_equal(out, np.arange(n) << k)
+        assert int(h.alloc_batch([1])[0]) == HEAP_NULL
+    rng = np.random.default_rng(7)
+    ks = np.sort(rng.integers(0, 8, size=40))[::-1]
+    h = OracleL(A, 1, tg.BUDDY)
+    out = h.alloc_batch((1 << ks).astype(np.uint64)).astype(np.int64)
+    assert np.array_equal(out, np.concatenate([[0], np.cumsum(1 << ks)[:-1]]))
+    # freeing every block restores the single root block (merge with a XOR 2^k)
+    h.free_batch(out.astype(np.uint64))
+    fp, lp = h.export()
+    assert fp.tolist() == [[0, A]] and len(lp) == 0
+
+
+def test_free_all_restores_whole_heap():
+    """'free-then-alloc of the full heap size succeeds when nothing else is live'
+     — full coalescing, Alg. 2 / Alg. 5."""
+    for policy in FIT_POLICIES:
+        h = OracleL(1 << 16, 16, policy)
+        t = tg.Trace(tg.custom(policy, 1 << 16, 16, 64, total_ops=2000, idx=91))
+        im = replay(h, t)
+        live = im.a[im.a != HEAP_NULL]
+        h.free_batch(live)
+        fp, lp = h.export()
+        assert fp.tolist() == [[0, 1 << 16]] and len(lp) == 0
+        assert int(h.alloc_batch([1 << 16])[0]) == (0 if policy != tg.TLSF else 0)
+
+
+def test_free_classification():
+    """Error taxonomy (C16): null, invalid (interior, unaligned,
+    out of range, never allocated), double (free block start, or second copy)."""
+    for H in (OracleL, OracleB):
+        h = H(1024, 16, tg.FIRST_FIT)
+        a = [int(x) for x in h.alloc_batch([16, 32, 16])]      # 0, 16, 48
+        assert a == [0, 16, 48]
+        h.free_batch(np.array([HEAP_NULL, 16, 16, 17, 32, 2048, 64, 0], dtype=np.uint64))
+        c = h.stats() if H is OracleL else h.counts
+        assert c["frees_null"] == 1 and c["frees_ok"] == 2 and c["frees_double"] == 2
+        assert c["frees_invalid"] == 3
+        fp, lp = h.export()
+        assert [tuple(int(v) for v in p) for p in lp] == [(48, 16)]
+        assert [tuple(int(v) for v in p) for p in fp] == [(0, 48), (64, 960)]
+
+
+# ---------------- cross-oracle ----------------
+
+def _run_both(policy, arena, align, batch, ops, sizes, rho, idx, size_kind=0):
+    cfg = tg.custom(policy, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes,
+                    size_kind=size_kind, idx=idx)
+    hl, hb = OracleL(arena, align, policy), OracleB(arena, align, policy)
+    im_l, im_b = IdMap(ops), IdMap(ops)
+    for bi, (fids, sz, first) in enumerate(tg.Trace(cfg)):
+        ol, ob = im_l.offsets(fids), im_b.offsets(fids)
+        assert np.array_equal(ol, ob)
+        hl.free_batch(ol)
+        hb.free_batch(ob)
+        xl, xb = hl.alloc_batch(sz), hb.alloc_batch(sz)
+        assert np.array_equal(xl, xb), (policy, bi)
+        im_l.record(first, xl)
+        im_b.record(first, xb)
+        fl, ll = hl.export()
+        fb, lb = hb.export()
+        assert np.array_equal(fl, fb) and np.array_equal(ll, lb), (policy, bi)
+        check_invariants(fl, ll, arena, align, policy == tg.BUDDY)
+    st = hl.stats()
+    for k, v in hb.counts.items():
+        assert st[k] == v, k
+
+
+@pytest.mark.parametrize("policy", ALL_POLICIES)
+@pytest.mark.parametrize("seed", range(4))
+def test_oracle_l_equals_oracle_b(policy, seed):
+    if policy == tg.BUDDY:
+        _run_both(policy, 1 << 14, 16, 24, 1500, (0, 8), (1, 2), 80 + seed, size_kind=1)
+    else:
+        _run_both(policy, 1 << 14, 16, 24, 1500, (4, 10), (2, 5) if seed % 2 else (1, 2), 80 + seed)
+
+
+def test_config1_oracle_l_equals_oracle_b():
+    """Config 1 exactly (first fit, 1 MiB, 16 B, slot trace, 1000 ops)."""
+    cfg = tg.CONFIGS[1]
+    hl = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
+    hb = OracleB(cfg.arena_bytes, cfg.align, cfg.policy)
+    im_l, im_b = IdMap(1000), IdMap(1000)
+    for fids, sz, first in tg.Trace(cfg):
+        hl.free_batch(im_l.offsets(fids))
+        hb.free_batch(im_b.offsets(fids))
+        xl, xb = hl.alloc_batch(sz), hb.alloc_batch(sz)
+        assert np.array_equal(xl, xb)
+        im_l.record(first, xl)
+        im_b.record(first, xb)
+    fl, ll = hl.export()
+    fb, lb = hb.export()
+    assert np.array_equal(fl, fb) and np.array_equal(ll, lb)
+
+
+@pytest.mark.parametrize("policy", ALL_POLICIES)
+def test_exhaustive_tiny_heaps(policy):
+    """Every op sequence of length <= 4 over an 8-unit heap (alloc 1..8 units, free any
+    live block; one op per batch), Oracle-L == Oracle-B on every output and state."""
+    A = 8
+
+    def leaves(depth, seq, hb):
+        yield seq
+        if depth == 0:
+            return
+        for s in range(1, A + 1):
+            hb2 = _clone_b(hb)
+            hb2.alloc_batch([s])
+            yield from leaves(depth - 1, seq + [("a", s)], hb2)
+        for o in list(hb.live):
+            hb2 = _clone_b(hb)
+            hb2.free_batch([o])
+            yield from leaves(depth - 1, seq + [("f", o)], hb2)
+
+    n = 0
+    for seq in leaves(4, [], OracleB(A, 1, policy)):
+        hl, hb = OracleL(A, 1, policy), OracleB(A, 1, policy)
+        for op, v in seq:
+            if op == "a":
+                assert int(hl.alloc_batch([v])[0]) == int(hb.alloc_batch([v])[0]), seq
+            else:
+                hl.free_batch([v])
+                hb.free_batch([v])
+        fl, ll = hl.export()
+        fb, lb = hb.export()
+        assert np.array_equal(fl, fb) and np.array_equal(ll, lb), seq
+        n += 1
+    assert n > 1000
+
+
+def _clone_b(h):
+    c = OracleB.__new__(OracleB)
+    c.__dict__.update(h.__dict__)
+    c.bits = h.bits.copy()
+    c.live = dict(h.live)
+    c.counts = dict(h.counts)
+    return c
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3, 4])
+def test_invariants_on_scaled_configs(cfg_id):
+    """I1-I4 after every batch of a scaled-down config trace, plus conservation of
+    bytes in the stats (live + free = arena) and counters = per-request outcomes."""
+    cfg = tg.CONFIGS[cfg_id]
+    arena = cfg.arena_bytes >> 6 if cfg_id != 2 else cfg.arena_bytes >> 2
+    batch = max(cfg.batch >> 6, 64)
+    t = tg.Trace(tg.custom(cfg.policy, arena, cfg.align, batch, rho=(cfg.rho_num, cfg.rho_den),
+                           total_ops=batch * 12, sizes=(cfg.a, cfg.b), size_kind=cfg.size_kind,
+                           idx=cfg.idx))
+    h = OracleL(arena, cfg.align, cfg.policy)
+    tot = dict(ok=0, fail=0)
+
+    def on_batch(bi, offs, sizes, out):
+        fp, lp = h.export()
+        check_invariants(fp, lp, arena, cfg.align, cfg.policy == tg.BUDDY)
+        st = h.stats()
+        assert st["live_bytes"] + st["free_bytes"] == arena
+        assert st["n_live"] == len(lp) and st["n_free"] == len(fp)
+        tot["ok"] += int(np.sum(out != HEAP_NULL))
+        tot["fail"] += int(np.sum(out == HEAP_NULL))
+        assert st["allocs_ok"] == tot["ok"] and st["allocs_failed"] == tot["fail"]
+    replay(h, t, on_batch=on_batch)
+
+
+def test_free_order_independence():
+    """L1: the state after a free batch does not depend on the order of its frees
+    (address-keyed selection), checked by freeing in random orders one by one."""
+    for policy in ALL_POLICIES:
+        arena = 1 << 12
+        base = OracleL(arena, 1, policy)
+        sizes = np.random.default_rng(policy).integers(1, 40, size=60).astype(np.uint64)
+        out = base.alloc_batch(sizes)
+        live = out[out != HEAP_NULL]
+        pick = live[::2]
+        ref = OracleL(arena, 1, policy)
+        ref.alloc_batch(sizes)
+        ref.free_batch(pick)
+        want = ref.export()
+        for perm_seed in range(3):
+            h = OracleL(arena, 1, policy)
+            h.alloc_batch(sizes)
+            for o in np.random.default_rng(perm_seed).permutation(pick):
+                h.free_batch([o])
+            got = h.export()
+            assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
