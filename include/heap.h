@@ -1,0 +1,140 @@
+/*
+ * heap.h — C ABI of libheap: a batched, device-resident heap whose metadata lives out of
+ * band (arXiv 2405.07079, "Host-Based Allocators for Device Memory").
+ *
+ * The problem statement: an allocator manages an arena it may never
+ * read, so no boundary tags; all block metadata lives elsewhere.  Here
+ * the arena is any device range the caller owns (e.g. a torch tensor); the library returns
+ * byte OFFSETS into it and never dereferences the arena.  The metadata (block table, free
+ * arrays, class indices) lives in a caller-provided device WORKSPACE and is maintained by
+ * sm_100a kernels, one batch of requests per call.
+ *
+ * Semantics of a batch (BASELINE.json north_star):
+ *   heap_free_batch  - every offset is classified against the batch-start state; the valid
+ *                      live block starts are freed as if one by one in ascending address
+ *                      order, each coalescing with its free neighbours (Alg. 2 PAPER.md:214-236,
+ *                      Alg. 5; buddy merge PAPER.md:118).
+ *   heap_alloc_batch - requests are served as if one by one in request order under the
+ *                      policy (first/best fit PAPER.md:87-88, Alg. 3 :298-317; segregated fit
+ *                      Alg. 4 :327-369 with the bitmap/ffs fallback :440; TLSF :444-458; binary
+ *                      buddy :111-125); each choice splits the block from its low end (Alg. 1
+ *                      :173-184).  Results are bit-exact with the CPU oracle (oracle/).
+ *
+ * Conventions
+ *   - Every pointer argument is DEVICE memory unless its name starts with h_.
+ *   - Calls are asynchronous and ordered on the given stream (cudaStream_t; 0 = legacy
+ *     default stream).  Request arrays must stay valid until the stream passes the call.
+ *     One heap must be used from one stream at a time; there is no internal locking.
+ *   - Per-request failures are data, not return codes: a failed alloc (size 0, larger
+ *     than the arena, or no candidate block) yields HEAP_NULL and changes nothing; a free
+ *     of HEAP_NULL is a no-op; a free of anything that is not a live block start is
+ *     skipped and counted (frees_invalid / frees_double).  Partial (interior) frees are
+ *     not supported (C6).
+ *   - Metadata capacity overflow inside a batch (more live blocks than max_live_blocks)
+ *     cannot be reported synchronously: it sets error_flags and the next heap_stats()
+ *     returns HEAP_ECAPACITY.  The heap state after such a batch is unspecified.
+ *   - Units: sizes are rounded up to a multiple of align; arena_bytes / align must be
+ *     <= 2^32 (C20).
+ */
+#ifndef LIBHEAP_HEAP_H
+#define LIBHEAP_HEAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct heap heap_t;
+/* ABI-compatible with cudaStream_t; declared opaquely so this header needs no CUDA headers */
+typedef struct CUstream_st *heap_stream_t;
+
+/* policies: which free block an alloc takes (lowest key wins; DESIGN.md §2 table) */
+enum heap_policy {
+    HEAP_FIRST_FIT = 1, /* lowest-address block with size >= r */
+    HEAP_BEST_FIT = 2,  /* min (size, address) over size >= r             PAPER.md:87, Alg. 3 */
+    HEAP_SEGFIT = 3,    /* power-of-two bins, request bin = ceil(log2 r),
+                           block bin = floor(log2 size), address order    Alg. 4/5 */
+    HEAP_TLSF = 4,      /* two-level bins (32 linear sub-bins per power
+                           of two), min (bin, address) over bin >= search PAPER.md:447-458 */
+    HEAP_BUDDY = 5      /* binary buddy, min order then address; align is
+                           the minimum block */
+};
+
+#define HEAP_NULL UINT64_MAX /* failed alloc; no-op in a free batch (offset 0 is valid, C18) */
+
+enum heap_error {
+    HEAP_OK = 0,
+    HEAP_EINVAL = -1,    /* bad argument (align not a power of two, arena not a multiple of
+                            align, arena/align > 2^32, n > max_batch, NULL handle, ...) */
+    HEAP_ENOMEM = -2,    /* workspace too small or host allocation failed */
+    HEAP_ECAPACITY = -3, /* a batch overflowed a metadata capacity (sticky, see above) */
+    HEAP_ECUDA = -4      /* a CUDA call failed */
+};
+
+/* 16 x u64 = 128 bytes; byte quantities unless noted */
+typedef struct heap_stats {
+    uint64_t arena_bytes, align;
+    uint64_t live_bytes, free_bytes;   /* live + free == arena (conservation, I2) */
+    uint64_t n_live, n_free;           /* live blocks, free blocks */
+    uint64_t largest_free;             /* size of the largest free block */
+    uint64_t high_water_end;           /* max over all successful allocs of offset + size */
+    uint64_t allocs_ok, allocs_failed; /* failed = OOM + zero size + oversize */
+    uint64_t frees_ok, frees_invalid, frees_double, frees_null;
+    uint64_t metadata_bytes;           /* device workspace bytes the heap occupies */
+    uint64_t error_flags;              /* bit 0: live-block capacity, bit 1: table full */
+} heap_stats_t;
+
+/* Bytes of device workspace heap_create needs for these capacities.
+ *   max_live_blocks: upper bound on simultaneously live blocks (sizes the block table and
+ *                    the free-block arrays); max_batch: largest n of a single batch call.
+ * Returns 0 for invalid arguments. */
+size_t heap_workspace_bytes(uint64_t arena_bytes, uint64_t align, int policy,
+                            uint64_t max_live_blocks, uint64_t max_batch);
+
+/* Create a heap over [0, arena_bytes) (offsets), all free: one free block,
+ * or for HEAP_BUDDY the greedy decomposition into maximal aligned power-of-two blocks.
+ * d_workspace (>= heap_workspace_bytes(...) bytes, 256-byte aligned) is caller-owned and
+ * must outlive the heap; initialisation kernels are enqueued on s.  *h_out receives the
+ * host handle (the only memory the library owns). */
+int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_live_blocks,
+                uint64_t max_batch, void *d_workspace, size_t workspace_bytes,
+                heap_stream_t s, heap_t **h_out);
+
+/* Release the host handle.  Does not free the workspace (caller-owned).  The caller must
+ * make sure no enqueued work of this heap is still pending on a stream. */
+int heap_destroy(heap_t *h);
+
+/* Free a batch of n offsets (bytes).  0 <= n <= max_batch. */
+int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_stream_t s);
+
+/* Allocate a batch of n requests: d_sizes[i] bytes -> d_out_offsets[i] (byte offset into the
+ * arena, or HEAP_NULL).  0 <= n <= max_batch.  d_out_offsets must not alias d_sizes. */
+int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out_offsets, uint64_t n,
+                     heap_stream_t s);
+
+/* Enqueue a reduction of the heap's statistics into d_out (device, 128 bytes).  No host
+ * synchronisation; this is what an NCCL all-gather of statistics consumes. */
+int heap_stats_async(heap_t *h, heap_stats_t *d_out, heap_stream_t s);
+
+/* heap_stats_async + copy to h_out + stream synchronise.  Returns HEAP_ECAPACITY if a
+ * capacity error flag is set (h_out is still filled). */
+int heap_stats(heap_t *h, heap_stats_t *h_out, heap_stream_t s);
+
+/* Export the state for parity checks: free blocks and live blocks as (start, size) byte
+ * pairs sorted by start, into device arrays of cap_free / cap_live pairs (2 x u64 each).
+ * h_counts[0] = #free blocks, h_counts[1] = #live blocks (true counts even if they exceed
+ * the capacities, in which case only the first cap pairs are written).  Synchronises s. */
+int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *d_live_pairs,
+                uint64_t cap_live, uint64_t *h_counts, heap_stream_t s);
+
+/* Number of kernel launches this heap has enqueued so far (for the bench's gpu_launches). */
+uint64_t heap_launch_count(const heap_t *h);
+
+const char *heap_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIBHEAP_HEAP_H */

@@ -1,0 +1,16 @@
+"""paper_2405_07079_b200 — a B200-native batched device heap with out-of-band metadata.
+
+arXiv 2405.07079 ("Host-Based Allocators for Device Memory") poses an allocator that may
+never read the memory it manages.  This package services whole
+batches of malloc/free requests against such a heap with sm_100a kernels behind the C ABI
+in include/heap.h; the Python layer only marshals arguments.
+"""
+from .heap import (HEAP_BEST_FIT, HEAP_BUDDY, HEAP_FIRST_FIT, HEAP_NULL, HEAP_NULL_I64, HEAP_SEGFIT,
+                   HEAP_TLSF, POLICY_NAMES, Heap, heap_alloc_batch, heap_create, heap_destroy,
+                   heap_export, heap_free_batch, heap_launch_count, heap_stats, heap_stats_async,
+                   heap_strerror, heap_workspace_bytes)
+
+__all__ = ["Heap", "heap_workspace_bytes", "heap_create", "heap_destroy", "heap_free_batch",
+           "heap_alloc_batch", "heap_stats_async", "heap_stats", "heap_export", "heap_launch_count",
+           "heap_strerror", "HEAP_FIRST_FIT", "HEAP_BEST_FIT", "HEAP_SEGFIT", "HEAP_TLSF", "HEAP_BUDDY",
+           "HEAP_NULL", "HEAP_NULL_I64", "POLICY_NAMES"]

@@ -1,0 +1,293 @@
+// buddy.cuh — binary buddy as level-by-level scans.
+//
+// State: for each order t (block = 2^t units) the free block starts, sorted, stored back to
+// back with offsets ctr->bud_off[t] (a CSR by order).
+//
+// Free phase (merge): for t = 0..K the order-t free set is the merge of the
+// resident order-t blocks, the freed order-t blocks and the blocks promoted from order t-1.
+// In that sorted list two buddies (a, a + 2^t with bit t of a clear) are adjacent; each such
+// pair is removed and its parent a is promoted to order t+1.  What stays is final for order t.
+// The result is the canonical set of maximal aligned free blocks (lemma L2), i.e. the same
+// set the one-by-one merge of the oracle produces.
+//
+// Alloc phase (split, "the first is split further"), lemma L6:
+//   bottom-up, order t: demands D_t = time-ordered merge of the order-t requests and the
+//   borrows from order t-1.  The first n_t demands take the batch-start order-t blocks in
+//   address order; excess demand x (0-based) is served by borrow floor(x/2) from order t+1:
+//   the low half for even x, +2^t for odd x.  Order t issues ceil(x_t/2) borrows, each
+//   carrying the time of the demand that triggered it.  Demands the top order cannot serve
+//   fail, and failure propagates down (it is absorbing: once orders >= t are empty they stay
+//   empty for the rest of the batch).
+//   top-down, order t = K..0: addresses flow from each demand to its request or borrow.
+//   Leftover: if x_t is odd and its last borrow succeeded, that borrow's high half stays free.
+// Both passes run in one CTA per heap (levels are dependent; the work per level is spread
+// over 1024 threads with merge-path partitions).
+#pragma once
+#include "common.cuh"
+
+namespace buddy {
+
+constexpr int NT = 1024;
+constexpr u32 BORROW = 0x80000000u;
+constexpr u64 FAIL = 0xFFFFFFFFFFFFFFFFull;
+
+// CTA-wide merge of two sorted u64 arrays (ties: a first) into out; all threads call.
+__device__ void cta_merge_u64(const u64 *a, u64 na, const u64 *b, u64 nb, u64 *out) {
+    const u64 n = na + nb;
+    const u64 per = (n + NT - 1) / NT;
+    u64 diag = (u64)threadIdx.x * per;
+    if (diag < n) {
+        u64 lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+        while (lo < hi) {
+            u64 mid = (lo + hi) >> 1;
+            if (a[mid] <= b[diag - mid - 1]) lo = mid + 1; else hi = mid;
+        }
+        u64 i = lo, j = diag - lo;
+        for (u64 k = 0; k < per && diag + k < n; k++) {
+            bool ta = (j >= nb) || (i < na && a[i] <= b[j]);
+            out[diag + k] = ta ? a[i++] : b[j++];
+        }
+    }
+}
+
+// CTA-wide merge by time of (tm, src) pairs
+__device__ void cta_merge_tm(const u32 *at, const u32 *as, u64 na, const u32 *bt, const u32 *bsrc, u64 nb,
+                             u32 *ot, u32 *os) {
+    const u64 n = na + nb;
+    const u64 per = (n + NT - 1) / NT;
+    u64 diag = (u64)threadIdx.x * per;
+    if (diag < n) {
+        u64 lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+        while (lo < hi) {
+            u64 mid = (lo + hi) >> 1;
+            if (at[mid] <= bt[diag - mid - 1]) lo = mid + 1; else hi = mid;
+        }
+        u64 i = lo, j = diag - lo;
+        for (u64 k = 0; k < per && diag + k < n; k++) {
+            bool ta = (j >= nb) || (i < na && at[i] <= bt[j]);
+            if (ta) { ot[diag + k] = at[i]; os[diag + k] = as[i]; i++; }
+            else { ot[diag + k] = bt[j]; os[diag + k] = bsrc[j]; j++; }
+        }
+    }
+}
+
+// CTA-wide stream compaction helper: each thread handles a contiguous chunk; returns the
+// number of kept elements.  keep(i) decides, emit(i, pos) writes.
+template <typename Keep, typename Emit>
+__device__ u64 cta_compact(u64 n, Keep keep, Emit emit, u32 *sm) {
+    const u64 per = (n + NT - 1) / NT;
+    const u64 b = (u64)threadIdx.x * per;
+    u32 cnt = 0;
+    for (u64 k = 0; k < per && b + k < n; k++) cnt += keep(b + k) ? 1 : 0;
+    u32 tot;
+    u32 pos = block_excl_scan<NT>(cnt, sm, &tot);
+    for (u64 k = 0; k < per && b + k < n; k++)
+        if (keep(b + k)) emit(b + k, (u64)pos++);
+    return tot;
+}
+
+// ------------------------------------------------------------------ free phase ----
+// freed blocks: fr_start (units) grouped by order via fr_off[t] (sorted within order)
+__global__ void __launch_bounds__(NT) k_free_levels(const u64 *__restrict__ old_list, u64 *__restrict__ new_list,
+                                                    const u64 *__restrict__ fr, const u32 *__restrict__ fr_off,
+                                                    u64 *bufA, u64 *bufB, u64 *promo, int K, DevCtr *ctr) {
+    __shared__ u32 sm[33];
+    __shared__ u64 ooff[41];
+    __shared__ u64 s_np, s_out;
+    if (threadIdx.x <= (unsigned)K + 1) ooff[threadIdx.x] = ctr->bud_off[threadIdx.x];
+    if (threadIdx.x == 0) { s_np = 0; s_out = 0; }
+    __syncthreads();
+    for (int t = 0; t <= K; t++) {
+        const u64 *old_t = old_list + ooff[t];
+        const u64 n_old = ooff[t + 1] - ooff[t];
+        const u64 *fr_t = fr + fr_off[t];
+        const u64 n_fr = fr_off[t + 1] - fr_off[t];
+        const u64 n_pr = s_np;
+        cta_merge_u64(old_t, n_old, fr_t, n_fr, bufA);
+        __syncthreads();
+        cta_merge_u64(bufA, n_old + n_fr, promo, n_pr, bufB);
+        __syncthreads();
+        const u64 n = n_old + n_fr + n_pr;
+        const u64 bit = 1ull << t;
+        auto paired_lo = [&](u64 i) { return t < K && !(bufB[i] & bit) && i + 1 < n && bufB[i + 1] == bufB[i] + bit; };
+        auto paired_hi = [&](u64 i) { return t < K && (bufB[i] & bit) && i > 0 && bufB[i - 1] == bufB[i] - bit; };
+        const u64 out0 = s_out;
+        // survivors -> new list (order t)
+        u64 ns = cta_compact(n, [&](u64 i) { return !paired_lo(i) && !paired_hi(i); },
+                             [&](u64 i, u64 p) { new_list[out0 + p] = bufB[i]; }, sm);
+        __syncthreads();
+        // promotions -> promo (read by the next level; bufB still holds this level)
+        u64 np = cta_compact(n, [&](u64 i) { return paired_lo(i); },
+                             [&](u64 i, u64 p) { promo[p] = bufB[i]; }, sm);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ctr->bud_off[t] = out0;
+            ctr->bud_cnt[t] = ns;
+            s_out = out0 + ns;
+            s_np = np;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ctr->bud_off[K + 1] = s_out;
+        ctr->bud_total = s_out;
+    }
+}
+
+// freed (start, end) -> sort key = order, payload = index
+__global__ void k_free_orders(const u64 *__restrict__ vs, const u64 *__restrict__ ve, const u64 *nv_dev,
+                              u32 *__restrict__ key, u32 *__restrict__ val) {
+    const u64 nv = *nv_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (u64)gridDim.x * blockDim.x) {
+        key[i] = (u32)flog2(ve[i] - vs[i]);
+        val[i] = (u32)i;
+    }
+}
+__global__ void k_gather_u64(const u64 *__restrict__ src, const u32 *__restrict__ idx, const u64 *n_dev,
+                             u64 *__restrict__ dst) {
+    const u64 n = *n_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+// ------------------------------------------------------------------ alloc phase ----
+// r -> order key (K+1 = fail bucket)
+__global__ void k_alloc_orders(const u64 *__restrict__ sizes, u64 n, int alog2, u64 A_u, int K,
+                               u32 *__restrict__ key, u32 *__restrict__ val, u64 *n_dev) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
+    const u64 amask = (1ull << alog2) - 1;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        u64 s = sizes[i];
+        u64 r = (s >> alog2) + ((s & amask) != 0);
+        u32 k = (u32)K + 1;
+        if (s != 0 && r <= A_u) {
+            u32 kk = (r <= 1) ? 0u : (u32)(flog2(r - 1) + 1);   // ceil(log2 r)
+            if (kk <= (u32)K && (1ull << kk) <= A_u) k = kk;
+        }
+        key[i] = k;
+        val[i] = (u32)i;
+    }
+}
+
+// Bottom-up + top-down L6 in one CTA.
+//   req_t/req_off: request indices sorted by (order, time); blocks: old per-order lists.
+//   dtm/dsrc: pool for the demand streams, daddr: their addresses; baddr: borrow addresses.
+__global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req, const u32 *__restrict__ req_off,
+                                                     const u64 *__restrict__ old_list, u64 *__restrict__ new_list,
+                                                     u32 *dtm, u32 *dsrc, u64 *daddr, u64 *baddr,
+                                                     u32 *btm, u32 *bsrc, u64 *__restrict__ out_u, int K,
+                                                     DevCtr *ctr) {
+    __shared__ u32 sm[33];
+    __shared__ u64 ooff[41];
+    __shared__ u64 doff[42], boff[42];
+    __shared__ u64 s_nb;
+    if (threadIdx.x <= (unsigned)K + 1) ooff[threadIdx.x] = ctr->bud_off[threadIdx.x];
+    if (threadIdx.x == 0) { doff[0] = 0; boff[0] = 0; s_nb = 0; }
+    __syncthreads();
+    // requests of the fail bucket
+    for (u64 i = req_off[K + 1] + threadIdx.x; i < req_off[K + 2]; i += NT) out_u[req[i]] = FAIL;
+    // ---- bottom-up ----
+    for (int t = 0; t <= K; t++) {
+        const u64 n_t = ooff[t + 1] - ooff[t];
+        const u64 nr = req_off[t + 1] - req_off[t];
+        const u32 *rq = req + req_off[t];
+        const u64 nb = s_nb;        // borrows from t-1 (already in btm/bsrc)
+        u32 *Dt = dtm + doff[t], *Ds = dsrc + doff[t];
+        // direct requests: time = request index, src = request index
+        // merge (rq, rq) with (btm, bsrc)
+        cta_merge_tm(rq, rq, nr, btm, bsrc, nb, Dt, Ds);
+        __syncthreads();
+        const u64 nd = nr + nb;
+        const u64 x = nd > n_t ? nd - n_t : 0;
+        const u64 nbor = (t < K) ? (x + 1) / 2 : 0;
+        for (u64 j = threadIdx.x; j < nbor; j += NT) {
+            btm[j] = Dt[n_t + 2 * j];
+            bsrc[j] = (u32)j | BORROW;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            doff[t + 1] = doff[t] + nd;
+            boff[t + 1] = boff[t] + nbor;
+            s_nb = nbor;
+        }
+        __syncthreads();
+    }
+    // ---- top-down ----
+    u64 out_pos = 0;   // running offset of the new per-order lists (thread-uniform)
+    __shared__ u64 s_left[41], s_cnt[41];
+    for (int t = K; t >= 0; t--) {
+        const u64 n_t = ooff[t + 1] - ooff[t];
+        const u64 *blk = old_list + ooff[t];
+        const u64 nd = doff[t + 1] - doff[t];
+        const u32 *Ds = dsrc + doff[t];
+        const u64 *bad = baddr + boff[t];   // borrows of order t (served by t+1)
+        const u64 nbor = boff[t + 1] - boff[t];
+        u64 *bad_lo = (t > 0) ? baddr + boff[t - 1] : nullptr;   // borrows of order t-1
+        for (u64 p = threadIdx.x; p < nd; p += NT) {
+            u64 a;
+            if (p < n_t) a = blk[p];
+            else {
+                u64 xx = p - n_t, j = xx >> 1;
+                a = (j < nbor && bad[j] != FAIL) ? bad[j] + ((xx & 1) ? (1ull << t) : 0) : FAIL;
+            }
+            u32 s = Ds[p];
+            if (s & BORROW) bad_lo[s & ~BORROW] = a;
+            else out_u[s] = a;
+        }
+        if (threadIdx.x == 0) {
+            u64 x = nd > n_t ? nd - n_t : 0;
+            u64 left = FAIL;
+            if ((x & 1) && nbor > 0 && bad[nbor - 1] != FAIL) left = bad[nbor - 1] + (1ull << t);
+            s_left[t] = left;
+            s_cnt[t] = (nd < n_t ? n_t - nd : 0) + (left != FAIL ? 1 : 0);
+        }
+        __syncthreads();
+    }
+    (void)out_pos;
+    // ---- new per-order lists: surviving batch-start blocks, or the one leftover ----
+    __shared__ u64 noff[42];
+    if (threadIdx.x == 0) {
+        u64 o = 0;
+        for (int t = 0; t <= K; t++) { noff[t] = o; o += s_cnt[t]; }
+        noff[K + 1] = o;
+    }
+    __syncthreads();
+    for (int t = 0; t <= K; t++) {
+        const u64 n_t = ooff[t + 1] - ooff[t];
+        const u64 nd = doff[t + 1] - doff[t];
+        const u64 *blk = old_list + ooff[t];
+        if (nd < n_t) {
+            for (u64 p = nd + threadIdx.x; p < n_t; p += NT) new_list[noff[t] + (p - nd)] = blk[p];
+        } else if (s_left[t] != FAIL && threadIdx.x == 0) {
+            new_list[noff[t]] = s_left[t];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x <= (unsigned)K + 1) {
+        ctr->bud_off[threadIdx.x] = noff[threadIdx.x];
+        if (threadIdx.x <= (unsigned)K) ctr->bud_cnt[threadIdx.x] = s_cnt[threadIdx.x];
+    }
+    if (threadIdx.x == 0) ctr->bud_total = noff[K + 1];
+}
+
+// buddy results: order -> units = 2^k; reuse fits::k_alloc_finish by materialising r
+__global__ void k_alloc_r(const u32 *__restrict__ key_by_req, u64 n, int K, u64 *__restrict__ r) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        u32 k = key_by_req[i];
+        r[i] = (k <= (u32)K) ? (1ull << k) : 0;
+    }
+}
+
+__device__ __forceinline__ bool is_free_start(const u64 *list, const DevCtr *ctr, int K, u64 key) {
+    for (int t = 0; t <= K; t++) {
+        u64 lo = ctr->bud_off[t], hi = ctr->bud_off[t + 1];
+        while (lo < hi) {
+            u64 mid = (lo + hi) >> 1;
+            if (list[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        if (lo < ctr->bud_off[t + 1] && list[lo] == key) return true;
+    }
+    return false;
+}
+
+}  // namespace buddy

@@ -1,0 +1,516 @@
+// fits.cuh — batched free and alloc phases for the non-buddy policies
+// (FIRST_FIT, BEST_FIT, SEGFIT, TLSF).
+//
+// State between batches: the free blocks as an address-sorted, fully coalesced SoA array
+// (start, end) in units (the role of the paper's address-sorted HAL free list, §3.1,
+// PAPER.md:166-168), plus the block table (table.cuh).
+//
+// Free phase (canonical order: every offset classified against the batch-start state, then
+// valid frees applied as if one by one in ascending address order, Alg. 2 / Alg. 5):
+//   classify -> compact -> radix sort of keys -> table lookup+delete (dedup, double/invalid)
+//   -> compact valid -> merge path with the free array -> coalesce by head flags + scan.
+// The result is the set of maximal free runs (lemma L2: the free set is a function of the
+// live set), so applying the frees "one by one" and "all at once" coincide.
+//
+// Alloc phase: requests are normalised in parallel, then matched by an exact engine that
+// walks them in request order (the paper's per-request semantics, C25 reading A).
+// Key fact used by every engine: during an alloc phase each batch-start free block f holds
+// at most ONE free piece, [start_f, end_f), which only shrinks from its low end (Alg. 1
+// splits at the low end and nothing is freed during the phase).  So the engine state is just
+// start_f per block, and address order among pieces is the order of f.
+#pragma once
+#include "common.cuh"
+#include "prims.cuh"
+#include "table.cuh"
+#include "buddy.cuh"
+
+namespace fits {
+
+// ------------------------------------------------------------------ free phase ----
+__global__ void k_free_classify(const u64 *__restrict__ offs, u64 n, int alog2, u64 A_u,
+                                u32 *__restrict__ keys, u32 *__restrict__ flags, u64 *n_dev,
+                                DevCtr *ctr) {
+    __shared__ u64 sm[33];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
+    u64 nnull = 0, ninv = 0;
+    const u64 amask = (1ull << alog2) - 1;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    const u64 nround = (n + stride - 1) / stride;
+    for (u64 r = 0; r < nround; r++) {
+        u64 i = r * stride + (u64)blockIdx.x * blockDim.x + threadIdx.x;
+        if (i < n) {
+            u64 o = offs[i];
+            u32 f = 0, key = 0;
+            if (o == HEAP_NULL_U64) nnull++;
+            else if ((o & amask) || (o >> alog2) >= A_u) ninv++;
+            else { f = 1; key = (u32)(o >> alog2); }
+            flags[i] = f;
+            keys[i] = key;
+        }
+    }
+    u64 a = block_sum64<prims::NT>(nnull, sm);
+    u64 b = block_sum64<prims::NT>(ninv, sm);
+    if (threadIdx.x == 0) {
+        if (a) atomicAdd(&ctr->frees_null, a);
+        if (b) atomicAdd(&ctr->frees_invalid, b);
+    }
+}
+
+template <typename T>
+__global__ void k_compact(const T *__restrict__ in, const u32 *__restrict__ flags,
+                          const u32 *__restrict__ pos, const u64 *n_dev, T *__restrict__ out) {
+    const u64 n = *n_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        if (flags[i]) out[pos[i]] = in[i];
+}
+
+__device__ __forceinline__ bool bsearch_u64(const u64 *a, u64 n, u64 key) {
+    u64 lo = 0, hi = n;
+    while (lo < hi) {
+        u64 mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && a[lo] == key;
+}
+
+// Per sorted key: the first copy of each run of equal keys looks the key up in the block
+// table (deleting it if live); the run's other copies are classified from that result.
+// Live -> 1 ok + (copies-1) double; start of a free block -> all double; else all invalid.
+__global__ void __launch_bounds__(256) k_free_lookup(const u32 *__restrict__ keys, const u64 *nk_dev,
+                                                     u64 *__restrict__ slots, u64 tmask, u64 max_lines,
+                                                     const u64 *__restrict__ fstart, const u64 *F_dev,
+                                                     const u64 *__restrict__ bud_list, int K,
+                                                     u32 *__restrict__ vflag, u64 *__restrict__ vs,
+                                                     u64 *__restrict__ ve, DevCtr *ctr) {
+    __shared__ u64 sm[33];
+    const u64 nk = *nk_dev, F = F_dev ? *F_dev : 0;
+    const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
+    const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+    u64 c_ok = 0, c_dbl = 0, c_inv = 0, c_units = 0;
+    for (u64 base = gw * 4; base < nk; base += nwarps * 4) {
+        u64 idx = base + g;
+        bool in = idx < nk;
+        u32 key = in ? keys[idx] : 0;
+        bool first = in && (idx == 0 || keys[idx - 1] != key);
+        u64 s = table::lookup(slots, tmask, key, first, true, max_lines);
+        if (in && sub == 0) {
+            u32 f = 0;
+            if (first) {
+                u64 ndup = 0;
+                for (u64 j = idx + 1; j < nk && keys[j] == key; j++) ndup++;
+                if (s != table::EMPTY) {
+                    u64 z = table::slot_size(s);
+                    f = 1;
+                    vs[idx] = key;
+                    ve[idx] = (u64)key + z;
+                    c_ok++; c_dbl += ndup; c_units += z;
+                } else if (bud_list ? buddy::is_free_start(bud_list, ctr, K, key)
+                                    : bsearch_u64(fstart, F, key)) {
+                    c_dbl += 1 + ndup;
+                } else {
+                    c_inv += 1 + ndup;
+                }
+            }
+            vflag[idx] = f;
+        }
+    }
+    u64 a = block_sum64<256>(c_ok, sm), b = block_sum64<256>(c_dbl, sm);
+    u64 c = block_sum64<256>(c_inv, sm), d = block_sum64<256>(c_units, sm);
+    if (threadIdx.x == 0) {
+        if (a) { atomicAdd(&ctr->frees_ok, a); atomicAdd(&ctr->n_live, (u64)0 - a); atomicAdd(&ctr->tbl_tombs, a); }
+        if (b) atomicAdd(&ctr->frees_double, b);
+        if (c) atomicAdd(&ctr->frees_invalid, c);
+        if (d) atomicAdd(&ctr->live_units, (u64)0 - d);
+    }
+}
+
+// head flag: element i starts a new maximal run unless the previous block ends where it starts
+__global__ void k_coal_flags(const u64 *__restrict__ ms, const u64 *__restrict__ me, const u64 *M_dev,
+                             u32 *__restrict__ head) {
+    const u64 M = *M_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (u64)gridDim.x * blockDim.x)
+        head[i] = (i == 0 || me[i - 1] != ms[i]) ? 1u : 0u;
+}
+
+// heads write the run start, tails the run end (the coalesced block is [first start, last end))
+__global__ void k_coal_write(const u64 *__restrict__ ms, const u64 *__restrict__ me, const u64 *M_dev,
+                             const u32 *__restrict__ head, const u32 *__restrict__ pos,
+                             u64 *__restrict__ os, u64 *__restrict__ oe, u64 cap, DevCtr *ctr) {
+    const u64 M = *M_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (u64)gridDim.x * blockDim.x) {
+        u32 h = head[i];
+        u64 run = pos[i] + h - 1;
+        if (run >= cap) { atomicOr(&ctr->error_flags, (u64)ERR_CAP_FREE); continue; }
+        if (h) os[run] = ms[i];
+        if (i + 1 == M || head[i + 1]) oe[run] = me[i];
+    }
+}
+
+// ------------------------------------------------------------------ alloc phase ----
+// r = ceil(s / align) units (0 = fail: size 0 or larger than the arena), c = search class
+__global__ void k_alloc_prep(const u64 *__restrict__ sizes, u64 n, int alog2, u64 A_u, int L, int want_cls,
+                             u64 *__restrict__ r_out, u32 *__restrict__ c_out) {
+    const u64 amask = (1ull << alog2) - 1;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        u64 s = sizes[i];
+        u64 r = (s >> alog2) + ((s & amask) != 0);
+        if (s == 0 || r > A_u) r = 0;
+        r_out[i] = r;
+        if (want_cls) c_out[i] = r ? cls_search(r, L) : 0xFFFFFFFFu;
+    }
+}
+
+// piece survives iff it still has units
+__global__ void k_piece_flags(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev,
+                              u32 *__restrict__ flags) {
+    const u64 F = *F_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x)
+        flags[i] = fs[i] < fe[i] ? 1u : 0u;
+}
+
+// write results, insert the new live blocks into the block table, update counters
+__global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r, const u64 *__restrict__ out_u,
+                                                      u64 n, int alog2, u64 *__restrict__ out_bytes,
+                                                      u64 *__restrict__ slots, u64 tmask, u64 max_lines,
+                                                      DevCtr *ctr, u64 max_live) {
+    __shared__ u64 sm[33];
+    const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
+    const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+    u64 c_ok = 0, c_fail = 0, c_units = 0, c_used = 0, c_tomb = 0, c_full = 0, hw = 0;
+    for (u64 base = gw * 4; base < n; base += nwarps * 4) {
+        u64 i = base + g;
+        bool in = i < n;
+        u64 o = in ? out_u[i] : HEAP_NULL_U64;
+        bool ok = in && o != HEAP_NULL_U64;
+        u64 ri = ok ? r[i] : 0;
+        int rc = table::insert(slots, tmask, o, ri, ok, max_lines);
+        if (rc == 1) c_used++;
+        if (rc == -1) c_tomb++;
+        if (rc == 2) c_full++;
+        if (in && sub == 0) {
+            out_bytes[i] = ok ? (o << alog2) : HEAP_NULL_U64;
+            if (ok) { c_ok++; c_units += ri; hw = max(hw, o + ri); }
+            else c_fail++;
+        }
+    }
+    u64 a = block_sum64<256>(c_ok, sm), b = block_sum64<256>(c_fail, sm), c = block_sum64<256>(c_units, sm);
+    u64 d = block_sum64<256>(c_used, sm), e = block_sum64<256>(c_tomb, sm), f = block_sum64<256>(c_full, sm);
+    hw = warp_max64(hw);
+    __shared__ u64 hwm;
+    if (threadIdx.x == 0) hwm = 0;
+    __syncthreads();
+    if (lane == 0 && hw) atomicMax(&hwm, hw);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (a) {
+            atomicAdd(&ctr->allocs_ok, a);
+            u64 nl = atomicAdd(&ctr->n_live, a) + a;
+            if (nl > max_live) atomicOr(&ctr->error_flags, (u64)ERR_CAP_LIVE);
+        }
+        if (b) atomicAdd(&ctr->allocs_failed, b);
+        if (c) atomicAdd(&ctr->live_units, c);
+        if (d) atomicAdd(&ctr->tbl_used, d);
+        if (e) atomicAdd(&ctr->tbl_tombs, (u64)0 - e);
+        if (f) atomicOr(&ctr->error_flags, (u64)ERR_TABLE_FULL);
+        if (hwm) atomicMax(&ctr->high_water_units, hwm);
+    }
+}
+
+// ---------------------------------------------------------------- TLSF / SEGFIT ----
+// Per batch the free blocks are grouped by their class (stable radix sort of (class, f)),
+// giving each class an address-ordered array consumed as a prefix.  A block whose carved
+// remainder drops to a lower class k' joins k' through a per-class pairing heap keyed by f
+// (a block can be in only one class at a time, so child/sibling arrays indexed by f
+// suffice).  Class emptiness is kept in two-level bitmaps (one u32 word per first level, 32
+// second-level classes = one word), searched with ffs.
+__global__ void k_cls_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev, int L,
+                           u32 *__restrict__ key, u32 *__restrict__ val) {
+    const u64 F = *F_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x) {
+        key[i] = cls_insert(fe[i] - fs[i], L);
+        val[i] = (u32)i;
+    }
+}
+
+// off[k] = first position in the class-sorted order whose class >= k, for k = 0..NC
+__global__ void k_cls_off(const u32 *__restrict__ key, const u64 *F_dev, int NC, u32 *__restrict__ off) {
+    const u64 F = *F_dev;
+    const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x, nth = (u64)gridDim.x * blockDim.x;
+    if (F == 0) {
+        for (u64 k = tid; k <= (u64)NC; k += nth) off[k] = 0;
+        return;
+    }
+    for (u64 i = tid; i <= F; i += nth) {
+        u32 lo = (i == 0) ? 0 : key[i - 1] + 1;
+        u32 hi = (i == F) ? (u32)NC : key[i];
+        for (u32 k = lo; k <= hi; k++) off[k] = (u32)i;
+    }
+}
+
+struct PHeap {
+    u32 *child, *sib;
+    __device__ __forceinline__ u32 meld(u32 a, u32 b) {
+        if (a == NIL32) return b;
+        if (b == NIL32) return a;
+        if (b < a) { u32 t = a; a = b; b = t; }
+        sib[b] = child[a];
+        child[a] = b;
+        return a;
+    }
+    __device__ u32 delmin(u32 root) {
+        u32 x = child[root];
+        u32 acc = NIL32;
+        while (x != NIL32) {
+            u32 a = x, b = sib[a];
+            if (b == NIL32) { sib[a] = acc; acc = a; break; }
+            u32 nx = sib[b];
+            sib[a] = NIL32;
+            sib[b] = NIL32;
+            u32 m = meld(a, b);
+            sib[m] = acc;
+            acc = m;
+            x = nx;
+        }
+        u32 res = NIL32;
+        while (acc != NIL32) {
+            u32 nx = sib[acc];
+            sib[acc] = NIL32;
+            res = meld(res, acc);
+            acc = nx;
+        }
+        return res;
+    }
+};
+
+constexpr int MAX_NC = 1024;
+
+__global__ void __launch_bounds__(32) k_tlsf_engine(const u32 *__restrict__ csr, const u32 *__restrict__ off,
+                                                    u64 *__restrict__ fs, const u64 *__restrict__ fe,
+                                                    const u64 *__restrict__ r, const u32 *__restrict__ c, u64 n,
+                                                    u64 *__restrict__ out_u, u32 *child, u32 *sib, int NC, int L) {
+    __shared__ u32 ptr[MAX_NC], endp[MAX_NC], root[MAX_NC], cnt[MAX_NC];
+    __shared__ u32 cw[32];
+    __shared__ u32 sw;
+    const u32 lane = lane_id();
+    for (int k = lane; k < NC; k += 32) {
+        ptr[k] = off[k];
+        endp[k] = off[k + 1];
+        root[k] = NIL32;
+        cnt[k] = off[k + 1] - off[k];
+    }
+    __syncwarp();
+    u32 swl = 0;
+    for (int w = 0; w < 32; w++) {
+        int k = w * 32 + lane;
+        u32 b = __ballot_sync(FULLMASK, k < NC && cnt[k] > 0);
+        if (lane == 0) cw[w] = b;
+        if (b) swl |= 1u << w;
+    }
+    if (lane == 0) sw = swl;
+    __syncwarp();
+    if (lane != 0) return;
+    PHeap ph{child, sib};
+    u32 summ = sw;
+    for (u64 i = 0; i < n; i++) {
+        u64 ri = r[i];
+        u32 ci = c[i];
+        if (ri == 0 || ci >= (u32)NC) { out_u[i] = HEAP_NULL_U64; continue; }
+        // first nonempty class >= ci: second-level word, then first-level summary (ffs)
+        u32 w = ci >> 5;
+        u32 m = cw[w] & (0xFFFFFFFFu << (ci & 31));
+        int k;
+        if (m) k = (int)(w << 5) + __ffs(m) - 1;
+        else {
+            u32 sm = (w >= 31) ? 0u : (summ & (0xFFFFFFFFu << (w + 1)));
+            if (!sm) { out_u[i] = HEAP_NULL_U64; continue; }
+            u32 w2 = __ffs(sm) - 1;
+            k = (int)(w2 << 5) + __ffs(cw[w2]) - 1;
+        }
+        u32 a = ptr[k] < endp[k] ? csr[ptr[k]] : NIL32;
+        u32 b = root[k];
+        bool from_heap = b < a;
+        u32 f = from_heap ? b : a;
+        u64 s = fs[f], e = fe[f];
+        out_u[i] = s;
+        s += ri;
+        fs[f] = s;
+        u64 z = e - s;
+        int nk = z ? (int)cls_insert(z, L) : -1;
+        if (nk != k) {
+            if (from_heap) root[k] = ph.delmin(b);
+            else ptr[k]++;
+            if (--cnt[k] == 0) {
+                cw[k >> 5] &= ~(1u << (k & 31));
+                if (!cw[k >> 5]) summ &= ~(1u << (k >> 5));
+            }
+            if (z) {
+                child[f] = NIL32;
+                sib[f] = NIL32;
+                root[nk] = ph.meld(root[nk], f);
+                if (cnt[nk]++ == 0) {
+                    cw[nk >> 5] |= 1u << (nk & 31);
+                    summ |= 1u << (nk >> 5);
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------- FIRST FIT ----
+// A 32-ary max tree over piece sizes: the first block with size >= r is found by one ballot
+// per level (warp-cooperative descent), then the carved piece's ancestors are refreshed.
+// Level l has ceil(F / 32^l) entries; levels are stored back to back at lvl_off[l].
+__global__ void k_ff_leaves(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev,
+                            u64 *__restrict__ lv0) {
+    const u64 F = *F_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x)
+        lv0[i] = fe[i] - fs[i];
+}
+
+__global__ void k_ff_level(const u64 *__restrict__ below, u64 *__restrict__ above, const u64 *F_dev, int l) {
+    u64 nb = *F_dev;
+    for (int i = 1; i < l; i++) nb = (nb + 31) >> 5;
+    const u64 na = (nb + 31) >> 5;
+    const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
+    for (u64 j = gw; j < na; j += nw) {
+        u64 idx = j * 32 + lane_id();
+        u64 v = idx < nb ? below[idx] : 0;
+        v = warp_max64(v);
+        if (lane_id() == 0) above[j] = v;
+    }
+}
+
+constexpr int FF_MAX_LEVELS = 8;
+
+__global__ void __launch_bounds__(32) k_ff_engine(u64 *tree, const u64 *__restrict__ lvl_off, int nlev,
+                                                  u64 *fs, const u64 *F_dev, const u64 *__restrict__ r, u64 n,
+                                                  u64 *__restrict__ out_u) {
+    const u32 lane = lane_id();
+    u64 sz[FF_MAX_LEVELS];
+    u64 F = *F_dev;
+    sz[0] = F;
+    for (int l = 1; l < nlev; l++) sz[l] = (sz[l - 1] + 31) >> 5;
+    int top = 0;
+    while (top + 1 < nlev && sz[top] > 32) top++;
+    for (u64 i = 0; i < n; i++) {
+        u64 ri = r[i];
+        if (ri == 0 || F == 0) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+        u64 j = 0;     // node index at the current level (level top has one node: 0)
+        bool fail = false;
+        for (int l = top; l >= 0; l--) {
+            u64 idx = j * 32 + lane;
+            u64 v = idx < sz[l] ? tree[lvl_off[l] + idx] : 0;
+            u32 b = __ballot_sync(FULLMASK, v >= ri);
+            if (!b) { fail = true; break; }
+            j = j * 32 + __ffs(b) - 1;
+        }
+        if (fail) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+        u64 f = j;
+        if (lane == 0) {
+            u64 s = fs[f];
+            out_u[i] = s;
+            fs[f] = s + ri;
+            tree[lvl_off[0] + f] -= ri;
+        }
+        __syncwarp();
+        u64 node = f;
+        for (int l = 1; l <= top; l++) {
+            u64 p = node >> 5;
+            u64 idx = p * 32 + lane;
+            u64 v = idx < sz[l - 1] ? tree[lvl_off[l - 1] + idx] : 0;
+            v = warp_max64(v);
+            if (lane == 0) tree[lvl_off[l] + p] = v;
+            __syncwarp();
+            node = p;
+        }
+    }
+}
+
+// -------------------------------------------------------------------- BEST FIT ----
+// Pieces sorted by key = (size << FB) | f, i.e. by (size, address).  Per request a 32-ary
+// warp search finds the first key >= (r << FB): the smallest fitting block, lowest address on
+// ties (Alg. 3 with reading C3).  The carved piece moves down to its new rank (warp shift).
+// The array lives in shared memory when it fits, otherwise in global memory.
+__global__ void k_bf_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev, int FB,
+                          u64 *__restrict__ key) {
+    const u64 F = *F_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x)
+        key[i] = ((fe[i] - fs[i]) << FB) | i;
+}
+
+__device__ __forceinline__ u64 warp_lower_bound(const u64 *a, u64 lo, u64 hi, u64 target) {
+    const u32 lane = lane_id();
+    while (hi - lo > 32) {
+        u64 step = (hi - lo + 31) >> 5;
+        u64 idx = lo + (u64)(lane + 1) * step - 1;
+        if (idx >= hi) idx = hi - 1;
+        u32 b = __ballot_sync(FULLMASK, a[idx] >= target);
+        if (!b) return hi;
+        u32 fl = __ffs(b) - 1;
+        u64 nlo = lo + (u64)fl * step;
+        u64 nhi = lo + (u64)(fl + 1) * step;
+        if (nhi > hi) nhi = hi;
+        lo = nlo;
+        hi = nhi;   // answer in [lo, hi]: a[hi-1] >= target
+    }
+    u64 idx = lo + lane;
+    u32 b = __ballot_sync(FULLMASK, idx < hi && a[idx] >= target);
+    return b ? lo + __ffs(b) - 1 : hi;
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
+                                                  const u64 *__restrict__ r, u64 n, u64 *__restrict__ out_u) {
+    extern __shared__ u64 skeys[];
+    const u32 lane = lane_id();
+    u64 nb = *F_dev;
+    u64 *keys = SMEM ? skeys : gkeys;
+    if (SMEM) {
+        for (u64 i = lane; i < nb; i += 32) skeys[i] = gkeys[i];
+        __syncwarp();
+    }
+    const u64 fmask = (1ull << FB) - 1;
+    for (u64 i = 0; i < n; i++) {
+        u64 ri = r[i];
+        if (ri == 0) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+        u64 p = warp_lower_bound(keys, 0, nb, ri << FB);
+        if (p >= nb) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+        u64 key = keys[p];
+        u64 z = key >> FB, f = key & fmask;
+        if (lane == 0) {
+            u64 s = fs[f];
+            out_u[i] = s;
+            fs[f] = s + ri;
+        }
+        u64 z2 = z - ri;
+        if (z2) {
+            u64 nkey = (z2 << FB) | f;
+            u64 q = warp_lower_bound(keys, 0, p, nkey);
+            // shift [q, p) up by one, highest chunk first
+            for (u64 hi = p; hi > q;) {
+                u64 lo = hi >= q + 32 ? hi - 32 : q;
+                u64 idx = lo + lane;
+                u64 v = idx < hi ? keys[idx] : 0;
+                __syncwarp();
+                if (idx < hi) keys[idx + 1] = v;
+                __syncwarp();
+                hi = lo;
+            }
+            if (lane == 0) keys[q] = nkey;
+        } else {
+            for (u64 lo = p + 1; lo < nb; lo += 32) {
+                u64 idx = lo + lane;
+                u64 v = idx < nb ? keys[idx] : 0;
+                __syncwarp();
+                if (idx < nb) keys[idx - 1] = v;
+                __syncwarp();
+            }
+            nb--;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace fits

@@ -1,0 +1,601 @@
+// heap.cu — libheap: the C ABI (include/heap.h) over the sm_100a kernels.
+//
+// Host side: argument checks, workspace carving, and the kernel sequence of each batch.
+// Nothing here synchronises with the device except heap_stats / heap_export.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <algorithm>
+#include "../../include/heap.h"
+#include "common.cuh"
+#include "prims.cuh"
+#include "table.cuh"
+#include "buddy.cuh"
+#include "fits.cuh"
+
+namespace {
+
+inline u64 align_up(u64 x, u64 a) { return (x + a - 1) / a * a; }
+inline int ilog2(u64 x) { int r = -1; while (x) { x >>= 1; r++; } return r; }
+inline u64 next_pow2(u64 x) { u64 p = 1; while (p < x) p <<= 1; return p; }
+
+// host mirror of the class mapping, used only to size the class range (NC)
+inline u64 h_cls_insert(u64 u, int L) {
+    if (u < (1ull << L)) return u;
+    int m = ilog2(u);
+    return ((u64)(m - L + 1) << L) + ((u >> (m - L)) - (1ull << L));
+}
+
+struct Layout {
+    u64 A_u, cap_f, cap_m, tcap, sort_cap, scan_cap, hist_cap, ff_tree, bud_cap, dpool, bpool;
+    int nlev, K, NC, L, FB;
+    // offsets
+    u64 o_ctr, o_stats, o_tbl, o_fs0, o_fs1, o_fe0, o_fe1, o_kA, o_kB, o_vA, o_vB, o_flags, o_pos,
+        o_hist, o_tsum, o_vs, o_ve, o_vsc, o_vec, o_ms, o_me, o_r, o_c, o_out, o_off, o_child,
+        o_sib, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
+        o_promo, o_fr, o_froff, o_reqoff, total;
+};
+
+bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, Layout *Lo) {
+    if (align == 0 || (align & (align - 1)) || arena == 0 || arena % align) return false;
+    if (policy < HEAP_FIRST_FIT || policy > HEAP_BUDDY) return false;
+    if (max_live == 0 || max_batch == 0 || max_batch >= (1ull << 31) || max_live >= (1ull << 30)) return false;
+    Layout &L = *Lo;
+    memset(&L, 0, sizeof(L));
+    L.A_u = arena / align;
+    if (L.A_u > (1ull << 32)) return false;
+    L.K = ilog2(L.A_u);
+    L.L = (policy == HEAP_TLSF) ? 5 : 0;
+    L.NC = (int)h_cls_insert(L.A_u, L.L) + 1;
+    L.cap_f = max_live + 1;
+    if (policy == HEAP_BUDDY) L.cap_f = (max_live + 1) * 2 * (u64)(L.K + 1);
+    L.cap_m = L.cap_f + max_batch;
+    L.tcap = next_pow2(2 * max_live);
+    if (L.tcap < 1024) L.tcap = 1024;
+    L.sort_cap = std::max(std::max(max_batch, L.cap_f), max_live) + 16;
+    L.hist_cap = 256 * prims::ntiles_of(L.sort_cap) + 16;
+    L.scan_cap = std::max(std::max(L.cap_m, L.sort_cap), L.hist_cap);
+    L.scan_cap = std::max(L.scan_cap, L.tcap);
+    L.FB = ilog2(L.cap_f) + 1;
+    // first-fit tree levels
+    u64 n = L.cap_f;
+    L.nlev = 1;
+    L.ff_tree = n;
+    while (n > 32) { n = (n + 31) / 32; L.ff_tree += n; L.nlev++; }
+    L.bud_cap = L.cap_f + max_batch;
+    L.dpool = 2 * max_batch + 256;
+    L.bpool = max_batch + 256;
+    u64 o = 0;
+    auto take = [&](u64 bytes) { u64 r = o; o = align_up(o + bytes, 256); return r; };
+    L.o_ctr = take(sizeof(DevCtr));
+    L.o_stats = take(sizeof(heap_stats_t));
+    L.o_tbl = take(L.tcap * 8);
+    L.o_fs0 = take(L.cap_f * 8);
+    L.o_fs1 = take(L.cap_f * 8);
+    if (policy != HEAP_BUDDY) { L.o_fe0 = take(L.cap_f * 8); L.o_fe1 = take(L.cap_f * 8); }
+    L.o_kA = take(L.sort_cap * 4);
+    L.o_kB = take(L.sort_cap * 4);
+    L.o_vA = take(L.sort_cap * 4);
+    L.o_vB = take(L.sort_cap * 4);
+    L.o_flags = take(L.scan_cap * 4);
+    L.o_pos = take(L.scan_cap * 4);
+    L.o_hist = take(L.hist_cap * 4);
+    L.o_tsum = take((prims::ntiles_of(L.scan_cap) + 16) * 4);
+    L.o_vs = take(max_batch * 8);
+    L.o_ve = take(max_batch * 8);
+    L.o_vsc = take(max_batch * 8);
+    L.o_vec = take(max_batch * 8);
+    L.o_ms = take(std::max(L.cap_m, max_live + 16) * 8);
+    L.o_me = take(std::max(L.cap_m, max_live + 16) * 8);
+    L.o_r = take(max_batch * 8);
+    L.o_c = take(max_batch * 4);
+    L.o_out = take(max_batch * 8);
+    L.o_off = take((fits::MAX_NC + 8) * 4);
+    if (policy == HEAP_TLSF || policy == HEAP_SEGFIT) {
+        L.o_child = take(L.cap_f * 4);
+        L.o_sib = take(L.cap_f * 4);
+    }
+    if (policy == HEAP_FIRST_FIT) {
+        L.o_tree = take(L.ff_tree * 8);
+        L.o_lvl = take(fits::FF_MAX_LEVELS * 8);
+    }
+    if (policy == HEAP_BEST_FIT) {
+        L.o_bk0 = take(L.cap_f * 8);
+        L.o_bk1 = take(L.cap_f * 8);
+    }
+    if (policy == HEAP_BUDDY) {
+        L.o_dtm = take(L.dpool * 4);
+        L.o_dsrc = take(L.dpool * 4);
+        L.o_baddr = take(L.bpool * 8);
+        L.o_btm = take(L.bpool * 4);
+        L.o_bsrc = take(L.bpool * 4);
+        L.o_bufA = take(L.bud_cap * 8);
+        L.o_bufB = take(L.bud_cap * 8);
+        L.o_promo = take(L.bud_cap * 8);
+        L.o_fr = take(max_batch * 8);
+        L.o_froff = take(64 * 4);
+        L.o_reqoff = take(64 * 4);
+    }
+    L.total = o;
+    return true;
+}
+
+template <typename T> T *at(void *ws, u64 off) { return reinterpret_cast<T *>(static_cast<char *>(ws) + off); }
+
+}  // namespace
+
+struct heap {
+    u64 arena, align, max_live, max_batch;
+    int policy, alog2, sms, G;
+    Layout L;
+    void *ws;
+    size_t ws_bytes;
+    int cur;
+    u64 launches;
+    DevCtr *ctr;
+    heap_stats_t *dstats;
+    u64 *tbl, *fs[2], *fe[2];
+    u32 *kA, *kB, *vA, *vB, *flags, *pos, *hist, *tsum;
+    u64 *vs, *ve, *vsc, *vec, *ms, *me, *r, *out;
+    u32 *c, *off, *child, *sib;
+    u64 *tree, *lvl;
+    u64 *bk[2];
+    u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
+    u64 *baddr, *bufA, *bufB, *promo, *fr;
+};
+
+#define LAUNCH(h, kern, grid, block, smem, stream, ...)                       \
+    do {                                                                      \
+        kern<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__); \
+        (h)->launches++;                                                      \
+    } while (0)
+
+namespace {
+
+__global__ void k_init(DevCtr *ctr, u64 *tbl, u64 tcap, u64 *fs, u64 *fe, u64 A_u, int buddy, int K) {
+    const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x, nth = (u64)gridDim.x * blockDim.x;
+    for (u64 i = tid; i < tcap; i += nth) tbl[i] = table::EMPTY;
+    if (tid == 0) {
+        memset(ctr, 0, sizeof(DevCtr));
+        if (!buddy) {
+            fs[0] = 0;      // the heap itself is the one free block (Alg. 6)
+            fe[0] = A_u;
+            ctr->F = 1;
+        } else {
+            // greedy decomposition into maximal aligned power-of-two blocks (C13):
+            // one block per set bit of A_u, largest first
+            u64 s = 0, o = 0;
+            for (int t = 0; t <= K + 1; t++) ctr->bud_off[t] = 0;
+            u64 addr[40];
+            for (int t = K; t >= 0; t--) {
+                addr[t] = s;
+                if ((A_u >> t) & 1) s += 1ull << t;
+            }
+            for (int t = 0; t <= K; t++) {
+                ctr->bud_off[t] = o;
+                u64 c = (A_u >> t) & 1;
+                ctr->bud_cnt[t] = c;
+                if (c) fs[o++] = addr[t];
+            }
+            ctr->bud_off[K + 1] = o;
+            ctr->bud_total = o;
+        }
+    }
+}
+
+// radix sort of *n_dev keys (ping-pong); returns the buffer index (0 = a, 1 = b) holding the result
+template <typename K, bool HV>
+int radix_sort(heap *h, K *ka, K *kb, u32 *va, u32 *vb, const u64 *n_dev, int bits, cudaStream_t s) {
+    int passes = (bits + 7) / 8;
+    K *kin = ka, *kout = kb;
+    u32 *vin = va, *vout = vb;
+    for (int p = 0; p < passes; p++) {
+        LAUNCH(h, prims::k_rs_hist<K>, h->G, prims::NT, 0, s, kin, n_dev, 8 * p, h->hist, &h->ctr->n_hist);
+        LAUNCH(h, prims::k_scan_reduce, h->G, prims::NT, 0, s, h->hist, &h->ctr->n_hist, h->tsum);
+        LAUNCH(h, prims::k_scan_tiles, 1, 1024, 0, s, h->tsum, &h->ctr->n_hist, &h->ctr->scan_total);
+        LAUNCH(h, prims::k_scan_down, h->G, prims::NT, 0, s, h->hist, h->hist, &h->ctr->n_hist, h->tsum);
+        LAUNCH(h, (prims::k_rs_scatter<K, HV>), h->G, prims::NT, 0, s, kin, vin, kout, vout, n_dev, 8 * p, h->hist);
+        K *tk = kin; kin = kout; kout = tk;
+        u32 *tv = vin; vin = vout; vout = tv;
+    }
+    return passes & 1;
+}
+
+// exclusive scan of u32 in[*n_dev] into out, grand total into *total
+void scan(heap *h, const u32 *in, u32 *out, const u64 *n_dev, u64 *total, cudaStream_t s) {
+    LAUNCH(h, prims::k_scan_reduce, h->G, prims::NT, 0, s, in, n_dev, h->tsum);
+    LAUNCH(h, prims::k_scan_tiles, 1, 1024, 0, s, h->tsum, n_dev, total);
+    LAUNCH(h, prims::k_scan_down, h->G, prims::NT, 0, s, in, out, n_dev, h->tsum);
+}
+
+__global__ void k_set_F(DevCtr *ctr) { ctr->F = ctr->tmp[1]; }
+
+// ---- table rebuild (tombstone purge), each kernel a no-op unless the flag is set ----
+__global__ void k_rb_check(DevCtr *ctr, u64 thresh) {
+    ctr->tmp[4] = (ctr->tbl_used > thresh) ? 1 : 0;
+    ctr->tmp[5] = 0;
+}
+__global__ void k_rb_collect(DevCtr *ctr, const u64 *tbl, u64 tcap, u64 *scratch) {
+    if (!ctr->tmp[4]) return;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x) {
+        u64 v = tbl[i];
+        if (table::is_live(v)) scratch[atomicAdd(&ctr->tmp[5], 1ull)] = v;
+    }
+}
+__global__ void k_rb_clear(const DevCtr *ctr, u64 *tbl, u64 tcap) {
+    if (!ctr->tmp[4]) return;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
+        tbl[i] = table::EMPTY;
+}
+__global__ void k_rb_insert(DevCtr *ctr, u64 *tbl, u64 tmask, u64 max_lines, const u64 *scratch) {
+    if (!ctr->tmp[4]) return;
+    const u64 n = ctr->tmp[5];
+    const u32 g = lane_id() >> 3;
+    const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
+    for (u64 base = gw * 4; base < n; base += nw * 4) {
+        u64 i = base + g;
+        bool in = i < n;
+        u64 v = in ? scratch[i] : 0;
+        int rc = table::insert(tbl, tmask, in ? table::slot_key(v) : 0, in ? table::slot_size(v) : 1, in, max_lines);
+        if (rc == 2) atomicOr(&ctr->error_flags, (u64)ERR_TABLE_FULL);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctr->tbl_used = n; ctr->tbl_tombs = 0; }
+}
+
+void maybe_rebuild(heap *h, cudaStream_t s) {
+    u64 thresh = h->L.tcap / 4 * 3;
+    LAUNCH(h, k_rb_check, 1, 1, 0, s, h->ctr, thresh);
+    LAUNCH(h, k_rb_collect, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap, h->ms);
+    LAUNCH(h, k_rb_clear, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap);
+    LAUNCH(h, k_rb_insert, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap - 1, h->L.tcap / table::LINE, h->ms);
+}
+
+// ---- statistics ----
+__global__ void __launch_bounds__(1024) k_stats(const DevCtr *ctr, const u64 *fs, const u64 *fe, int buddy, int K,
+                                                u64 arena, u64 align, int alog2, u64 meta, heap_stats_t *out) {
+    __shared__ u64 sm[33];
+    u64 nfree, fu = 0, big = 0;
+    if (!buddy) {
+        nfree = ctr->F;
+        for (u64 i = threadIdx.x; i < nfree; i += blockDim.x) {
+            u64 z = fe[i] - fs[i];
+            fu += z;
+            big = z > big ? z : big;
+        }
+        fu = block_sum64<1024>(fu, sm);
+        big = warp_max64(big);
+        __shared__ u64 bm;
+        if (threadIdx.x == 0) bm = 0;
+        __syncthreads();
+        if (lane_id() == 0) atomicMax(&bm, big);
+        __syncthreads();
+        big = bm;
+    } else {
+        nfree = 0;
+        for (int t = 0; t <= K; t++) {
+            nfree += ctr->bud_cnt[t];
+            fu += ctr->bud_cnt[t] << t;
+            if (ctr->bud_cnt[t]) big = 1ull << t;
+        }
+    }
+    if (threadIdx.x == 0) {
+        out->arena_bytes = arena;
+        out->align = align;
+        out->live_bytes = ctr->live_units << alog2;
+        out->free_bytes = fu << alog2;
+        out->n_live = ctr->n_live;
+        out->n_free = nfree;
+        out->largest_free = big << alog2;
+        out->high_water_end = ctr->high_water_units << alog2;
+        out->allocs_ok = ctr->allocs_ok;
+        out->allocs_failed = ctr->allocs_failed;
+        out->frees_ok = ctr->frees_ok;
+        out->frees_invalid = ctr->frees_invalid;
+        out->frees_double = ctr->frees_double;
+        out->frees_null = ctr->frees_null;
+        out->metadata_bytes = meta;
+        out->error_flags = ctr->error_flags;
+    }
+}
+
+// ---- export ----
+__global__ void k_export_free(const u64 *fs, const u64 *fe, const u64 *F_dev, int alog2, u64 *pairs, u64 cap) {
+    const u64 F = *F_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F && i < cap; i += (u64)gridDim.x * blockDim.x) {
+        pairs[2 * i] = fs[i] << alog2;
+        pairs[2 * i + 1] = (fe[i] - fs[i]) << alog2;
+    }
+}
+__global__ void k_bud_keys(const u64 *list, const DevCtr *ctr, int K, u32 *key, u32 *val) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < ctr->bud_total; i += (u64)gridDim.x * blockDim.x) {
+        int t = 0;
+        while (t < K && ctr->bud_off[t + 1] <= i) t++;
+        key[i] = (u32)list[i];
+        val[i] = (u32)t;
+    }
+}
+__global__ void k_export_pairs_u32(const u32 *key, const u32 *val, const u64 *n_dev, int alog2, int val_is_order,
+                                   u64 *pairs, u64 cap) {
+    const u64 n = *n_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n && i < cap; i += (u64)gridDim.x * blockDim.x) {
+        pairs[2 * i] = (u64)key[i] << alog2;
+        u64 z = val_is_order ? (1ull << val[i]) : ((u64)val[i] + 1);
+        pairs[2 * i + 1] = z << alog2;
+    }
+}
+__global__ void k_tbl_flags(const u64 *tbl, u64 tcap, u32 *flags) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
+        flags[i] = table::is_live(tbl[i]) ? 1u : 0u;
+}
+__global__ void k_tbl_compact(const u64 *tbl, u64 tcap, const u32 *flags, const u32 *pos, u32 *key, u32 *val) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
+        if (flags[i]) {
+            u64 v = tbl[i];
+            key[pos[i]] = (u32)table::slot_key(v);
+            val[pos[i]] = (u32)(v & 0xFFFFFFFFull);
+        }
+}
+__global__ void k_set_u64(u64 *p, u64 v) { *p = v; }
+
+}  // namespace
+
+extern "C" {
+
+size_t heap_workspace_bytes(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_live_blocks,
+                            uint64_t max_batch) {
+    Layout L;
+    if (!make_layout(arena_bytes, align, policy, max_live_blocks, max_batch, &L)) return 0;
+    return (size_t)L.total;
+}
+
+int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_live_blocks, uint64_t max_batch,
+                void *d_workspace, size_t workspace_bytes, heap_stream_t s, heap_t **h_out) {
+    if (!h_out) return HEAP_EINVAL;
+    *h_out = nullptr;
+    Layout L;
+    if (!make_layout(arena_bytes, align, policy, max_live_blocks, max_batch, &L)) return HEAP_EINVAL;
+    if (!d_workspace || ((uintptr_t)d_workspace & 255)) return HEAP_EINVAL;
+    if (workspace_bytes < L.total) return HEAP_ENOMEM;
+    heap *h = new (std::nothrow) heap();
+    if (!h) return HEAP_ENOMEM;
+    h->arena = arena_bytes; h->align = align; h->policy = policy;
+    h->max_live = max_live_blocks; h->max_batch = max_batch;
+    h->alog2 = ilog2(align);
+    h->L = L;
+    h->ws = d_workspace; h->ws_bytes = workspace_bytes;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    h->sms = sms;
+    h->G = sms * 4;
+    void *w = d_workspace;
+    h->ctr = at<DevCtr>(w, L.o_ctr);
+    h->dstats = at<heap_stats_t>(w, L.o_stats);
+    h->tbl = at<u64>(w, L.o_tbl);
+    h->fs[0] = at<u64>(w, L.o_fs0); h->fs[1] = at<u64>(w, L.o_fs1);
+    h->fe[0] = L.o_fe0 ? at<u64>(w, L.o_fe0) : nullptr; h->fe[1] = L.o_fe1 ? at<u64>(w, L.o_fe1) : nullptr;
+    h->kA = at<u32>(w, L.o_kA); h->kB = at<u32>(w, L.o_kB); h->vA = at<u32>(w, L.o_vA); h->vB = at<u32>(w, L.o_vB);
+    h->flags = at<u32>(w, L.o_flags); h->pos = at<u32>(w, L.o_pos); h->hist = at<u32>(w, L.o_hist);
+    h->tsum = at<u32>(w, L.o_tsum);
+    h->vs = at<u64>(w, L.o_vs); h->ve = at<u64>(w, L.o_ve); h->vsc = at<u64>(w, L.o_vsc); h->vec = at<u64>(w, L.o_vec);
+    h->ms = at<u64>(w, L.o_ms); h->me = at<u64>(w, L.o_me);
+    h->r = at<u64>(w, L.o_r); h->c = at<u32>(w, L.o_c); h->out = at<u64>(w, L.o_out);
+    h->off = at<u32>(w, L.o_off);
+    h->child = L.o_child ? at<u32>(w, L.o_child) : nullptr; h->sib = L.o_sib ? at<u32>(w, L.o_sib) : nullptr;
+    h->tree = L.o_tree ? at<u64>(w, L.o_tree) : nullptr; h->lvl = L.o_lvl ? at<u64>(w, L.o_lvl) : nullptr;
+    h->bk[0] = L.o_bk0 ? at<u64>(w, L.o_bk0) : nullptr; h->bk[1] = L.o_bk1 ? at<u64>(w, L.o_bk1) : nullptr;
+    if (policy == HEAP_BUDDY) {
+        h->dtm = at<u32>(w, L.o_dtm); h->dsrc = at<u32>(w, L.o_dsrc); h->baddr = at<u64>(w, L.o_baddr);
+        h->btm = at<u32>(w, L.o_btm); h->bsrc = at<u32>(w, L.o_bsrc);
+        h->bufA = at<u64>(w, L.o_bufA); h->bufB = at<u64>(w, L.o_bufB); h->promo = at<u64>(w, L.o_promo);
+        h->fr = at<u64>(w, L.o_fr); h->froff = at<u32>(w, L.o_froff); h->reqoff = at<u32>(w, L.o_reqoff);
+    }
+    h->cur = 0;
+    h->launches = 0;
+    cudaStream_t st = (cudaStream_t)s;
+    LAUNCH(h, k_init, h->G, 256, 0, st, h->ctr, h->tbl, L.tcap, h->fs[0], h->fe[0], L.A_u,
+           policy == HEAP_BUDDY ? 1 : 0, L.K);
+    if (policy == HEAP_FIRST_FIT) {
+        u64 offs[fits::FF_MAX_LEVELS] = {0};
+        u64 n = L.cap_f, o = 0;
+        for (int l = 0; l < L.nlev && l < fits::FF_MAX_LEVELS; l++) { offs[l] = o; o += n; n = (n + 31) / 32; }
+        for (int l = 0; l < fits::FF_MAX_LEVELS; l++) LAUNCH(h, k_set_u64, 1, 1, 0, st, h->lvl + l, offs[l]);
+    }
+    if (cudaGetLastError() != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    *h_out = h;
+    return HEAP_OK;
+}
+
+int heap_destroy(heap_t *h) {
+    if (!h) return HEAP_EINVAL;
+    delete h;
+    return HEAP_OK;
+}
+
+uint64_t heap_launch_count(const heap_t *h) { return h ? h->launches : 0; }
+
+int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_stream_t sp) {
+    if (!h || n > h->max_batch || (n && !d_offsets)) return HEAP_EINVAL;
+    if (n == 0) return HEAP_OK;
+    cudaStream_t s = (cudaStream_t)sp;
+    const Layout &L = h->L;
+    const int cur = h->cur, nxt = cur ^ 1;
+    const bool bud = h->policy == HEAP_BUDDY;
+    DevCtr *C = h->ctr;
+    u64 *n_dev = &C->tmp[0];
+    // 1. classify (null / unaligned / out of range) and compact the candidate keys
+    LAUNCH(h, fits::k_free_classify, h->G, prims::NT, 0, s, (const u64 *)d_offsets, n, h->alog2, L.A_u, h->kA, h->flags, n_dev, C);
+    scan(h, h->flags, h->pos, n_dev, &C->nk, s);
+    LAUNCH(h, fits::k_compact<u32>, h->G, 256, 0, s, h->kA, h->flags, h->pos, n_dev, h->kB);
+    // 2. sort the keys (address order; duplicates become adjacent)
+    int kbits = ilog2(L.A_u - 1 > 0 ? L.A_u - 1 : 1) + 1;
+    int rb = radix_sort<u32, false>(h, h->kB, h->kA, nullptr, nullptr, &C->nk, kbits, s);
+    u32 *keys = rb ? h->kA : h->kB;
+    // 3. block-table lookup + delete; classify double / invalid
+    LAUNCH(h, fits::k_free_lookup, h->G, 256, 0, s, keys, &C->nk, h->tbl, L.tcap - 1, L.tcap / table::LINE,
+           bud ? nullptr : h->fs[cur], bud ? nullptr : &C->F, bud ? h->fs[cur] : nullptr, L.K,
+           h->flags, h->vs, h->ve, C);
+    scan(h, h->flags, h->pos, &C->nk, &C->nv, s);
+    LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->vs, h->flags, h->pos, &C->nk, h->vsc);
+    LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->ve, h->flags, h->pos, &C->nk, h->vec);
+    if (!bud) {
+        // 4. merge path with the free array, 5. coalesce maximal runs
+        LAUNCH(h, prims::k_merge, h->G, prims::NT, 0, s, h->fs[cur], h->fe[cur], &C->F, h->vsc, h->vec, &C->nv,
+               h->ms, h->me, &C->M);
+        LAUNCH(h, fits::k_coal_flags, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags);
+        scan(h, h->flags, h->pos, &C->M, &C->F, s);
+        LAUNCH(h, fits::k_coal_write, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags, h->pos, h->fs[nxt],
+               h->fe[nxt], L.cap_f, C);
+    } else {
+        // 4b. group freed blocks by order, 5b. level-by-level buddy merge
+        LAUNCH(h, buddy::k_free_orders, h->G, 256, 0, s, h->vsc, h->vec, &C->nv, h->kA, h->vA);
+        int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->nv, 8, s);
+        u32 *ok = r2 ? h->kB : h->kA, *ov = r2 ? h->vB : h->vA;
+        LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, ok, &C->nv, L.K + 1, h->froff);
+        LAUNCH(h, buddy::k_gather_u64, h->G, 256, 0, s, h->vsc, ov, &C->nv, h->fr);
+        LAUNCH(h, buddy::k_free_levels, 1, buddy::NT, 0, s, h->fs[cur], h->fs[nxt], h->fr, h->froff, h->bufA,
+               h->bufB, h->promo, L.K, C);
+    }
+    h->cur = nxt;
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    return HEAP_OK;
+}
+
+int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, heap_stream_t sp) {
+    if (!h || n > h->max_batch || (n && (!d_sizes || !d_out))) return HEAP_EINVAL;
+    if (n == 0) return HEAP_OK;
+    cudaStream_t s = (cudaStream_t)sp;
+    const Layout &L = h->L;
+    const int cur = h->cur, nxt = cur ^ 1;
+    DevCtr *C = h->ctr;
+    if (h->policy == HEAP_BUDDY) {
+        LAUNCH(h, buddy::k_alloc_orders, h->G, 256, 0, s, (const u64 *)d_sizes, n, h->alog2, L.A_u, L.K, h->kA, h->vA, &C->tmp[0]);
+        radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s);   // 1 pass: result in kB/vB
+        LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kB, &C->tmp[0], L.K + 2, h->reqoff);
+        LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, 0, s, h->vB, h->reqoff, h->fs[cur], h->fs[nxt], h->dtm,
+               h->dsrc, nullptr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
+        LAUNCH(h, buddy::k_alloc_r, h->G, 256, 0, s, h->kA, n, L.K, h->r);
+        LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
+               L.tcap / table::LINE, C, h->max_live);
+        h->cur = nxt;
+        maybe_rebuild(h, s);
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        return HEAP_OK;
+    }
+    const bool cls = (h->policy == HEAP_TLSF || h->policy == HEAP_SEGFIT);
+    LAUNCH(h, fits::k_alloc_prep, h->G, 256, 0, s, (const u64 *)d_sizes, n, h->alog2, L.A_u, L.L, cls ? 1 : 0, h->r, h->c);
+    if (cls) {
+        LAUNCH(h, fits::k_cls_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.L, h->kA, h->vA);
+        int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->F, ilog2((u64)L.NC) + 1, s);
+        u32 *sk = rb ? h->kB : h->kA, *sv = rb ? h->vB : h->vA;
+        LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, sk, &C->F, L.NC, h->off);
+        LAUNCH(h, fits::k_tlsf_engine, 1, 32, 0, s, sv, h->off, h->fs[cur], h->fe[cur], h->r, h->c, n, h->out,
+               h->child, h->sib, L.NC, L.L);
+    } else if (h->policy == HEAP_FIRST_FIT) {
+        u64 offs[fits::FF_MAX_LEVELS] = {0};
+        u64 m = L.cap_f, o = 0;
+        for (int l = 0; l < L.nlev; l++) { offs[l] = o; o += m; m = (m + 31) / 32; }
+        LAUNCH(h, fits::k_ff_leaves, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->tree);
+        for (int l = 1; l < L.nlev; l++)
+            LAUNCH(h, fits::k_ff_level, h->G, 256, 0, s, h->tree + offs[l - 1], h->tree + offs[l], &C->F, l);
+        LAUNCH(h, fits::k_ff_engine, 1, 32, 0, s, h->tree, h->lvl, L.nlev, h->fs[cur], &C->F, h->r, n, h->out);
+    } else {   // BEST_FIT
+        LAUNCH(h, fits::k_bf_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.FB, h->bk[0]);
+        int bits = 33 + L.FB;
+        int rb = radix_sort<u64, false>(h, h->bk[0], h->bk[1], nullptr, nullptr, &C->F, bits, s);
+        u64 *keys = h->bk[rb];
+        size_t smem = L.cap_f * 8;
+        if (smem <= 200 * 1024) {
+            cudaFuncSetAttribute(fits::k_bf_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            LAUNCH(h, fits::k_bf_engine<true>, 1, 32, smem, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, h->out);
+        } else {
+            LAUNCH(h, fits::k_bf_engine<false>, 1, 32, 0, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, h->out);
+        }
+    }
+    // compact the surviving pieces into the other buffer (address order is kept)
+    LAUNCH(h, fits::k_piece_flags, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->flags);
+    scan(h, h->flags, h->pos, &C->F, &C->tmp[1], s);
+    LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->fs[cur], h->flags, h->pos, &C->F, h->fs[nxt]);
+    LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->fe[cur], h->flags, h->pos, &C->F, h->fe[nxt]);
+    LAUNCH(h, k_set_F, 1, 1, 0, s, C);
+    LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
+           L.tcap / table::LINE, C, h->max_live);
+    h->cur = nxt;
+    maybe_rebuild(h, s);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    return HEAP_OK;
+}
+
+static u64 meta_bytes(const heap *h) { return (u64)h->L.total; }
+
+int heap_stats_async(heap_t *h, heap_stats_t *d_out, heap_stream_t sp) {
+    if (!h || !d_out) return HEAP_EINVAL;
+    cudaStream_t s = (cudaStream_t)sp;
+    LAUNCH(h, k_stats, 1, 1024, 0, s, h->ctr, h->fs[h->cur], h->fe[h->cur], h->policy == HEAP_BUDDY ? 1 : 0, h->L.K,
+           h->arena, h->align, h->alog2, meta_bytes(h), d_out);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    return HEAP_OK;
+}
+
+int heap_stats(heap_t *h, heap_stats_t *h_out, heap_stream_t sp) {
+    if (!h || !h_out) return HEAP_EINVAL;
+    int rc = heap_stats_async(h, h->dstats, sp);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)sp;
+    CUDA_TRY(cudaMemcpyAsync(h_out, h->dstats, sizeof(heap_stats_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (h_out->error_flags) return HEAP_ECAPACITY;
+    return HEAP_OK;
+}
+
+int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *d_live_pairs, uint64_t cap_live,
+                uint64_t *h_counts, heap_stream_t sp) {
+    if (!h || !h_counts) return HEAP_EINVAL;
+    cudaStream_t s = (cudaStream_t)sp;
+    const Layout &L = h->L;
+    DevCtr *C = h->ctr;
+    int alog = h->alog2;
+    u64 counts[2] = {0, 0};
+    // free blocks
+    if (h->policy != HEAP_BUDDY) {
+        if (d_free_pairs && cap_free)
+            LAUNCH(h, k_export_free, h->G, 256, 0, s, h->fs[h->cur], h->fe[h->cur], &C->F, alog, (u64 *)d_free_pairs, cap_free);
+        CUDA_TRY(cudaMemcpyAsync(&counts[0], &C->F, 8, cudaMemcpyDeviceToHost, s));
+    } else {
+        LAUNCH(h, k_bud_keys, h->G, 256, 0, s, h->fs[h->cur], C, L.K, h->kA, h->vA);
+        int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->bud_total, 32, s);
+        u32 *k = rb ? h->kB : h->kA, *v = rb ? h->vB : h->vA;
+        if (d_free_pairs && cap_free)
+            LAUNCH(h, k_export_pairs_u32, h->G, 256, 0, s, k, v, &C->bud_total, alog, 1, (u64 *)d_free_pairs, cap_free);
+        CUDA_TRY(cudaMemcpyAsync(&counts[0], &C->bud_total, 8, cudaMemcpyDeviceToHost, s));
+    }
+    // live blocks: collect table slots, sort by key
+    LAUNCH(h, k_set_u64, 1, 1, 0, s, &C->tmp[6], L.tcap);
+    LAUNCH(h, k_tbl_flags, h->G, 256, 0, s, h->tbl, L.tcap, h->flags);
+    scan(h, h->flags, h->pos, &C->tmp[6], &C->tmp[7], s);
+    LAUNCH(h, k_tbl_compact, h->G, 256, 0, s, h->tbl, L.tcap, h->flags, h->pos, h->kA, h->vA);
+    int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[7], 32, s);
+    u32 *k = rb ? h->kB : h->kA, *v = rb ? h->vB : h->vA;
+    if (d_live_pairs && cap_live)
+        LAUNCH(h, k_export_pairs_u32, h->G, 256, 0, s, k, v, &C->tmp[7], alog, 0, (u64 *)d_live_pairs, cap_live);
+    CUDA_TRY(cudaMemcpyAsync(&counts[1], &C->tmp[7], 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    h_counts[0] = counts[0];
+    h_counts[1] = counts[1];
+    return HEAP_OK;
+}
+
+const char *heap_strerror(int code) {
+    switch (code) {
+    case HEAP_OK: return "ok";
+    case HEAP_EINVAL: return "invalid argument";
+    case HEAP_ENOMEM: return "workspace too small / out of host memory";
+    case HEAP_ECAPACITY: return "metadata capacity exceeded in a batch";
+    case HEAP_ECUDA: return "CUDA error";
+    default: return "unknown error";
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+"""Python binding with the C-ABI's names (include/heap.h) plus a small ``Heap`` wrapper.
+
+PyTorch only provides device memory (the workspace tensor, request/result tensors)
+and streams.  Offsets and sizes are passed as int64 tensors whose bits are read as
+uint64 by the library (HEAP_NULL = -1 as int64).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native
+from ._native import HeapStats, check, lib
+
+HEAP_FIRST_FIT, HEAP_BEST_FIT, HEAP_SEGFIT, HEAP_TLSF, HEAP_BUDDY = 1, 2, 3, 4, 5
+HEAP_NULL = (1 << 64) - 1
+HEAP_NULL_I64 = -1
+POLICY_NAMES = {1: "first_fit", 2: "best_fit", 3: "segfit", 4: "tlsf", 5: "buddy"}
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _dev_ptr(t: torch.Tensor, name: str) -> int:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype not in (torch.int64, torch.uint64) or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous int64/uint64 tensor")
+    return t.data_ptr()
+
+
+# ---- same names as the C ABI ----
+def heap_workspace_bytes(arena_bytes: int, align: int, policy: int, max_live_blocks: int,
+                         max_batch: int) -> int:
+    return int(lib().heap_workspace_bytes(arena_bytes, align, policy, max_live_blocks, max_batch))
+
+
+def heap_create(arena_bytes: int, align: int, policy: int, max_live_blocks: int, max_batch: int,
+                workspace: torch.Tensor, stream=None) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    check("heap_create", lib().heap_create(arena_bytes, align, policy, max_live_blocks, max_batch,
+                                           workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                           _stream_handle(stream), ctypes.byref(h)))
+    return h
+
+
+def heap_destroy(h) -> None:
+    check("heap_destroy", lib().heap_destroy(h))
+
+
+def heap_free_batch(h, offsets: torch.Tensor, stream=None) -> None:
+    n = offsets.numel()
+    check("heap_free_batch", lib().heap_free_batch(h, _dev_ptr(offsets, "offsets") if n else None, n,
+                                                   _stream_handle(stream)))
+
+
+def heap_alloc_batch(h, sizes: torch.Tensor, out_offsets: torch.Tensor, stream=None) -> None:
+    n = sizes.numel()
+    if out_offsets.numel() < n:
+        raise ValueError("out_offsets too small")
+    check("heap_alloc_batch", lib().heap_alloc_batch(
+        h, _dev_ptr(sizes, "sizes") if n else None, _dev_ptr(out_offsets, "out_offsets") if n else None,
+        n, _stream_handle(stream)))
+
+
+def heap_stats_async(h, d_out: torch.Tensor, stream=None) -> None:
+    """Write the 16 x u64 statistics into a CUDA int64/uint64 tensor of 16 elements."""
+    check("heap_stats_async", lib().heap_stats_async(h, _dev_ptr(d_out, "d_out"), _stream_handle(stream)))
+
+
+def heap_stats(h, stream=None) -> dict:
+    st = HeapStats()
+    rc = lib().heap_stats(h, ctypes.byref(st), _stream_handle(stream))
+    d = st.as_dict()
+    d["rc"] = rc
+    return d
+
+
+def heap_export(h, stream=None):
+    """Returns (free_pairs, live_pairs) as CPU int64 tensors [n, 2] of (start, size) bytes."""
+    counts = (ctypes.c_uint64 * 2)()
+    check("heap_export", lib().heap_export(h, None, 0, None, 0, counts, _stream_handle(stream)))
+    nf, nl = int(counts[0]), int(counts[1])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    fp = torch.empty((max(nf, 1), 2), dtype=torch.int64, device=dev)
+    lp = torch.empty((max(nl, 1), 2), dtype=torch.int64, device=dev)
+    check("heap_export", lib().heap_export(h, fp.data_ptr(), nf, lp.data_ptr(), nl, counts,
+                                           _stream_handle(stream)))
+    return fp[:nf].cpu(), lp[:nl].cpu()
+
+
+def heap_launch_count(h) -> int:
+    return int(lib().heap_launch_count(h))
+
+
+def heap_strerror(code: int) -> str:
+    return lib().heap_strerror(code).decode()
+
+
+class Heap:
+    """Owns the workspace tensor and the handle; every call enqueues on ``stream``."""
+
+    def __init__(self, arena_bytes: int, align: int, policy: int, max_live_blocks: int,
+                 max_batch: int, device=None, stream=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2405_07079_b200.Heap needs a CUDA device (no CPU fallback)")
+        self.device = torch.device(device if device is not None else "cuda")
+        self.arena_bytes, self.align, self.policy = arena_bytes, align, policy
+        self.max_live, self.max_batch = max_live_blocks, max_batch
+        self.stream = stream
+        nbytes = heap_workspace_bytes(arena_bytes, align, policy, max_live_blocks, max_batch)
+        if nbytes == 0:
+            raise ValueError("invalid heap arguments")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self._h = heap_create(arena_bytes, align, policy, max_live_blocks, max_batch, self.workspace,
+                              stream)
+        self._out = torch.empty(max_batch, dtype=torch.int64, device=self.device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            torch.cuda.synchronize(self.device)
+            heap_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free_batch(self, offsets: torch.Tensor) -> None:
+        heap_free_batch(self._h, offsets, self.stream)
+
+    def alloc_batch(self, sizes: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        n = sizes.numel()
+        if out is None:
+            out = self._out[:n]
+        heap_alloc_batch(self._h, sizes, out, self.stream)
+        return out
+
+    def stats(self) -> dict:
+        return heap_stats(self._h, self.stream)
+
+    def export(self):
+        return heap_export(self._h, self.stream)
+
+    def launch_count(self) -> int:
+        return heap_launch_count(self._h)

@@ -1,0 +1,176 @@
+"""GPU parity: the CUDA path (through the C ABI) against Oracle-L, bit-exact.
+
+Integer work throughout, so the bar is exact equality of every returned offset, the final
+free-block set, the live set, and the counters (north_star).  Small cases compare every
+batch; the BASELINE configs are run at full size where the oracle finishes in seconds to
+minutes, and config 5 compares its first batches exactly plus invariants.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import tracegen as tg
+from oracle import OracleL
+from tests.helpers import HEAP_NULL, IdMap, check_invariants
+
+pytestmark = pytest.mark.gpu
+
+COUNTERS = ("live_bytes", "free_bytes", "n_live", "n_free", "largest_free", "high_water_end",
+            "allocs_ok", "allocs_failed", "frees_ok", "frees_invalid", "frees_double", "frees_null")
+
+
+class Gpu:
+    """numpy-in / numpy-out adapter over the product binding (same interface as OracleL)."""
+
+    def __init__(self, arena, align, policy, max_live, max_batch):
+        from paper_2405_07079_b200 import Heap
+        self.h = Heap(arena, align, policy, max_live, max_batch)
+
+    def free_batch(self, offs):
+        a = np.ascontiguousarray(np.asarray(offs, dtype=np.uint64))
+        self.h.free_batch(torch.from_numpy(a.view(np.int64)).cuda())
+
+    def alloc_batch(self, sizes):
+        a = np.ascontiguousarray(np.asarray(sizes, dtype=np.uint64))
+        out = self.h.alloc_batch(torch.from_numpy(a.view(np.int64)).cuda())
+        return out.cpu().numpy().view(np.uint64).copy()
+
+    def stats(self):
+        return self.h.stats()
+
+    def export(self):
+        fp, lp = self.h.export()
+        return fp.numpy().view(np.uint64), lp.numpy().view(np.uint64)
+
+
+def compare_state(g, o, ctx=""):
+    gf, gl = g.export()
+    of, ol = o.export()
+    assert gf.shape == of.shape and np.array_equal(gf, of), f"free set differs {ctx}"
+    assert gl.shape == ol.shape and np.array_equal(gl, ol), f"live set differs {ctx}"
+    gs, os_ = g.stats(), o.stats()
+    assert gs["rc"] == 0 and gs["error_flags"] == 0, gs
+    for k in COUNTERS:
+        assert gs[k] == os_[k], (k, gs[k], os_[k], ctx)
+
+
+def run_parity(cfg, max_live, max_batch, total_ops=None, every_batch_state=False, max_batches=None,
+               batch=None):
+    t = tg.Trace(cfg, total_ops=total_ops, batch=batch)
+    g = Gpu(cfg.arena_bytes, cfg.align, cfg.policy, max_live, max_batch)
+    o = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
+    im = IdMap(1 << 16)
+    for bi, (fids, sizes, first) in enumerate(t):
+        if max_batches is not None and bi >= max_batches:
+            break
+        offs = im.offsets(fids)
+        g.free_batch(offs)
+        o.free_batch(offs)
+        go = g.alloc_batch(sizes)
+        oo = o.alloc_batch(sizes)
+        if not np.array_equal(go, oo):
+            bad = np.flatnonzero(go != oo)
+            raise AssertionError(f"{cfg.name} batch {bi}: {len(bad)} offsets differ, first at {bad[0]}: "
+                                 f"gpu {go[bad[0]]} oracle {oo[bad[0]]}")
+        im.record(first, go)
+        if every_batch_state:
+            compare_state(g, o, f"{cfg.name} batch {bi}")
+    compare_state(g, o, cfg.name)
+    return g, o
+
+
+SMALL = [
+    # (policy, arena, align, batch, ops, sizes, rho, size_kind)
+    (tg.FIRST_FIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2), 0),
+    (tg.BEST_FIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2), 0),
+    (tg.SEGFIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2), 0),
+    (tg.TLSF, 1 << 16, 16, 24, 1500, (4, 10), (1, 2), 0),
+    (tg.BUDDY, 1 << 16, 16, 24, 1500, (0, 8), (1, 2), 1),
+    (tg.FIRST_FIT, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
+    (tg.BEST_FIT, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
+    (tg.SEGFIT, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
+    (tg.TLSF, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
+    (tg.BUDDY, 1 << 24, 64, 3000, 40000, (6, 16), (1, 2), 1),
+    (tg.TLSF, (1 << 22) + 48, 16, 5000, 60000, (4, 12), (1, 3), 0),     # non power-of-two arena
+    (tg.BUDDY, (1 << 20) + (1 << 14) + 256, 256, 700, 9000, (8, 18), (1, 2), 1),
+]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: f"p{c[0]}-A{c[1]}-B{c[3]}")
+def test_small_every_batch(case):
+    pol, arena, align, batch, ops, sizes, rho, kind = case
+    cfg = tg.custom(pol, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes, size_kind=kind,
+                    idx=60 + pol)
+    run_parity(cfg, max_live=8192, max_batch=batch, every_batch_state=batch < 100)
+
+
+def test_config1_exact():
+    cfg = tg.CONFIGS[1]
+    run_parity(cfg, cfg.max_live, 1000, every_batch_state=True)
+
+
+def test_config2_full():
+    cfg = tg.CONFIGS[2]
+    run_parity(cfg, cfg.max_live, cfg.batch)
+
+
+def test_config3_full():
+    cfg = tg.CONFIGS[3]
+    run_parity(cfg, cfg.max_live, cfg.batch)
+
+
+def test_config4_full():
+    cfg = tg.CONFIGS[4]
+    run_parity(cfg, cfg.max_live, cfg.batch)
+
+
+def test_config5_first_batches():
+    """Config 5 at full size (64 GiB arena = 2^32 units, 1M-request batches): the first
+    batches exactly (the oracle computes them in seconds), state compared after each."""
+    cfg = tg.CONFIGS[5]
+    run_parity(cfg, cfg.max_live, cfg.batch, max_batches=3)
+
+
+def test_edge_cases():
+    """Empty batches, NULL / interior / unaligned / out-of-range / duplicate frees,
+    zero and oversize requests, OOM in a tiny arena, the last unit of a 2^32-unit arena."""
+    for pol in (1, 2, 3, 4, 5):
+        arena, align = 1 << 12, 16
+        g = Gpu(arena, align, pol, 256, 64)
+        o = OracleL(arena, align, pol)
+        for h in (g, o):
+            h.free_batch(np.zeros(0, np.uint64))
+        sizes = np.array([16, 0, 5000, 64, 1, 100, 4096, 32], dtype=np.uint64)
+        go, oo = g.alloc_batch(sizes), o.alloc_batch(sizes)
+        assert np.array_equal(go, oo), pol
+        live = oo[oo != HEAP_NULL]
+        frees = np.array([HEAP_NULL, live[0], live[0], live[0] + 16, 3, arena * 2, live[-1], 7 * 16],
+                         dtype=np.uint64)
+        g.free_batch(frees)
+        o.free_batch(frees)
+        compare_state(g, o, f"edge p{pol}")
+        # fill to OOM
+        big = np.full(64, 200, dtype=np.uint64)
+        assert np.array_equal(g.alloc_batch(big), o.alloc_batch(big))
+        compare_state(g, o, f"edge-oom p{pol}")
+    # 2^32-unit arena: allocate right up to the end
+    g = Gpu(1 << 36, 16, tg.TLSF, 64, 64)
+    o = OracleL(1 << 36, 16, tg.TLSF)
+    sizes = np.array([(1 << 36) - 32, 16, 16, 16], dtype=np.uint64)
+    assert np.array_equal(g.alloc_batch(sizes), o.alloc_batch(sizes))
+    compare_state(g, o, "2^32 units")
+
+
+def test_table_rebuild_under_churn():
+    """Small live capacity with heavy churn forces tombstone purges of the block table."""
+    cfg = tg.custom(tg.TLSF, 1 << 22, 16, 256, rho=(1, 2), total_ops=60000, sizes=(4, 10), idx=77)
+    run_parity(cfg, max_live=600, max_batch=256)
+
+
+def test_invariants_config3_prefix():
+    cfg = tg.CONFIGS[3]
+    g, _ = run_parity(cfg, cfg.max_live, cfg.batch, max_batches=10)
+    fp, lp = g.export()
+    check_invariants(fp, lp, cfg.arena_bytes, cfg.align, False)
