@@ -328,15 +328,17 @@ __global__ void k_tbl_flags(const u64 *tbl, u64 tcap, u32 *flags) {
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
         flags[i] = table::is_live(tbl[i]) ? 1u : 0u;
 }
-__global__ void k_tbl_compact(const u64 *tbl, u64 tcap, const u32 *flags, const u32 *pos, u32 *key, u32 *val) {
+__global__ void k_tbl_compact(const u64 *tbl, u64 tcap, const u32 *flags, const u32 *pos, u32 *key, u32 *val,
+                              u64 cap) {
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
-        if (flags[i]) {
+        if (flags[i] && pos[i] < cap) {
             u64 v = tbl[i];
             key[pos[i]] = (u32)table::slot_key(v);
             val[pos[i]] = (u32)(v & 0xFFFFFFFFull);
         }
 }
 __global__ void k_set_u64(u64 *p, u64 v) { *p = v; }
+__global__ void k_clamp(const u64 *in, u64 *out, u64 cap) { *out = *in < cap ? *in : cap; }
 
 }  // namespace
 
@@ -574,11 +576,12 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
     LAUNCH(h, k_set_u64, 1, 1, 0, s, &C->tmp[6], L.tcap);
     LAUNCH(h, k_tbl_flags, h->G, 256, 0, s, h->tbl, L.tcap, h->flags);
     scan(h, h->flags, h->pos, &C->tmp[6], &C->tmp[7], s);
-    LAUNCH(h, k_tbl_compact, h->G, 256, 0, s, h->tbl, L.tcap, h->flags, h->pos, h->kA, h->vA);
-    int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[7], 32, s);
+    LAUNCH(h, k_tbl_compact, h->G, 256, 0, s, h->tbl, L.tcap, h->flags, h->pos, h->kA, h->vA, L.sort_cap);
+    LAUNCH(h, k_clamp, 1, 1, 0, s, &C->tmp[7], &C->tmp[3], L.sort_cap);
+    int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[3], 32, s);
     u32 *k = rb ? h->kB : h->kA, *v = rb ? h->vB : h->vA;
     if (d_live_pairs && cap_live)
-        LAUNCH(h, k_export_pairs_u32, h->G, 256, 0, s, k, v, &C->tmp[7], alog, 0, (u64 *)d_live_pairs, cap_live);
+        LAUNCH(h, k_export_pairs_u32, h->G, 256, 0, s, k, v, &C->tmp[3], alog, 0, (u64 *)d_live_pairs, cap_live);
     CUDA_TRY(cudaMemcpyAsync(&counts[1], &C->tmp[7], 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;

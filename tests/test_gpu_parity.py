@@ -46,6 +46,8 @@ class Gpu:
 
 
 def compare_state(g, o, ctx=""):
+    gs0 = g.stats()
+    assert gs0["error_flags"] == 0, f"capacity error flags {gs0['error_flags']} {ctx}"
     gf, gl = g.export()
     of, ol = o.export()
     assert gf.shape == of.shape and np.array_equal(gf, of), f"free set differs {ctx}"
@@ -103,7 +105,7 @@ def test_small_every_batch(case):
     pol, arena, align, batch, ops, sizes, rho, kind = case
     cfg = tg.custom(pol, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes, size_kind=kind,
                     idx=60 + pol)
-    run_parity(cfg, max_live=8192, max_batch=batch, every_batch_state=batch < 100)
+    run_parity(cfg, max_live=1 << 15, max_batch=batch, every_batch_state=batch < 100)
 
 
 def test_config1_exact():
