@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the batched device heap on BASELINE.json's headline workload.
+
+Workload: BASELINE config 5 per GPU — TLSF, 64 GiB arena (2^32 units of
+16 B), batches of 1,048,576 requests with a 60/40 alloc/free mix, sizes LU8[16 B, 4 KiB).
+A *step* is one canonical batch through the whole hot path: id -> offset gather of the
+batch's frees, heap_free_batch (classify, sort, block-table delete, merge, coalesce) and
+heap_alloc_batch (normalise, class index, exact engine, compaction, block-table insert),
+plus the NCCL all-gather of heap statistics when N > 1.
+
+``value`` = submitted alloc+free requests of all ranks / max-over-ranks device time of the
+K timed steps (inputs resident in HBM, L2 flushed between steps).  ``e2e`` = the same
+metric through the C ABI with host buffers: pinned-host -> device copies of the step's
+offsets and sizes and the device -> host copy of its results inside the timed region.
+
+``--impl reference`` times the CPU oracle (oracle/, the tier's reference arm) on the same
+workload, one batch per step, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import tracegen as tg  # noqa: E402
+
+METRIC = "alloc+free ops/sec per GPU and 8-GPU aggregate vs cudaMalloc/cudaMallocAsync"
+UNIT = "ops/s"
+
+# Algorithmic bytes per processed unit for each kernel group: what the step
+# must move at minimum with the 8-byte ABI words and 8/16-byte metadata records.
+#   unit "alloc": one alloc request; "free": one free request; "elem": one element of the
+#   tag's own array per launch (sort: keys+payload of a pass; merge/coalesce/compact: blocks)
+TAG_BYTES = {
+    "engine": ("alloc", 8 + 4 + 16 + 8 + 8),        # r, class in; block (start,end) in; start, out
+    "table_lookup": ("free", 4 + 8 + 8 + 16 + 4),   # key in; slot read + tombstone; (start,end) + flag out
+    "finish": ("alloc", 8 + 8 + 8 + 8),             # r, offset in; bytes out; table slot write
+    "alloc_prep": ("alloc", 8 + 8 + 4),             # size in; r, class out
+    "classify": ("free", 8 + 4 + 4),                # offset in; key, flag out
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", type=int, default=5)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-batches", type=int, default=0, help="0 = auto")
+    p.add_argument("--no-arena", action="store_true", help="do not allocate the arena tensor")
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def make_trace(cfg, rank, nbatches):
+    t = tg.Trace(cfg, rank=rank, total_ops=cfg.batch * nbatches)
+    return [b for b in t]
+
+
+# ------------------------------------------------------------------ clocks ----
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        finally:
+            os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        load = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(tag):
+    """Per-launch DRAM bytes of the tag's dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(tag)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- reference ----
+def run_reference(args, cfg):
+    from oracle import OracleL
+    nb = args.warmup + args.steps
+    batches = make_trace(cfg, 0, nb)
+    h = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
+    idmap = np.full(cfg.batch * nb + 1, tg.HEAP_NULL if hasattr(tg, "HEAP_NULL") else (1 << 64) - 1, dtype=np.uint64)
+    t_total, ops = 0.0, 0
+    for bi, (fids, sizes, first) in enumerate(batches):
+        offs = idmap[fids.astype(np.int64)]
+        t0 = time.perf_counter()
+        h.free_batch(offs)
+        out = h.alloc_batch(sizes)
+        dt = time.perf_counter() - t0
+        idmap[first:first + len(sizes)] = out
+        if bi >= args.warmup:
+            t_total += dt
+            ops += len(fids) + len(sizes)
+    value = ops / t_total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (tracegen, seed 2405070790+1000c+r)",
+        "config": {"workload": cfg.name, "policy": "tlsf", "arena_bytes": cfg.arena_bytes,
+                   "align": cfg.align, "batch": cfg.batch, "alloc_free_mix": "60/40",
+                   "sizes": "LU8[16,4096)", "batches": f"{args.warmup}..{nb - 1} of the trace"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"config {cfg.idx} batches {args.warmup}..{nb - 1} ({ops} ops), Oracle-L, 1 thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- ours ----
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2405_07079_b200 import Heap, heap_stats_async
+    from paper_2405_07079_b200._native import NTAGS
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    nb = args.warmup + args.steps
+    batches = make_trace(cfg, rank, nb)
+    n_alloc_total = sum(len(b[1]) for b in batches) + 1
+    dev_batches = [(torch.from_numpy(f.astype(np.int64)).to(dev), torch.from_numpy(s.view(np.int64)).to(dev), first)
+                   for f, s, first in batches]
+    max_live = cfg.max_live
+    arena = None
+    if not args.no_arena:
+        try:   # the arena the offsets index into; the heap never touches it
+            arena = torch.empty(cfg.arena_bytes, dtype=torch.uint8, device=dev)
+        except RuntimeError:
+            arena = None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stats_dev = torch.zeros(16, dtype=torch.int64, device=dev)
+    stats_all = torch.zeros(16 * world, dtype=torch.int64, device=dev) if world > 1 else None
+
+    def run_device(h, idmap, outbuf, b, stream_stats=True):
+        fids, sizes, first = b
+        offs = idmap[fids] if fids.numel() else fids
+        h.free_batch(offs)
+        na = sizes.numel()
+        out = h.alloc_batch(sizes, out=outbuf[:na])
+        idmap[first:first + na] = out
+        if world > 1 and stream_stats:
+            heap_stats_async(h.handle, stats_dev)
+            dist.all_gather_into_tensor(stats_all, stats_dev)
+
+    # ---------------- device-resident run ----------------
+    h = Heap(cfg.arena_bytes, cfg.align, cfg.policy, max_live, cfg.batch, device=dev)
+    idmap = torch.full((n_alloc_total,), -1, dtype=torch.int64, device=dev)
+    outbuf = torch.empty(cfg.batch, dtype=torch.int64, device=dev)
+    for b in dev_batches[:args.warmup]:
+        run_device(h, idmap, outbuf, b)
+    torch.cuda.synchronize()
+    h.profile((1 << NTAGS) - 1)
+    h.profile_read()
+    l0 = h.launch_count()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ops = 0
+    for k, b in enumerate(dev_batches[args.warmup:]):
+        flush.fill_(k & 255)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[k][0].record()
+        run_device(h, idmap, outbuf, b)
+        ev[k][1].record()
+        torch.cuda.synchronize()
+        ops += b[0].numel() + b[1].numel()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = h.launch_count() - l0
+    prof = h.profile_read()
+    h.profile(0)
+    step_ms = [a.elapsed_time(e) for a, e in ev]
+    t_ms = sum(step_ms)
+    st = h.stats()
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        oo = torch.tensor([ops], dtype=torch.int64, device=dev)
+        dist.all_reduce(oo, op=dist.ReduceOp.SUM)
+        t_max, ops_all = float(tt.item()), int(oo.item())
+    else:
+        t_max, ops_all = t_ms, ops
+    value = ops_all / (t_max / 1e3)
+    del h
+    torch.cuda.empty_cache()
+
+    # ---------------- e2e through the C ABI with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        h = Heap(cfg.arena_bytes, cfg.align, cfg.policy, max_live, cfg.batch, device=dev)
+        hmap = np.full(n_alloc_total, -1, dtype=np.int64)
+        pin_off = torch.empty(cfg.batch, dtype=torch.int64).pin_memory()
+        pin_sz = torch.empty(cfg.batch, dtype=torch.int64).pin_memory()
+        pin_out = torch.empty(cfg.batch, dtype=torch.int64).pin_memory()
+        d_off = torch.empty(cfg.batch, dtype=torch.int64, device=dev)
+        d_sz = torch.empty(cfg.batch, dtype=torch.int64, device=dev)
+        e_ms, e_ops, h2d, d2h = 0.0, 0, 0, 0
+        for bi, (fids, sizes, first) in enumerate(batches):
+            nf, na = len(fids), len(sizes)
+            pin_off[:nf].numpy()[:] = hmap[fids.astype(np.int64)]
+            pin_sz[:na].numpy()[:] = sizes.view(np.int64)
+            flush.fill_(bi & 255)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            d_off[:nf].copy_(pin_off[:nf], non_blocking=True)
+            d_sz[:na].copy_(pin_sz[:na], non_blocking=True)
+            h.free_batch(d_off[:nf])
+            out = h.alloc_batch(d_sz[:na])
+            pin_out[:na].copy_(out, non_blocking=True)
+            e.record()
+            torch.cuda.synchronize()
+            hmap[first:first + na] = pin_out[:na].numpy()
+            if bi >= args.warmup:
+                e_ms += a.elapsed_time(e)
+                e_ops += nf + na
+                h2d += 8 * (nf + na)
+                d2h += 8 * na
+        if world > 1:
+            tt = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            oo = torch.tensor([e_ops], dtype=torch.int64, device=dev)
+            dist.all_reduce(oo, op=dist.ReduceOp.SUM)
+            e_ms, e_ops_all = float(tt.item()), int(oo.item())
+        else:
+            e_ops_all = e_ops
+        e2e = {"value": e_ops_all / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
+        del h
+
+    # ---------------- roofline of the dominant kernel group ----------------
+    dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else None
+    roof = None
+    shares = {k: round(v[0] / max(t_ms, 1e-9), 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    if dom:
+        tag, (ms, nl) = dom
+        peak, peak_src = measured_peak_hbm()
+        unit, bpu = TAG_BYTES.get(tag, ("alloc", 64))
+        n_units = sum(len(b[1]) if unit == "alloc" else len(b[0]) for b in batches[args.warmup:])
+        per_launch_bytes = bpu * n_units / max(nl, 1)
+        avg_s = ms / max(nl, 1) / 1e3
+        achieved = per_launch_bytes / avg_s / 1e9
+        tr = ncu_traffic(tag)
+        roof = {"bound": "hbm", "kernel": tag, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
+                "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_s * 1e3}
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import OracleL
+        ns = args.cpu_sample_batches or min(len(batches), 8)
+        o = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
+        omap = np.full(n_alloc_total, (1 << 64) - 1, dtype=np.uint64)
+        c_t, c_ops = 0.0, 0
+        for fids, sizes, first in batches[:ns]:
+            offs = omap[fids.astype(np.int64)]
+            t0 = time.perf_counter()
+            o.free_batch(offs)
+            out = o.alloc_batch(sizes)
+            c_t += time.perf_counter() - t0
+            c_ops += len(fids) + len(sizes)
+            omap[first:first + len(sizes)] = out
+        cpu = {"value": c_ops / c_t, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"config {cfg.idx} batches 0..{ns - 1} ({c_ops} ops) replayed by Oracle-L on 1 host thread"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (tracegen, seed 2405070790+1000c+r; per-rank independent traces)",
+            "config": {"workload": cfg.name, "policy": "tlsf", "arena_bytes": cfg.arena_bytes,
+                       "align": cfg.align, "batch": cfg.batch, "alloc_free_mix": "60/40",
+                       "sizes": "LU8[16,4096)", "timed_batches": f"{args.warmup}..{nb - 1}",
+                       "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"replicas x{world} (independent heaps, NCCL all-gather of heap_stats)",
+                       "arena_allocated": arena is not None},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "kernel_shares": shares,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "heap": {"n_live": st["n_live"], "n_free": st["n_free"], "allocs_failed": st["allocs_failed"],
+                     "error_flags": st["error_flags"]},
+            "step_ms": [round(x, 3) for x in step_ms],
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    cfg = tg.CONFIGS[args.config]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, cfg)
+    else:
+        run_ours(args, cfg, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -132,6 +132,21 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
 /* Number of kernel launches this heap has enqueued so far (for the bench's gpu_launches). */
 uint64_t heap_launch_count(const heap_t *h);
 
+/* Per-kernel timing (tracing).  Kernels are grouped by tag (HEAP_TAG_*); for every tag whose
+ * bit is set in tag_mask, each launch is bracketed by two CUDA events on its stream.
+ * heap_profile_read synchronises those events, adds each tag's summed milliseconds and launch
+ * count into h_ms[tag] / h_launches[tag] (arrays of HEAP_NTAGS), and forgets the records.
+ * tag_mask = 0 disables (the default); enabling costs two event records per bracketed launch. */
+enum heap_tag {
+    HEAP_TAG_CLASSIFY = 0, HEAP_TAG_SCAN = 1, HEAP_TAG_SORT = 2, HEAP_TAG_LOOKUP = 3,
+    HEAP_TAG_COMPACT = 4, HEAP_TAG_MERGE = 5, HEAP_TAG_COALESCE = 6, HEAP_TAG_ALLOC_PREP = 7,
+    HEAP_TAG_INDEX = 8, HEAP_TAG_ENGINE = 9, HEAP_TAG_FINISH = 10, HEAP_TAG_REBUILD = 11,
+    HEAP_TAG_BUDDY_FREE = 12, HEAP_TAG_BUDDY_ALLOC = 13, HEAP_TAG_MISC = 14, HEAP_NTAGS = 16
+};
+int heap_profile_enable(heap_t *h, uint64_t tag_mask);
+int heap_profile_read(heap_t *h, double *h_ms, uint64_t *h_launches);
+const char *heap_tag_name(int tag);
+
 const char *heap_strerror(int code);
 
 #ifdef __cplusplus

@@ -50,7 +50,9 @@ class HeapStats(ctypes.Structure):
 
 EXPORTS = ("heap_workspace_bytes", "heap_create", "heap_destroy", "heap_free_batch",
            "heap_alloc_batch", "heap_stats_async", "heap_stats", "heap_export",
-           "heap_launch_count", "heap_strerror")
+           "heap_launch_count", "heap_profile_enable", "heap_profile_read", "heap_tag_name",
+           "heap_strerror")
+NTAGS = 16
 
 _lib = None
 
@@ -81,6 +83,12 @@ def lib():
         L.heap_export.argtypes = [vp, vp, u64, vp, u64, ctypes.POINTER(u64), vp]
         L.heap_launch_count.restype = u64
         L.heap_launch_count.argtypes = [vp]
+        L.heap_profile_enable.restype = i32
+        L.heap_profile_enable.argtypes = [vp, u64]
+        L.heap_profile_read.restype = i32
+        L.heap_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
+        L.heap_tag_name.restype = ctypes.c_char_p
+        L.heap_tag_name.argtypes = [i32]
         L.heap_strerror.restype = ctypes.c_char_p
         L.heap_strerror.argtypes = [i32]
         _lib = L

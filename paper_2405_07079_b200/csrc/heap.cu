@@ -7,6 +7,7 @@
 #include <cstring>
 #include <new>
 #include <algorithm>
+#include <vector>
 #include "../../include/heap.h"
 #include "common.cuh"
 #include "prims.cuh"
@@ -143,13 +144,33 @@ struct heap {
     u64 *bk[2];
     u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
     u64 *baddr, *bufA, *bufB, *promo, *fr;
+    // tracing
+    u64 prof_mask;
+    int tag;                                  // tag of the launches being issued
+    struct Rec { int tag; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
 };
 
-#define LAUNCH(h, kern, grid, block, smem, stream, ...)                       \
-    do {                                                                      \
-        kern<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__); \
-        (h)->launches++;                                                      \
+namespace {
+cudaEvent_t prof_event(heap *h) {
+    if (!h->pool.empty()) { cudaEvent_t e = h->pool.back(); h->pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+#define LAUNCH(h, kern, grid, block, smem, stream, ...)                                   \
+    do {                                                                                  \
+        bool _p = ((h)->prof_mask >> (h)->tag) & 1;                                       \
+        heap::Rec _r{(h)->tag, nullptr, nullptr};                                         \
+        if (_p) { _r.a = prof_event(h); _r.b = prof_event(h); cudaEventRecord(_r.a, (cudaStream_t)(stream)); } \
+        kern<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__);             \
+        if (_p) { cudaEventRecord(_r.b, (cudaStream_t)(stream)); (h)->recs.push_back(_r); } \
+        (h)->launches++;                                                                  \
     } while (0)
+#define TAG(h, t) ((h)->tag = (t))
 
 namespace {
 
@@ -245,6 +266,7 @@ __global__ void k_rb_insert(DevCtr *ctr, u64 *tbl, u64 tmask, u64 max_lines, con
 
 void maybe_rebuild(heap *h, cudaStream_t s) {
     u64 thresh = h->L.tcap / 4 * 3;
+    TAG(h, HEAP_TAG_REBUILD);
     LAUNCH(h, k_rb_check, 1, 1, 0, s, h->ctr, thresh);
     LAUNCH(h, k_rb_collect, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap, h->ms);
     LAUNCH(h, k_rb_clear, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap);
@@ -395,6 +417,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     }
     h->cur = 0;
     h->launches = 0;
+    h->prof_mask = 0;
+    h->tag = HEAP_TAG_MISC;
     cudaStream_t st = (cudaStream_t)s;
     LAUNCH(h, k_init, h->G, 256, 0, st, h->ctr, h->tbl, L.tcap, h->fs[0], h->fe[0], L.A_u,
            policy == HEAP_BUDDY ? 1 : 0, L.K);
@@ -411,6 +435,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
 
 int heap_destroy(heap_t *h) {
     if (!h) return HEAP_EINVAL;
+    for (auto &r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : h->pool) cudaEventDestroy(e);
     delete h;
     return HEAP_OK;
 }
@@ -427,30 +453,40 @@ int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_strea
     DevCtr *C = h->ctr;
     u64 *n_dev = &C->tmp[0];
     // 1. classify (null / unaligned / out of range) and compact the candidate keys
+    TAG(h, HEAP_TAG_CLASSIFY);
     LAUNCH(h, fits::k_free_classify, h->G, prims::NT, 0, s, (const u64 *)d_offsets, n, h->alog2, L.A_u, h->kA, h->flags, n_dev, C);
+    TAG(h, HEAP_TAG_SCAN);
     scan(h, h->flags, h->pos, n_dev, &C->nk, s);
+    TAG(h, HEAP_TAG_COMPACT);
     LAUNCH(h, fits::k_compact<u32>, h->G, 256, 0, s, h->kA, h->flags, h->pos, n_dev, h->kB);
     // 2. sort the keys (address order; duplicates become adjacent)
     int kbits = ilog2(L.A_u - 1 > 0 ? L.A_u - 1 : 1) + 1;
+    TAG(h, HEAP_TAG_SORT);
     int rb = radix_sort<u32, false>(h, h->kB, h->kA, nullptr, nullptr, &C->nk, kbits, s);
     u32 *keys = rb ? h->kA : h->kB;
     // 3. block-table lookup + delete; classify double / invalid
+    TAG(h, HEAP_TAG_LOOKUP);
     LAUNCH(h, fits::k_free_lookup, h->G, 256, 0, s, keys, &C->nk, h->tbl, L.tcap - 1, L.tcap / table::LINE,
            bud ? nullptr : h->fs[cur], bud ? nullptr : &C->F, bud ? h->fs[cur] : nullptr, L.K,
            h->flags, h->vs, h->ve, C);
+    TAG(h, HEAP_TAG_SCAN);
     scan(h, h->flags, h->pos, &C->nk, &C->nv, s);
+    TAG(h, HEAP_TAG_COMPACT);
     LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->vs, h->flags, h->pos, &C->nk, h->vsc);
     LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->ve, h->flags, h->pos, &C->nk, h->vec);
     if (!bud) {
         // 4. merge path with the free array, 5. coalesce maximal runs
+        TAG(h, HEAP_TAG_MERGE);
         LAUNCH(h, prims::k_merge, h->G, prims::NT, 0, s, h->fs[cur], h->fe[cur], &C->F, h->vsc, h->vec, &C->nv,
                h->ms, h->me, &C->M);
+        TAG(h, HEAP_TAG_COALESCE);
         LAUNCH(h, fits::k_coal_flags, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags);
         scan(h, h->flags, h->pos, &C->M, &C->F, s);
         LAUNCH(h, fits::k_coal_write, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags, h->pos, h->fs[nxt],
                h->fe[nxt], L.cap_f, C);
     } else {
         // 4b. group freed blocks by order, 5b. level-by-level buddy merge
+        TAG(h, HEAP_TAG_BUDDY_FREE);
         LAUNCH(h, buddy::k_free_orders, h->G, 256, 0, s, h->vsc, h->vec, &C->nv, h->kA, h->vA);
         int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->nv, 8, s);
         u32 *ok = r2 ? h->kB : h->kA, *ov = r2 ? h->vB : h->vA;
@@ -472,12 +508,14 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
     const int cur = h->cur, nxt = cur ^ 1;
     DevCtr *C = h->ctr;
     if (h->policy == HEAP_BUDDY) {
+        TAG(h, HEAP_TAG_BUDDY_ALLOC);
         LAUNCH(h, buddy::k_alloc_orders, h->G, 256, 0, s, (const u64 *)d_sizes, n, h->alog2, L.A_u, L.K, h->kA, h->vA, &C->tmp[0]);
         radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s);   // 1 pass: result in kB/vB
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kB, &C->tmp[0], L.K + 2, h->reqoff);
         LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, 0, s, h->vB, h->reqoff, h->fs[cur], h->fs[nxt], h->dtm,
                h->dsrc, nullptr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
         LAUNCH(h, buddy::k_alloc_r, h->G, 256, 0, s, h->kA, n, L.K, h->r);
+        TAG(h, HEAP_TAG_FINISH);
         LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
                L.tcap / table::LINE, C, h->max_live);
         h->cur = nxt;
@@ -486,28 +524,35 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         return HEAP_OK;
     }
     const bool cls = (h->policy == HEAP_TLSF || h->policy == HEAP_SEGFIT);
+    TAG(h, HEAP_TAG_ALLOC_PREP);
     LAUNCH(h, fits::k_alloc_prep, h->G, 256, 0, s, (const u64 *)d_sizes, n, h->alog2, L.A_u, L.L, cls ? 1 : 0, h->r, h->c);
     if (cls) {
+        TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_cls_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.L, h->kA, h->vA);
         int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->F, ilog2((u64)L.NC) + 1, s);
         u32 *sk = rb ? h->kB : h->kA, *sv = rb ? h->vB : h->vA;
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, sk, &C->F, L.NC, h->off);
+        TAG(h, HEAP_TAG_ENGINE);
         LAUNCH(h, fits::k_tlsf_engine, 1, 32, 0, s, sv, h->off, h->fs[cur], h->fe[cur], h->r, h->c, n, h->out,
                h->child, h->sib, L.NC, L.L);
     } else if (h->policy == HEAP_FIRST_FIT) {
         u64 offs[fits::FF_MAX_LEVELS] = {0};
         u64 m = L.cap_f, o = 0;
         for (int l = 0; l < L.nlev; l++) { offs[l] = o; o += m; m = (m + 31) / 32; }
+        TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_ff_leaves, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->tree);
         for (int l = 1; l < L.nlev; l++)
             LAUNCH(h, fits::k_ff_level, h->G, 256, 0, s, h->tree + offs[l - 1], h->tree + offs[l], &C->F, l);
+        TAG(h, HEAP_TAG_ENGINE);
         LAUNCH(h, fits::k_ff_engine, 1, 32, 0, s, h->tree, h->lvl, L.nlev, h->fs[cur], &C->F, h->r, n, h->out);
     } else {   // BEST_FIT
+        TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_bf_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.FB, h->bk[0]);
         int bits = 33 + L.FB;
         int rb = radix_sort<u64, false>(h, h->bk[0], h->bk[1], nullptr, nullptr, &C->F, bits, s);
         u64 *keys = h->bk[rb];
         size_t smem = L.cap_f * 8;
+        TAG(h, HEAP_TAG_ENGINE);
         if (smem <= 200 * 1024) {
             cudaFuncSetAttribute(fits::k_bf_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             LAUNCH(h, fits::k_bf_engine<true>, 1, 32, smem, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, h->out);
@@ -516,11 +561,13 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         }
     }
     // compact the surviving pieces into the other buffer (address order is kept)
+    TAG(h, HEAP_TAG_COMPACT);
     LAUNCH(h, fits::k_piece_flags, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->flags);
     scan(h, h->flags, h->pos, &C->F, &C->tmp[1], s);
     LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->fs[cur], h->flags, h->pos, &C->F, h->fs[nxt]);
     LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->fe[cur], h->flags, h->pos, &C->F, h->fe[nxt]);
     LAUNCH(h, k_set_F, 1, 1, 0, s, C);
+    TAG(h, HEAP_TAG_FINISH);
     LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
            L.tcap / table::LINE, C, h->max_live);
     h->cur = nxt;
@@ -534,6 +581,7 @@ static u64 meta_bytes(const heap *h) { return (u64)h->L.total; }
 int heap_stats_async(heap_t *h, heap_stats_t *d_out, heap_stream_t sp) {
     if (!h || !d_out) return HEAP_EINVAL;
     cudaStream_t s = (cudaStream_t)sp;
+    TAG(h, HEAP_TAG_MISC);
     LAUNCH(h, k_stats, 1, 1024, 0, s, h->ctr, h->fs[h->cur], h->fe[h->cur], h->policy == HEAP_BUDDY ? 1 : 0, h->L.K,
            h->arena, h->align, h->alog2, meta_bytes(h), d_out);
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
@@ -555,6 +603,7 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
                 uint64_t *h_counts, heap_stream_t sp) {
     if (!h || !h_counts) return HEAP_EINVAL;
     cudaStream_t s = (cudaStream_t)sp;
+    TAG(h, HEAP_TAG_MISC);
     const Layout &L = h->L;
     DevCtr *C = h->ctr;
     int alog = h->alog2;
@@ -588,6 +637,35 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
     h_counts[0] = counts[0];
     h_counts[1] = counts[1];
     return HEAP_OK;
+}
+
+int heap_profile_enable(heap_t *h, uint64_t tag_mask) {
+    if (!h) return HEAP_EINVAL;
+    h->prof_mask = tag_mask;
+    return HEAP_OK;
+}
+
+int heap_profile_read(heap_t *h, double *h_ms, uint64_t *h_launches) {
+    if (!h) return HEAP_EINVAL;
+    for (auto &r : h->recs) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return HEAP_ECUDA;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        if (h_ms) h_ms[r.tag] += ms;
+        if (h_launches) h_launches[r.tag] += 1;
+        h->pool.push_back(r.a);
+        h->pool.push_back(r.b);
+    }
+    h->recs.clear();
+    return HEAP_OK;
+}
+
+const char *heap_tag_name(int tag) {
+    static const char *names[HEAP_NTAGS] = {"classify", "scan", "sort", "table_lookup", "compact", "merge",
+                                            "coalesce", "alloc_prep", "index_build", "engine", "finish",
+                                            "table_rebuild", "buddy_free_levels", "buddy_alloc_levels",
+                                            "misc", "unused"};
+    return (tag >= 0 && tag < HEAP_NTAGS) ? names[tag] : "?";
 }
 
 const char *heap_strerror(int code) {

@@ -97,6 +97,22 @@ def heap_launch_count(h) -> int:
     return int(lib().heap_launch_count(h))
 
 
+def heap_profile_enable(h, tag_mask: int) -> None:
+    check("heap_profile_enable", lib().heap_profile_enable(h, tag_mask))
+
+
+def heap_profile_read(h) -> dict:
+    """{tag_name: (milliseconds, launches)} accumulated since the last read (synchronises)."""
+    ms = (ctypes.c_double * _native.NTAGS)()
+    cnt = (ctypes.c_uint64 * _native.NTAGS)()
+    check("heap_profile_read", lib().heap_profile_read(h, ms, cnt))
+    return {heap_tag_name(t): (ms[t], int(cnt[t])) for t in range(_native.NTAGS) if cnt[t]}
+
+
+def heap_tag_name(tag: int) -> str:
+    return lib().heap_tag_name(tag).decode()
+
+
 def heap_strerror(code: int) -> str:
     return lib().heap_strerror(code).decode()
 
@@ -154,3 +170,9 @@ class Heap:
 
     def launch_count(self) -> int:
         return heap_launch_count(self._h)
+
+    def profile(self, tag_mask: int) -> None:
+        heap_profile_enable(self._h, tag_mask)
+
+    def profile_read(self) -> dict:
+        return heap_profile_read(self._h)
