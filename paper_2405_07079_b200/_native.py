@@ -12,7 +12,7 @@ import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_HERE)
-LIB_PATH = os.path.join(_HERE, "libheap.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("HEAP_DEV_LIB", "libheap.so"))  # dev override: debug build
 SRC_DIR = os.path.join(_HERE, "csrc")
 HEADER = os.path.join(ROOT, "include", "heap.h")
 
@@ -51,7 +51,7 @@ class HeapStats(ctypes.Structure):
 EXPORTS = ("heap_workspace_bytes", "heap_create", "heap_destroy", "heap_free_batch",
            "heap_alloc_batch", "heap_stats_async", "heap_stats", "heap_export",
            "heap_launch_count", "heap_profile_enable", "heap_profile_read", "heap_tag_name",
-           "heap_strerror")
+           "heap_debug_counters", "heap_strerror")
 NTAGS = 16
 
 _lib = None
@@ -87,6 +87,8 @@ def lib():
         L.heap_profile_enable.argtypes = [vp, u64]
         L.heap_profile_read.restype = i32
         L.heap_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
+        L.heap_debug_counters.restype = i32
+        L.heap_debug_counters.argtypes = [vp, ctypes.POINTER(u64), i32, vp]
         L.heap_tag_name.restype = ctypes.c_char_p
         L.heap_tag_name.argtypes = [i32]
         L.heap_strerror.restype = ctypes.c_char_p

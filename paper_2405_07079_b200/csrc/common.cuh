@@ -37,9 +37,10 @@ struct DevCtr {
     u64 bud_cnt[40];
     u64 bud_off[41];
     u64 bud_total;
+    u64 eng[16];        // alloc engine diagnostics (engine_tlsf.cuh)
 };
 
-enum { ERR_CAP_LIVE = 1, ERR_TABLE_FULL = 2, ERR_CAP_FREE = 4 };
+enum { ERR_CAP_LIVE = 1, ERR_TABLE_FULL = 2, ERR_CAP_FREE = 4, ERR_ENGINE = 8 };
 
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ u32 lanemask_lt() {
@@ -127,6 +128,11 @@ __device__ __forceinline__ u32 cls_insert(u64 u, int L) {
     if (u < (1ull << L)) return (u32)u;
     int m = flog2(u);
     return (u32)(((u64)(m - L + 1) << L) + ((u >> (m - L)) - (1ull << L)));
+}
+// smallest block size (units) of class c
+__device__ __forceinline__ u64 cls_lo(u32 c, int L) {
+    u32 fl = c >> L, sl = c & ((1u << L) - 1);
+    return fl == 0 ? (u64)sl : ((u64)((1u << L) + sl) << (fl - 1));
 }
 __device__ __forceinline__ u32 cls_search(u64 u, int L) {
     if (u < (1ull << L)) return (u32)u;

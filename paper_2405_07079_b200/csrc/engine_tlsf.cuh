@@ -1,0 +1,469 @@
+// engine_tlsf.cuh — warp-speculative exact engine for SEGFIT / TLSF allocation batches.
+//
+// Semantics (must equal the oracle): requests are served in request order; request i takes,
+// among free pieces whose class is >= its search class c_i, the one with the smallest
+// (class, address) key (Alg. 4 + the bitmap/ffs fallback PAPER.md:332-337,440; TLSF two-level
+// lookup PAPER.md:449; address order within a class, C9), and carves r_i units off
+// its low end (Alg. 1).  Pieces are indexed by f = address rank of their batch-start free block
+// (each batch-start block holds at most one piece during the phase; see fits.cuh).
+//
+// One warp walks the batch in chunks of up to 32 consecutive requests (one per lane):
+//   1. every lane finds the first nonempty class >= c_i in the chunk-start two-level bitmap
+//      (ffs on the second-level word, then on the first-level summary);
+//   2. lanes aiming at the same class are grouped with __match_any_sync and ranked in time
+//      order; the group's members come from a per-class head cache in shared memory holding
+//      the class's H smallest members with their (start, end) — no global memory on this path;
+//   3. each group leader replays its group in time order: a block keeps serving the next
+//      request while its remainder stays in the class (head carve), otherwise the next member
+//      is used; requests finding the class exhausted are re-aimed at the next nonempty class
+//      and the chunk is replayed;
+//   4. a request is *dirty* if an earlier request of the chunk dropped a remainder into a
+//      class >= its search class with a smaller key than the one it chose, or if its rank
+//      fell past the head cache; the chunk commits every request before the first dirty one
+//      (exactly the sequential results), updates the class state, and the next chunk starts
+//      at the first dirty request.  Request 0 of a chunk is never dirty, so chunks progress.
+// Class state: per class a CSR range of batch-start members (address order, consumed as a
+// prefix; class-sorted copies of (f, start, end)), the sorted head cache, and a pairing heap
+// (keyed by f, arrays indexed by f) of remainders that dropped into the class and did not fit
+// the cache.  Invariant: the cache holds the min(H, members) smallest members of the class.
+#pragma once
+#include "common.cuh"
+
+namespace tlsfw {
+
+constexpr int H = 8;              // head-cache depth per class
+constexpr int MAX_NC = 1024;
+constexpr int RB = 1024;          // request staging buffer
+constexpr u32 NONE = 0xFFFFFFFFu;
+constexpr u32 HEAPBIT = 0x80000000u;
+constexpr u32 SAME = 0xFFFFFFFEu; // block stays in its class after the carve
+constexpr u32 F_OK = 0, F_OVER = 1, F_MISS = 2;
+
+struct Smem {
+    u32 ptr[MAX_NC], endp[MAX_NC], cnt[MAX_NC], root[MAX_NC];
+    u32 hf[MAX_NC * H];           // cached member f (| HEAPBIT when it came from the heap)
+    u32 hs[MAX_NC * H];           // its current start (units)
+    u32 he[MAX_NC * H];           // its end - 1 (units; ends can be 2^32)
+    unsigned char hn[MAX_NC];
+    u32 cw[32];
+    u32 sw;
+    u64 rbuf[RB];
+    u32 cbuf[RB];
+    u32 lor[32 * 32];             // lane of rank q in the group led by lane l: lor[l*32+q]
+    u64 res_s[32];
+    u32 res_f[32], res_nk[32], res_flag[32], res_e[32];
+};
+
+struct Heap {
+    u32 *child, *sib;
+    __device__ __forceinline__ u32 meld(u32 a, u32 b) {
+        if (a == NIL32) return b;
+        if (b == NIL32) return a;
+        if (b < a) { u32 t = a; a = b; b = t; }
+        sib[b] = child[a];
+        child[a] = b;
+        return a;
+    }
+    u64 visits = 0;
+    u64 limit = 0;          // watchdog: a corrupted heap must never hang the GPU
+    bool broken = false;
+    __device__ u32 delmin(u32 root) {
+        u32 x = child[root], acc = NIL32;
+        u64 steps = 0;
+        while (x != NIL32) {
+            visits++;
+            if (++steps > limit) { broken = true; return NIL32; }
+            u32 a = x, b = sib[a];
+            if (b == NIL32) { sib[a] = acc; acc = a; break; }
+            u32 nx = sib[b];
+            sib[a] = NIL32;
+            sib[b] = NIL32;
+            u32 m = meld(a, b);
+            sib[m] = acc;
+            acc = m;
+            x = nx;
+        }
+        u32 res = NIL32;
+        while (acc != NIL32) {
+            if (++steps > 2 * limit) { broken = true; return NIL32; }
+            u32 nx = sib[acc];
+            sib[acc] = NIL32;
+            res = meld(res, acc);
+            acc = nx;
+        }
+        return res;
+    }
+};
+
+__device__ __forceinline__ u32 first_ge(const Smem &S, u32 sw, u32 c, int NC) {
+    if (c >= (u32)NC) return NONE;
+    u32 w = c >> 5;
+    u32 m = S.cw[w] & (0xFFFFFFFFu << (c & 31));
+    if (m) return (w << 5) + __ffs(m) - 1;
+    u32 sm = (w >= 31) ? 0u : (sw & (0xFFFFFFFFu << (w + 1)));
+    if (!sm) return NONE;
+    u32 w2 = __ffs(sm) - 1;
+    return (w2 << 5) + __ffs(S.cw[w2]) - 1;
+}
+
+__device__ __forceinline__ void set_bit(Smem &S, u32 k) {
+    atomicOr(&S.cw[k >> 5], 1u << (k & 31));
+    atomicOr(&S.sw, 1u << (k >> 5));
+}
+__device__ __forceinline__ void clear_bit(Smem &S, u32 k) {
+    u32 old = atomicAnd(&S.cw[k >> 5], ~(1u << (k & 31)));
+    if ((old & ~(1u << (k & 31))) == 0) atomicAnd(&S.sw, ~(1u << (k >> 5)));
+}
+
+struct Csr {
+    const u32 *f;   // class-sorted f
+    const u32 *s;   // class-sorted batch-start start
+    const u32 *e;   // class-sorted end - 1
+};
+
+// refill the head cache of class k from min(CSR[ptr], heap root)
+__device__ void refill(Smem &S, Heap &hp, const Csr &csr, const u64 *__restrict__ fs,
+                       const u64 *__restrict__ fe, u32 k, u64 &delmins) {
+    u32 n = S.hn[k];
+    u32 p = S.ptr[k], e = S.endp[k], rt = S.root[k];
+    if (n >= (u32)H || (p >= e && rt == NIL32)) return;
+    // prefetch the CSR candidates in one round of independent loads
+    u32 cf[H], cs[H], ce[H];
+    const u32 want = (u32)H - n;
+#pragma unroll
+    for (int j = 0; j < H; j++) {
+        bool ok = (u32)j < want && p + j < e;
+        cf[j] = ok ? csr.f[p + j] : NIL32;
+        cs[j] = ok ? csr.s[p + j] : 0;
+        ce[j] = ok ? csr.e[p + j] : 0;
+    }
+    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    u32 j = 0;
+    while (n < (u32)H && ((j < want && p < e) || rt != NIL32)) {
+        u32 a = (j < want && p < e) ? cf[j] : NIL32;
+        if (a < rt) {
+            hf[n] = a; hs[n] = cs[j]; he[n] = ce[j];
+            n++; j++; p++;
+        } else {
+            hf[n] = rt | HEAPBIT;
+            hs[n] = (u32)fs[rt];
+            he[n] = (u32)(fe[rt] - 1);
+            n++;
+            rt = hp.delmin(rt);
+            delmins++;
+        }
+    }
+    S.hn[k] = (unsigned char)n;
+    S.ptr[k] = p;
+    S.root[k] = rt;
+}
+
+// a remainder piece f = [s, e1 + 1) joins class k
+__device__ void arrive(Smem &S, Heap &hp, u32 k, u32 f, u32 s, u32 e1) {
+    if (S.cnt[k]++ == 0) set_bit(S, k);
+    u32 n = S.hn[k];
+    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    hp.child[f] = NIL32;
+    hp.sib[f] = NIL32;
+    if (n < (u32)H || f < (hf[H - 1] & ~HEAPBIT)) {
+        u32 j;
+        if (n == (u32)H) {      // evict the largest cached member
+            u32 ev = hf[H - 1];
+            if (ev & HEAPBIT) {
+                u32 x = ev & ~HEAPBIT;
+                hp.child[x] = NIL32;
+                hp.sib[x] = NIL32;
+                S.root[k] = hp.meld(S.root[k], x);
+            } else {
+                S.ptr[k]--;     // the largest cached CSR member is CSR[ptr-1]
+            }
+            j = H - 1;
+        } else {
+            j = n;
+            S.hn[k] = (unsigned char)(n + 1);
+        }
+        while (j > 0 && (hf[j - 1] & ~HEAPBIT) > f) {
+            hf[j] = hf[j - 1]; hs[j] = hs[j - 1]; he[j] = he[j - 1];
+            j--;
+        }
+        hf[j] = f | HEAPBIT; hs[j] = s; he[j] = e1;
+    } else {
+        S.root[k] = hp.meld(S.root[k], f);
+    }
+}
+
+__global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict__ off,
+                                                  u64 *__restrict__ fs, const u64 *__restrict__ fe,
+                                                  const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
+                                                  u64 *__restrict__ out_u, u32 *child, u32 *sib, int NC, int L,
+                                                  u64 *stats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+    const u32 lane = lane_id();
+    Heap hp{child, sib, 0, 4 * (u64)n + 4096, false};
+    // ---- init: CSR ranges, head caches, bitmaps ----
+    for (int k = lane; k < NC; k += 32) {
+        u32 b = off[k], e = off[k + 1];
+        S.cnt[k] = e - b;
+        S.hn[k] = 0;
+        S.ptr[k] = b;
+        S.endp[k] = e;
+        S.root[k] = NIL32;
+    }
+    __syncwarp();
+    u64 n_delmin = 0;
+    for (int k = lane; k < NC; k += 32) refill(S, hp, csr, fs, fe, k, n_delmin);
+    __syncwarp();
+    {
+        u32 swl = 0;
+        for (int w = 0; w < 32; w++) {
+            int k = w * 32 + lane;
+            u32 b = __ballot_sync(FULLMASK, k < NC && S.cnt[k] > 0);
+            if (lane == 0) S.cw[w] = b;
+            if (b) swl |= 1u << w;
+        }
+        if (lane == 0) S.sw = swl;
+    }
+    __syncwarp();
+    u64 rb_base = 0, rb_end = 0;
+    u64 n_iter = 0, n_retarget = 0, n_rounds = 0, n_qsteps = 0;
+    long long t_spec = 0, t_dirty = 0, t_cls = 0, t_arr = 0, t0;
+    u64 pos = 0;
+    while (pos < n) {
+        n_iter++;
+        // watchdogs: the engine must terminate even if an invariant broke (reported as error)
+        if (__any_sync(FULLMASK, hp.broken) || n_iter > n + 64) {
+            if (lane == 0 && stats) stats[2] = hp.broken ? 4 : 3;
+            return;
+        }
+        if (pos + 32 > rb_end) {                 // stage requests
+            rb_base = pos;
+            rb_end = pos + RB < n ? pos + RB : n;
+            for (u64 j = lane; j < rb_end - rb_base; j += 32) {
+                S.rbuf[j] = R[rb_base + j];
+                S.cbuf[j] = C[rb_base + j];
+            }
+            __syncwarp();
+        }
+        t0 = clock64();
+        const u32 sw = S.sw;
+        const u64 i = pos + lane;
+        const bool act = i < n;
+        const u64 ri = act ? S.rbuf[i - rb_base] : 0;
+        const u32 ci = act ? S.cbuf[i - rb_base] : NONE;
+        const bool fail0 = act && (ri == 0 || ci >= (u32)NC);
+        u32 k = (act && !fail0) ? first_ge(S, sw, ci, NC) : NONE;
+        u32 peers = 0, rank = 0, flag = F_OK, myf = 0, mynk = NONE, mye = 0;
+        u64 mys = 0;
+        for (u32 round = 0;; round++) {
+            n_rounds++;
+            if (round > (u32)NC + 2) {
+                if (lane == 0 && stats) stats[2] = 2;
+                return;
+            }
+            const bool part = act && k != NONE;
+            peers = __match_any_sync(FULLMASK, part ? k : (0x40000000u | lane));
+            rank = __popc(peers & lanemask_lt());
+            const u32 leader = __ffs(peers) - 1;
+            if (part) S.lor[leader * 32 + rank] = lane;
+            __syncwarp();
+            // Two parallel patterns cover almost every group; mixed groups fall back to the
+            // leader's sequential replay below.
+            //  (A) one block per request: request of rank q takes cached member q, valid when
+            //      no request but the last leaves its block in the class;
+            //  (B) one block for all: member 0 serves every request (head carve), valid when
+            //      the remainder before each request is still in the class.
+            const u32 npeer = __popc(peers);
+            const u32 nh = part ? S.hn[k] : 0, nc = part ? S.cnt[k] : 0;
+            const bool hasA = part && rank < nh;
+            u32 fA = 0, nkA = NONE;
+            u64 sA = 0;
+            if (hasA) {
+                fA = S.hf[k * H + rank] & ~HEAPBIT;
+                sA = S.hs[k * H + rank];
+                const u64 zA = (u64)S.he[k * H + rank] + 1 - sA - ri;
+                nkA = zA ? cls_insert(zA, L) : NONE;
+            }
+            const bool okA = (__ballot_sync(FULLMASK, hasA && nkA == k && rank + 1 < npeer) & peers) == 0;
+            // segmented exclusive prefix of r over the group (Hillis-Steele over ranks)
+            u64 incl = part ? ri : 0;
+            const u32 maxpeer = __reduce_max_sync(FULLMASK, part ? npeer : 0u);
+            for (u32 st = 1; st < maxpeer; st <<= 1) {
+                const u32 src = (part && rank >= st) ? S.lor[leader * 32 + rank - st] : lane;
+                const u64 t = __shfl_sync(FULLMASK, incl, src);
+                if (part && rank >= st) incl += t;
+            }
+            const u64 P = incl - (part ? ri : 0);
+            u64 s0 = 0, z0 = 0;
+            u32 f0 = 0;
+            if (part && nh) {
+                f0 = S.hf[k * H] & ~HEAPBIT;
+                s0 = S.hs[k * H];
+                z0 = (u64)S.he[k * H] + 1 - s0;
+            }
+            const bool covB = part && nh && (rank == 0 || (P < z0 && z0 - P >= cls_lo(k, L)));
+            const u32 uncov = __ballot_sync(FULLMASK, part && !covB);   // every lane must vote
+            const bool okB = !okA && (uncov & peers) == 0;
+            if (part && okA) {
+                if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = S.he[k * H + rank]; }
+                else flag = (rank < nc) ? F_MISS : F_OVER;
+            } else if (part && okB) {
+                flag = F_OK; myf = f0; mys = s0 + P; mye = S.he[k * H];
+                const u64 z = z0 - P - ri;
+                const u32 nk = z ? cls_insert(z, L) : NONE;
+                mynk = (nk == k) ? SAME : nk;
+            }
+            const bool seq = part && !okA && !okB;
+            if (seq && rank == 0) {
+                // replay the group in time order (shared memory only)
+                n_qsteps += npeer;
+                u32 b = 0, curf = 0;
+                u64 cur_s = 0, cur_e = 0;
+                bool need = true;
+                u32 q = 0;
+                for (; q < npeer; q++) {
+                    const u32 lq = S.lor[lane * 32 + q];
+                    if (need) {
+                        if (b >= nh) break;
+                        curf = S.hf[k * H + b] & ~HEAPBIT;
+                        cur_s = S.hs[k * H + b];
+                        cur_e = (u64)S.he[k * H + b] + 1;
+                        need = false;
+                    }
+                    const u64 rq = S.rbuf[pos + lq - rb_base];
+                    S.res_flag[lq] = F_OK;
+                    S.res_f[lq] = curf;
+                    S.res_s[lq] = cur_s;
+                    S.res_e[lq] = (u32)(cur_e - 1);
+                    cur_s += rq;
+                    const u64 z = cur_e - cur_s;
+                    const u32 nk = z ? cls_insert(z, L) : NONE;
+                    if (nk == k) S.res_nk[lq] = SAME;
+                    else { S.res_nk[lq] = nk; b++; need = true; }
+                }
+                const u32 fl = (b < nc) ? F_MISS : F_OVER;
+                for (; q < npeer; q++) S.res_flag[S.lor[lane * 32 + q]] = fl;
+            }
+            __syncwarp();
+            if (seq) {
+                flag = S.res_flag[lane];
+                myf = S.res_f[lane];
+                mys = S.res_s[lane];
+                mynk = S.res_nk[lane];
+                mye = S.res_e[lane];
+            }
+            __syncwarp();
+            const bool over = part && flag == F_OVER;
+#ifdef ENGINE_DEBUG
+            if (n_iter < 8)
+                printf("it %llu pos %llu round %u lane %u act %d k %u rank %u flag %u f %u s %llu nk %u okA %d okB %d seq %d\n",
+                       n_iter, pos, round, lane, (int)act, k, rank, flag, myf, mys, mynk, (int)okA, (int)okB, (int)seq);
+#endif
+            if (!__any_sync(FULLMASK, over)) break;
+            if (over) { k = first_ge(S, sw, k + 1, NC); flag = F_OK; n_retarget++; }
+        }
+        if (act && k != NONE) { S.res_f[lane] = myf; S.res_s[lane] = mys; S.res_e[lane] = mye; }
+        __syncwarp();
+        t_spec += clock64() - t0;
+        t0 = clock64();
+        // ---- dirty requests: remainders dropped earlier in the chunk, cache misses ----
+        const bool part = act && k != NONE;
+        const u64 key = part ? (((u64)k << 32) | myf) : ~0ull;
+        bool bad = part && flag == F_MISS;
+        const bool dropper = part && flag == F_OK && mynk != SAME && mynk != NONE;
+        u32 dm = __ballot_sync(FULLMASK, dropper);
+        while (dm) {
+            const u32 d = __ffs(dm) - 1;
+            dm &= dm - 1;
+            const u32 dk = __shfl_sync(FULLMASK, mynk, d);
+            const u32 dfb = __shfl_sync(FULLMASK, myf, d);
+            if (act && !fail0 && lane > d && ci <= dk && ((((u64)dk) << 32) | dfb) < key) bad = true;
+        }
+        const u32 badm = __ballot_sync(FULLMASK, bad);
+        const u32 limit = (n - pos) < 32 ? (u32)(n - pos) : 32u;
+        const u32 commit = badm ? (u32)(__ffs(badm) - 1) : limit;
+#ifdef ENGINE_DEBUG
+        if (lane == 0 && n_iter < 8) printf("it %llu commit %u badm %x\n", n_iter, commit, badm);
+#endif
+        if (commit == 0) {               // cannot happen (lane 0 is never dirty); never hang
+            if (lane == 0 && stats) stats[2] = 1;
+            return;
+        }
+        const bool cm = act && lane < commit;
+        t_dirty += clock64() - t0;
+        t0 = clock64();
+        // ---- commit: results and piece starts ----
+        const u32 nxt = lane < 31 ? __fns(peers, lane + 1, 1) : NONE;
+        const bool last_on_block = mynk != SAME || nxt >= commit;
+        if (cm) {
+            if (!part) out_u[i] = HEAP_NULL_U64;
+            else {
+                out_u[i] = mys;
+                if (last_on_block) fs[myf] = mys + ri;
+            }
+        }
+        // ---- class updates by group leaders: blocks that left the class; head carve ----
+        const u32 leftm = __ballot_sync(FULLMASK, cm && part && mynk != SAME);
+        const u32 staym = __ballot_sync(FULLMASK, cm && part && mynk == SAME && last_on_block);
+        if (cm && part && rank == 0) {
+            const u32 left = __popc(leftm & peers);
+            u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+            const u32 st = staym & peers;        // the surviving head was carved: new start
+            if (st) {
+                const u32 d = __ffs(st) - 1;
+                hs[left] = (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]);
+            }
+            if (left) {
+                const u32 nh = S.hn[k];
+                for (u32 j = left; j < nh; j++) { hf[j - left] = hf[j]; hs[j - left] = hs[j]; he[j - left] = he[j]; }
+                S.hn[k] = (unsigned char)(nh - left);
+                S.cnt[k] -= left;
+                refill(S, hp, csr, fs, fe, k, n_delmin);
+                if (S.cnt[k] == 0) clear_bit(S, k);
+            }
+        }
+        __syncwarp();
+        t_cls += clock64() - t0;
+        t0 = clock64();
+        // ---- remainders join their new classes (grouped by class, time order) ----
+        const bool cdrop = cm && dropper;
+        const u32 g = __match_any_sync(FULLMASK, cdrop ? mynk : (0x40000000u | lane));
+        if (cdrop && __popc(g & lanemask_lt()) == 0) {
+            u32 mm = g;
+            while (mm) {
+                const u32 d = __ffs(mm) - 1;
+                mm &= mm - 1;
+                arrive(S, hp, mynk, S.res_f[d], (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]), S.res_e[d]);
+            }
+        }
+        __syncwarp();
+        t_arr += clock64() - t0;
+        pos += commit;
+    }
+    if (stats) {
+        u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits;
+        for (int o = 16; o > 0; o >>= 1) {
+            vis += __shfl_xor_sync(FULLMASK, vis, o);
+            t += __shfl_xor_sync(FULLMASK, t, o);
+            q += __shfl_xor_sync(FULLMASK, q, o);
+            dl += __shfl_xor_sync(FULLMASK, dl, o);
+        }
+        if (lane == 0) {
+            stats[0] += n_iter; stats[1] += t; stats[3] += n_rounds; stats[4] += q;
+            stats[5] += t_spec; stats[6] += t_dirty; stats[7] += t_cls; stats[8] += t_arr; stats[9] += dl; stats[10] += vis;
+        }
+    }
+}
+
+// class-sorted copies of (start, end - 1) for the CSR (one gather after the class sort)
+__global__ void k_csr_data(const u32 *__restrict__ csr_f, const u64 *__restrict__ fs, const u64 *__restrict__ fe,
+                           const u64 *F_dev, u32 *__restrict__ cs, u32 *__restrict__ ce) {
+    const u64 F = *F_dev;
+    for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < F; p += (u64)gridDim.x * blockDim.x) {
+        u32 f = csr_f[p];
+        cs[p] = (u32)fs[f];
+        ce[p] = (u32)(fe[f] - 1);
+    }
+}
+
+}  // namespace tlsfw

@@ -14,6 +14,7 @@
 #include "table.cuh"
 #include "buddy.cuh"
 #include "fits.cuh"
+#include "engine_tlsf.cuh"
 
 namespace {
 
@@ -34,7 +35,7 @@ struct Layout {
     // offsets
     u64 o_ctr, o_stats, o_tbl, o_fs0, o_fs1, o_fe0, o_fe1, o_kA, o_kB, o_vA, o_vB, o_flags, o_pos,
         o_hist, o_tsum, o_vs, o_ve, o_vsc, o_vec, o_ms, o_me, o_r, o_c, o_out, o_off, o_child,
-        o_sib, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
+        o_sib, o_cs, o_ce, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
         o_promo, o_fr, o_froff, o_reqoff, total;
 };
 
@@ -96,6 +97,8 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
     if (policy == HEAP_TLSF || policy == HEAP_SEGFIT) {
         L.o_child = take(L.cap_f * 4);
         L.o_sib = take(L.cap_f * 4);
+        L.o_cs = take(L.cap_f * 4);
+        L.o_ce = take(L.cap_f * 4);
     }
     if (policy == HEAP_FIRST_FIT) {
         L.o_tree = take(L.ff_tree * 8);
@@ -139,7 +142,7 @@ struct heap {
     u64 *tbl, *fs[2], *fe[2];
     u32 *kA, *kB, *vA, *vB, *flags, *pos, *hist, *tsum;
     u64 *vs, *ve, *vsc, *vec, *ms, *me, *r, *out;
-    u32 *c, *off, *child, *sib;
+    u32 *c, *off, *child, *sib, *cs, *ce;
     u64 *tree, *lvl;
     u64 *bk[2];
     u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
@@ -230,7 +233,10 @@ void scan(heap *h, const u32 *in, u32 *out, const u64 *n_dev, u64 *total, cudaSt
     LAUNCH(h, prims::k_scan_down, h->G, prims::NT, 0, s, in, out, n_dev, h->tsum);
 }
 
-__global__ void k_set_F(DevCtr *ctr) { ctr->F = ctr->tmp[1]; }
+__global__ void k_set_F(DevCtr *ctr) {
+    ctr->F = ctr->tmp[1];
+    if (ctr->eng[2]) ctr->error_flags |= ERR_ENGINE;   // engine watchdog fired: results invalid
+}
 
 // ---- table rebuild (tombstone purge), each kernel a no-op unless the flag is set ----
 __global__ void k_rb_check(DevCtr *ctr, u64 thresh) {
@@ -393,6 +399,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     h->sms = sms;
     h->G = sms * 4;
+    if (cudaFuncSetAttribute(tlsfw::k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     void *w = d_workspace;
     h->ctr = at<DevCtr>(w, L.o_ctr);
     h->dstats = at<heap_stats_t>(w, L.o_stats);
@@ -407,6 +415,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->r = at<u64>(w, L.o_r); h->c = at<u32>(w, L.o_c); h->out = at<u64>(w, L.o_out);
     h->off = at<u32>(w, L.o_off);
     h->child = L.o_child ? at<u32>(w, L.o_child) : nullptr; h->sib = L.o_sib ? at<u32>(w, L.o_sib) : nullptr;
+    h->cs = L.o_cs ? at<u32>(w, L.o_cs) : nullptr; h->ce = L.o_ce ? at<u32>(w, L.o_ce) : nullptr;
     h->tree = L.o_tree ? at<u64>(w, L.o_tree) : nullptr; h->lvl = L.o_lvl ? at<u64>(w, L.o_lvl) : nullptr;
     h->bk[0] = L.o_bk0 ? at<u64>(w, L.o_bk0) : nullptr; h->bk[1] = L.o_bk1 ? at<u64>(w, L.o_bk1) : nullptr;
     if (policy == HEAP_BUDDY) {
@@ -533,8 +542,11 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         u32 *sk = rb ? h->kB : h->kA, *sv = rb ? h->vB : h->vA;
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, sk, &C->F, L.NC, h->off);
         TAG(h, HEAP_TAG_ENGINE);
-        LAUNCH(h, fits::k_tlsf_engine, 1, 32, 0, s, sv, h->off, h->fs[cur], h->fe[cur], h->r, h->c, n, h->out,
-               h->child, h->sib, L.NC, L.L);
+        LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs, h->ce);
+        TAG(h, HEAP_TAG_ENGINE);
+        tlsfw::Csr csr{sv, h->cs, h->ce};
+        LAUNCH(h, tlsfw::k_engine, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r, h->c,
+               n, h->out, h->child, h->sib, L.NC, L.L, C->eng);
     } else if (h->policy == HEAP_FIRST_FIT) {
         u64 offs[fits::FF_MAX_LEVELS] = {0};
         u64 m = L.cap_f, o = 0;
@@ -636,6 +648,14 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
     h_counts[0] = counts[0];
     h_counts[1] = counts[1];
+    return HEAP_OK;
+}
+
+int heap_debug_counters(heap_t *h, uint64_t *h_out, int n, heap_stream_t sp) {
+    if (!h || !h_out || n < 0 || n > 16) return HEAP_EINVAL;
+    cudaStream_t s = (cudaStream_t)sp;
+    CUDA_TRY(cudaMemcpyAsync(h_out, h->ctr->eng, n * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return HEAP_OK;
 }
 

@@ -176,3 +176,8 @@ class Heap:
 
     def profile_read(self) -> dict:
         return heap_profile_read(self._h)
+
+    def debug_counters(self) -> list:
+        out = (ctypes.c_uint64 * 16)()
+        check("heap_debug_counters", lib().heap_debug_counters(self._h, out, 16, _stream_handle(self.stream)))
+        return [int(x) for x in out]
