@@ -31,16 +31,18 @@
 
 namespace tlsfw {
 
-constexpr int H = 8;              // head-cache depth per class
-constexpr int MAX_NC = 1024;
-constexpr int RB = 1024;          // request staging buffer
+constexpr int H = 16;             // head-cache depth per class
+constexpr int REFILL_AT = 8;      // refill a class's cache when it holds fewer members
+constexpr int MAX_NC = 928;       // classes of 2^32 units at SL_LOG2 = 5 (fl <= 28)
+constexpr int RB = 512;           // request staging buffer
 constexpr u32 NONE = 0xFFFFFFFFu;
 constexpr u32 HEAPBIT = 0x80000000u;
 constexpr u32 SAME = 0xFFFFFFFEu; // block stays in its class after the carve
 constexpr u32 F_OK = 0, F_OVER = 1, F_MISS = 2;
 
 struct Smem {
-    u32 ptr[MAX_NC], endp[MAX_NC], cnt[MAX_NC], root[MAX_NC];
+    u32 ptr[MAX_NC], endp[MAX_NC], cnt[MAX_NC], root[MAX_NC], slot[MAX_NC];
+    u32 nslot;
     u32 hf[MAX_NC * H];           // cached member f (| HEAPBIT when it came from the heap)
     u32 hs[MAX_NC * H];           // its current start (units)
     u32 he[MAX_NC * H];           // its end - 1 (units; ends can be 2^32)
@@ -54,44 +56,66 @@ struct Smem {
     u32 res_f[32], res_nk[32], res_flag[32], res_e[32];
 };
 
+// Overflow members of a class (remainders that arrived while its head cache was full) live in
+// a three-level bitmap over f (a bit per piece, a bit per nonempty word, a bit per nonempty
+// second-level word), one bitmap slot per class that needs it.  Keys taken out of a class's
+// overflow set only grow (every insert is above the cache, which is above everything already
+// taken), so the minimum is tracked in shared memory (root[k]) and extract-min is one atomic
+// on the minimum's word plus, rarely, a walk up the summary levels.  All bits still set when
+// the engine finishes belong to pieces sitting in their final class; k_bitheap_clear zeroes
+// them for the next batch.
 struct Heap {
-    u32 *child, *sib;
-    __device__ __forceinline__ u32 meld(u32 a, u32 b) {
-        if (a == NIL32) return b;
-        if (b == NIL32) return a;
-        if (b < a) { u32 t = a; a = b; b = t; }
-        sib[b] = child[a];
-        child[a] = b;
-        return a;
-    }
+    u32 *l0, *l1, *l2;       // slot s: l0 + s*w0, ...
+    u64 w0, w1, w2;          // words per slot at each level
+    u32 *slot;               // smem: slot of class k (NONE = none yet)
+    u32 *nslot;              // smem counter
     u64 visits = 0;
-    u64 limit = 0;          // watchdog: a corrupted heap must never hang the GPU
     bool broken = false;
-    __device__ u32 delmin(u32 root) {
-        u32 x = child[root], acc = NIL32;
-        u64 steps = 0;
-        while (x != NIL32) {
-            visits++;
-            if (++steps > limit) { broken = true; return NIL32; }
-            u32 a = x, b = sib[a];
-            if (b == NIL32) { sib[a] = acc; acc = a; break; }
-            u32 nx = sib[b];
-            sib[a] = NIL32;
-            sib[b] = NIL32;
-            u32 m = meld(a, b);
-            sib[m] = acc;
-            acc = m;
-            x = nx;
+    __device__ __forceinline__ u32 slot_of(u32 k) {
+        u32 s = slot[k];
+        if (s == NONE) { s = atomicAdd(nslot, 1u); slot[k] = s; }
+        return s;
+    }
+    // add f to class k's overflow set whose current minimum is root; returns the new minimum
+    __device__ __forceinline__ u32 insert(u32 k, u32 root, u32 f) {
+        const u64 s = slot_of(k);
+        atomicOr(&l0[s * w0 + (f >> 5)], 1u << (f & 31));
+        atomicOr(&l1[s * w1 + (f >> 10)], 1u << ((f >> 5) & 31));
+        atomicOr(&l2[s * w2 + (f >> 15)], 1u << ((f >> 10) & 31));
+        return f < root ? f : root;
+    }
+    // remove the minimum h of class k's overflow set; returns the next minimum (NIL32 if empty)
+    __device__ u32 extract(u32 k, u32 h) {
+        const u64 s = slot[k];
+        u32 *a0 = l0 + s * w0, *a1 = l1 + s * w1, *a2 = l2 + s * w2;
+        visits++;
+        const u32 w = h >> 5;
+        u32 rest = atomicAnd(&a0[w], ~(1u << (h & 31))) & ~(1u << (h & 31));
+        if (rest) return (w << 5) + __ffs(rest) - 1;          // bits below h are never set
+        const u32 v = w >> 5;
+        rest = atomicAnd(&a1[v], ~(1u << (w & 31))) & ~(1u << (w & 31));
+        u32 ww;
+        if (rest) ww = (v << 5) + __ffs(rest) - 1;
+        else {
+            const u32 x = v >> 5;
+            rest = atomicAnd(&a2[x], ~(1u << (v & 31))) & ~(1u << (v & 31));
+            u32 vv = NONE;
+            if (rest) vv = (x << 5) + __ffs(rest) - 1;
+            else {
+                for (u64 j = x + 1; j < w2; j++) {
+                    visits++;
+                    const u32 t = __ldcg(&a2[j]);
+                    if (t) { vv = (u32)(j << 5) + __ffs(t) - 1; break; }
+                }
+                if (vv == NONE) return NIL32;
+            }
+            const u32 t1 = __ldcg(&a1[vv]);
+            if (!t1) { broken = true; return NIL32; }
+            ww = (vv << 5) + __ffs(t1) - 1;
         }
-        u32 res = NIL32;
-        while (acc != NIL32) {
-            if (++steps > 2 * limit) { broken = true; return NIL32; }
-            u32 nx = sib[acc];
-            sib[acc] = NIL32;
-            res = meld(res, acc);
-            acc = nx;
-        }
-        return res;
+        const u32 t0 = __ldcg(&a0[ww]);
+        if (!t0) { broken = true; return NIL32; }
+        return (ww << 5) + __ffs(t0) - 1;
     }
 };
 
@@ -126,32 +150,41 @@ __device__ void refill(Smem &S, Heap &hp, const Csr &csr, const u64 *__restrict_
                        const u64 *__restrict__ fe, u32 k, u64 &delmins) {
     u32 n = S.hn[k];
     u32 p = S.ptr[k], e = S.endp[k], rt = S.root[k];
-    if (n >= (u32)H || (p >= e && rt == NIL32)) return;
-    // prefetch the CSR candidates in one round of independent loads
-    u32 cf[H], cs[H], ce[H];
-    const u32 want = (u32)H - n;
+    if (n >= (u32)REFILL_AT || (p >= e && rt == NIL32)) return;
+    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    // 1) append the next CSR members (one round of independent loads, straight into smem)
+    const u32 m = min((u32)H - n, e - p);
 #pragma unroll
     for (int j = 0; j < H; j++) {
-        bool ok = (u32)j < want && p + j < e;
-        cf[j] = ok ? csr.f[p + j] : NIL32;
-        cs[j] = ok ? csr.s[p + j] : 0;
-        ce[j] = ok ? csr.e[p + j] : 0;
-    }
-    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
-    u32 j = 0;
-    while (n < (u32)H && ((j < want && p < e) || rt != NIL32)) {
-        u32 a = (j < want && p < e) ? cf[j] : NIL32;
-        if (a < rt) {
-            hf[n] = a; hs[n] = cs[j]; he[n] = ce[j];
-            n++; j++; p++;
-        } else {
-            hf[n] = rt | HEAPBIT;
-            hs[n] = (u32)fs[rt];
-            he[n] = (u32)(fe[rt] - 1);
-            n++;
-            rt = hp.delmin(rt);
-            delmins++;
+        if ((u32)j < m) {
+            hf[n + j] = csr.f[p + j];
+            hs[n + j] = csr.s[p + j];
+            he[n + j] = csr.e[p + j];
         }
+    }
+    n += m;
+    p += m;
+    // 2) merge in overflow members smaller than the cache's tail (or filling it), evicting
+    //    CSR members back to the CSR range (they are its last consumed entries)
+    // (overflow pulls are serial atomics: pull only what correctness needs — members below the
+    //  tail — plus enough to get back to REFILL_AT)
+    while (rt != NIL32 && (n < (u32)REFILL_AT || rt < (hf[n - 1] & ~HEAPBIT))) {
+        const u32 s0 = (u32)fs[rt], e0 = (u32)(fe[rt] - 1);
+        if (n == (u32)H) {                       // evict the tail (it is > rt)
+            const u32 ev = hf[H - 1];
+            if (ev & HEAPBIT) rt = hp.insert(k, rt, ev & ~HEAPBIT);
+            else p--;
+            n--;
+        }
+        u32 j = n;
+        while (j > 0 && (hf[j - 1] & ~HEAPBIT) > rt) {
+            hf[j] = hf[j - 1]; hs[j] = hs[j - 1]; he[j] = he[j - 1];
+            j--;
+        }
+        hf[j] = rt | HEAPBIT; hs[j] = s0; he[j] = e0;
+        n++;
+        rt = hp.extract(k, rt);
+        delmins++;
     }
     S.hn[k] = (unsigned char)n;
     S.ptr[k] = p;
@@ -160,20 +193,18 @@ __device__ void refill(Smem &S, Heap &hp, const Csr &csr, const u64 *__restrict_
 
 // a remainder piece f = [s, e1 + 1) joins class k
 __device__ void arrive(Smem &S, Heap &hp, u32 k, u32 f, u32 s, u32 e1) {
-    if (S.cnt[k]++ == 0) set_bit(S, k);
+    const u32 before = S.cnt[k]++;
+    if (before == 0) set_bit(S, k);
     u32 n = S.hn[k];
     u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
-    hp.child[f] = NIL32;
-    hp.sib[f] = NIL32;
-    if (n < (u32)H || f < (hf[H - 1] & ~HEAPBIT)) {
+    // the cache must stay "the n smallest members": f enters it if it is below the cache's
+    // tail, or if every member is cached (nothing outside could be smaller)
+    if ((n > 0 && f < (hf[n - 1] & ~HEAPBIT)) || (n < (u32)H && before == n)) {
         u32 j;
         if (n == (u32)H) {      // evict the largest cached member
             u32 ev = hf[H - 1];
             if (ev & HEAPBIT) {
-                u32 x = ev & ~HEAPBIT;
-                hp.child[x] = NIL32;
-                hp.sib[x] = NIL32;
-                S.root[k] = hp.meld(S.root[k], x);
+                S.root[k] = hp.insert(k, S.root[k], ev & ~HEAPBIT);
             } else {
                 S.ptr[k]--;     // the largest cached CSR member is CSR[ptr-1]
             }
@@ -188,22 +219,25 @@ __device__ void arrive(Smem &S, Heap &hp, u32 k, u32 f, u32 s, u32 e1) {
         }
         hf[j] = f | HEAPBIT; hs[j] = s; he[j] = e1;
     } else {
-        S.root[k] = hp.meld(S.root[k], f);
+        S.root[k] = hp.insert(k, S.root[k], f);
     }
 }
 
 __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict__ off,
                                                   u64 *__restrict__ fs, const u64 *__restrict__ fe,
                                                   const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
-                                                  u64 *__restrict__ out_u, u32 *child, u32 *sib, int NC, int L,
-                                                  u64 *stats) {
+                                                  u64 *__restrict__ out_u, u32 *bm, u64 w0, u64 w1, u64 w2,
+                                                  u32 *slot_map, int NC, int L, u64 *stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const u32 lane = lane_id();
-    Heap hp{child, sib, 0, 4 * (u64)n + 4096, false};
+    const u64 nslots = (u64)NC;
+    Heap hp{bm, bm + nslots * w0, bm + nslots * (w0 + w1), w0, w1, w2, S.slot, &S.nslot, 0, false};
+    if (lane == 0) S.nslot = 0;
     // ---- init: CSR ranges, head caches, bitmaps ----
     for (int k = lane; k < NC; k += 32) {
         u32 b = off[k], e = off[k + 1];
+        S.slot[k] = NONE;
         S.cnt[k] = e - b;
         S.hn[k] = 0;
         S.ptr[k] = b;
@@ -227,14 +261,14 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     __syncwarp();
     u64 rb_base = 0, rb_end = 0;
     u64 n_iter = 0, n_retarget = 0, n_rounds = 0, n_qsteps = 0;
-    long long t_spec = 0, t_dirty = 0, t_cls = 0, t_arr = 0, t0;
+    long long t_spec = 0, t_dirty = 0, t_cls = 0, t_arr = 0, t_store = 0, t0;
     u64 pos = 0;
     while (pos < n) {
         n_iter++;
         // watchdogs: the engine must terminate even if an invariant broke (reported as error)
         if (__any_sync(FULLMASK, hp.broken) || n_iter > n + 64) {
             if (lane == 0 && stats) stats[2] = hp.broken ? 4 : 3;
-            return;
+            break;
         }
         if (pos + 32 > rb_end) {                 // stage requests
             rb_base = pos;
@@ -403,6 +437,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             }
         }
         // ---- class updates by group leaders: blocks that left the class; head carve ----
+        __syncwarp();
+        t_store += clock64() - t0;
         const u32 leftm = __ballot_sync(FULLMASK, cm && part && mynk != SAME);
         const u32 staym = __ballot_sync(FULLMASK, cm && part && mynk == SAME && last_on_block);
         if (cm && part && rank == 0) {
@@ -440,6 +476,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         t_arr += clock64() - t0;
         pos += commit;
     }
+    for (int k = lane; k < NC; k += 32) slot_map[k] = S.slot[k];   // for k_bitheap_clear
     if (stats) {
         u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits;
         for (int o = 16; o > 0; o >>= 1) {
@@ -450,8 +487,27 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         }
         if (lane == 0) {
             stats[0] += n_iter; stats[1] += t; stats[3] += n_rounds; stats[4] += q;
-            stats[5] += t_spec; stats[6] += t_dirty; stats[7] += t_cls; stats[8] += t_arr; stats[9] += dl; stats[10] += vis;
+            stats[5] += t_spec; stats[6] += t_dirty; stats[7] += t_cls; stats[8] += t_arr; stats[9] += dl; stats[10] += vis; stats[11] += t_store;
         }
+    }
+}
+
+// zero the overflow-bitmap words still holding members after the engine: every such member is
+// a piece in its final class, so visiting each surviving piece clears them all
+__global__ void k_bitheap_clear(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev,
+                                const u32 *__restrict__ slot_map, u32 *bm, u64 w0, u64 w1, u64 w2, int NC,
+                                int L) {
+    const u64 F = *F_dev;
+    const u64 nslots = (u64)NC;
+    u32 *l0 = bm, *l1 = bm + nslots * w0, *l2 = bm + nslots * (w0 + w1);
+    for (u64 f = (u64)blockIdx.x * blockDim.x + threadIdx.x; f < F; f += (u64)gridDim.x * blockDim.x) {
+        const u64 z = fe[f] - fs[f];
+        if (!z) continue;
+        const u32 s = slot_map[cls_insert(z, L)];
+        if (s == NONE) continue;
+        l0[s * w0 + (f >> 5)] = 0;
+        l1[s * w1 + (f >> 10)] = 0;
+        l2[s * w2 + (f >> 15)] = 0;
     }
 }
 

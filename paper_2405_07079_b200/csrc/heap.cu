@@ -35,7 +35,7 @@ struct Layout {
     // offsets
     u64 o_ctr, o_stats, o_tbl, o_fs0, o_fs1, o_fe0, o_fe1, o_kA, o_kB, o_vA, o_vB, o_flags, o_pos,
         o_hist, o_tsum, o_vs, o_ve, o_vsc, o_vec, o_ms, o_me, o_r, o_c, o_out, o_off, o_child,
-        o_sib, o_cs, o_ce, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
+        o_sib, o_cs, o_ce, o_bm, o_slot, bm_w0, bm_w1, bm_w2, bm_bytes, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
         o_promo, o_fr, o_froff, o_reqoff, total;
 };
 
@@ -99,6 +99,13 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.o_sib = take(L.cap_f * 4);
         L.o_cs = take(L.cap_f * 4);
         L.o_ce = take(L.cap_f * 4);
+        // overflow bitmaps: one three-level slot per class (engine_tlsf.cuh)
+        L.bm_w0 = (L.cap_f + 31) / 32;
+        L.bm_w1 = (L.bm_w0 + 31) / 32;
+        L.bm_w2 = (L.bm_w1 + 31) / 32;
+        L.bm_bytes = (u64)L.NC * (L.bm_w0 + L.bm_w1 + L.bm_w2) * 4;
+        L.o_bm = take(L.bm_bytes);
+        L.o_slot = take(tlsfw::MAX_NC * 4);
     }
     if (policy == HEAP_FIRST_FIT) {
         L.o_tree = take(L.ff_tree * 8);
@@ -142,7 +149,7 @@ struct heap {
     u64 *tbl, *fs[2], *fe[2];
     u32 *kA, *kB, *vA, *vB, *flags, *pos, *hist, *tsum;
     u64 *vs, *ve, *vsc, *vec, *ms, *me, *r, *out;
-    u32 *c, *off, *child, *sib, *cs, *ce;
+    u32 *c, *off, *child, *sib, *cs, *ce, *bm, *slot;
     u64 *tree, *lvl;
     u64 *bk[2];
     u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
@@ -416,6 +423,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->off = at<u32>(w, L.o_off);
     h->child = L.o_child ? at<u32>(w, L.o_child) : nullptr; h->sib = L.o_sib ? at<u32>(w, L.o_sib) : nullptr;
     h->cs = L.o_cs ? at<u32>(w, L.o_cs) : nullptr; h->ce = L.o_ce ? at<u32>(w, L.o_ce) : nullptr;
+    h->bm = L.o_bm ? at<u32>(w, L.o_bm) : nullptr; h->slot = L.o_slot ? at<u32>(w, L.o_slot) : nullptr;
+    if (h->bm && cudaMemsetAsync(h->bm, 0, L.bm_bytes, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     h->tree = L.o_tree ? at<u64>(w, L.o_tree) : nullptr; h->lvl = L.o_lvl ? at<u64>(w, L.o_lvl) : nullptr;
     h->bk[0] = L.o_bk0 ? at<u64>(w, L.o_bk0) : nullptr; h->bk[1] = L.o_bk1 ? at<u64>(w, L.o_bk1) : nullptr;
     if (policy == HEAP_BUDDY) {
@@ -546,7 +555,9 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         TAG(h, HEAP_TAG_ENGINE);
         tlsfw::Csr csr{sv, h->cs, h->ce};
         LAUNCH(h, tlsfw::k_engine, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r, h->c,
-               n, h->out, h->child, h->sib, L.NC, L.L, C->eng);
+               n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng);
+        LAUNCH(h, tlsfw::k_bitheap_clear, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->slot, h->bm,
+               L.bm_w0, L.bm_w1, L.bm_w2, L.NC, L.L);
     } else if (h->policy == HEAP_FIRST_FIT) {
         u64 offs[fits::FF_MAX_LEVELS] = {0};
         u64 m = L.cap_f, o = 0;
