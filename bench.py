@@ -68,6 +68,30 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def aggregate(t_ms, ops, world, dev):
+    """Whole-job numbers: max over ranks of the device time, sum over ranks of the ops."""
+    if world == 1:
+        return t_ms, ops
+    import torch
+    import torch.distributed as dist
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    oo = torch.tensor([ops], dtype=torch.int64, device=dev)
+    dist.all_reduce(oo, op=dist.ReduceOp.SUM)
+    return float(tt.item()), int(oo.item())
+
+
+def gather_stats(local, world):
+    """All-gather of the 16 x u64 heap statistics (the path's only collective)."""
+    if world == 1:
+        return local.view(1, -1)
+    import torch
+    import torch.distributed as dist
+    out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local)
+    return out.view(world, -1)
+
+
 def make_trace(cfg, rank, nbatches):
     t = tg.Trace(cfg, rank=rank, total_ops=cfg.batch * nbatches)
     return [b for b in t]
@@ -243,14 +267,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     step_ms = [a.elapsed_time(e) for a, e in ev]
     t_ms = sum(step_ms)
     st = h.stats()
-    if world > 1:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        oo = torch.tensor([ops], dtype=torch.int64, device=dev)
-        dist.all_reduce(oo, op=dist.ReduceOp.SUM)
-        t_max, ops_all = float(tt.item()), int(oo.item())
-    else:
-        t_max, ops_all = t_ms, ops
+    t_max, ops_all = aggregate(t_ms, ops, world, dev)
     value = ops_all / (t_max / 1e3)
     del h
     torch.cuda.empty_cache()
@@ -289,14 +306,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 e_ops += nf + na
                 h2d += 8 * (nf + na)
                 d2h += 8 * na
-        if world > 1:
-            tt = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            oo = torch.tensor([e_ops], dtype=torch.int64, device=dev)
-            dist.all_reduce(oo, op=dist.ReduceOp.SUM)
-            e_ms, e_ops_all = float(tt.item()), int(oo.item())
-        else:
-            e_ops_all = e_ops
+        e_ms, e_ops_all = aggregate(e_ms, e_ops, world, dev)
         e2e = {"value": e_ops_all / (e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
         del h
