@@ -61,6 +61,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-batches", type=int, default=0, help="0 = auto")
     p.add_argument("--no-arena", action="store_true", help="do not allocate the arena tensor")
+    p.add_argument("--no-driver-baselines", action="store_true")
+    p.add_argument("--driver-max-ops", type=int, default=2_000_000)
     return p.parse_args()
 
 
@@ -328,6 +330,20 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
                 "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_s * 1e3}
 
+    # ---------------- driver-allocator baselines (the paper's comparison) ----------------
+    drv = None
+    if rank == 0 and not args.no_driver_baselines:
+        import baselines
+        drv = {}
+        for name, mode in (("cudaMalloc", 0), ("cudaMallocAsync", 1)):
+            try:
+                r = baselines.replay(mode, batches, max_ops=args.driver_max_ops, max_seconds=60.0)
+            except Exception as e:  # never lose the main line over a baseline
+                r = {"error": str(e)[:200]}
+            r["sample"] = (f"config {cfg.idx} batches from 0, same per-batch op order, 1 host thread, "
+                           f"capped at {args.driver_max_ops} ops / 60 s")
+            drv[name] = r
+
     # ---------------- CPU oracle baseline (rank 0, N = 1) ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -363,6 +379,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "roofline": roof,
             "kernel_shares": shares,
             "cpu_baseline": cpu,
+            "driver_baselines": drv,
             "e2e": e2e,
             "clocks": clocks,
             "heap": {"n_live": st["n_live"], "n_free": st["n_free"], "allocs_failed": st["allocs_failed"],
