@@ -47,6 +47,7 @@ struct Smem {
     u32 hs[MAX_NC * H];           // its current start (units)
     u32 he[MAX_NC * H];           // its end - 1 (units; ends can be 2^32)
     unsigned char hn[MAX_NC];
+    unsigned char hb[MAX_NC];     // ring-buffer base of the cache (entry j at (hb + j) % H)
     u32 cw[32];
     u32 sw;
     u64 rbuf[RB];
@@ -152,14 +153,16 @@ __device__ void refill(Smem &S, Heap &hp, const Csr &csr, const u64 *__restrict_
     u32 p = S.ptr[k], e = S.endp[k], rt = S.root[k];
     if (n >= (u32)REFILL_AT || (p >= e && rt == NIL32)) return;
     u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    const u32 b = S.hb[k];                      // ring buffer: entry j lives at (b + j) % H
+#define RI(j) ((b + (j)) & (H - 1))
     // 1) append the next CSR members (one round of independent loads, straight into smem)
     const u32 m = min((u32)H - n, e - p);
 #pragma unroll
     for (int j = 0; j < H; j++) {
         if ((u32)j < m) {
-            hf[n + j] = csr.f[p + j];
-            hs[n + j] = csr.s[p + j];
-            he[n + j] = csr.e[p + j];
+            hf[RI(n + j)] = csr.f[p + j];
+            hs[RI(n + j)] = csr.s[p + j];
+            he[RI(n + j)] = csr.e[p + j];
         }
     }
     n += m;
@@ -168,22 +171,24 @@ __device__ void refill(Smem &S, Heap &hp, const Csr &csr, const u64 *__restrict_
     //    CSR members back to the CSR range (they are its last consumed entries)
     // (overflow pulls are serial atomics: pull only what correctness needs — members below the
     //  tail — plus enough to get back to REFILL_AT)
-    while (rt != NIL32 && (n < (u32)REFILL_AT || rt < (hf[n - 1] & ~HEAPBIT))) {
+    while (rt != NIL32 && (n < (u32)REFILL_AT || rt < (hf[RI(n - 1)] & ~HEAPBIT))) {
+        // issue the extract's atomic and the member's data loads together (independent)
+        u32 nxt = hp.extract(k, rt);
         const u32 s0 = (u32)fs[rt], e0 = (u32)(fe[rt] - 1);
         if (n == (u32)H) {                       // evict the tail (it is > rt)
-            const u32 ev = hf[H - 1];
-            if (ev & HEAPBIT) rt = hp.insert(k, rt, ev & ~HEAPBIT);
+            const u32 ev = hf[RI(H - 1)];
+            if (ev & HEAPBIT) nxt = hp.insert(k, nxt, ev & ~HEAPBIT);
             else p--;
             n--;
         }
         u32 j = n;
-        while (j > 0 && (hf[j - 1] & ~HEAPBIT) > rt) {
-            hf[j] = hf[j - 1]; hs[j] = hs[j - 1]; he[j] = he[j - 1];
+        while (j > 0 && (hf[RI(j - 1)] & ~HEAPBIT) > rt) {
+            hf[RI(j)] = hf[RI(j - 1)]; hs[RI(j)] = hs[RI(j - 1)]; he[RI(j)] = he[RI(j - 1)];
             j--;
         }
-        hf[j] = rt | HEAPBIT; hs[j] = s0; he[j] = e0;
+        hf[RI(j)] = rt | HEAPBIT; hs[RI(j)] = s0; he[RI(j)] = e0;
         n++;
-        rt = hp.extract(k, rt);
+        rt = nxt;
         delmins++;
     }
     S.hn[k] = (unsigned char)n;
@@ -197,12 +202,13 @@ __device__ void arrive(Smem &S, Heap &hp, u32 k, u32 f, u32 s, u32 e1) {
     if (before == 0) set_bit(S, k);
     u32 n = S.hn[k];
     u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    const u32 b = S.hb[k];
     // the cache must stay "the n smallest members": f enters it if it is below the cache's
     // tail, or if every member is cached (nothing outside could be smaller)
-    if ((n > 0 && f < (hf[n - 1] & ~HEAPBIT)) || (n < (u32)H && before == n)) {
+    if ((n > 0 && f < (hf[RI(n - 1)] & ~HEAPBIT)) || (n < (u32)H && before == n)) {
         u32 j;
         if (n == (u32)H) {      // evict the largest cached member
-            u32 ev = hf[H - 1];
+            u32 ev = hf[RI(H - 1)];
             if (ev & HEAPBIT) {
                 S.root[k] = hp.insert(k, S.root[k], ev & ~HEAPBIT);
             } else {
@@ -213,11 +219,11 @@ __device__ void arrive(Smem &S, Heap &hp, u32 k, u32 f, u32 s, u32 e1) {
             j = n;
             S.hn[k] = (unsigned char)(n + 1);
         }
-        while (j > 0 && (hf[j - 1] & ~HEAPBIT) > f) {
-            hf[j] = hf[j - 1]; hs[j] = hs[j - 1]; he[j] = he[j - 1];
+        while (j > 0 && (hf[RI(j - 1)] & ~HEAPBIT) > f) {
+            hf[RI(j)] = hf[RI(j - 1)]; hs[RI(j)] = hs[RI(j - 1)]; he[RI(j)] = he[RI(j - 1)];
             j--;
         }
-        hf[j] = f | HEAPBIT; hs[j] = s; he[j] = e1;
+        hf[RI(j)] = f | HEAPBIT; hs[RI(j)] = s; he[RI(j)] = e1;
     } else {
         S.root[k] = hp.insert(k, S.root[k], f);
     }
@@ -240,6 +246,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         S.slot[k] = NONE;
         S.cnt[k] = e - b;
         S.hn[k] = 0;
+        S.hb[k] = 0;
         S.ptr[k] = b;
         S.endp[k] = e;
         S.root[k] = NIL32;
@@ -309,19 +316,22 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             //      the remainder before each request is still in the class.
             const u32 npeer = __popc(peers);
             const u32 nh = part ? S.hn[k] : 0, nc = part ? S.cnt[k] : 0;
+            const u32 hb = part ? S.hb[k] : 0;
+            const u32 slotA = k * H + ((hb + rank) & (H - 1)), slot0 = k * H + hb;
             const bool hasA = part && rank < nh;
             u32 fA = 0, nkA = NONE;
             u64 sA = 0;
             if (hasA) {
-                fA = S.hf[k * H + rank] & ~HEAPBIT;
-                sA = S.hs[k * H + rank];
-                const u64 zA = (u64)S.he[k * H + rank] + 1 - sA - ri;
+                fA = S.hf[slotA] & ~HEAPBIT;
+                sA = S.hs[slotA];
+                const u64 zA = (u64)S.he[slotA] + 1 - sA - ri;
                 nkA = zA ? cls_insert(zA, L) : NONE;
             }
             const bool okA = (__ballot_sync(FULLMASK, hasA && nkA == k && rank + 1 < npeer) & peers) == 0;
             // segmented exclusive prefix of r over the group (Hillis-Steele over ranks)
             u64 incl = part ? ri : 0;
-            const u32 maxpeer = __reduce_max_sync(FULLMASK, part ? npeer : 0u);
+            // only groups that fail pattern A need the prefix (skip the scan when none does)
+            const u32 maxpeer = __reduce_max_sync(FULLMASK, (part && !okA) ? npeer : 0u);
             for (u32 st = 1; st < maxpeer; st <<= 1) {
                 const u32 src = (part && rank >= st) ? S.lor[leader * 32 + rank - st] : lane;
                 const u64 t = __shfl_sync(FULLMASK, incl, src);
@@ -331,18 +341,18 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             u64 s0 = 0, z0 = 0;
             u32 f0 = 0;
             if (part && nh) {
-                f0 = S.hf[k * H] & ~HEAPBIT;
-                s0 = S.hs[k * H];
-                z0 = (u64)S.he[k * H] + 1 - s0;
+                f0 = S.hf[slot0] & ~HEAPBIT;
+                s0 = S.hs[slot0];
+                z0 = (u64)S.he[slot0] + 1 - s0;
             }
             const bool covB = part && nh && (rank == 0 || (P < z0 && z0 - P >= cls_lo(k, L)));
             const u32 uncov = __ballot_sync(FULLMASK, part && !covB);   // every lane must vote
             const bool okB = !okA && (uncov & peers) == 0;
             if (part && okA) {
-                if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = S.he[k * H + rank]; }
+                if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = S.he[slotA]; }
                 else flag = (rank < nc) ? F_MISS : F_OVER;
             } else if (part && okB) {
-                flag = F_OK; myf = f0; mys = s0 + P; mye = S.he[k * H];
+                flag = F_OK; myf = f0; mys = s0 + P; mye = S.he[slot0];
                 const u64 z = z0 - P - ri;
                 const u32 nk = z ? cls_insert(z, L) : NONE;
                 mynk = (nk == k) ? SAME : nk;
@@ -359,9 +369,10 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                     const u32 lq = S.lor[lane * 32 + q];
                     if (need) {
                         if (b >= nh) break;
-                        curf = S.hf[k * H + b] & ~HEAPBIT;
-                        cur_s = S.hs[k * H + b];
-                        cur_e = (u64)S.he[k * H + b] + 1;
+                        const u32 sl = k * H + ((hb + b) & (H - 1));
+                        curf = S.hf[sl] & ~HEAPBIT;
+                        cur_s = S.hs[sl];
+                        cur_e = (u64)S.he[sl] + 1;
                         need = false;
                     }
                     const u64 rq = S.rbuf[pos + lq - rb_base];
@@ -443,16 +454,15 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         const u32 staym = __ballot_sync(FULLMASK, cm && part && mynk == SAME && last_on_block);
         if (cm && part && rank == 0) {
             const u32 left = __popc(leftm & peers);
-            u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
             const u32 st = staym & peers;        // the surviving head was carved: new start
+            const u32 b = S.hb[k];
             if (st) {
                 const u32 d = __ffs(st) - 1;
-                hs[left] = (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]);
+                S.hs[k * H + ((b + left) & (H - 1))] = (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]);
             }
-            if (left) {
-                const u32 nh = S.hn[k];
-                for (u32 j = left; j < nh; j++) { hf[j - left] = hf[j]; hs[j - left] = hs[j]; he[j - left] = he[j]; }
-                S.hn[k] = (unsigned char)(nh - left);
+            if (left) {                          // pop `left` members: advance the ring base
+                S.hb[k] = (unsigned char)((b + left) & (H - 1));
+                S.hn[k] = (unsigned char)(S.hn[k] - left);
                 S.cnt[k] -= left;
                 refill(S, hp, csr, fs, fe, k, n_delmin);
                 if (S.cnt[k] == 0) clear_bit(S, k);
