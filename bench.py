@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--no-arena", action="store_true", help="do not allocate the arena tensor")
     p.add_argument("--no-driver-baselines", action="store_true")
     p.add_argument("--driver-max-ops", type=int, default=2_000_000)
+    p.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
+    p.add_argument("--dev-share-gpu", action="store_true", help=argparse.SUPPRESS)
     return p.parse_args()
 
 
@@ -392,12 +394,17 @@ def run_ours(args, cfg, rank, world, local_rank):
 def main():
     args = parse()
     rank, world, local_rank = dist_env()
+    if args.dev_share_gpu:        # dev only: run every rank on GPU 0 (tests the N > 1 logic on one GPU)
+        local_rank = 0
     cfg = tg.CONFIGS[args.config]
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(args.dist_backend)
     if args.impl == "reference":
         if rank == 0:
             run_reference(args, cfg)
