@@ -438,7 +438,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         t_dirty += clock64() - t0;
         t0 = clock64();
         // ---- commit: results and piece starts ----
-        const u32 nxt = lane < 31 ? __fns(peers, lane + 1, 1) : NONE;
+        const u32 later = (lane < 31) ? (peers & (0xFFFFFFFEu << lane)) : 0u;   // peers after this lane
+        const u32 nxt = later ? (u32)(__ffs(later) - 1) : NONE;
         const bool last_on_block = mynk != SAME || nxt >= commit;
         if (cm) {
             if (!part) out_u[i] = HEAP_NULL_U64;
