@@ -28,8 +28,51 @@
 namespace buddy {
 
 constexpr int NT = 1024;
+constexpr int FREE_CAP = 16384;     // per-level staging capacity (units) of k_free_levels
+constexpr size_t FREE_SMEM = 3 * FREE_CAP * sizeof(u32);
+constexpr int ALLOC_CAP = 49152;    // per-level staging capacity (u32 words) of k_alloc_levels
+constexpr size_t ALLOC_SMEM = ALLOC_CAP * sizeof(u32);
 constexpr u32 BORROW = 0x80000000u;
 constexpr u64 FAIL = 0xFFFFFFFFFFFFFFFFull;
+
+// CTA-wide copy global -> shared with 8 independent loads per thread in flight (a plain
+// strided loop would serialise one global round trip per element)
+template <typename TS, typename TD>
+__device__ __forceinline__ void cta_copy(TD *dst, const TS *src, u64 n) {
+    for (u64 base = 0; base < n; base += 8 * NT) {
+        TS v[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            u64 i = base + (u64)k * NT + threadIdx.x;
+            v[k] = i < n ? src[i] : (TS)0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            u64 i = base + (u64)k * NT + threadIdx.x;
+            if (i < n) dst[i] = (TD)v[k];
+        }
+    }
+}
+
+// CTA-wide merge of two sorted arrays (ties: a first) into out; all threads call.
+template <typename TA, typename TO>
+__device__ void cta_merge(const TA *a, u64 na, const TA *b, u64 nb, TO *out) {
+    const u64 n = na + nb;
+    const u64 per = (n + NT - 1) / NT;
+    u64 diag = (u64)threadIdx.x * per;
+    if (diag < n) {
+        u64 lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+        while (lo < hi) {
+            u64 mid = (lo + hi) >> 1;
+            if (a[mid] <= b[diag - mid - 1]) lo = mid + 1; else hi = mid;
+        }
+        u64 i = lo, j = diag - lo;
+        for (u64 k = 0; k < per && diag + k < n; k++) {
+            bool ta = (j >= nb) || (i < na && a[i] <= b[j]);
+            out[diag + k] = (TO)(ta ? a[i++] : b[j++]);
+        }
+    }
+}
 
 // CTA-wide merge of two sorted u64 arrays (ties: a first) into out; all threads call.
 __device__ void cta_merge_u64(const u64 *a, u64 na, const u64 *b, u64 nb, u64 *out) {
@@ -94,32 +137,82 @@ __global__ void __launch_bounds__(NT) k_free_levels(const u64 *__restrict__ old_
     __shared__ u32 sm[33];
     __shared__ u64 ooff[41];
     __shared__ u64 s_np, s_out;
-    if (threadIdx.x <= (unsigned)K + 1) ooff[threadIdx.x] = ctr->bud_off[threadIdx.x];
+    __shared__ u32 foff[42];
+    if (threadIdx.x <= (unsigned)K + 1) {
+        ooff[threadIdx.x] = ctr->bud_off[threadIdx.x];
+        foff[threadIdx.x] = fr_off[threadIdx.x];
+    }
     if (threadIdx.x == 0) { s_np = 0; s_out = 0; }
     __syncthreads();
+    extern __shared__ u32 stage[];      // 3 x FREE_CAP units (addresses < 2^32 units)
+    u32 *X = stage, *Y = stage + FREE_CAP, *Z = stage + 2 * FREE_CAP;
     for (int t = 0; t <= K; t++) {
         const u64 *old_t = old_list + ooff[t];
         const u64 n_old = ooff[t + 1] - ooff[t];
-        const u64 *fr_t = fr + fr_off[t];
-        const u64 n_fr = fr_off[t + 1] - fr_off[t];
+        const u64 *fr_t = fr + foff[t];
+        const u64 n_fr = foff[t + 1] - foff[t];
         const u64 n_pr = s_np;
-        cta_merge_u64(old_t, n_old, fr_t, n_fr, bufA);
-        __syncthreads();
-        cta_merge_u64(bufA, n_old + n_fr, promo, n_pr, bufB);
-        __syncthreads();
         const u64 n = n_old + n_fr + n_pr;
         const u64 bit = 1ull << t;
-        auto paired_lo = [&](u64 i) { return t < K && !(bufB[i] & bit) && i + 1 < n && bufB[i + 1] == bufB[i] + bit; };
-        auto paired_hi = [&](u64 i) { return t < K && (bufB[i] & bit) && i > 0 && bufB[i - 1] == bufB[i] - bit; };
         const u64 out0 = s_out;
-        // survivors -> new list (order t)
-        u64 ns = cta_compact(n, [&](u64 i) { return !paired_lo(i) && !paired_hi(i); },
+        if (n == 0) {                    // empty level: nothing to merge, keep the offsets
+            if (threadIdx.x == 0) { ctr->bud_off[t] = out0; ctr->bud_cnt[t] = 0; }
+            continue;
+        }
+        u64 ns, np;
+        if (n <= (u64)FREE_CAP) {
+            // stage the level in shared memory (coalesced), merge there: binary searches at
+            // shared-memory latency instead of global
+            cta_copy(X, old_t, n_old);                     // 8 independent loads in flight per thread
+            cta_copy(X + n_old, fr_t, n_fr);
+            cta_copy(X + n_old + n_fr, promo, n_pr);
+            __syncthreads();
+            cta_merge(X, n_old, X + n_old, n_fr, Y);
+            __syncthreads();
+            cta_merge(Y, n_old + n_fr, X + n_old + n_fr, n_pr, Z);
+            __syncthreads();
+            // one fused pass: flags for survivors and promotions (bit masks over this thread's
+            // contiguous chunk of <= 16 elements), one packed block scan, then the writes
+            const u32 nn = (u32)n, per = (nn + NT - 1) / NT, b0 = threadIdx.x * per;
+            const u32 bt = (u32)bit;
+            const bool top = (t >= K);
+            u32 ms = 0, mp = 0;
+            for (u32 k = 0; k < per; k++) {
+                const u32 i = b0 + k;
+                if (i >= nn) break;
+                const u32 zi = Z[i];
+                const bool lo = !top && !(zi & bt) && i + 1 < nn && Z[i + 1] == zi + bt;
+                const bool hi = !top && (zi & bt) && i > 0 && Z[i - 1] == zi - bt;
+                if (!lo && !hi) ms |= 1u << k;
+                if (lo) mp |= 1u << k;
+            }
+            u32 tot;
+            const u32 pos = block_excl_scan<NT>(__popc(ms) | (__popc(mp) << 16), sm, &tot);
+            u32 ps = pos & 0xFFFF, pp = pos >> 16;
+            for (u32 k = 0; k < per; k++) {
+                const u32 i = b0 + k;
+                if ((ms >> k) & 1) new_list[out0 + ps++] = Z[i];
+                if ((mp >> k) & 1) promo[pp++] = Z[i];
+            }
+            ns = tot & 0xFFFF;
+            np = tot >> 16;
+            __syncthreads();
+        } else {
+            cta_merge_u64(old_t, n_old, fr_t, n_fr, bufA);
+            __syncthreads();
+            cta_merge_u64(bufA, n_old + n_fr, promo, n_pr, bufB);
+            __syncthreads();
+            auto paired_lo = [&](u64 i) { return t < K && !(bufB[i] & bit) && i + 1 < n && bufB[i + 1] == bufB[i] + bit; };
+            auto paired_hi = [&](u64 i) { return t < K && (bufB[i] & bit) && i > 0 && bufB[i - 1] == bufB[i] - bit; };
+            // survivors -> new list (order t)
+            ns = cta_compact(n, [&](u64 i) { return !paired_lo(i) && !paired_hi(i); },
                              [&](u64 i, u64 p) { new_list[out0 + p] = bufB[i]; }, sm);
-        __syncthreads();
-        // promotions -> promo (read by the next level; bufB still holds this level)
-        u64 np = cta_compact(n, [&](u64 i) { return paired_lo(i); },
+            __syncthreads();
+            // promotions -> promo (read by the next level; bufB still holds this level)
+            np = cta_compact(n, [&](u64 i) { return paired_lo(i); },
                              [&](u64 i, u64 p) { promo[p] = bufB[i]; }, sm);
-        __syncthreads();
+            __syncthreads();
+        }
         if (threadIdx.x == 0) {
             ctr->bud_off[t] = out0;
             ctr->bud_cnt[t] = ns;
@@ -194,15 +287,34 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         const u64 nb = s_nb;        // borrows from t-1 (already in btm/bsrc)
         u32 *Dt = dtm + doff[t], *Ds = dsrc + doff[t];
         // direct requests: time = request index, src = request index
-        // merge (rq, rq) with (btm, bsrc)
-        cta_merge_tm(rq, rq, nr, btm, bsrc, nb, Dt, Ds);
+        // merge (rq, rq) with (btm, bsrc); staged in shared memory when the level fits
+        if (nr + 2 * nb <= (u64)ALLOC_CAP) {
+            extern __shared__ u32 astage[];
+            u32 *sr = astage, *st = astage + nr, *ss = astage + nr + nb;
+            cta_copy(sr, rq, nr);
+            cta_copy(st, btm, nb);
+            cta_copy(ss, bsrc, nb);
+            __syncthreads();
+            cta_merge_tm(sr, sr, nr, st, ss, nb, Dt, Ds);
+        } else {
+            cta_merge_tm(rq, rq, nr, btm, bsrc, nb, Dt, Ds);
+        }
         __syncthreads();
         const u64 nd = nr + nb;
         const u64 x = nd > n_t ? nd - n_t : 0;
         const u64 nbor = (t < K) ? (x + 1) / 2 : 0;
-        for (u64 j = threadIdx.x; j < nbor; j += NT) {
-            btm[j] = Dt[n_t + 2 * j];
-            bsrc[j] = (u32)j | BORROW;
+        for (u64 base = 0; base < nbor; base += 8 * NT) {
+            u32 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const u64 j = base + (u64)k * NT + threadIdx.x;
+                v[k] = j < nbor ? Dt[n_t + 2 * j] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const u64 j = base + (u64)k * NT + threadIdx.x;
+                if (j < nbor) { btm[j] = v[k]; bsrc[j] = (u32)j | BORROW; }
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -223,16 +335,28 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         const u64 *bad = baddr + boff[t];   // borrows of order t (served by t+1)
         const u64 nbor = boff[t + 1] - boff[t];
         u64 *bad_lo = (t > 0) ? baddr + boff[t - 1] : nullptr;   // borrows of order t-1
-        for (u64 p = threadIdx.x; p < nd; p += NT) {
-            u64 a;
-            if (p < n_t) a = blk[p];
-            else {
-                u64 xx = p - n_t, j = xx >> 1;
-                a = (j < nbor && bad[j] != FAIL) ? bad[j] + ((xx & 1) ? (1ull << t) : 0) : FAIL;
+        for (u64 base = 0; base < nd; base += 8 * NT) {    // 8 independent element chains per thread
+            u64 a[8];
+            u32 s[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const u64 p = base + (u64)k * NT + threadIdx.x;
+                s[k] = p < nd ? Ds[p] : 0u;
+                if (p >= nd) a[k] = FAIL;
+                else if (p < n_t) a[k] = blk[p];
+                else {
+                    const u64 xx = p - n_t, j = xx >> 1;
+                    const u64 bj = j < nbor ? bad[j] : FAIL;
+                    a[k] = (bj != FAIL) ? bj + ((xx & 1) ? (1ull << t) : 0) : FAIL;
+                }
             }
-            u32 s = Ds[p];
-            if (s & BORROW) bad_lo[s & ~BORROW] = a;
-            else out_u[s] = a;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const u64 p = base + (u64)k * NT + threadIdx.x;
+                if (p >= nd) continue;
+                if (s[k] & BORROW) bad_lo[s[k] & ~BORROW] = a[k];
+                else out_u[s[k]] = a[k];
+            }
         }
         if (threadIdx.x == 0) {
             u64 x = nd > n_t ? nd - n_t : 0;

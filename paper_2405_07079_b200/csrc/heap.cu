@@ -408,6 +408,10 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->G = sms * 4;
     if (cudaFuncSetAttribute(tlsfw::k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(buddy::k_free_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)buddy::FREE_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(buddy::k_alloc_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)buddy::ALLOC_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     void *w = d_workspace;
     h->ctr = at<DevCtr>(w, L.o_ctr);
     h->dstats = at<heap_stats_t>(w, L.o_stats);
@@ -510,7 +514,7 @@ int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_strea
         u32 *ok = r2 ? h->kB : h->kA, *ov = r2 ? h->vB : h->vA;
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, ok, &C->nv, L.K + 1, h->froff);
         LAUNCH(h, buddy::k_gather_u64, h->G, 256, 0, s, h->vsc, ov, &C->nv, h->fr);
-        LAUNCH(h, buddy::k_free_levels, 1, buddy::NT, 0, s, h->fs[cur], h->fs[nxt], h->fr, h->froff, h->bufA,
+        LAUNCH(h, buddy::k_free_levels, 1, buddy::NT, buddy::FREE_SMEM, s, h->fs[cur], h->fs[nxt], h->fr, h->froff, h->bufA,
                h->bufB, h->promo, L.K, C);
     }
     h->cur = nxt;
@@ -530,7 +534,7 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         LAUNCH(h, buddy::k_alloc_orders, h->G, 256, 0, s, (const u64 *)d_sizes, n, h->alog2, L.A_u, L.K, h->kA, h->vA, &C->tmp[0]);
         radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s);   // 1 pass: result in kB/vB
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kB, &C->tmp[0], L.K + 2, h->reqoff);
-        LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, 0, s, h->vB, h->reqoff, h->fs[cur], h->fs[nxt], h->dtm,
+        LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, buddy::ALLOC_SMEM, s, h->vB, h->reqoff, h->fs[cur], h->fs[nxt], h->dtm,
                h->dsrc, nullptr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
         LAUNCH(h, buddy::k_alloc_r, h->G, 256, 0, s, h->kA, n, L.K, h->r);
         TAG(h, HEAP_TAG_FINISH);
