@@ -43,6 +43,7 @@ constexpr u32 F_OK = 0, F_OVER = 1, F_MISS = 2;
 struct Smem {
     u32 ptr[MAX_NC], endp[MAX_NC], cnt[MAX_NC], root[MAX_NC], slot[MAX_NC];
     u32 nslot;
+    u32 ow_i[MAX_NC], ow_v[MAX_NC];   // cached overflow word per class (see Heap)
     u32 hf[MAX_NC * H];           // cached member f (| HEAPBIT when it came from the heap)
     u32 hs[MAX_NC * H];           // its current start (units)
     u32 he[MAX_NC * H];           // its end - 1 (units; ends can be 2^32)
@@ -70,6 +71,7 @@ struct Heap {
     u64 w0, w1, w2;          // words per slot at each level
     u32 *slot;               // smem: slot of class k (NONE = none yet)
     u32 *nslot;              // smem counter
+    u32 *ow_i, *ow_v;        // smem: cached level-0 word (index, value) holding class k's minimum
     u64 visits = 0;
     bool broken = false;
     __device__ __forceinline__ u32 slot_of(u32 k) {
@@ -81,6 +83,7 @@ struct Heap {
     __device__ __forceinline__ u32 insert(u32 k, u32 root, u32 f) {
         const u64 s = slot_of(k);
         atomicOr(&l0[s * w0 + (f >> 5)], 1u << (f & 31));
+        if (ow_i[k] == (f >> 5)) ow_v[k] |= 1u << (f & 31);   // keep the cached word coherent
         atomicOr(&l1[s * w1 + (f >> 10)], 1u << ((f >> 5) & 31));
         atomicOr(&l2[s * w2 + (f >> 15)], 1u << ((f >> 10) & 31));
         return f < root ? f : root;
@@ -91,8 +94,18 @@ struct Heap {
         u32 *a0 = l0 + s * w0, *a1 = l1 + s * w1, *a2 = l2 + s * w2;
         visits++;
         const u32 w = h >> 5;
-        u32 rest = atomicAnd(&a0[w], ~(1u << (h & 31))) & ~(1u << (h & 31));
+        u32 rest;
+        if (ow_i[k] == w) {                                   // cached word: no atomic round trip
+            rest = ow_v[k] & ~(1u << (h & 31));
+            ow_v[k] = rest;
+            a0[w] = rest;
+        } else {
+            rest = atomicAnd(&a0[w], ~(1u << (h & 31))) & ~(1u << (h & 31));
+            ow_i[k] = w;
+            ow_v[k] = rest;
+        }
         if (rest) return (w << 5) + __ffs(rest) - 1;          // bits below h are never set
+        ow_i[k] = NONE;
         const u32 v = w >> 5;
         rest = atomicAnd(&a1[v], ~(1u << (w & 31))) & ~(1u << (w & 31));
         u32 ww;
@@ -116,6 +129,8 @@ struct Heap {
         }
         const u32 t0 = __ldcg(&a0[ww]);
         if (!t0) { broken = true; return NIL32; }
+        ow_i[k] = ww;
+        ow_v[k] = t0;
         return (ww << 5) + __ffs(t0) - 1;
     }
 };
@@ -238,12 +253,13 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const u32 lane = lane_id();
     const u64 nslots = (u64)NC;
-    Heap hp{bm, bm + nslots * w0, bm + nslots * (w0 + w1), w0, w1, w2, S.slot, &S.nslot, 0, false};
+    Heap hp{bm, bm + nslots * w0, bm + nslots * (w0 + w1), w0, w1, w2, S.slot, &S.nslot, S.ow_i, S.ow_v, 0, false};
     if (lane == 0) S.nslot = 0;
     // ---- init: CSR ranges, head caches, bitmaps ----
     for (int k = lane; k < NC; k += 32) {
         u32 b = off[k], e = off[k + 1];
         S.slot[k] = NONE;
+        S.ow_i[k] = NONE;
         S.cnt[k] = e - b;
         S.hn[k] = 0;
         S.hb[k] = 0;
@@ -267,7 +283,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     }
     __syncwarp();
     u64 rb_base = 0, rb_end = 0;
-    u64 n_iter = 0, n_retarget = 0, n_rounds = 0, n_qsteps = 0;
+    u64 n_iter = 0, n_retarget = 0, n_rounds = 0, n_qsteps = 0, n_refill = 0;
+    long long t_refill = 0;
     long long t_spec = 0, t_dirty = 0, t_cls = 0, t_arr = 0, t_store = 0, t0;
     u64 pos = 0;
     while (pos < n) {
@@ -465,7 +482,10 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 S.hb[k] = (unsigned char)((b + left) & (H - 1));
                 S.hn[k] = (unsigned char)(S.hn[k] - left);
                 S.cnt[k] -= left;
+                const long long tr0 = clock64();
                 refill(S, hp, csr, fs, fe, k, n_delmin);
+                t_refill += clock64() - tr0;
+                n_refill++;
                 if (S.cnt[k] == 0) clear_bit(S, k);
             }
         }
@@ -489,7 +509,13 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     }
     for (int k = lane; k < NC; k += 32) slot_map[k] = S.slot[k];   // for k_bitheap_clear
     if (stats) {
-        u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits;
+        u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits, nr = n_refill;
+        u64 tmax = (u64)t_refill;
+        for (int o = 16; o > 0; o >>= 1) {
+            nr += __shfl_xor_sync(FULLMASK, nr, o);
+            const u64 x = __shfl_xor_sync(FULLMASK, tmax, o);
+            tmax = x > tmax ? x : tmax;
+        }
         for (int o = 16; o > 0; o >>= 1) {
             vis += __shfl_xor_sync(FULLMASK, vis, o);
             t += __shfl_xor_sync(FULLMASK, t, o);
@@ -499,6 +525,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         if (lane == 0) {
             stats[0] += n_iter; stats[1] += t; stats[3] += n_rounds; stats[4] += q;
             stats[5] += t_spec; stats[6] += t_dirty; stats[7] += t_cls; stats[8] += t_arr; stats[9] += dl; stats[10] += vis; stats[11] += t_store;
+            stats[12] += nr; stats[13] += tmax;
         }
     }
 }
