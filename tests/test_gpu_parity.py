@@ -176,3 +176,42 @@ def test_invariants_config3_prefix():
     g, _ = run_parity(cfg, cfg.max_live, cfg.batch, max_batches=10)
     fp, lp = g.export()
     check_invariants(fp, lp, cfg.arena_bytes, cfg.align, False)
+
+
+def test_config5_full_size_properties():
+    """Config 5 at full size for 12 batches (the bench's launch configuration): the first two
+    batches exactly against the oracle, then properties that hold at any size — I1-I4 on the
+    exported state, conservation, counter consistency, and every returned offset of the last
+    batch is a live block of the rounded request size, pairwise disjoint."""
+    cfg = tg.CONFIGS[5]
+    g = Gpu(cfg.arena_bytes, cfg.align, cfg.policy, cfg.max_live, cfg.batch)
+    o = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
+    im = IdMap(cfg.batch * 12)
+    nreq = 0
+    last = None
+    for bi, (fids, sizes, first) in enumerate(tg.Trace(cfg, total_ops=cfg.batch * 12)):
+        offs = im.offsets(fids)
+        g.free_batch(offs)
+        go = g.alloc_batch(sizes)
+        if bi < 2:
+            o.free_batch(offs)
+            assert np.array_equal(go, o.alloc_batch(sizes)), bi
+        im.record(first, go)
+        nreq += len(sizes)
+        last = (sizes, go)
+    st = g.stats()
+    assert st["error_flags"] == 0 and st["rc"] == 0
+    assert st["allocs_ok"] + st["allocs_failed"] == nreq
+    assert st["live_bytes"] + st["free_bytes"] == cfg.arena_bytes
+    fp, lp = g.export()
+    assert len(lp) == st["n_live"] and len(fp) == st["n_free"]
+    check_invariants(fp, lp, cfg.arena_bytes, cfg.align, False)
+    sizes, out = last
+    ok = out != HEAP_NULL
+    starts = lp[:, 0]
+    idx = np.searchsorted(starts, out[ok])
+    assert np.all(starts[idx] == out[ok])
+    r = -(-sizes[ok].astype(np.int64) // cfg.align) * cfg.align
+    assert np.array_equal(lp[idx, 1].astype(np.int64), r)
+    so = np.sort(out[ok])
+    assert len(np.unique(so)) == len(so)
