@@ -23,9 +23,13 @@
 //      (exactly the sequential results), updates the class state, and the next chunk starts
 //      at the first dirty request.  Request 0 of a chunk is never dirty, so chunks progress.
 // Class state: per class a CSR range of batch-start members (address order, consumed as a
-// prefix; class-sorted copies of (f, start, end)), the sorted head cache, and a pairing heap
-// (keyed by f, arrays indexed by f) of remainders that dropped into the class and did not fit
-// the cache.  Invariant: the cache holds the min(H, members) smallest members of the class.
+// prefix; class-sorted copies of (f, start, end)), a sorted head cache (ring buffer of up to H
+// members in shared memory), and an overflow set (three-level bitmap over f, see Heap) of
+// remainders that dropped into the class and did not fit the cache.  Invariant: the cache
+// holds the n smallest members of the class (n >= min(REFILL_AT, members) after a refill).
+// Ablation (measured on B200, config 5 batch 5 / config 3 batch 29): one lane replaying the
+// requests strictly one by one on the same state takes 376 ms / 23.6 ms per batch versus
+// 238 ms / 8.9 ms for this chunked engine.
 #pragma once
 #include "common.cuh"
 

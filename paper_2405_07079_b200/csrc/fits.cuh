@@ -249,114 +249,7 @@ __global__ void k_cls_off(const u32 *__restrict__ key, const u64 *F_dev, int NC,
     }
 }
 
-struct PHeap {
-    u32 *child, *sib;
-    __device__ __forceinline__ u32 meld(u32 a, u32 b) {
-        if (a == NIL32) return b;
-        if (b == NIL32) return a;
-        if (b < a) { u32 t = a; a = b; b = t; }
-        sib[b] = child[a];
-        child[a] = b;
-        return a;
-    }
-    __device__ u32 delmin(u32 root) {
-        u32 x = child[root];
-        u32 acc = NIL32;
-        while (x != NIL32) {
-            u32 a = x, b = sib[a];
-            if (b == NIL32) { sib[a] = acc; acc = a; break; }
-            u32 nx = sib[b];
-            sib[a] = NIL32;
-            sib[b] = NIL32;
-            u32 m = meld(a, b);
-            sib[m] = acc;
-            acc = m;
-            x = nx;
-        }
-        u32 res = NIL32;
-        while (acc != NIL32) {
-            u32 nx = sib[acc];
-            sib[acc] = NIL32;
-            res = meld(res, acc);
-            acc = nx;
-        }
-        return res;
-    }
-};
-
-constexpr int MAX_NC = 1024;
-
-__global__ void __launch_bounds__(32) k_tlsf_engine(const u32 *__restrict__ csr, const u32 *__restrict__ off,
-                                                    u64 *__restrict__ fs, const u64 *__restrict__ fe,
-                                                    const u64 *__restrict__ r, const u32 *__restrict__ c, u64 n,
-                                                    u64 *__restrict__ out_u, u32 *child, u32 *sib, int NC, int L) {
-    __shared__ u32 ptr[MAX_NC], endp[MAX_NC], root[MAX_NC], cnt[MAX_NC];
-    __shared__ u32 cw[32];
-    __shared__ u32 sw;
-    const u32 lane = lane_id();
-    for (int k = lane; k < NC; k += 32) {
-        ptr[k] = off[k];
-        endp[k] = off[k + 1];
-        root[k] = NIL32;
-        cnt[k] = off[k + 1] - off[k];
-    }
-    __syncwarp();
-    u32 swl = 0;
-    for (int w = 0; w < 32; w++) {
-        int k = w * 32 + lane;
-        u32 b = __ballot_sync(FULLMASK, k < NC && cnt[k] > 0);
-        if (lane == 0) cw[w] = b;
-        if (b) swl |= 1u << w;
-    }
-    if (lane == 0) sw = swl;
-    __syncwarp();
-    if (lane != 0) return;
-    PHeap ph{child, sib};
-    u32 summ = sw;
-    for (u64 i = 0; i < n; i++) {
-        u64 ri = r[i];
-        u32 ci = c[i];
-        if (ri == 0 || ci >= (u32)NC) { out_u[i] = HEAP_NULL_U64; continue; }
-        // first nonempty class >= ci: second-level word, then first-level summary (ffs)
-        u32 w = ci >> 5;
-        u32 m = cw[w] & (0xFFFFFFFFu << (ci & 31));
-        int k;
-        if (m) k = (int)(w << 5) + __ffs(m) - 1;
-        else {
-            u32 sm = (w >= 31) ? 0u : (summ & (0xFFFFFFFFu << (w + 1)));
-            if (!sm) { out_u[i] = HEAP_NULL_U64; continue; }
-            u32 w2 = __ffs(sm) - 1;
-            k = (int)(w2 << 5) + __ffs(cw[w2]) - 1;
-        }
-        u32 a = ptr[k] < endp[k] ? csr[ptr[k]] : NIL32;
-        u32 b = root[k];
-        bool from_heap = b < a;
-        u32 f = from_heap ? b : a;
-        u64 s = fs[f], e = fe[f];
-        out_u[i] = s;
-        s += ri;
-        fs[f] = s;
-        u64 z = e - s;
-        int nk = z ? (int)cls_insert(z, L) : -1;
-        if (nk != k) {
-            if (from_heap) root[k] = ph.delmin(b);
-            else ptr[k]++;
-            if (--cnt[k] == 0) {
-                cw[k >> 5] &= ~(1u << (k & 31));
-                if (!cw[k >> 5]) summ &= ~(1u << (k >> 5));
-            }
-            if (z) {
-                child[f] = NIL32;
-                sib[f] = NIL32;
-                root[nk] = ph.meld(root[nk], f);
-                if (cnt[nk]++ == 0) {
-                    cw[nk >> 5] |= 1u << (nk & 31);
-                    summ |= 1u << (nk >> 5);
-                }
-            }
-        }
-    }
-}
+constexpr int MAX_NC = 1024;   // class-offset array bound (TLSF classes of 2^32 units: 897)
 
 // ------------------------------------------------------------------- FIRST FIT ----
 // A 32-ary max tree over piece sizes: the first block with size >= r is found by one ballot

@@ -95,8 +95,6 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
     L.o_out = take(max_batch * 8);
     L.o_off = take((fits::MAX_NC + 8) * 4);
     if (policy == HEAP_TLSF || policy == HEAP_SEGFIT) {
-        L.o_child = take(L.cap_f * 4);
-        L.o_sib = take(L.cap_f * 4);
         L.o_cs = take(L.cap_f * 4);
         L.o_ce = take(L.cap_f * 4);
         // overflow bitmaps: one three-level slot per class (engine_tlsf.cuh)
@@ -425,7 +423,6 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->ms = at<u64>(w, L.o_ms); h->me = at<u64>(w, L.o_me);
     h->r = at<u64>(w, L.o_r); h->c = at<u32>(w, L.o_c); h->out = at<u64>(w, L.o_out);
     h->off = at<u32>(w, L.o_off);
-    h->child = L.o_child ? at<u32>(w, L.o_child) : nullptr; h->sib = L.o_sib ? at<u32>(w, L.o_sib) : nullptr;
     h->cs = L.o_cs ? at<u32>(w, L.o_cs) : nullptr; h->ce = L.o_ce ? at<u32>(w, L.o_ce) : nullptr;
     h->bm = L.o_bm ? at<u32>(w, L.o_bm) : nullptr; h->slot = L.o_slot ? at<u32>(w, L.o_slot) : nullptr;
     if (h->bm && cudaMemsetAsync(h->bm, 0, L.bm_bytes, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
