@@ -35,8 +35,12 @@
 
 namespace tlsfw {
 
+#ifndef REFILL_AT_DEF
+#define REFILL_AT_DEF 12
+#endif
+
 constexpr int H = 16;             // head-cache depth per class
-constexpr int REFILL_AT = 8;      // refill a class's cache when it holds fewer members
+constexpr int REFILL_AT = REFILL_AT_DEF;      // refill a class's cache when it holds fewer members
 constexpr int MAX_NC = 928;       // classes of 2^32 units at SL_LOG2 = 5 (fl <= 28)
 constexpr int RB = 512;           // request staging buffer
 constexpr u32 NONE = 0xFFFFFFFFu;
