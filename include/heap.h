@@ -58,8 +58,12 @@ enum heap_policy {
                            block bin = floor(log2 size), address order    Alg. 4/5 */
     HEAP_TLSF = 4,      /* two-level bins (32 linear sub-bins per power
                            of two), min (bin, address) over bin >= search PAPER.md:447-458 */
-    HEAP_BUDDY = 5      /* binary buddy, min order then address; align is
+    HEAP_BUDDY = 5,     /* binary buddy, min order then address; align is
                            the minimum block */
+    HEAP_SEGFIT_LIFO = 6 /* the paper's segregated fit verbatim: power-of-two
+                           bins as stacks — an alloc pops the head (most recent
+                           push) of the first nonempty bin >= ceil(log2 r); frees
+                           and split remainders are pushed at the head      Alg. 4/5 */
 };
 
 #define HEAP_NULL UINT64_MAX /* failed alloc; no-op in a free batch (offset 0 is valid, C18) */

@@ -162,3 +162,99 @@ class OracleB:
         lp = np.array(sorted((s * self.align, z * self.align) for s, z in self.live.items()),
                       dtype=np.uint64).reshape(-1, 2)
         return fp, lp
+
+
+class OracleBLifo:
+    """Brute-force twin of Oracle-L's SEGFIT_LIFO (the paper's Alg. 4/5 with stack bins).
+
+    Free blocks are a flat Python list of [start, size, stamp]; every decision is a linear
+    scan: alloc takes the minimum (bin, -stamp) over blocks whose bin >= ceil-bin of the
+    request (Alg. 4 pops the head of the first nonempty bin, :332-337, :440); a free removes
+    the free neighbours ending at / starting right after the block and pushes the merged block
+    (Alg. 5 :374-436).  Every push takes the next tick of a logical clock."""
+
+    def __init__(self, arena_bytes: int, align: int, policy: int = 6):
+        assert policy == 6
+        self.align, self.A = align, arena_bytes // align
+        self.free = [[0, self.A, 0]]
+        self.clock = 1
+        self.live: dict[int, int] = {}
+        self.counts = dict(allocs_ok=0, allocs_failed=0, frees_ok=0, frees_invalid=0,
+                           frees_double=0, frees_null=0)
+
+    @staticmethod
+    def _bin(size):            # floor(log2 size) + 1 (our class numbering, SL_LOG2 = 0)
+        return size.bit_length()
+
+    @staticmethod
+    def _req_bin(r):           # ceil(log2 r) + 1
+        return (r - 1).bit_length() + 1
+
+    def _push(self, s, z):
+        self.free.append([s, z, self.clock])
+        self.clock += 1
+
+    def alloc_units(self, r):
+        c = self._req_bin(r)
+        cand = [(self._bin(z), -st, i) for i, (s, z, st) in enumerate(self.free) if self._bin(z) >= c]
+        if not cand:
+            return None
+        _, _, i = min(cand)
+        s, z, _ = self.free.pop(i)
+        if z > r:
+            self._push(s + r, z - r)
+        self.live[s] = r
+        return s
+
+    def alloc_batch(self, sizes):
+        out = np.empty(len(sizes), dtype=np.uint64)
+        for i, sz in enumerate(int(x) for x in sizes):
+            r = -(-sz // self.align)
+            u = self.alloc_units(r) if sz != 0 and r <= self.A else None
+            if u is None:
+                out[i] = HEAP_NULL
+                self.counts["allocs_failed"] += 1
+            else:
+                out[i] = u * self.align
+                self.counts["allocs_ok"] += 1
+        return out
+
+    def free_batch(self, offsets):
+        free_starts = {s for s, _, _ in self.free}
+        seen, to_free = set(), []
+        for o in sorted(int(x) for x in offsets):
+            if o == HEAP_NULL:
+                self.counts["frees_null"] += 1
+            elif o % self.align or o // self.align >= self.A:
+                self.counts["frees_invalid"] += 1
+            else:
+                u = o // self.align
+                if u in self.live:
+                    if u in seen:
+                        self.counts["frees_double"] += 1
+                    else:
+                        seen.add(u)
+                        self.counts["frees_ok"] += 1
+                        to_free.append(u)
+                elif u in free_starts:
+                    self.counts["frees_double"] += 1
+                else:
+                    self.counts["frees_invalid"] += 1
+        for u in to_free:
+            z = self.live.pop(u)
+            s, e = u, u + z
+            for blk in list(self.free):
+                if blk[0] + blk[1] == u:
+                    s = blk[0]
+                    self.free.remove(blk)
+                elif blk[0] == u + z:
+                    e = blk[0] + blk[1]
+                    self.free.remove(blk)
+            self._push(s, e - s)
+
+    def export(self):
+        fp = np.array(sorted((s * self.align, z * self.align) for s, z, _ in self.free),
+                      dtype=np.uint64).reshape(-1, 2)
+        lp = np.array(sorted((s * self.align, z * self.align) for s, z in self.live.items()),
+                      dtype=np.uint64).reshape(-1, 2)
+        return fp, lp

@@ -23,6 +23,9 @@
  *
  *       BUDDY      binary buddy: smallest nonempty order >= k, lowest address, split keeping
  *                  the low half, merge with a free buddy a XOR 2^k
+ *       SEGFIT_LIFO the paper's segregated fit verbatim: power-of-two bins used as stacks —
+ *                  alloc pops the head (newest push) of the first nonempty bin >= ceil(log2 r),
+ *                  every free / remainder is pushed at the head of its bin (Alg. 4/5)
  *   - batch driver (canonical order, BASELINE.json north_star): a free batch classifies every
  *     offset against the batch-start state, then frees the valid ones in ascending address
  *     order; an alloc batch serves requests in request order, HEAP_NULL on failure.
@@ -36,11 +39,12 @@
 #include <vector>
 #include <algorithm>
 #include <utility>
+#include <tuple>
 
 namespace {
 
 const uint64_t HEAP_NULL = ~0ull;
-enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5 };
+enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6 };
 
 /* floor(log2 u) for u >= 1, written as a plain loop */
 int floor_log2(uint64_t u) {
@@ -79,6 +83,10 @@ struct Heap {
     std::map<uint64_t, uint64_t> live;    /* start -> size (units): the block table */
     std::map<uint64_t, uint64_t> freeb;   /* start -> size (units): free list, address order */
     std::set<std::pair<uint64_t, uint64_t>> cls_index;   /* (class, start): SEGFIT/TLSF bins */
+    /* SEGFIT_LIFO bins: (class, ~push stamp, start) — the head of a bin is its newest push */
+    std::set<std::tuple<uint64_t, uint64_t, uint64_t>> lifo_index;
+    std::map<uint64_t, uint64_t> stamp_of;                 /* start -> push stamp */
+    uint64_t clock = 0;
     std::vector<std::set<uint64_t>> bfree;                /* BUDDY: free starts per order */
     int K = 0;                                            /* BUDDY: max order */
     Counters c;
@@ -87,10 +95,22 @@ struct Heap {
     void free_insert(uint64_t s, uint64_t z) {
         freeb[s] = z;
         if (policy == SEGFIT || policy == TLSF) cls_index.insert({insert_class(z, L), s});
+        if (policy == SEGFIT_LIFO) {
+            /* "Place new block at head of free list in its size class" (Alg. 4 :350-355,
+             * Alg. 5 :427-433): a push gets the next tick of a logical clock; the bin's head
+             * is its most recent push. */
+            uint64_t st = clock++;
+            stamp_of[s] = st;
+            lifo_index.insert({insert_class(z, 0), ~st, s});
+        }
     }
     void free_erase(uint64_t s) {
         auto it = freeb.find(s);
         if (policy == SEGFIT || policy == TLSF) cls_index.erase({insert_class(it->second, L), s});
+        if (policy == SEGFIT_LIFO) {
+            lifo_index.erase({insert_class(it->second, 0), ~stamp_of[s], s});   /* unlink (remove()) */
+            stamp_of.erase(s);
+        }
         freeb.erase(it);
     }
 
@@ -168,6 +188,16 @@ struct Heap {
             if (it == cls_index.end()) return HEAP_NULL;
             return take(it->second, r);
         }
+        if (policy == SEGFIT_LIFO) {
+            /* Alg. 4 as written: bin = ceil(log2 size) (+1 shift), the first nonempty bin at or
+             * above it (availability bitmap + ffs), pop its HEAD (the block pushed
+             * last, "it = ht[free_lists[order]]", :336-337), split from the low end and push the
+             * remainder at the head of its bin (:342-356). */
+            uint64_t c = search_class(r, 0);
+            auto it = lifo_index.lower_bound({c, 0, 0});
+            if (it == lifo_index.end()) return HEAP_NULL;
+            return take(std::get<2>(*it), r);
+        }
         /* BUDDY: r is already a power of two */
         int k = floor_log2(r);
         int j = k;
@@ -187,7 +217,7 @@ extern "C" {
 
 void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
     if (align == 0 || (align & (align - 1)) || arena_bytes == 0 || arena_bytes % align) return nullptr;
-    if (policy < FIRST_FIT || policy > BUDDY) return nullptr;
+    if (policy < FIRST_FIT || policy > SEGFIT_LIFO) return nullptr;
     Heap *h = new Heap();
     h->policy = policy;
     h->L = (policy == TLSF) ? 5 : 0;

@@ -38,6 +38,7 @@ struct DevCtr {
     u64 bud_off[41];
     u64 bud_total;
     u64 eng[16];        // alloc engine diagnostics (engine_tlsf.cuh)
+    u64 lifo_clock;     // SEGFIT_LIFO logical push clock (fits.cuh)
 };
 
 enum { ERR_CAP_LIVE = 1, ERR_TABLE_FULL = 2, ERR_CAP_FREE = 4, ERR_ENGINE = 8 };

@@ -252,11 +252,83 @@ __device__ void arrive(Smem &S, Heap &hp, u32 k, u32 f, u32 s, u32 e1) {
     }
 }
 
+// ---------------------------------------------------------------- SEGFIT_LIFO ----
+// The paper's own segregated fit (Alg. 4/5): each bin is a stack; a class's member order is
+// push recency (newest first) instead of address.  Every remainder dropped during the batch is
+// the newest member of its class, so it enters the head cache at the FRONT; when the cache is
+// full its oldest entry is evicted — a CSR member goes back to the CSR range, an earlier
+// remainder onto a per-class spill stack (links in global memory, indexed by f).  Spilled
+// remainders are all newer than every CSR member, and the stack top is the newest spilled, so a
+// refill pops the stack before touching the CSR range.
+struct Lifo {
+    u32 *next;          // spill-stack links, indexed by f
+    u32 *stamp;         // per-piece push stamp (persisted for the next batch)
+    const u64 *clock;   // logical push clock at the start of this alloc batch
+};
+
+__device__ void refill_lifo(Smem &S, const Lifo &lf, const Csr &csr, const u64 *__restrict__ fs,
+                            const u64 *__restrict__ fe, u32 k, u64 &pops) {
+    u32 n = S.hn[k];
+    u32 p = S.ptr[k], e = S.endp[k], rt = S.root[k];
+    if (n >= (u32)REFILL_AT || (p >= e && rt == NIL32)) return;
+    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    const u32 b = S.hb[k];
+    while (rt != NIL32 && n < (u32)REFILL_AT) {         // spilled remainders first (newer)
+        const u32 nx = lf.next[rt];
+        hf[RI(n)] = rt | HEAPBIT;
+        hs[RI(n)] = (u32)fs[rt];
+        he[RI(n)] = (u32)(fe[rt] - 1);
+        n++;
+        rt = nx;
+        pops++;
+    }
+    if (rt == NIL32) {                                   // then the CSR range (oldest members)
+        const u32 m = min((u32)H - n, e - p);
+#pragma unroll
+        for (int j = 0; j < H; j++) {
+            if ((u32)j < m) {
+                hf[RI(n + j)] = csr.f[p + j];
+                hs[RI(n + j)] = csr.s[p + j];
+                he[RI(n + j)] = csr.e[p + j];
+            }
+        }
+        n += m;
+        p += m;
+    }
+    S.hn[k] = (unsigned char)n;
+    S.ptr[k] = p;
+    S.root[k] = rt;
+}
+
+// a remainder f = [s, e1 + 1) is pushed at the head of class k (Alg. 4 :350-356)
+__device__ void arrive_lifo(Smem &S, const Lifo &lf, u32 k, u32 f, u32 s, u32 e1) {
+    if (S.cnt[k]++ == 0) set_bit(S, k);
+    u32 n = S.hn[k];
+    u32 b = S.hb[k];
+    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    if (n == (u32)H) {                                   // evict the oldest cached member
+        const u32 ev = hf[RI(H - 1)];
+        if (ev & HEAPBIT) {
+            const u32 x = ev & ~HEAPBIT;
+            lf.next[x] = S.root[k];
+            S.root[k] = x;
+        } else {
+            S.ptr[k]--;
+        }
+        n--;
+    }
+    b = (b - 1) & (H - 1);
+    S.hb[k] = (unsigned char)b;
+    hf[RI(0)] = f | HEAPBIT; hs[RI(0)] = s; he[RI(0)] = e1;
+    S.hn[k] = (unsigned char)(n + 1);
+}
+
+template <bool LIFO>
 __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict__ off,
                                                   u64 *__restrict__ fs, const u64 *__restrict__ fe,
                                                   const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
                                                   u64 *__restrict__ out_u, u32 *bm, u64 w0, u64 w1, u64 w2,
-                                                  u32 *slot_map, int NC, int L, u64 *stats) {
+                                                  u32 *slot_map, int NC, int L, u64 *stats, Lifo lf) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const u32 lane = lane_id();
@@ -277,7 +349,11 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     }
     __syncwarp();
     u64 n_delmin = 0;
-    for (int k = lane; k < NC; k += 32) refill(S, hp, csr, fs, fe, k, n_delmin);
+    for (int k = lane; k < NC; k += 32) {
+        if constexpr (LIFO) refill_lifo(S, lf, csr, fs, fe, k, n_delmin);
+        else refill(S, hp, csr, fs, fe, k, n_delmin);
+    }
+    const u64 t_alloc = LIFO ? *lf.clock : 0;    // push stamp of request i's remainder: t_alloc + i
     __syncwarp();
     {
         u32 swl = 0;
@@ -438,7 +514,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         t0 = clock64();
         // ---- dirty requests: remainders dropped earlier in the chunk, cache misses ----
         const bool part = act && k != NONE;
-        const u64 key = part ? (((u64)k << 32) | myf) : ~0ull;
+        // in-class order key: address (f) — or, for LIFO bins, "after any fresh remainder"
+        const u64 key = part ? (((u64)k << 32) | (LIFO ? 1u : myf)) : ~0ull;
         bool bad = part && flag == F_MISS;
         const bool dropper = part && flag == F_OK && mynk != SAME && mynk != NONE;
         u32 dm = __ballot_sync(FULLMASK, dropper);
@@ -447,7 +524,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             dm &= dm - 1;
             const u32 dk = __shfl_sync(FULLMASK, mynk, d);
             const u32 dfb = __shfl_sync(FULLMASK, myf, d);
-            if (act && !fail0 && lane > d && ci <= dk && ((((u64)dk) << 32) | dfb) < key) bad = true;
+            if (act && !fail0 && lane > d && ci <= dk && ((((u64)dk) << 32) | (LIFO ? 0u : dfb)) < key) bad = true;
         }
         const u32 badm = __ballot_sync(FULLMASK, bad);
         const u32 limit = (n - pos) < 32 ? (u32)(n - pos) : 32u;
@@ -470,7 +547,10 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             if (!part) out_u[i] = HEAP_NULL_U64;
             else {
                 out_u[i] = mys;
-                if (last_on_block) fs[myf] = mys + ri;
+                if (last_on_block) {
+                    fs[myf] = mys + ri;
+                    if (LIFO && mynk != NONE) lf.stamp[myf] = (u32)(t_alloc + i);   // pushed remainder
+                }
             }
         }
         // ---- class updates by group leaders: blocks that left the class; head carve ----
@@ -483,15 +563,22 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             const u32 st = staym & peers;        // the surviving head was carved: new start
             const u32 b = S.hb[k];
             if (st) {
+                // the carved block is the head now; it is no longer its batch-start CSR entry
+                // (new start; for LIFO bins also the newest push), so mark it overflow-origin:
+                // evicted later, it goes to the overflow set / spill stack and its start is
+                // re-read from fs, never from the stale CSR copy
                 const u32 d = __ffs(st) - 1;
-                S.hs[k * H + ((b + left) & (H - 1))] = (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]);
+                const u32 sl = k * H + ((b + left) & (H - 1));
+                S.hs[sl] = (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]);
+                S.hf[sl] |= HEAPBIT;
             }
             if (left) {                          // pop `left` members: advance the ring base
                 S.hb[k] = (unsigned char)((b + left) & (H - 1));
                 S.hn[k] = (unsigned char)(S.hn[k] - left);
                 S.cnt[k] -= left;
                 const long long tr0 = clock64();
-                refill(S, hp, csr, fs, fe, k, n_delmin);
+                if constexpr (LIFO) refill_lifo(S, lf, csr, fs, fe, k, n_delmin);
+                else refill(S, hp, csr, fs, fe, k, n_delmin);
                 t_refill += clock64() - tr0;
                 n_refill++;
                 if (S.cnt[k] == 0) clear_bit(S, k);
@@ -508,14 +595,17 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             while (mm) {
                 const u32 d = __ffs(mm) - 1;
                 mm &= mm - 1;
-                arrive(S, hp, mynk, S.res_f[d], (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]), S.res_e[d]);
+                const u32 s2 = (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]);
+                if constexpr (LIFO) arrive_lifo(S, lf, mynk, S.res_f[d], s2, S.res_e[d]);
+                else arrive(S, hp, mynk, S.res_f[d], s2, S.res_e[d]);
             }
         }
         __syncwarp();
         t_arr += clock64() - t0;
         pos += commit;
     }
-    for (int k = lane; k < NC; k += 32) slot_map[k] = S.slot[k];   // for k_bitheap_clear
+    if (slot_map)
+        for (int k = lane; k < NC; k += 32) slot_map[k] = S.slot[k];   // for k_bitheap_clear
     if (stats) {
         u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits, nr = n_refill;
         u64 tmax = (u64)t_refill;

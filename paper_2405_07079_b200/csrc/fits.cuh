@@ -147,6 +147,51 @@ __global__ void k_coal_write(const u64 *__restrict__ ms, const u64 *__restrict__
     }
 }
 
+// ---------------------------------------------------------- SEGFIT_LIFO push stamps ----
+// The paper's segregated fit keeps each bin as a stack (Alg. 4/5: every free and every split
+// remainder is pushed at the head of its bin).  A block's position in its bin is its push time
+// on a logical clock ctr->lifo_clock: the valid frees of a batch are pushed in ascending address
+// order (clock + rank), an alloc's remainder at clock + request index.
+__global__ void k_free_stamps(const u64 *nv_dev, const DevCtr *ctr, u32 *__restrict__ vstamp) {
+    const u64 nv = *nv_dev, t0 = ctr->lifo_clock;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (u64)gridDim.x * blockDim.x)
+        vstamp[i] = (u32)(t0 + i);
+}
+__global__ void k_clock_add(DevCtr *ctr, const u64 *n_dev, u64 n_host) {
+    ctr->lifo_clock += n_dev ? *n_dev : n_host;
+    if (ctr->lifo_clock >= 0xFFFFFFF0ull) ctr->error_flags |= ERR_CAP_LIVE;   // u32 stamps exhausted
+}
+// a coalesced run is pushed when its last free happens: its stamp is the largest in the run
+// (freed stamps exceed every resident stamp); heads wrote their own stamp, the rest max into it
+__global__ void k_coal_stamp(const u32 *__restrict__ mt, const u64 *M_dev, const u32 *__restrict__ head,
+                             const u32 *__restrict__ pos, u32 *__restrict__ ot, u64 cap) {
+    const u64 M = *M_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (u64)gridDim.x * blockDim.x) {
+        const u64 run = pos[i] + head[i] - 1;
+        if (!head[i] && run < cap) atomicMax(&ot[run], mt[i]);
+    }
+}
+__global__ void k_coal_stamp_head(const u32 *__restrict__ mt, const u64 *M_dev, const u32 *__restrict__ head,
+                                  const u32 *__restrict__ pos, u32 *__restrict__ ot, u64 cap) {
+    const u64 M = *M_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (u64)gridDim.x * blockDim.x)
+        if (head[i] && pos[i] < cap) ot[pos[i]] = mt[i];
+}
+// CSR key for SEGFIT_LIFO pieces: class major, newest push first
+__global__ void k_lifo_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u32 *__restrict__ ft,
+                            const u64 *F_dev, u64 *__restrict__ key, u32 *__restrict__ val) {
+    const u64 F = *F_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x) {
+        key[i] = ((u64)cls_insert(fe[i] - fs[i], 0) << 32) | (u64)(~ft[i]);
+        val[i] = (u32)i;
+    }
+}
+__global__ void k_u64_hi(const u64 *__restrict__ key, const u64 *n_dev, u32 *__restrict__ out) {
+    const u64 n = *n_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        out[i] = (u32)(key[i] >> 32);
+}
+
 // ------------------------------------------------------------------ alloc phase ----
 // r = ceil(s / align) units (0 = fail: size 0 or larger than the arena), c = search class
 __global__ void k_alloc_prep(const u64 *__restrict__ sizes, u64 n, int alog2, u64 A_u, int L, int want_cls,

@@ -36,12 +36,12 @@ struct Layout {
     u64 o_ctr, o_stats, o_tbl, o_fs0, o_fs1, o_fe0, o_fe1, o_kA, o_kB, o_vA, o_vB, o_flags, o_pos,
         o_hist, o_tsum, o_vs, o_ve, o_vsc, o_vec, o_ms, o_me, o_r, o_c, o_out, o_off, o_child,
         o_sib, o_cs, o_ce, o_bm, o_slot, bm_w0, bm_w1, bm_w2, bm_bytes, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
-        o_promo, o_fr, o_froff, o_reqoff, total;
+        o_promo, o_fr, o_froff, o_reqoff, o_ft0, o_ft1, o_vt, o_mt, o_lnext, total;
 };
 
 bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, Layout *Lo) {
     if (align == 0 || (align & (align - 1)) || arena == 0 || arena % align) return false;
-    if (policy < HEAP_FIRST_FIT || policy > HEAP_BUDDY) return false;
+    if (policy < HEAP_FIRST_FIT || policy > HEAP_SEGFIT_LIFO) return false;
     if (max_live == 0 || max_batch == 0 || max_batch >= (1ull << 31) || max_live >= (1ull << 30)) return false;
     Layout &L = *Lo;
     memset(&L, 0, sizeof(L));
@@ -105,6 +105,17 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.o_bm = take(L.bm_bytes);
         L.o_slot = take(tlsfw::MAX_NC * 4);
     }
+    if (policy == HEAP_SEGFIT_LIFO) {
+        L.o_cs = take(L.cap_f * 4);
+        L.o_ce = take(L.cap_f * 4);
+        L.o_ft0 = take(L.cap_f * 4);          // push stamps of the free pieces (double buffer)
+        L.o_ft1 = take(L.cap_f * 4);
+        L.o_vt = take(max_batch * 4);         // stamps of this batch's frees
+        L.o_mt = take(L.cap_m * 4);           // stamps of the merged array
+        L.o_lnext = take(L.cap_f * 4);        // spill-stack links
+        L.o_bk0 = take(L.cap_f * 8);          // (class, stamp) sort keys
+        L.o_bk1 = take(L.cap_f * 8);
+    }
     if (policy == HEAP_FIRST_FIT) {
         L.o_tree = take(L.ff_tree * 8);
         L.o_lvl = take(fits::FF_MAX_LEVELS * 8);
@@ -148,6 +159,7 @@ struct heap {
     u32 *kA, *kB, *vA, *vB, *flags, *pos, *hist, *tsum;
     u64 *vs, *ve, *vsc, *vec, *ms, *me, *r, *out;
     u32 *c, *off, *child, *sib, *cs, *ce, *bm, *slot;
+    u32 *ft[2], *vt, *mt, *lnext;             // SEGFIT_LIFO stamps and spill links
     u64 *tree, *lvl;
     u64 *bk[2];
     u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
@@ -191,6 +203,7 @@ __global__ void k_init(DevCtr *ctr, u64 *tbl, u64 tcap, u64 *fs, u64 *fe, u64 A_
             fs[0] = 0;      // the heap itself is the one free block (Alg. 6)
             fe[0] = A_u;
             ctr->F = 1;
+            ctr->lifo_clock = 1;
         } else {
             // greedy decomposition into maximal aligned power-of-two blocks (C13):
             // one block per set bit of A_u, largest first
@@ -404,7 +417,9 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     h->sms = sms;
     h->G = sms * 4;
-    if (cudaFuncSetAttribute(tlsfw::k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(tlsfw::k_engine<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(tlsfw::k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_free_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)buddy::FREE_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
@@ -428,6 +443,12 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     if (h->bm && cudaMemsetAsync(h->bm, 0, L.bm_bytes, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     h->tree = L.o_tree ? at<u64>(w, L.o_tree) : nullptr; h->lvl = L.o_lvl ? at<u64>(w, L.o_lvl) : nullptr;
     h->bk[0] = L.o_bk0 ? at<u64>(w, L.o_bk0) : nullptr; h->bk[1] = L.o_bk1 ? at<u64>(w, L.o_bk1) : nullptr;
+    if (policy == HEAP_SEGFIT_LIFO) {
+        h->ft[0] = at<u32>(w, L.o_ft0); h->ft[1] = at<u32>(w, L.o_ft1);
+        h->vt = at<u32>(w, L.o_vt); h->mt = at<u32>(w, L.o_mt); h->lnext = at<u32>(w, L.o_lnext);
+        // the initial whole-heap block was pushed at time 0; pushes of batches start at 1
+        if (cudaMemsetAsync(h->ft[0], 0, 4, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    }
     if (policy == HEAP_BUDDY) {
         h->dtm = at<u32>(w, L.o_dtm); h->dsrc = at<u32>(w, L.o_dsrc); h->baddr = at<u64>(w, L.o_baddr);
         h->btm = at<u32>(w, L.o_btm); h->bsrc = at<u32>(w, L.o_bsrc);
@@ -495,14 +516,22 @@ int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_strea
     LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->ve, h->flags, h->pos, &C->nk, h->vec);
     if (!bud) {
         // 4. merge path with the free array, 5. coalesce maximal runs
+        const bool lifo = h->policy == HEAP_SEGFIT_LIFO;
         TAG(h, HEAP_TAG_MERGE);
+        if (lifo)   // the valid frees are pushed in ascending address order: stamps clock + rank
+            LAUNCH(h, fits::k_free_stamps, h->G, 256, 0, s, &C->nv, C, h->vt);
         LAUNCH(h, prims::k_merge, h->G, prims::NT, 0, s, h->fs[cur], h->fe[cur], &C->F, h->vsc, h->vec, &C->nv,
-               h->ms, h->me, &C->M);
+               h->ms, h->me, &C->M, lifo ? h->ft[cur] : nullptr, lifo ? h->vt : nullptr, lifo ? h->mt : nullptr);
         TAG(h, HEAP_TAG_COALESCE);
         LAUNCH(h, fits::k_coal_flags, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags);
         scan(h, h->flags, h->pos, &C->M, &C->F, s);
         LAUNCH(h, fits::k_coal_write, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags, h->pos, h->fs[nxt],
                h->fe[nxt], L.cap_f, C);
+        if (lifo) {   // a coalesced run is pushed by its last free: the run's largest stamp
+            LAUNCH(h, fits::k_coal_stamp_head, h->G, 256, 0, s, h->mt, &C->M, h->flags, h->pos, h->ft[nxt], L.cap_f);
+            LAUNCH(h, fits::k_coal_stamp, h->G, 256, 0, s, h->mt, &C->M, h->flags, h->pos, h->ft[nxt], L.cap_f);
+            LAUNCH(h, fits::k_clock_add, 1, 1, 0, s, C, &C->nv, 0ull);
+        }
     } else {
         // 4b. group freed blocks by order, 5b. level-by-level buddy merge
         TAG(h, HEAP_TAG_BUDDY_FREE);
@@ -542,10 +571,28 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
         return HEAP_OK;
     }
-    const bool cls = (h->policy == HEAP_TLSF || h->policy == HEAP_SEGFIT);
+    const bool lifo = (h->policy == HEAP_SEGFIT_LIFO);
+    const bool cls = (h->policy == HEAP_TLSF || h->policy == HEAP_SEGFIT || lifo);
     TAG(h, HEAP_TAG_ALLOC_PREP);
     LAUNCH(h, fits::k_alloc_prep, h->G, 256, 0, s, (const u64 *)d_sizes, n, h->alog2, L.A_u, L.L, cls ? 1 : 0, h->r, h->c);
-    if (cls) {
+    if (lifo) {
+        // class-major, newest-push-first CSR (the bins as the paper's stacks), then the engine
+        TAG(h, HEAP_TAG_INDEX);
+        LAUNCH(h, fits::k_lifo_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], h->ft[cur], &C->F, h->bk[0], h->vA);
+        int rb = radix_sort<u64, true>(h, h->bk[0], h->bk[1], h->vA, h->vB, &C->F, 32 + ilog2((u64)L.NC) + 1, s);
+        u64 *sk = h->bk[rb];
+        u32 *sv = rb ? h->vB : h->vA;
+        LAUNCH(h, fits::k_u64_hi, h->G, 256, 0, s, sk, &C->F, h->kA);
+        LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kA, &C->F, L.NC, h->off);
+        LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs, h->ce);
+        TAG(h, HEAP_TAG_ENGINE);
+        tlsfw::Csr csr{sv, h->cs, h->ce};
+        tlsfw::Lifo lf{h->lnext, h->ft[cur], &C->lifo_clock};
+        LAUNCH(h, tlsfw::k_engine<true>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
+               h->c, n, h->out, nullptr, 0ull, 0ull, 0ull, h->slot, L.NC, L.L, C->eng, lf);
+        TAG(h, HEAP_TAG_INDEX);
+        LAUNCH(h, fits::k_clock_add, 1, 1, 0, s, C, (const u64 *)nullptr, (u64)n);
+    } else if (cls) {
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_cls_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.L, h->kA, h->vA);
         int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->F, ilog2((u64)L.NC) + 1, s);
@@ -554,8 +601,8 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs, h->ce);
         TAG(h, HEAP_TAG_ENGINE);
         tlsfw::Csr csr{sv, h->cs, h->ce};
-        LAUNCH(h, tlsfw::k_engine, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r, h->c,
-               n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng);
+        LAUNCH(h, tlsfw::k_engine<false>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
+               h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{});
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, tlsfw::k_bitheap_clear, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->slot, h->bm,
                L.bm_w0, L.bm_w1, L.bm_w2, L.NC, L.L);
@@ -590,6 +637,7 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
     scan(h, h->flags, h->pos, &C->F, &C->tmp[1], s);
     LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->fs[cur], h->flags, h->pos, &C->F, h->fs[nxt]);
     LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->fe[cur], h->flags, h->pos, &C->F, h->fe[nxt]);
+    if (lifo) LAUNCH(h, fits::k_compact<u32>, h->G, 256, 0, s, h->ft[cur], h->flags, h->pos, &C->F, h->ft[nxt]);
     LAUNCH(h, k_set_F, 1, 1, 0, s, C);
     TAG(h, HEAP_TAG_FINISH);
     LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,

@@ -156,7 +156,10 @@ constexpr int MIPT = 8;
 __global__ void __launch_bounds__(NT) k_merge(const u64 *__restrict__ as, const u64 *__restrict__ ae,
                                               const u64 *na_dev, const u64 *__restrict__ bs,
                                               const u64 *__restrict__ be, const u64 *nb_dev,
-                                              u64 *__restrict__ os, u64 *__restrict__ oe, u64 *total) {
+                                              u64 *__restrict__ os, u64 *__restrict__ oe, u64 *total,
+                                              const u32 *__restrict__ at = nullptr,
+                                              const u32 *__restrict__ bt = nullptr, u32 *__restrict__ ot = nullptr) {
+    // at/bt/ot: optional per-block payload merged alongside (push stamps of SEGFIT_LIFO)
     const u64 na = *na_dev, nb = *nb_dev, n = na + nb;
     if (blockIdx.x == 0 && threadIdx.x == 0 && total) *total = n;
     const u64 nchunks = (n + MIPT - 1) / MIPT;
@@ -173,8 +176,8 @@ __global__ void __launch_bounds__(NT) k_merge(const u64 *__restrict__ as, const 
             u64 o = diag + k;
             if (o >= n) break;
             bool take_a = (j >= nb) || (i < na && as[i] <= bs[j]);
-            if (take_a) { os[o] = as[i]; oe[o] = ae[i]; i++; }
-            else { os[o] = bs[j]; oe[o] = be[j]; j++; }
+            if (take_a) { os[o] = as[i]; oe[o] = ae[i]; if (ot) ot[o] = at[i]; i++; }
+            else { os[o] = bs[j]; oe[o] = be[j]; if (ot) ot[o] = bt[j]; j++; }
         }
     }
 }

@@ -96,6 +96,9 @@ SMALL = [
     (tg.TLSF, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
     (tg.BUDDY, 1 << 24, 64, 3000, 40000, (6, 16), (1, 2), 1),
     (tg.TLSF, (1 << 22) + 48, 16, 5000, 60000, (4, 12), (1, 3), 0),     # non power-of-two arena
+    (tg.SEGFIT_LIFO, 1 << 16, 16, 24, 1500, (4, 10), (1, 2), 0),        # the paper's stack bins
+    (tg.SEGFIT_LIFO, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
+    (tg.SEGFIT_LIFO, 1 << 28, 16, 16384, 200000, (4, 12), (2, 5), 0),
     (tg.BUDDY, (1 << 20) + (1 << 14) + 256, 256, 700, 9000, (8, 18), (1, 2), 1),
 ]
 
@@ -105,7 +108,7 @@ def test_small_every_batch(case):
     pol, arena, align, batch, ops, sizes, rho, kind = case
     cfg = tg.custom(pol, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes, size_kind=kind,
                     idx=60 + pol)
-    run_parity(cfg, max_live=1 << 15, max_batch=batch, every_batch_state=batch < 100)
+    run_parity(cfg, max_live=max(1 << 15, 8 * batch), max_batch=batch, every_batch_state=batch < 100)
 
 
 def test_config1_exact():
@@ -138,7 +141,7 @@ def test_config5_first_batches():
 def test_edge_cases():
     """Empty batches, NULL / interior / unaligned / out-of-range / duplicate frees,
     zero and oversize requests, OOM in a tiny arena, the last unit of a 2^32-unit arena."""
-    for pol in (1, 2, 3, 4, 5):
+    for pol in (1, 2, 3, 4, 5, 6):
         arena, align = 1 << 12, 16
         g = Gpu(arena, align, pol, 256, 64)
         o = OracleL(arena, align, pol)

@@ -18,11 +18,11 @@ import pytest
 
 import tracegen as tg
 from oracle import OracleL, insert_class, search_class
-from oracle.oracle_b import OracleB, cls_lo, cls_of, search_cls
+from oracle.oracle_b import OracleB, OracleBLifo, cls_lo, cls_of, search_cls
 from tests.helpers import HEAP_NULL, IdMap, check_invariants, parse_golden, replay
 
 FIT_POLICIES = [1, 2, 3, 4]
-ALL_POLICIES = [1, 2, 3, 4, 5]
+ALL_POLICIES = [1, 2, 3, 4, 5, 6]
 
 
 def run_case(H, case):
@@ -38,7 +38,7 @@ def run_case(H, case):
 def test_golden_examples(case):
     impls = [OracleL]
     if case["arena"] // case["align"] <= 1 << 16:
-        impls.append(OracleB)
+        impls.append(OracleBLifo if case["policy"] == 6 else OracleB)
     for H in impls:
         h, outs = run_case(H, case)
         assert outs == case["outs"], (H.__name__, case["cite"])
@@ -197,7 +197,7 @@ def test_free_classification():
 def _run_both(policy, arena, align, batch, ops, sizes, rho, idx, size_kind=0):
     cfg = tg.custom(policy, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes,
                     size_kind=size_kind, idx=idx)
-    hl, hb = OracleL(arena, align, policy), OracleB(arena, align, policy)
+    hl, hb = OracleL(arena, align, policy), _twin(policy)(arena, align, policy)
     im_l, im_b = IdMap(ops), IdMap(ops)
     for bi, (fids, sz, first) in enumerate(tg.Trace(cfg)):
         ol, ob = im_l.offsets(fids), im_b.offsets(fids)
@@ -264,8 +264,8 @@ def test_exhaustive_tiny_heaps(policy):
             yield from leaves(depth - 1, seq + [("f", o)], hb2)
 
     n = 0
-    for seq in leaves(4, [], OracleB(A, 1, policy)):
-        hl, hb = OracleL(A, 1, policy), OracleB(A, 1, policy)
+    for seq in leaves(4, [], _twin(policy)(A, 1, policy)):
+        hl, hb = OracleL(A, 1, policy), _twin(policy)(A, 1, policy)
         for op, v in seq:
             if op == "a":
                 assert int(hl.alloc_batch([v])[0]) == int(hb.alloc_batch([v])[0]), seq
@@ -279,7 +279,18 @@ def test_exhaustive_tiny_heaps(policy):
     assert n > 1000
 
 
+def _twin(policy):
+    return OracleBLifo if policy == 6 else OracleB
+
+
 def _clone_b(h):
+    if isinstance(h, OracleBLifo):
+        c = OracleBLifo.__new__(OracleBLifo)
+        c.__dict__.update(h.__dict__)
+        c.free = [list(b) for b in h.free]
+        c.live = dict(h.live)
+        c.counts = dict(h.counts)
+        return c
     c = OracleB.__new__(OracleB)
     c.__dict__.update(h.__dict__)
     c.bits = h.bits.copy()
@@ -334,3 +345,27 @@ def test_free_order_independence():
                 h.free_batch([o])
             got = h.export()
             assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_lifo_differs_from_address_order_and_fragments_more():
+    """The paper's segregated fit (LIFO bins) and our address-ordered reading (C9) diverge on
+    the paper's own workload shape (malloc-large: 1 KiB-16 MiB), and TLSF
+    fragments less than segregated fit ("A Two-Level Segregated Fit allocator would see
+    improved fragmentation").  Fragmentation = 1 - live / high-water."""
+    frag = {}
+    outs = {}
+    for pol in (6, 3, 4):
+        cfg = tg.Config(95, "malloc-large", pol, 1 << 36, 1024, 1, 0, 1, 2, 5000, 0, 10, 24, n_slots=1000)
+        h = OracleL(cfg.arena_bytes, cfg.align, pol)
+        im, fr, allout = IdMap(6000), [], []
+        for fids, sz, first in tg.Trace(cfg, batch=2):      # one step (free, alloc) per batch
+            h.free_batch(im.offsets(fids))
+            out = h.alloc_batch(sz)
+            im.record(first, out)
+            allout.append(out)
+            st = h.stats()
+            fr.append(1 - st["live_bytes"] / max(st["high_water_end"], 1))
+        frag[pol] = float(np.mean(fr[len(fr) // 2:]))
+        outs[pol] = np.concatenate(allout)
+    assert not np.array_equal(outs[6], outs[3])
+    assert frag[4] < frag[3] and frag[4] < frag[6]

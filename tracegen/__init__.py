@@ -30,7 +30,7 @@ _LIB = os.path.join(_HERE, "libtracegen.so")
 HEAP_NULL = (1 << 64) - 1
 
 # policy ids (numbers only; the meaning lives in include/heap.h and oracle/)
-FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY = 1, 2, 3, 4, 5
+FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY, SEGFIT_LIFO = 1, 2, 3, 4, 5, 6
 
 
 @dataclass(frozen=True)
@@ -110,7 +110,10 @@ class Trace:
         self.cfg = cfg
         self.batch = batch if batch is not None else cfg.batch
         ops = cfg.total_ops if total_ops is None else total_ops
-        self.max_n = max(self.batch, 1) if cfg.model == 0 else max(ops, 1)
+        if cfg.model == 0:
+            self.max_n = max(self.batch, 1)
+        else:   # slot model: `batch` caps a batch's ops (2 = one step per batch)
+            self.max_n = max(batch, 1) if batch is not None else max(ops, 1)
         L = lib()
         self._h = L.tg_create(cfg.model, cfg.seed(rank), self.batch, cfg.rho_num, cfg.rho_den,
                               ops, cfg.size_kind, cfg.a, cfg.b, cfg.n_slots)
