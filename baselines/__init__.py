@@ -45,3 +45,23 @@ def replay(mode, batches, max_ops=10**6, max_seconds=60.0):
     return {"value": ops.value / sec.value if sec.value else None, "unit": "ops/s", "ops": ops.value,
             "seconds": sec.value, "failed": fail.value,
             "capped": bool(ops.value < int(ao[-1] + fo[-1]))}
+
+
+def replay_latency(mode, kind, arg):
+    """Per-op host latency (ns) and process device-memory use after each op for the
+    batch-size-1 study.  kind: uint8 [n] (0 free id / 1 alloc bytes), arg: uint64 [n]."""
+    L = ctypes.CDLL(build())
+    kind = np.ascontiguousarray(kind, dtype=np.uint8)
+    arg = np.ascontiguousarray(arg, dtype=np.uint64)
+    n = len(kind)
+    lat = np.zeros(n, dtype=np.float64)
+    used = np.zeros(n, dtype=np.uint64)
+    fail = ctypes.c_uint64(0)
+    L.replay_latency.restype = ctypes.c_int
+    rc = L.replay_latency(mode, ctypes.c_uint64(n), kind.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                          arg.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                          lat.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                          used.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(fail))
+    if rc != 0:
+        raise RuntimeError(f"replay_latency rc {rc}")
+    return lat, used, int(fail.value)
