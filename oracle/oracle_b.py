@@ -258,3 +258,97 @@ class OracleBLifo:
         lp = np.array(sorted((s * self.align, z * self.align) for s, z in self.live.items()),
                       dtype=np.uint64).reshape(-1, 2)
         return fp, lp
+
+
+class OracleBHybrid:
+    """Brute-force twin of Oracle-L's HYBRID (§5.3).
+
+    The pools are kept literally as the paper's bitmasks (§3.2): one numpy
+    boolean per object, True = free; an allocation takes the first True (np.flatnonzero) and a
+    free sets it back.  Requests the pools do not take go to an OracleB TLSF heap (unit bitmap,
+    blocks derived on every call) covering [pool_end, arena).  The layout is recomputed here from
+    the words of DESIGN.md reading C26, not from Oracle-L's code."""
+
+    PAGE = 4096
+
+    def __init__(self, arena_bytes: int, align: int, policy: int = 7):
+        assert policy == 7
+        self.align, self.arena = align, arena_bytes
+        self.obj = [align << j for j in range(64) if (align << j) <= self.PAGE]
+        share = arena_bytes // (2 * len(self.obj)) if self.obj else 0
+        self.S = share - share % self.PAGE
+        self.pool_end = len(self.obj) * self.S
+        self.pools = [np.ones(self.S // o, dtype=bool) for o in self.obj]
+        self.sub = OracleB(arena_bytes - self.pool_end, align, TLSF)
+        self.own = dict(allocs_ok=0, frees_ok=0, frees_invalid=0, frees_double=0, frees_null=0)
+
+    @property
+    def counts(self):
+        c = dict(self.sub.counts)
+        for k, v in self.own.items():
+            c[k] = c.get(k, 0) + v
+        return c
+
+    @property
+    def live(self):        # for the exhaustive enumerations: every live start (bytes)
+        return [int(o) for o, _ in self.export()[1]]
+
+    def alloc_batch(self, sizes):
+        out = np.empty(len(sizes), dtype=np.uint64)
+        for i, s in enumerate(int(x) for x in sizes):
+            fits = [j for j, o in enumerate(self.obj) if o >= s]
+            if 0 < s < self.PAGE and fits:
+                j = fits[0]
+                free = np.flatnonzero(self.pools[j])
+                if len(free):
+                    t = int(free[0])
+                    self.pools[j][t] = False
+                    out[i] = j * self.S + t * self.obj[j]
+                    self.own["allocs_ok"] += 1
+                    continue
+            o = int(self.sub.alloc_batch(np.array([s], dtype=np.uint64))[0])
+            out[i] = HEAP_NULL if o == HEAP_NULL else o + self.pool_end
+        return out
+
+    def free_batch(self, offsets):
+        sub, seen, to_free = [], set(), []
+        for o in sorted(int(x) for x in offsets):
+            if o == HEAP_NULL:
+                self.own["frees_null"] += 1
+            elif o >= self.pool_end:
+                sub.append(o - self.pool_end)
+            else:
+                j = o // self.S
+                rel = o - j * self.S
+                if rel % self.obj[j]:
+                    self.own["frees_invalid"] += 1
+                    continue
+                t = rel // self.obj[j]
+                if self.pools[j][t] or (j, t) in seen:
+                    self.own["frees_double"] += 1
+                else:
+                    seen.add((j, t))
+                    to_free.append((j, t))
+                    self.own["frees_ok"] += 1
+        for j, t in to_free:
+            self.pools[j][t] = True
+        self.sub.free_batch(np.array(sub, dtype=np.uint64))
+
+    def export(self):
+        fp, lp = [], []
+        for j, (o, bits) in enumerate(zip(self.obj, self.pools)):
+            base = j * self.S
+            t = 0
+            while t < len(bits):
+                if not bits[t]:
+                    lp.append((base + t * o, o))
+                    t += 1
+                    continue
+                a = t
+                while t < len(bits) and bits[t]:
+                    t += 1
+                fp.append((base + a * o, (t - a) * o))
+        sf, sl = self.sub.export()
+        fp += [(int(s) + self.pool_end, int(z)) for s, z in sf]
+        lp += [(int(s) + self.pool_end, int(z)) for s, z in sl]
+        return (np.array(fp, dtype=np.uint64).reshape(-1, 2), np.array(lp, dtype=np.uint64).reshape(-1, 2))

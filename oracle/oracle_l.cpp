@@ -26,6 +26,12 @@
  *       SEGFIT_LIFO the paper's segregated fit verbatim: power-of-two bins used as stacks —
  *                  alloc pops the head (newest push) of the first nonempty bin >= ceil(log2 r),
  *                  every free / remainder is pushed at the head of its bin (Alg. 4/5)
+ *       HYBRID     §5.3's hybrid: requests below a page (0 < s < 4096 B) go
+ *                  to object pools managed by bitmasks (§3.2) — pool j holds
+ *                  objects of align*2^j bytes, an allocation takes the pool's lowest free slot
+ *                  (first fit over the bitmask), a full pool falls back to the segregated-fit
+ *                  heap — and everything else to a TLSF heap on the rest of the arena
+ *                  (layout: DESIGN.md reading C26)
  *   - batch driver (canonical order, BASELINE.json north_star): a free batch classifies every
  *     offset against the batch-start state, then frees the valid ones in ascending address
  *     order; an alloc batch serves requests in request order, HEAP_NULL on failure.
@@ -44,7 +50,8 @@
 namespace {
 
 const uint64_t HEAP_NULL = ~0ull;
-enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6 };
+enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6, HYBRID = 7 };
+const uint64_t PAGE = 4096;   /* "allocations smaller than a page (<4kB)" */
 
 /* floor(log2 u) for u >= 1, written as a plain loop */
 int floor_log2(uint64_t u) {
@@ -90,6 +97,27 @@ struct Heap {
     std::vector<std::set<uint64_t>> bfree;                /* BUDDY: free starts per order */
     int K = 0;                                            /* BUDDY: max order */
     Counters c;
+    /* HYBRID: J pools of S bytes each at [j*S, (j+1)*S), then the TLSF heap `sub` on
+     * [pool_end, arena).  A pool's bitmask is kept as "every slot >= fresh[j] is free" plus the
+     * set of free slots below fresh[j]; its lowest free slot is min(freed.begin(), fresh). */
+    int J = 0;
+    uint64_t S = 0, pool_end = 0;
+    std::vector<uint64_t> fresh, nslots;
+    std::vector<std::set<uint64_t>> freed;
+    uint64_t pool_live_n = 0, pool_live_b = 0;
+    Heap *sub = nullptr;
+    ~Heap() { delete sub; }
+
+    bool slot_free(int j, uint64_t t) const { return t >= fresh[j] || freed[j].count(t); }
+    /* lowest free slot of pool j, or HEAP_NULL when the pool is full */
+    uint64_t pool_lowest_free(int j) const {
+        if (!freed[j].empty()) return *freed[j].begin();
+        return fresh[j] < nslots[j] ? fresh[j] : HEAP_NULL;
+    }
+    void pool_take(int j, uint64_t t) {
+        if (t == fresh[j]) fresh[j]++;
+        else freed[j].erase(t);
+    }
 
     /* ---- free-list edits (keep the class index in step) ---- */
     void free_insert(uint64_t s, uint64_t z) {
@@ -217,7 +245,26 @@ extern "C" {
 
 void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
     if (align == 0 || (align & (align - 1)) || arena_bytes == 0 || arena_bytes % align) return nullptr;
-    if (policy < FIRST_FIT || policy > SEGFIT_LIFO) return nullptr;
+    if (policy < FIRST_FIT || policy > HYBRID) return nullptr;
+    if (policy == HYBRID) {
+        /* reading C26: pool classes align*2^j <= PAGE; the first half of the arena is split
+         * evenly between the pools, each share rounded down to a whole number of pages */
+        Heap *h = new Heap();
+        h->policy = HYBRID;
+        h->align = align;
+        h->arena_bytes = arena_bytes;
+        h->A_u = arena_bytes / align;
+        for (uint64_t o = align; o <= PAGE; o <<= 1) h->J++;
+        if (h->J) h->S = arena_bytes / (2 * (uint64_t)h->J) / PAGE * PAGE;
+        h->pool_end = (uint64_t)h->J * h->S;
+        for (int j = 0; j < h->J; j++) {
+            h->nslots.push_back(h->S / (align << j));
+            h->fresh.push_back(0);
+            h->freed.emplace_back();
+        }
+        h->sub = (Heap *)oracle_create(arena_bytes - h->pool_end, align, TLSF);
+        return h;
+    }
     Heap *h = new Heap();
     h->policy = policy;
     h->L = (policy == TLSF) ? 5 : 0;
@@ -247,8 +294,37 @@ void oracle_destroy(void *p) { delete (Heap *)p; }
  * in ascending address order.  Classification (reading C16):
  *   HEAP_NULL -> null; unaligned / out of range / neither live nor free start -> invalid;
  *   live start -> first copy frees, other copies double; start of a free block -> double. */
+void oracle_free_batch(void *p, const uint64_t *offsets, uint64_t n);
+
+/* HYBRID frees: the same per-copy classification; a pool offset must be a slot start of its
+ * pool (a multiple of the object size inside the pool's share) — an allocated slot frees
+ * (its bit returns to one), a free slot is a double free; every offset at or
+ * above pool_end is the TLSF heap's, relative to pool_end. */
+static void hybrid_free_batch(Heap *h, const uint64_t *offsets, uint64_t n) {
+    std::vector<uint64_t> v(offsets, offsets + n);
+    std::sort(v.begin(), v.end());
+    std::vector<uint64_t> sub_offs;
+    for (uint64_t i = 0; i < n; i++) {
+        uint64_t o = v[i];
+        bool dup = (i > 0 && v[i - 1] == o);
+        if (o == HEAP_NULL) { h->c.frees_null++; continue; }
+        if (o >= h->pool_end) { sub_offs.push_back(o - h->pool_end); continue; }
+        int j = (int)(o / h->S);
+        uint64_t rel = o % h->S, oj = h->align << j;
+        if (rel % oj) { h->c.frees_invalid++; continue; }
+        uint64_t t = rel / oj;
+        if (h->slot_free(j, t) || dup) { h->c.frees_double++; continue; }
+        h->c.frees_ok++;
+        h->freed[j].insert(t);
+        h->pool_live_n--;
+        h->pool_live_b -= oj;
+    }
+    oracle_free_batch(h->sub, sub_offs.data(), sub_offs.size());
+}
+
 void oracle_free_batch(void *p, const uint64_t *offsets, uint64_t n) {
     Heap *h = (Heap *)p;
+    if (h->policy == HYBRID) { hybrid_free_batch(h, offsets, n); return; }
     std::vector<uint64_t> v(offsets, offsets + n);
     std::sort(v.begin(), v.end());
     std::vector<uint64_t> to_free;
@@ -272,6 +348,32 @@ void oracle_free_batch(void *p, const uint64_t *offsets, uint64_t n) {
 
 void oracle_alloc_batch(void *p, const uint64_t *sizes, uint64_t n, uint64_t *out) {
     Heap *h = (Heap *)p;
+    if (h->policy == HYBRID) {
+        /* request order; a sub-page request takes the lowest free slot of the smallest pool whose
+         * objects hold it, else (pool full, or s >= PAGE, or s = 0) the TLSF heap serves it */
+        for (uint64_t i = 0; i < n; i++) {
+            uint64_t s = sizes[i];
+            if (s > 0 && s < PAGE && h->J > 0) {
+                int j = 0;
+                while ((h->align << j) < s) j++;
+                uint64_t t = h->pool_lowest_free(j);
+                if (t != HEAP_NULL) {
+                    uint64_t oj = h->align << j;
+                    h->pool_take(j, t);
+                    out[i] = (uint64_t)j * h->S + t * oj;
+                    h->pool_live_n++;
+                    h->pool_live_b += oj;
+                    h->c.allocs_ok++;
+                    h->c.high_water_end = std::max(h->c.high_water_end, out[i] + oj);
+                    continue;
+                }
+            }
+            uint64_t o = HEAP_NULL;
+            oracle_alloc_batch(h->sub, &s, 1, &o);
+            out[i] = (o == HEAP_NULL) ? HEAP_NULL : o + h->pool_end;
+        }
+        return;
+    }
     for (uint64_t i = 0; i < n; i++) {
         uint64_t s = sizes[i];
         uint64_t r = s / h->align + (s % h->align != 0);     /* ceil(s / align) */
@@ -296,8 +398,37 @@ void oracle_alloc_batch(void *p, const uint64_t *sizes, uint64_t n, uint64_t *ou
 }
 
 /* stats in the heap_stats_t field order (include/heap.h): 16 x u64, bytes */
+/* maximal runs of free slots of pool j as (first slot, count) — "coalescence is implicit" in a
+ * bitmask; runs never cross a pool boundary */
+static std::vector<std::pair<uint64_t, uint64_t>> pool_runs(const Heap *h, int j) {
+    std::vector<std::pair<uint64_t, uint64_t>> runs;
+    uint64_t t = 0, N = h->nslots[j];
+    while (t < N) {
+        if (!h->slot_free(j, t)) { t++; continue; }
+        uint64_t a = t;
+        while (t < N && h->slot_free(j, t)) t++;
+        runs.push_back({a, t - a});
+    }
+    return runs;
+}
+
 void oracle_stats(void *p, uint64_t *o) {
     Heap *h = (Heap *)p;
+    if (h->policy == HYBRID) {
+        /* pools + TLSF heap; largest_free is the TLSF heap's (reading C26); counters add up */
+        uint64_t sv[16];
+        oracle_stats(h->sub, sv);
+        uint64_t runs = 0;
+        for (int j = 0; j < h->J; j++) runs += pool_runs(h, j).size();
+        uint64_t live_b = h->pool_live_b + sv[2];
+        uint64_t hw = std::max(h->c.high_water_end, sv[7] ? sv[7] + h->pool_end : 0);
+        uint64_t vals[16] = {h->arena_bytes, h->align, live_b, h->arena_bytes - live_b, h->pool_live_n + sv[4],
+                             runs + sv[5], sv[6], hw, h->c.allocs_ok + sv[8], h->c.allocs_failed + sv[9],
+                             h->c.frees_ok + sv[10], h->c.frees_invalid + sv[11], h->c.frees_double + sv[12],
+                             h->c.frees_null + sv[13], 0, 0};
+        memcpy(o, vals, sizeof(vals));
+        return;
+    }
     uint64_t live_b = 0, free_b = 0, nfree = 0, largest = 0;
     for (const auto &kv : h->live) live_b += kv.second;
     if (h->policy == BUDDY) {
@@ -321,6 +452,27 @@ void oracle_stats(void *p, uint64_t *o) {
 void oracle_export(void *p, uint64_t *free_pairs, uint64_t cap_free, uint64_t *live_pairs,
                    uint64_t cap_live, uint64_t *counts) {
     Heap *h = (Heap *)p;
+    if (h->policy == HYBRID) {
+        /* pool runs / objects first (they lie below pool_end), then the TLSF heap's, shifted */
+        std::vector<uint64_t> fp, lp;
+        for (int j = 0; j < h->J; j++) {
+            uint64_t oj = h->align << j, base = (uint64_t)j * h->S;
+            for (auto &r : pool_runs(h, j)) { fp.push_back(base + r.first * oj); fp.push_back(r.second * oj); }
+            for (uint64_t t = 0; t < h->fresh[j]; t++)
+                if (!h->freed[j].count(t)) { lp.push_back(base + t * oj); lp.push_back(oj); }
+        }
+        uint64_t sc[2];
+        oracle_export(h->sub, nullptr, 0, nullptr, 0, sc);
+        std::vector<uint64_t> sf(2 * sc[0] + 2), sl(2 * sc[1] + 2);
+        oracle_export(h->sub, sf.data(), sc[0], sl.data(), sc[1], sc);
+        for (uint64_t k = 0; k < sc[0]; k++) { fp.push_back(sf[2 * k] + h->pool_end); fp.push_back(sf[2 * k + 1]); }
+        for (uint64_t k = 0; k < sc[1]; k++) { lp.push_back(sl[2 * k] + h->pool_end); lp.push_back(sl[2 * k + 1]); }
+        counts[0] = fp.size() / 2;
+        counts[1] = lp.size() / 2;
+        for (uint64_t k = 0; k < counts[0] && k < cap_free; k++) { free_pairs[2 * k] = fp[2 * k]; free_pairs[2 * k + 1] = fp[2 * k + 1]; }
+        for (uint64_t k = 0; k < counts[1] && k < cap_live; k++) { live_pairs[2 * k] = lp[2 * k]; live_pairs[2 * k + 1] = lp[2 * k + 1]; }
+        return;
+    }
     uint64_t a = h->align, i = 0;
     if (h->policy == BUDDY) {
         std::map<uint64_t, uint64_t> all;

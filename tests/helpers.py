@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HEAP_NULL = (1 << 64) - 1
-POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6}
+POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6, "HYBRID": 7}
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
@@ -49,8 +49,18 @@ def replay(heap, trace, idmap: IdMap | None = None, on_batch=None, max_batches=N
     return idmap
 
 
-def check_invariants(free_pairs, live_pairs, arena: int, align: int, buddy: bool):
-    """I1 no overlap, I2 tiling/conservation, I3 full coalescing, I4 alignment."""
+def hybrid_layout(arena: int, align: int):
+    """(share S, pool_end, object sizes) of a HYBRID heap, reading C26."""
+    obj = [align << j for j in range(64) if (align << j) <= 4096]
+    share = arena // (2 * len(obj)) if obj else 0
+    S = share - share % 4096
+    return S, len(obj) * S, obj
+
+
+def check_invariants(free_pairs, live_pairs, arena: int, align: int, buddy: bool, region_edges=()):
+    """I1 no overlap, I2 tiling/conservation, I3 full coalescing, I4 alignment.
+    ``region_edges``: addresses where two free blocks may touch (HYBRID pool boundaries: pools
+    and the TLSF heap never coalesce with each other)."""
     fp = np.asarray(free_pairs, dtype=np.uint64).reshape(-1, 2)
     lp = np.asarray(live_pairs, dtype=np.uint64).reshape(-1, 2)
     allb = np.concatenate([np.c_[fp, np.zeros(len(fp), np.uint64)],
@@ -72,7 +82,9 @@ def check_invariants(free_pairs, live_pairs, arena: int, align: int, buddy: bool
     if len(fp):
         fps = fp[np.argsort(fp[:, 0])]
         if not buddy:
-            assert np.all(fps[:-1, 0] + fps[:-1, 1] != fps[1:, 0]), "adjacent free blocks"
+            touch = fps[:-1, 0] + fps[:-1, 1] == fps[1:, 0]
+            edges = np.array(sorted(region_edges), dtype=np.uint64)
+            assert np.all(~touch | np.isin(fps[1:, 0], edges)), "adjacent free blocks"
         else:
             sz = fps[:, 1]
             assert np.all(sz & (sz - 1) == 0)

@@ -18,8 +18,10 @@ import pytest
 
 import tracegen as tg
 from oracle import OracleL, insert_class, search_class
-from oracle.oracle_b import OracleB, OracleBLifo, cls_lo, cls_of, search_cls
-from tests.helpers import HEAP_NULL, IdMap, check_invariants, parse_golden, replay
+import copy
+
+from oracle.oracle_b import OracleB, OracleBHybrid, OracleBLifo, cls_lo, cls_of, search_cls
+from tests.helpers import HEAP_NULL, IdMap, check_invariants, hybrid_layout, parse_golden, replay
 
 FIT_POLICIES = [1, 2, 3, 4]
 ALL_POLICIES = [1, 2, 3, 4, 5, 6]
@@ -38,7 +40,7 @@ def run_case(H, case):
 def test_golden_examples(case):
     impls = [OracleL]
     if case["arena"] // case["align"] <= 1 << 16:
-        impls.append(OracleBLifo if case["policy"] == 6 else OracleB)
+        impls.append(_twin(case["policy"]))
     for H in impls:
         h, outs = run_case(H, case)
         assert outs == case["outs"], (H.__name__, case["cite"])
@@ -211,7 +213,7 @@ def _run_both(policy, arena, align, batch, ops, sizes, rho, idx, size_kind=0):
         fl, ll = hl.export()
         fb, lb = hb.export()
         assert np.array_equal(fl, fb) and np.array_equal(ll, lb), (policy, bi)
-        check_invariants(fl, ll, arena, align, policy == tg.BUDDY)
+        check_invariants(fl, ll, arena, align, policy == tg.BUDDY, _edges(policy, arena, align))
     st = hl.stats()
     for k, v in hb.counts.items():
         assert st[k] == v, k
@@ -280,7 +282,14 @@ def test_exhaustive_tiny_heaps(policy):
 
 
 def _twin(policy):
-    return OracleBLifo if policy == 6 else OracleB
+    return {6: OracleBLifo, 7: OracleBHybrid}.get(policy, OracleB)
+
+
+def _edges(policy, arena, align):
+    if policy != 7:
+        return ()
+    S, pool_end, obj = hybrid_layout(arena, align)
+    return tuple(j * S for j in range(1, len(obj) + 1)) if S else ()
 
 
 def _clone_b(h):
@@ -369,3 +378,75 @@ def test_lifo_differs_from_address_order_and_fragments_more():
         outs[pol] = np.concatenate(allout)
     assert not np.array_equal(outs[6], outs[3])
     assert frag[4] < frag[3] and frag[4] < frag[6]
+
+
+# ---------------- HYBRID (§5.3 pools + TLSF; reading C26) ----------------
+
+@pytest.mark.parametrize("seed", range(4))
+def test_hybrid_oracle_l_equals_oracle_b(seed):
+    """Sizes LU8[16 B, 16 KiB): most requests go to the pools, the rest (and pool overflow,
+    forced by the small shares) to the TLSF heap; Oracle-L == the bitmask twin everywhere."""
+    _run_both(7, 1 << 18, 16, 48, 3000, (4, 14), (2, 5) if seed % 2 else (1, 3), 90 + seed)
+
+
+def test_hybrid_layout_and_classification():
+    """The layout read from C26 (share = half the arena split over the pools, whole pages) and
+    the free taxonomy on pool offsets: interior of an object -> invalid, free slot -> double,
+    second copy -> double, TLSF-region rules unchanged."""
+    S, pool_end, obj = hybrid_layout(1 << 20, 16)
+    assert (S, pool_end, obj[0], obj[-1], len(obj)) == (57344, 516096, 16, 4096, 9)
+    assert hybrid_layout(1 << 16, 16)[0] == 0               # too small for a page per pool
+    for H in (OracleL, OracleBHybrid):
+        h = H(1 << 20, 16, 7)
+        a = [int(x) for x in h.alloc_batch([16, 16, 100, 5000])]
+        assert a == [0, 16, 3 * S, pool_end]
+        h.free_batch(np.array([HEAP_NULL, 8, 16, 16, 32, 3 * S + 64, 3 * S, pool_end + 16, 1 << 21,
+                               pool_end], dtype=np.uint64))
+        c = h.stats() if H is OracleL else h.counts
+        assert (c["frees_null"], c["frees_ok"], c["frees_double"], c["frees_invalid"]) == (1, 3, 2, 4), H
+        fp, lp = h.export()
+        assert [tuple(int(v) for v in p) for p in lp] == [(0, 16)]
+        assert int(h.alloc_batch([1])[0]) == 16              # lowest free slot again
+    h = OracleL(1 << 16, 16, 7)                             # no pools: plain TLSF
+    t = OracleL(1 << 16, 16, 4)
+    sz = np.array([100, 16, 3000, 5], dtype=np.uint64)
+    assert np.array_equal(h.alloc_batch(sz), t.alloc_batch(sz))
+
+
+def test_hybrid_exhaustive_tiny():
+    """Every sequence of <= 4 ops (alloc of 8 sizes spanning every pool, the pool/TLSF edge and
+    OOM, or free of any live block) on a 24 KiB heap with 1 KiB alignment: pools of 4 x 1 KiB,
+    2 x 2 KiB, 1 x 4 KiB and a 12 KiB TLSF heap.  Oracle-L == Oracle-B on every output/state."""
+    arena, align = 24576, 1024
+    sizes = [1, 1024, 1025, 2049, 4095, 4096, 5000, 12288]
+
+    def leaves(depth, seq, hb):
+        yield seq
+        if depth == 0:
+            return
+        for s in sizes:
+            hb2 = copy.deepcopy(hb)
+            hb2.alloc_batch([s])
+            yield from leaves(depth - 1, seq + [("a", s)], hb2)
+        for o in hb.live:
+            hb2 = copy.deepcopy(hb)
+            hb2.free_batch([o])
+            yield from leaves(depth - 1, seq + [("f", o)], hb2)
+
+    n = 0
+    for seq in leaves(4, [], OracleBHybrid(arena, align)):
+        hl, hb = OracleL(arena, align, 7), OracleBHybrid(arena, align)
+        for op, v in seq:
+            if op == "a":
+                assert int(hl.alloc_batch([v])[0]) == int(hb.alloc_batch([v])[0]), seq
+            else:
+                hl.free_batch([v])
+                hb.free_batch([v])
+        fl, ll = hl.export()
+        fb, lb = hb.export()
+        assert np.array_equal(fl, fb) and np.array_equal(ll, lb), seq
+        st = hl.stats()
+        assert st["n_free"] == len(fl) and st["n_live"] == len(ll)
+        assert st["live_bytes"] + st["free_bytes"] == arena
+        n += 1
+    assert n > 4000
