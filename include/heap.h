@@ -60,10 +60,22 @@ enum heap_policy {
                            of two), min (bin, address) over bin >= search PAPER.md:447-458 */
     HEAP_BUDDY = 5,     /* binary buddy, min order then address; align is
                            the minimum block */
-    HEAP_SEGFIT_LIFO = 6 /* the paper's segregated fit verbatim: power-of-two
+    HEAP_SEGFIT_LIFO = 6, /* the paper's segregated fit verbatim: power-of-two
                            bins as stacks — an alloc pops the head (most recent
                            push) of the first nonempty bin >= ceil(log2 r); frees
                            and split remainders are pushed at the head      Alg. 4/5 */
+    HEAP_HYBRID = 7     /* §5.3 hybrid: requests of 0 < s < 4096 B
+                           take the LOWEST free slot of a bitmask object pool
+                           (§3.2) of align*2^j-byte objects, the
+                           smallest that holds s; a full pool and every other
+                           request use a TLSF heap.  Layout (C26): the
+                           pools share the first half of the arena evenly, each a
+                           whole number of 4 KiB pages; the TLSF heap covers the rest.
+                           A pool offset frees iff it is an allocated slot start.
+                           heap_stats: n_free counts maximal runs of free pool slots
+                           plus TLSF free blocks; largest_free is the TLSF heap's.
+                           heap_export lists pool runs / objects, then TLSF blocks.
+                           max_live_blocks bounds the TLSF heap's live blocks only. */
 };
 
 #define HEAP_NULL UINT64_MAX /* failed alloc; no-op in a free batch (offset 0 is valid, C18) */

@@ -328,8 +328,10 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                                                   u64 *__restrict__ fs, const u64 *__restrict__ fe,
                                                   const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
                                                   u64 *__restrict__ out_u, u32 *bm, u64 w0, u64 w1, u64 w2,
-                                                  u32 *slot_map, int NC, int L, u64 *stats, Lifo lf) {
+                                                  u32 *slot_map, int NC, int L, u64 *stats, Lifo lf,
+                                                  const u64 *n_in) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (n_in) n = *n_in;   // request count on the device (a hybrid heap's TLSF share)
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const u32 lane = lane_id();
     const u64 nslots = (u64)NC;

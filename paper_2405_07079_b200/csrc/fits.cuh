@@ -27,10 +27,11 @@
 namespace fits {
 
 // ------------------------------------------------------------------ free phase ----
-__global__ void k_free_classify(const u64 *__restrict__ offs, u64 n, int alog2, u64 A_u,
+__global__ void k_free_classify(const u64 *__restrict__ offs, u64 n, const u64 *n_in, int alog2, u64 A_u,
                                 u32 *__restrict__ keys, u32 *__restrict__ flags, u64 *n_dev,
                                 DevCtr *ctr) {
     __shared__ u64 sm[33];
+    if (n_in) n = *n_in;   // count on the device (a hybrid heap's TLSF share)
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
     u64 nnull = 0, ninv = 0;
     const u64 amask = (1ull << alog2) - 1;
@@ -194,8 +195,9 @@ __global__ void k_u64_hi(const u64 *__restrict__ key, const u64 *n_dev, u32 *__r
 
 // ------------------------------------------------------------------ alloc phase ----
 // r = ceil(s / align) units (0 = fail: size 0 or larger than the arena), c = search class
-__global__ void k_alloc_prep(const u64 *__restrict__ sizes, u64 n, int alog2, u64 A_u, int L, int want_cls,
-                             u64 *__restrict__ r_out, u32 *__restrict__ c_out) {
+__global__ void k_alloc_prep(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2, u64 A_u, int L,
+                             int want_cls, u64 *__restrict__ r_out, u32 *__restrict__ c_out) {
+    if (n_in) n = *n_in;
     const u64 amask = (1ull << alog2) - 1;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         u64 s = sizes[i];
@@ -216,10 +218,11 @@ __global__ void k_piece_flags(const u64 *__restrict__ fs, const u64 *__restrict_
 
 // write results, insert the new live blocks into the block table, update counters
 __global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r, const u64 *__restrict__ out_u,
-                                                      u64 n, int alog2, u64 *__restrict__ out_bytes,
+                                                      u64 n, const u64 *n_in, int alog2, u64 *__restrict__ out_bytes,
                                                       u64 *__restrict__ slots, u64 tmask, u64 max_lines,
                                                       DevCtr *ctr, u64 max_live) {
     __shared__ u64 sm[33];
+    if (n_in) n = *n_in;
     const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;

@@ -15,6 +15,7 @@
 #include "buddy.cuh"
 #include "fits.cuh"
 #include "engine_tlsf.cuh"
+#include "pool.cuh"
 
 namespace {
 
@@ -37,16 +38,67 @@ struct Layout {
         o_hist, o_tsum, o_vs, o_ve, o_vsc, o_vec, o_ms, o_me, o_r, o_c, o_out, o_off, o_child,
         o_sib, o_cs, o_ce, o_bm, o_slot, bm_w0, bm_w1, bm_w2, bm_bytes, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
         o_promo, o_fr, o_froff, o_reqoff, o_ft0, o_ft1, o_vt, o_mt, o_lnext, total;
+    // HEAP_HYBRID: pool geometry and arrays, then the TLSF heap's own workspace at o_sub
+    pool::Geom geo;
+    u64 o_pctr, o_bits, o_sbcnt, o_sbpre, o_tsz, o_tout, o_toff, o_tidx, o_coff, o_sstats, o_sub, sub_total;
 };
 
 bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, Layout *Lo) {
     if (align == 0 || (align & (align - 1)) || arena == 0 || arena % align) return false;
-    if (policy < HEAP_FIRST_FIT || policy > HEAP_SEGFIT_LIFO) return false;
+    if (policy < HEAP_FIRST_FIT || policy > HEAP_HYBRID) return false;
     if (max_live == 0 || max_batch == 0 || max_batch >= (1ull << 31) || max_live >= (1ull << 30)) return false;
     Layout &L = *Lo;
     memset(&L, 0, sizeof(L));
     L.A_u = arena / align;
     if (L.A_u > (1ull << 32)) return false;
+    if (policy == HEAP_HYBRID) {
+        // reading C26 (pool.cuh): pools of align*2^j <= 4096 B objects share the first half of the
+        // arena, each a whole number of pages; the TLSF heap covers the rest
+        pool::Geom &G = L.geo;
+        G.alog2 = ilog2(align);
+        for (u64 o = align; o <= pool::PAGE; o <<= 1) G.J++;
+        G.S = G.J ? arena / (2 * (u64)G.J) / pool::PAGE * pool::PAGE : 0;
+        G.pool_end = (u64)G.J * G.S;
+        u64 wb = 0;
+        for (int j = 0; j < G.J; j++) {
+            G.wbase[j] = wb;
+            G.nslots[j] = G.S >> (G.alog2 + j);
+            wb += align_up((G.nslots[j] + 31) / 32, 32);
+        }
+        G.wbase[G.J] = wb;
+        G.nwords = wb;
+        G.nsb = wb / 32;
+        if (G.nslots[0] >= (1ull << 32)) return false;          // u32 slot ranks
+        Layout sub;
+        if (!make_layout(arena - G.pool_end, align, HEAP_TLSF, max_live, max_batch, &sub)) return false;
+        const u64 scan_cap = std::max(std::max(max_batch, G.nwords), (u64)256 * prims::ntiles_of(max_batch) + 16);
+        u64 o = 0;
+        auto take = [&](u64 bytes) { u64 r = o; o = align_up(o + bytes, 256); return r; };
+        L.o_ctr = take(sizeof(DevCtr));
+        L.o_stats = take(sizeof(heap_stats_t));
+        L.o_pctr = take(sizeof(pool::Ctr));
+        L.o_bits = take(G.nwords * 4 + 4);
+        L.o_sbcnt = take(G.nsb * 4 + 4);
+        L.o_sbpre = take(G.nsb * 4 + 4);
+        L.o_kA = take(max_batch * 4);
+        L.o_kB = take(max_batch * 4);
+        L.o_vA = take(max_batch * 4);
+        L.o_vB = take(max_batch * 4);
+        L.o_flags = take(scan_cap * 4);
+        L.o_pos = take(scan_cap * 4);
+        L.o_hist = take((256 * prims::ntiles_of(max_batch) + 16) * 4);
+        L.o_tsum = take((prims::ntiles_of(scan_cap) + 16) * 4);
+        L.o_tsz = take(max_batch * 8);
+        L.o_tout = take(max_batch * 8);
+        L.o_toff = take(max_batch * 8);
+        L.o_tidx = take(max_batch * 4);
+        L.o_coff = take((pool::MAXJ + 2) * 4);
+        L.o_sstats = take(sizeof(heap_stats_t));
+        L.o_sub = take(sub.total);
+        L.sub_total = sub.total;
+        L.total = o;
+        return true;
+    }
     L.K = ilog2(L.A_u);
     L.L = (policy == HEAP_TLSF) ? 5 : 0;
     L.NC = (int)h_cls_insert(L.A_u, L.L) + 1;
@@ -164,6 +216,12 @@ struct heap {
     u64 *bk[2];
     u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
     u64 *baddr, *bufA, *bufB, *promo, *fr;
+    // HEAP_HYBRID
+    heap *sub;                                // the TLSF heap on [pool_end, arena)
+    pool::Ctr *pctr;
+    u32 *bits, *sbcnt, *sbpre, *tidx, *coff;
+    u64 *tsz, *tout, *toff;
+    heap_stats_t *sstats;
     // tracing
     u64 prof_mask;
     int tag;                                  // tag of the launches being issued
@@ -426,6 +484,28 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     if (cudaFuncSetAttribute(buddy::k_alloc_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)buddy::ALLOC_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     void *w = d_workspace;
+    if (policy == HEAP_HYBRID) {
+        cudaStream_t st = (cudaStream_t)s;
+        h->ctr = at<DevCtr>(w, L.o_ctr);
+        h->dstats = at<heap_stats_t>(w, L.o_stats);
+        h->pctr = at<pool::Ctr>(w, L.o_pctr);
+        h->bits = at<u32>(w, L.o_bits); h->sbcnt = at<u32>(w, L.o_sbcnt); h->sbpre = at<u32>(w, L.o_sbpre);
+        h->kA = at<u32>(w, L.o_kA); h->kB = at<u32>(w, L.o_kB); h->vA = at<u32>(w, L.o_vA); h->vB = at<u32>(w, L.o_vB);
+        h->flags = at<u32>(w, L.o_flags); h->pos = at<u32>(w, L.o_pos); h->hist = at<u32>(w, L.o_hist);
+        h->tsum = at<u32>(w, L.o_tsum);
+        h->tsz = at<u64>(w, L.o_tsz); h->tout = at<u64>(w, L.o_tout); h->toff = at<u64>(w, L.o_toff);
+        h->tidx = at<u32>(w, L.o_tidx); h->coff = at<u32>(w, L.o_coff); h->sstats = at<heap_stats_t>(w, L.o_sstats);
+        h->cur = 0; h->launches = 0; h->prof_mask = 0; h->tag = HEAP_TAG_MISC;
+        if (cudaMemsetAsync(h->ctr, 0, sizeof(DevCtr), st) != cudaSuccess ||
+            cudaMemsetAsync(h->pctr, 0, sizeof(pool::Ctr), st) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+        LAUNCH(h, pool::k_init, h->G, 256, 0, st, L.geo, h->bits, h->sbcnt, h->pctr);
+        int rc = heap_create(arena_bytes - L.geo.pool_end, align, HEAP_TLSF, max_live_blocks, max_batch,
+                             at<char>(w, L.o_sub), L.sub_total, s, &h->sub);
+        if (rc != HEAP_OK) { delete h; return rc; }
+        if (cudaGetLastError() != cudaSuccess) { heap_destroy(h->sub); delete h; return HEAP_ECUDA; }
+        *h_out = h;
+        return HEAP_OK;
+    }
     h->ctr = at<DevCtr>(w, L.o_ctr);
     h->dstats = at<heap_stats_t>(w, L.o_stats);
     h->tbl = at<u64>(w, L.o_tbl);
@@ -475,18 +555,21 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
 
 int heap_destroy(heap_t *h) {
     if (!h) return HEAP_EINVAL;
+    if (h->sub) heap_destroy(h->sub);
     for (auto &r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : h->pool) cudaEventDestroy(e);
     delete h;
     return HEAP_OK;
 }
 
-uint64_t heap_launch_count(const heap_t *h) { return h ? h->launches : 0; }
+uint64_t heap_launch_count(const heap_t *h) { return h ? h->launches + (h->sub ? h->sub->launches : 0) : 0; }
 
-int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_stream_t sp) {
-    if (!h || n > h->max_batch || (n && !d_offsets)) return HEAP_EINVAL;
-    if (n == 0) return HEAP_OK;
-    cudaStream_t s = (cudaStream_t)sp;
+}  // extern "C"
+
+// The batch sequences.  `n` bounds the request count; when `n_in` is given the actual count is
+// read from device memory by the first kernel (a hybrid heap hands its TLSF heap the requests
+// its pools did not take without a host round trip).
+static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *n_in, cudaStream_t s) {
     const Layout &L = h->L;
     const int cur = h->cur, nxt = cur ^ 1;
     const bool bud = h->policy == HEAP_BUDDY;
@@ -494,7 +577,7 @@ int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_strea
     u64 *n_dev = &C->tmp[0];
     // 1. classify (null / unaligned / out of range) and compact the candidate keys
     TAG(h, HEAP_TAG_CLASSIFY);
-    LAUNCH(h, fits::k_free_classify, h->G, prims::NT, 0, s, (const u64 *)d_offsets, n, h->alog2, L.A_u, h->kA, h->flags, n_dev, C);
+    LAUNCH(h, fits::k_free_classify, h->G, prims::NT, 0, s, (const u64 *)d_offsets, n, n_in, h->alog2, L.A_u, h->kA, h->flags, n_dev, C);
     TAG(h, HEAP_TAG_SCAN);
     scan(h, h->flags, h->pos, n_dev, &C->nk, s);
     TAG(h, HEAP_TAG_COMPACT);
@@ -548,10 +631,7 @@ int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_strea
     return HEAP_OK;
 }
 
-int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, heap_stream_t sp) {
-    if (!h || n > h->max_batch || (n && (!d_sizes || !d_out))) return HEAP_EINVAL;
-    if (n == 0) return HEAP_OK;
-    cudaStream_t s = (cudaStream_t)sp;
+static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, const u64 *n_in, cudaStream_t s) {
     const Layout &L = h->L;
     const int cur = h->cur, nxt = cur ^ 1;
     DevCtr *C = h->ctr;
@@ -564,8 +644,8 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
                h->dsrc, nullptr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
         LAUNCH(h, buddy::k_alloc_r, h->G, 256, 0, s, h->kA, n, L.K, h->r);
         TAG(h, HEAP_TAG_FINISH);
-        LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
-               L.tcap / table::LINE, C, h->max_live);
+        LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, (const u64 *)nullptr, h->alog2, (u64 *)d_out,
+               h->tbl, L.tcap - 1, L.tcap / table::LINE, C, h->max_live);
         h->cur = nxt;
         maybe_rebuild(h, s);
         if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
@@ -574,7 +654,7 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
     const bool lifo = (h->policy == HEAP_SEGFIT_LIFO);
     const bool cls = (h->policy == HEAP_TLSF || h->policy == HEAP_SEGFIT || lifo);
     TAG(h, HEAP_TAG_ALLOC_PREP);
-    LAUNCH(h, fits::k_alloc_prep, h->G, 256, 0, s, (const u64 *)d_sizes, n, h->alog2, L.A_u, L.L, cls ? 1 : 0, h->r, h->c);
+    LAUNCH(h, fits::k_alloc_prep, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, L.A_u, L.L, cls ? 1 : 0, h->r, h->c);
     if (lifo) {
         // class-major, newest-push-first CSR (the bins as the paper's stacks), then the engine
         TAG(h, HEAP_TAG_INDEX);
@@ -589,7 +669,7 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         tlsfw::Csr csr{sv, h->cs, h->ce};
         tlsfw::Lifo lf{h->lnext, h->ft[cur], &C->lifo_clock};
         LAUNCH(h, tlsfw::k_engine<true>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
-               h->c, n, h->out, nullptr, 0ull, 0ull, 0ull, h->slot, L.NC, L.L, C->eng, lf);
+               h->c, n, h->out, nullptr, 0ull, 0ull, 0ull, h->slot, L.NC, L.L, C->eng, lf, n_in);
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_clock_add, 1, 1, 0, s, C, (const u64 *)nullptr, (u64)n);
     } else if (cls) {
@@ -602,7 +682,7 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
         TAG(h, HEAP_TAG_ENGINE);
         tlsfw::Csr csr{sv, h->cs, h->ce};
         LAUNCH(h, tlsfw::k_engine<false>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
-               h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{});
+               h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{}, n_in);
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, tlsfw::k_bitheap_clear, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->slot, h->bm,
                L.bm_w0, L.bm_w1, L.bm_w2, L.NC, L.L);
@@ -640,12 +720,72 @@ int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64
     if (lifo) LAUNCH(h, fits::k_compact<u32>, h->G, 256, 0, s, h->ft[cur], h->flags, h->pos, &C->F, h->ft[nxt]);
     LAUNCH(h, k_set_F, 1, 1, 0, s, C);
     TAG(h, HEAP_TAG_FINISH);
-    LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
+    LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, n_in, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
            L.tcap / table::LINE, C, h->max_live);
     h->cur = nxt;
     maybe_rebuild(h, s);
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
     return HEAP_OK;
+}
+
+// ---- HEAP_HYBRID (pool.cuh): pools in front of the TLSF heap `sub` ----
+static int hybrid_free(heap *h, const uint64_t *d_offsets, uint64_t n, cudaStream_t s) {
+    const pool::Geom &G = h->L.geo;
+    pool::Ctr *P = h->pctr;
+    TAG(h, HEAP_TAG_CLASSIFY);
+    LAUNCH(h, pool::k_free, h->G, 256, 0, s, (const u64 *)d_offsets, n, G, h->bits, h->sbcnt, P, h->flags, h->toff);
+    TAG(h, HEAP_TAG_SCAN);
+    scan(h, h->flags, h->pos, &P->nreq, &P->n_tl, s);
+    TAG(h, HEAP_TAG_COMPACT);
+    LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->toff, h->flags, h->pos, &P->nreq, h->tsz);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    return free_impl(h->sub, (const uint64_t *)h->tsz, n, &P->n_tl, s);
+}
+
+static int hybrid_alloc(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, cudaStream_t s) {
+    const pool::Geom &G = h->L.geo;
+    pool::Ctr *P = h->pctr;
+    // 1. pool class per request, stable counting sort by class (request order within a class)
+    TAG(h, HEAP_TAG_ALLOC_PREP);
+    LAUNCH(h, pool::k_keys, h->G, 256, 0, s, (const u64 *)d_sizes, n, G, h->kA, h->vA, P);
+    TAG(h, HEAP_TAG_SORT);
+    int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &P->nreq, 4, s);
+    u32 *sk = rb ? h->kB : h->kA, *sv = rb ? h->vB : h->vA;
+    TAG(h, HEAP_TAG_INDEX);
+    LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, sk, &P->nreq, G.J + 1, h->coff);
+    LAUNCH(h, pool::k_take, 1, 1, 0, s, h->coff, G, P);
+    // 2. ranks of the free slots: scan of the superblock free counts, then one warp per superblock
+    scan(h, h->sbcnt, h->sbpre, &P->nsb, &P->scan_total, s);
+    TAG(h, HEAP_TAG_ENGINE);
+    LAUNCH(h, pool::k_select, h->G, 256, 0, s, G, h->bits, h->sbcnt, h->sbpre, h->coff, sv, P, (u64 *)d_out);
+    // 3. everything else, in request order, through the TLSF heap
+    TAG(h, HEAP_TAG_COMPACT);
+    LAUNCH(h, pool::k_tl_flags, h->G, 256, 0, s, sk, sv, h->coff, &P->nreq, G, P, h->flags);
+    scan(h, h->flags, h->pos, &P->nreq, &P->n_tl, s);
+    LAUNCH(h, pool::k_tl_compact, h->G, 256, 0, s, (const u64 *)d_sizes, h->flags, h->pos, &P->nreq, h->tsz, h->tidx);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    int rc = alloc_impl(h->sub, (const uint64_t *)h->tsz, (uint64_t *)h->tout, n, &P->n_tl, s);
+    if (rc != HEAP_OK) return rc;
+    TAG(h, HEAP_TAG_FINISH);
+    LAUNCH(h, pool::k_tl_scatter, h->G, 256, 0, s, h->tout, h->tidx, &P->n_tl, G.pool_end, (u64 *)d_out);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    return HEAP_OK;
+}
+
+extern "C" {
+
+int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_stream_t sp) {
+    if (!h || n > h->max_batch || (n && !d_offsets)) return HEAP_EINVAL;
+    if (n == 0) return HEAP_OK;
+    if (h->policy == HEAP_HYBRID) return hybrid_free(h, d_offsets, n, (cudaStream_t)sp);
+    return free_impl(h, d_offsets, n, nullptr, (cudaStream_t)sp);
+}
+
+int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, heap_stream_t sp) {
+    if (!h || n > h->max_batch || (n && (!d_sizes || !d_out))) return HEAP_EINVAL;
+    if (n == 0) return HEAP_OK;
+    if (h->policy == HEAP_HYBRID) return hybrid_alloc(h, d_sizes, d_out, n, (cudaStream_t)sp);
+    return alloc_impl(h, d_sizes, d_out, n, nullptr, (cudaStream_t)sp);
 }
 
 static u64 meta_bytes(const heap *h) { return (u64)h->L.total; }
@@ -654,6 +794,15 @@ int heap_stats_async(heap_t *h, heap_stats_t *d_out, heap_stream_t sp) {
     if (!h || !d_out) return HEAP_EINVAL;
     cudaStream_t s = (cudaStream_t)sp;
     TAG(h, HEAP_TAG_MISC);
+    if (h->policy == HEAP_HYBRID) {
+        int rc = heap_stats_async(h->sub, h->sstats, sp);
+        if (rc != HEAP_OK) return rc;
+        CUDA_TRY(cudaMemsetAsync(&h->pctr->runs, 0, 2 * sizeof(u64), s));
+        LAUNCH(h, pool::k_marks, h->G, 256, 0, s, h->L.geo, h->bits, (u32 *)nullptr, (u32 *)nullptr, h->pctr);
+        LAUNCH(h, pool::k_stats, 1, 1, 0, s, h->sstats, h->pctr, h->L.geo, h->arena, h->align, meta_bytes(h), d_out);
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        return HEAP_OK;
+    }
     LAUNCH(h, k_stats, 1, 1024, 0, s, h->ctr, h->fs[h->cur], h->fe[h->cur], h->policy == HEAP_BUDDY ? 1 : 0, h->L.K,
            h->arena, h->align, h->alog2, meta_bytes(h), d_out);
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
@@ -676,6 +825,38 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
     if (!h || !h_counts) return HEAP_EINVAL;
     cudaStream_t s = (cudaStream_t)sp;
     TAG(h, HEAP_TAG_MISC);
+    if (h->policy == HEAP_HYBRID) {
+        // pool runs / live objects first (below pool_end, address order), then the TLSF heap's
+        const pool::Geom &G = h->L.geo;
+        pool::Ctr *P = h->pctr;
+        CUDA_TRY(cudaMemsetAsync(&P->runs, 0, 2 * sizeof(u64), s));
+        LAUNCH(h, pool::k_marks, h->G, 256, 0, s, G, h->bits, h->flags, h->pos, P);
+        scan(h, h->flags, h->flags, &P->nwords, &P->scan_total, s);
+        scan(h, h->pos, h->pos, &P->nwords, &P->scan_total, s);
+        u64 pc[2] = {0, 0};
+        CUDA_TRY(cudaMemcpyAsync(pc, &P->runs, 2 * sizeof(u64), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const u64 R = pc[0], LV = pc[1];
+        if ((d_free_pairs && cap_free) || (d_live_pairs && cap_live)) {
+            LAUNCH(h, pool::k_emit, h->G, 256, 0, s, G, h->bits, h->flags, h->pos, (u64 *)d_free_pairs,
+                   d_free_pairs ? cap_free : 0, (u64 *)d_live_pairs, d_live_pairs ? cap_live : 0);
+            if (d_free_pairs && cap_free)
+                LAUNCH(h, pool::k_end_to_size, h->G, 256, 0, s, (u64 *)d_free_pairs, std::min<u64>(R, cap_free));
+        }
+        uint64_t *fp2 = (d_free_pairs && cap_free > R) ? d_free_pairs + 2 * R : nullptr;
+        uint64_t *lp2 = (d_live_pairs && cap_live > LV) ? d_live_pairs + 2 * LV : nullptr;
+        const u64 cf2 = fp2 ? cap_free - R : 0, cl2 = lp2 ? cap_live - LV : 0;
+        uint64_t sc[2] = {0, 0};
+        int rc = heap_export(h->sub, fp2, cf2, lp2, cl2, sc, sp);
+        if (rc != HEAP_OK) return rc;
+        if (fp2) LAUNCH(h, pool::k_shift_pairs, h->G, 256, 0, s, (u64 *)fp2, std::min((u64)sc[0], cf2), G.pool_end);
+        if (lp2) LAUNCH(h, pool::k_shift_pairs, h->G, 256, 0, s, (u64 *)lp2, std::min((u64)sc[1], cl2), G.pool_end);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        h_counts[0] = R + sc[0];
+        h_counts[1] = LV + sc[1];
+        return HEAP_OK;
+    }
     const Layout &L = h->L;
     DevCtr *C = h->ctr;
     int alog = h->alog2;
@@ -714,7 +895,7 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
 int heap_debug_counters(heap_t *h, uint64_t *h_out, int n, heap_stream_t sp) {
     if (!h || !h_out || n < 0 || n > 16) return HEAP_EINVAL;
     cudaStream_t s = (cudaStream_t)sp;
-    CUDA_TRY(cudaMemcpyAsync(h_out, h->ctr->eng, n * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(h_out, (h->sub ? h->sub : h)->ctr->eng, n * sizeof(u64), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return HEAP_OK;
 }
@@ -722,6 +903,7 @@ int heap_debug_counters(heap_t *h, uint64_t *h_out, int n, heap_stream_t sp) {
 int heap_profile_enable(heap_t *h, uint64_t tag_mask) {
     if (!h) return HEAP_EINVAL;
     h->prof_mask = tag_mask;
+    if (h->sub) h->sub->prof_mask = tag_mask;
     return HEAP_OK;
 }
 
@@ -737,6 +919,7 @@ int heap_profile_read(heap_t *h, double *h_ms, uint64_t *h_launches) {
         h->pool.push_back(r.b);
     }
     h->recs.clear();
+    if (h->sub) return heap_profile_read(h->sub, h_ms, h_launches);
     return HEAP_OK;
 }
 

@@ -13,7 +13,7 @@ import torch
 
 import tracegen as tg
 from oracle import OracleL
-from tests.helpers import HEAP_NULL, IdMap, check_invariants
+from tests.helpers import HEAP_NULL, IdMap, check_invariants, hybrid_layout
 
 pytestmark = pytest.mark.gpu
 
@@ -100,6 +100,9 @@ SMALL = [
     (tg.SEGFIT_LIFO, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
     (tg.SEGFIT_LIFO, 1 << 28, 16, 16384, 200000, (4, 12), (2, 5), 0),
     (tg.BUDDY, (1 << 20) + (1 << 14) + 256, 256, 700, 9000, (8, 18), (1, 2), 1),
+    (tg.HYBRID, 1 << 18, 16, 48, 3000, (4, 14), (1, 3), 0),              # §5.3 pools + TLSF
+    (tg.HYBRID, 1 << 22, 16, 3000, 40000, (4, 14), (2, 5), 0),
+    (tg.HYBRID, 1 << 24, 64, 5000, 60000, (4, 13), (1, 2), 0),
 ]
 
 
@@ -141,7 +144,7 @@ def test_config5_first_batches():
 def test_edge_cases():
     """Empty batches, NULL / interior / unaligned / out-of-range / duplicate frees,
     zero and oversize requests, OOM in a tiny arena, the last unit of a 2^32-unit arena."""
-    for pol in (1, 2, 3, 4, 5, 6):
+    for pol in (1, 2, 3, 4, 5, 6, 7):
         arena, align = 1 << 12, 16
         g = Gpu(arena, align, pol, 256, 64)
         o = OracleL(arena, align, pol)
@@ -218,3 +221,53 @@ def test_config5_full_size_properties():
     assert np.array_equal(lp[idx, 1].astype(np.int64), r)
     so = np.sort(out[ok])
     assert len(np.unique(so)) == len(so)
+
+
+def test_hybrid_edges_and_full_pools():
+    """HYBRID with real pools: pool-offset taxonomy (interior, free slot, duplicate copies),
+    request sizes at the pool/TLSF edge (4095 / 4096 / 0), pools driven to exhaustion so
+    requests fall back to the TLSF heap, then freed back."""
+    arena, align = 1 << 20, 16
+    S, pool_end, obj = hybrid_layout(arena, align)
+    g = Gpu(arena, align, tg.HYBRID, 4096, 4096)
+    o = OracleL(arena, align, tg.HYBRID)
+    sizes = np.array([16, 0, 4095, 4096, 1, 100, 2048, 2049, 5000, 1 << 21], dtype=np.uint64)
+    go, oo = g.alloc_batch(sizes), o.alloc_batch(sizes)
+    assert np.array_equal(go, oo)
+    frees = np.array([HEAP_NULL, oo[0], oo[0], oo[0] + 8, 3 * S + 64, 16 * 5, oo[3], pool_end + 16, arena * 3],
+                     dtype=np.uint64)
+    g.free_batch(frees)
+    o.free_batch(frees)
+    compare_state(g, o, "hybrid taxonomy")
+    big = np.full(4000, 3000, dtype=np.uint64)          # pool 8 holds S/4096 = 14 objects
+    assert np.array_equal(g.alloc_batch(big), o.alloc_batch(big))
+    small = np.full(4096, 16, dtype=np.uint64)           # pool 0 holds 3584: the rest fall back
+    gs, os_ = g.alloc_batch(small), o.alloc_batch(small)
+    assert np.array_equal(gs, os_)
+    compare_state(g, o, "hybrid full pools")
+    g.free_batch(gs[::3].copy())
+    o.free_batch(os_[::3].copy())
+    assert np.array_equal(g.alloc_batch(small[:1000]), o.alloc_batch(small[:1000]))
+    compare_state(g, o, "hybrid refill")
+    fp, lp = g.export()
+    check_invariants(fp, lp, arena, align, False, tuple(j * S for j in range(1, len(obj) + 1)))
+
+
+def test_hybrid_config5_shape():
+    """The config-5 trace (64 GiB, 1M-request batches, LU8[16 B, 4 KiB)) on a HYBRID heap: every
+    request is below a page, so the pools serve it; three batches exact, counters compared."""
+    cfg = tg.CONFIGS[5]
+    g = Gpu(cfg.arena_bytes, cfg.align, tg.HYBRID, 1 << 16, cfg.batch)
+    o = OracleL(cfg.arena_bytes, cfg.align, tg.HYBRID)
+    im = IdMap(cfg.batch * 3)
+    for bi, (fids, sizes, first) in enumerate(tg.Trace(cfg, total_ops=cfg.batch * 3)):
+        offs = im.offsets(fids)
+        g.free_batch(offs)
+        o.free_batch(offs)
+        go = g.alloc_batch(sizes)
+        assert np.array_equal(go, o.alloc_batch(sizes)), bi
+        im.record(first, go)
+    gs, os_ = g.stats(), o.stats()
+    assert gs["error_flags"] == 0
+    for k in COUNTERS:
+        assert gs[k] == os_[k], k

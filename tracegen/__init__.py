@@ -30,7 +30,7 @@ _LIB = os.path.join(_HERE, "libtracegen.so")
 HEAP_NULL = (1 << 64) - 1
 
 # policy ids (numbers only; the meaning lives in include/heap.h and oracle/)
-FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY, SEGFIT_LIFO = 1, 2, 3, 4, 5, 6
+FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY, SEGFIT_LIFO, HYBRID = 1, 2, 3, 4, 5, 6, 7
 
 
 @dataclass(frozen=True)
