@@ -48,6 +48,13 @@ TAG_BYTES = {
     "alloc_prep": ("alloc", 8 + 8 + 4),             # size in; r, class out
     "classify": ("free", 8 + 4 + 4),                # offset in; key, flag out
 }
+# HEAP_HYBRID (pool.cuh): its tags name different kernels
+TAG_BYTES_HYBRID = {
+    "engine": ("alloc", 4 + 8 + 1),                 # k_select: request index in, offset out, ~1 B of bitmap
+    "classify": ("free", 8 + 4 + 8 + 4),            # k_free: offset in, flag out, bitmap word r/w, superblock count
+    "alloc_prep": ("alloc", 8 + 4 + 4),             # k_keys: size in, key + index out
+    "sort": ("alloc", 2 * (4 + 4)),                 # one counting-sort pass: key + index in and out
+}
 
 
 def parse():
@@ -65,6 +72,8 @@ def parse():
     p.add_argument("--driver-max-ops", type=int, default=2_000_000)
     p.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
     p.add_argument("--dev-share-gpu", action="store_true", help=argparse.SUPPRESS)
+    p.add_argument("--no-hybrid", action="store_true",
+                   help="skip the extra HEAP_HYBRID measurement on the same trace")
     return p.parse_args()
 
 
@@ -240,41 +249,47 @@ def run_ours(args, cfg, rank, world, local_rank):
             dist.all_gather_into_tensor(stats_all, stats_dev)
 
     # ---------------- device-resident run ----------------
-    h = Heap(cfg.arena_bytes, cfg.align, cfg.policy, max_live, cfg.batch, device=dev)
-    idmap = torch.full((n_alloc_total,), -1, dtype=torch.int64, device=dev)
-    outbuf = torch.empty(cfg.batch, dtype=torch.int64, device=dev)
-    for b in dev_batches[:args.warmup]:
-        run_device(h, idmap, outbuf, b)
-    torch.cuda.synchronize()
-    h.profile((1 << NTAGS) - 1)
-    h.profile_read()
-    l0 = h.launch_count()
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    ops = 0
-    for k, b in enumerate(dev_batches[args.warmup:]):
-        flush.fill_(k & 255)
-        if world > 1:
-            dist.barrier()
+    def device_run(policy):
+        h = Heap(cfg.arena_bytes, cfg.align, policy, max_live, cfg.batch, device=dev)
+        idmap = torch.full((n_alloc_total,), -1, dtype=torch.int64, device=dev)
+        outbuf = torch.empty(cfg.batch, dtype=torch.int64, device=dev)
+        for b in dev_batches[:args.warmup]:
+            run_device(h, idmap, outbuf, b)
         torch.cuda.synchronize()
-        ev[k][0].record()
-        run_device(h, idmap, outbuf, b)
-        ev[k][1].record()
+        h.profile((1 << NTAGS) - 1)
+        h.profile_read()
+        l0 = h.launch_count()
+        sampler = ClockSampler(local_rank)
+        sampler.start()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        ops = 0
+        for k, b in enumerate(dev_batches[args.warmup:]):
+            flush.fill_(k & 255)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev[k][0].record()
+            run_device(h, idmap, outbuf, b)
+            ev[k][1].record()
+            torch.cuda.synchronize()
+            ops += b[0].numel() + b[1].numel()
         torch.cuda.synchronize()
-        ops += b[0].numel() + b[1].numel()
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    launches = h.launch_count() - l0
-    prof = h.profile_read()
-    h.profile(0)
-    step_ms = [a.elapsed_time(e) for a, e in ev]
-    t_ms = sum(step_ms)
-    st = h.stats()
-    t_max, ops_all = aggregate(t_ms, ops, world, dev)
-    value = ops_all / (t_max / 1e3)
-    del h
-    torch.cuda.empty_cache()
+        clocks = sampler.stop()
+        launches = h.launch_count() - l0
+        prof = h.profile_read()
+        h.profile(0)
+        step_ms = [a.elapsed_time(e) for a, e in ev]
+        t_ms = sum(step_ms)
+        st = h.stats()
+        t_max, ops_all = aggregate(t_ms, ops, world, dev)
+        del h
+        torch.cuda.empty_cache()
+        return dict(value=ops_all / (t_max / 1e3), t_ms=t_ms, t_max=t_max, step_ms=step_ms, prof=prof,
+                    launches=launches, st=st, clocks=clocks)
+
+    R = device_run(cfg.policy)
+    value, t_ms, t_max, step_ms, prof, launches, st, clocks = (R[k] for k in (
+        "value", "t_ms", "t_max", "step_ms", "prof", "launches", "st", "clocks"))
 
     # ---------------- e2e through the C ABI with host buffers ----------------
     e2e = None
@@ -316,21 +331,36 @@ def run_ours(args, cfg, rank, world, local_rank):
         del h
 
     # ---------------- roofline of the dominant kernel group ----------------
-    dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else None
-    roof = None
-    shares = {k: round(v[0] / max(t_ms, 1e-9), 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
-    if dom:
+    def roofline(prof, t_ms, table):
+        dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else None
+        shares = {k: round(v[0] / max(t_ms, 1e-9), 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+        if not dom:
+            return None, shares
         tag, (ms, nl) = dom
         peak, peak_src = measured_peak_hbm()
-        unit, bpu = TAG_BYTES.get(tag, ("alloc", 64))
+        unit, bpu = table.get(tag, ("alloc", 64))
         n_units = sum(len(b[1]) if unit == "alloc" else len(b[0]) for b in batches[args.warmup:])
         per_launch_bytes = bpu * n_units / max(nl, 1)
         avg_s = ms / max(nl, 1) / 1e3
         achieved = per_launch_bytes / avg_s / 1e9
-        tr = ncu_traffic(tag)
-        roof = {"bound": "hbm", "kernel": tag, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
-                "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_s * 1e3}
+        return ({"bound": "hbm", "kernel": tag, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                 "frac": achieved / peak, "traffic": ncu_traffic(tag) if table is TAG_BYTES else None,
+                 "peak_source": peak_src, "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_s * 1e3},
+                shares)
+
+    roof, shares = roofline(prof, t_ms, TAG_BYTES)
+
+    # ---------------- the same trace on the §5.3 hybrid (pools below a page + TLSF) ----------------
+    hyb = None
+    if not args.no_hybrid and cfg.policy != tg.HYBRID:
+        H = device_run(tg.HYBRID)
+        hroof, hshares = roofline(H["prof"], H["t_ms"], TAG_BYTES_HYBRID)
+        hyb = {"policy": "hybrid", "value": H["value"], "unit": UNIT, "ms_per_step": H["t_max"] / args.steps,
+               "gpu_launches": H["launches"], "roofline": hroof, "kernel_shares": hshares,
+               "heap": {"n_live": H["st"]["n_live"], "allocs_failed": H["st"]["allocs_failed"],
+                        "error_flags": H["st"]["error_flags"]},
+               "note": "same trace and timing protocol; every request of this workload is below a page, "
+                       "so the bitmask pools serve it (DESIGN.md C26) — a different allocator, not the headline"}
 
     # ---------------- driver-allocator baselines (the paper's comparison) ----------------
     drv = None
@@ -371,7 +401,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (tracegen, seed 2405070790+1000c+r; per-rank independent traces)",
-            "config": {"workload": cfg.name, "policy": "tlsf", "arena_bytes": cfg.arena_bytes,
+            "config": {"workload": cfg.name, "policy": tg.POLICY_NAME.get(cfg.policy, str(cfg.policy)), "arena_bytes": cfg.arena_bytes,
                        "align": cfg.align, "batch": cfg.batch, "alloc_free_mix": "60/40",
                        "sizes": "LU8[16,4096)", "timed_batches": f"{args.warmup}..{nb - 1}",
                        "l2": "flushed between steps (256 MiB write)",
@@ -382,6 +412,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "kernel_shares": shares,
             "cpu_baseline": cpu,
             "driver_baselines": drv,
+            "hybrid_same_trace": hyb,
             "e2e": e2e,
             "clocks": clocks,
             "heap": {"n_live": st["n_live"], "n_free": st["n_free"], "allocs_failed": st["allocs_failed"],

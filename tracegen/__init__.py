@@ -31,6 +31,7 @@ HEAP_NULL = (1 << 64) - 1
 
 # policy ids (numbers only; the meaning lives in include/heap.h and oracle/)
 FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY, SEGFIT_LIFO, HYBRID = 1, 2, 3, 4, 5, 6, 7
+POLICY_NAME = {1: "first_fit", 2: "best_fit", 3: "segfit", 4: "tlsf", 5: "buddy", 6: "segfit_lifo", 7: "hybrid"}
 
 
 @dataclass(frozen=True)
