@@ -145,8 +145,18 @@ int heap_stats(heap_t *h, heap_stats_t *h_out, heap_stream_t s);
 int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *d_live_pairs,
                 uint64_t cap_live, uint64_t *h_counts, heap_stream_t s);
 
-/* Number of kernel launches this heap has enqueued so far (for the bench's gpu_launches). */
+/* Number of kernel launches this heap has enqueued so far (for the bench's gpu_launches);
+ * kernels run inside a batch graph count individually. */
 uint64_t heap_launch_count(const heap_t *h);
+
+/* Batch graphs (default: enabled).  When enabled, heap_free_batch / heap_alloc_batch run each
+ * batch as ONE CUDA-graph launch: the first call per (operation, internal ping-pong state)
+ * captures the batch's kernels once (a few ms); later calls of any n patch the request count
+ * and the request/result copies (staged through the workspace) and relaunch.  Semantics and
+ * results are identical to direct launches.  Direct launches are used instead while tracing is
+ * enabled (heap_profile_enable) or when the stream is itself being captured.  enable = 0
+ * switches to direct launches.  Returns HEAP_EINVAL for a NULL handle. */
+int heap_set_graphs(heap_t *h, int enable);
 
 /* Per-kernel timing (tracing).  Kernels are grouped by tag (HEAP_TAG_*); for every tag whose
  * bit is set in tag_mask, each launch is bracketed by two CUDA events on its stream.

@@ -50,7 +50,7 @@ class HeapStats(ctypes.Structure):
 
 EXPORTS = ("heap_workspace_bytes", "heap_create", "heap_destroy", "heap_free_batch",
            "heap_alloc_batch", "heap_stats_async", "heap_stats", "heap_export",
-           "heap_launch_count", "heap_profile_enable", "heap_profile_read", "heap_tag_name",
+           "heap_launch_count", "heap_set_graphs", "heap_profile_enable", "heap_profile_read", "heap_tag_name",
            "heap_debug_counters", "heap_strerror")
 NTAGS = 16
 
@@ -83,6 +83,8 @@ def lib():
         L.heap_export.argtypes = [vp, vp, u64, vp, u64, ctypes.POINTER(u64), vp]
         L.heap_launch_count.restype = u64
         L.heap_launch_count.argtypes = [vp]
+        L.heap_set_graphs.restype = i32
+        L.heap_set_graphs.argtypes = [vp, i32]
         L.heap_profile_enable.restype = i32
         L.heap_profile_enable.argtypes = [vp, u64]
         L.heap_profile_read.restype = i32

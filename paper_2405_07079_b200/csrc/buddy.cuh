@@ -245,8 +245,9 @@ __global__ void k_gather_u64(const u64 *__restrict__ src, const u32 *__restrict_
 
 // ------------------------------------------------------------------ alloc phase ----
 // r -> order key (K+1 = fail bucket)
-__global__ void k_alloc_orders(const u64 *__restrict__ sizes, u64 n, int alog2, u64 A_u, int K,
+__global__ void k_alloc_orders(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2, u64 A_u, int K,
                                u32 *__restrict__ key, u32 *__restrict__ val, u64 *n_dev) {
+    if (n_in) n = *n_in;
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
     const u64 amask = (1ull << alog2) - 1;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
@@ -395,7 +396,8 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
 }
 
 // buddy results: order -> units = 2^k; reuse fits::k_alloc_finish by materialising r
-__global__ void k_alloc_r(const u32 *__restrict__ key_by_req, u64 n, int K, u64 *__restrict__ r) {
+__global__ void k_alloc_r(const u32 *__restrict__ key_by_req, u64 n, const u64 *n_in, int K, u64 *__restrict__ r) {
+    if (n_in) n = *n_in;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         u32 k = key_by_req[i];
         r[i] = (k <= (u32)K) ? (1ull << k) : 0;

@@ -327,8 +327,9 @@ constexpr int FF_MAX_LEVELS = 8;
 
 __global__ void __launch_bounds__(32) k_ff_engine(u64 *tree, const u64 *__restrict__ lvl_off, int nlev,
                                                   u64 *fs, const u64 *F_dev, const u64 *__restrict__ r, u64 n,
-                                                  u64 *__restrict__ out_u) {
+                                                  const u64 *n_in, u64 *__restrict__ out_u) {
     const u32 lane = lane_id();
+    if (n_in) n = *n_in;
     u64 sz[FF_MAX_LEVELS];
     u64 F = *F_dev;
     sz[0] = F;
@@ -403,8 +404,10 @@ __device__ __forceinline__ u64 warp_lower_bound(const u64 *a, u64 lo, u64 hi, u6
 
 template <bool SMEM>
 __global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
-                                                  const u64 *__restrict__ r, u64 n, u64 *__restrict__ out_u) {
+                                                  const u64 *__restrict__ r, u64 n, const u64 *n_in,
+                                                  u64 *__restrict__ out_u) {
     extern __shared__ u64 skeys[];
+    if (n_in) n = *n_in;
     const u32 lane = lane_id();
     u64 nb = *F_dev;
     u64 *keys = SMEM ? skeys : gkeys;

@@ -41,6 +41,7 @@ struct Layout {
     // HEAP_HYBRID: pool geometry and arrays, then the TLSF heap's own workspace at o_sub
     pool::Geom geo;
     u64 o_pctr, o_bits, o_sbcnt, o_sbpre, o_tsz, o_tout, o_toff, o_tidx, o_coff, o_sstats, o_sub, sub_total;
+    u64 o_gin, o_gout;   // graph path: staging of the request / result words
 };
 
 bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, Layout *Lo) {
@@ -94,6 +95,8 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.o_tidx = take(max_batch * 4);
         L.o_coff = take((pool::MAXJ + 2) * 4);
         L.o_sstats = take(sizeof(heap_stats_t));
+        L.o_gin = take(max_batch * 8);
+        L.o_gout = take(max_batch * 8);
         L.o_sub = take(sub.total);
         L.sub_total = sub.total;
         L.total = o;
@@ -145,6 +148,8 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
     L.o_r = take(max_batch * 8);
     L.o_c = take(max_batch * 4);
     L.o_out = take(max_batch * 8);
+    L.o_gin = take(max_batch * 8);
+    L.o_gout = take(max_batch * 8);
     L.o_off = take((fits::MAX_NC + 8) * 4);
     if (policy == HEAP_TLSF || policy == HEAP_SEGFIT) {
         L.o_cs = take(L.cap_f * 4);
@@ -222,6 +227,18 @@ struct heap {
     u32 *bits, *sbcnt, *sbpre, *tidx, *coff;
     u64 *tsz, *tout, *toff;
     heap_stats_t *sstats;
+    // graph path: one instantiated graph per (op, ping-pong state); see graph_batch()
+    struct GSlot {
+        cudaGraphExec_t exec = nullptr;
+        cudaGraph_t graph = nullptr;          // kept alive: the exec's node handles refer to it
+        cudaGraphNode_t set_n = nullptr, cin = nullptr, cout = nullptr;
+        int cur_after = 0, subcur_after = 0;
+        u64 nlaunch = 0;
+    };
+    int graphs;
+    cudaStream_t cap;
+    GSlot gs[2][2][2];
+    u64 *gin, *gout;
     // tracing
     u64 prof_mask;
     int tag;                                  // tag of the launches being issued
@@ -495,6 +512,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->tsum = at<u32>(w, L.o_tsum);
         h->tsz = at<u64>(w, L.o_tsz); h->tout = at<u64>(w, L.o_tout); h->toff = at<u64>(w, L.o_toff);
         h->tidx = at<u32>(w, L.o_tidx); h->coff = at<u32>(w, L.o_coff); h->sstats = at<heap_stats_t>(w, L.o_sstats);
+        h->gin = at<u64>(w, L.o_gin); h->gout = at<u64>(w, L.o_gout);
+        h->graphs = 1;
         h->cur = 0; h->launches = 0; h->prof_mask = 0; h->tag = HEAP_TAG_MISC;
         if (cudaMemsetAsync(h->ctr, 0, sizeof(DevCtr), st) != cudaSuccess ||
             cudaMemsetAsync(h->pctr, 0, sizeof(pool::Ctr), st) != cudaSuccess) { delete h; return HEAP_ECUDA; }
@@ -518,6 +537,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->ms = at<u64>(w, L.o_ms); h->me = at<u64>(w, L.o_me);
     h->r = at<u64>(w, L.o_r); h->c = at<u32>(w, L.o_c); h->out = at<u64>(w, L.o_out);
     h->off = at<u32>(w, L.o_off);
+    h->gin = at<u64>(w, L.o_gin); h->gout = at<u64>(w, L.o_gout);
+    h->graphs = 1;
     h->cs = L.o_cs ? at<u32>(w, L.o_cs) : nullptr; h->ce = L.o_ce ? at<u32>(w, L.o_ce) : nullptr;
     h->bm = L.o_bm ? at<u32>(w, L.o_bm) : nullptr; h->slot = L.o_slot ? at<u32>(w, L.o_slot) : nullptr;
     if (h->bm && cudaMemsetAsync(h->bm, 0, L.bm_bytes, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
@@ -556,6 +577,13 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
 int heap_destroy(heap_t *h) {
     if (!h) return HEAP_EINVAL;
     if (h->sub) heap_destroy(h->sub);
+    for (auto &a : h->gs)
+        for (auto &b : a)
+            for (auto &g : b) {
+                if (g.exec) cudaGraphExecDestroy(g.exec);
+                if (g.graph) cudaGraphDestroy(g.graph);
+            }
+    if (h->cap) cudaStreamDestroy(h->cap);
     for (auto &r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : h->pool) cudaEventDestroy(e);
     delete h;
@@ -637,14 +665,14 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
     DevCtr *C = h->ctr;
     if (h->policy == HEAP_BUDDY) {
         TAG(h, HEAP_TAG_BUDDY_ALLOC);
-        LAUNCH(h, buddy::k_alloc_orders, h->G, 256, 0, s, (const u64 *)d_sizes, n, h->alog2, L.A_u, L.K, h->kA, h->vA, &C->tmp[0]);
+        LAUNCH(h, buddy::k_alloc_orders, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, L.A_u, L.K, h->kA, h->vA, &C->tmp[0]);
         radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s);   // 1 pass: result in kB/vB
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kB, &C->tmp[0], L.K + 2, h->reqoff);
         LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, buddy::ALLOC_SMEM, s, h->vB, h->reqoff, h->fs[cur], h->fs[nxt], h->dtm,
                h->dsrc, nullptr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
-        LAUNCH(h, buddy::k_alloc_r, h->G, 256, 0, s, h->kA, n, L.K, h->r);
+        LAUNCH(h, buddy::k_alloc_r, h->G, 256, 0, s, h->kA, n, n_in, L.K, h->r);
         TAG(h, HEAP_TAG_FINISH);
-        LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, (const u64 *)nullptr, h->alog2, (u64 *)d_out,
+        LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, n_in, h->alog2, (u64 *)d_out,
                h->tbl, L.tcap - 1, L.tcap / table::LINE, C, h->max_live);
         h->cur = nxt;
         maybe_rebuild(h, s);
@@ -671,7 +699,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         LAUNCH(h, tlsfw::k_engine<true>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
                h->c, n, h->out, nullptr, 0ull, 0ull, 0ull, h->slot, L.NC, L.L, C->eng, lf, n_in);
         TAG(h, HEAP_TAG_INDEX);
-        LAUNCH(h, fits::k_clock_add, 1, 1, 0, s, C, (const u64 *)nullptr, (u64)n);
+        LAUNCH(h, fits::k_clock_add, 1, 1, 0, s, C, n_in, (u64)n);
     } else if (cls) {
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_cls_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.L, h->kA, h->vA);
@@ -695,7 +723,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         for (int l = 1; l < L.nlev; l++)
             LAUNCH(h, fits::k_ff_level, h->G, 256, 0, s, h->tree + offs[l - 1], h->tree + offs[l], &C->F, l);
         TAG(h, HEAP_TAG_ENGINE);
-        LAUNCH(h, fits::k_ff_engine, 1, 32, 0, s, h->tree, h->lvl, L.nlev, h->fs[cur], &C->F, h->r, n, h->out);
+        LAUNCH(h, fits::k_ff_engine, 1, 32, 0, s, h->tree, h->lvl, L.nlev, h->fs[cur], &C->F, h->r, n, n_in, h->out);
     } else {   // BEST_FIT
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_bf_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.FB, h->bk[0]);
@@ -706,9 +734,9 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         TAG(h, HEAP_TAG_ENGINE);
         if (smem <= 200 * 1024) {
             cudaFuncSetAttribute(fits::k_bf_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            LAUNCH(h, fits::k_bf_engine<true>, 1, 32, smem, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, h->out);
+            LAUNCH(h, fits::k_bf_engine<true>, 1, 32, smem, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in, h->out);
         } else {
-            LAUNCH(h, fits::k_bf_engine<false>, 1, 32, 0, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, h->out);
+            LAUNCH(h, fits::k_bf_engine<false>, 1, 32, 0, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in, h->out);
         }
     }
     // compact the surviving pieces into the other buffer (address order is kept)
@@ -728,12 +756,104 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
     return HEAP_OK;
 }
 
+static int hybrid_free(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *n_in, cudaStream_t s);
+static int hybrid_alloc(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, const u64 *n_in, cudaStream_t s);
+
+static int batch_free(heap *h, const uint64_t *in, uint64_t n, const u64 *n_in, cudaStream_t s) {
+    return h->policy == HEAP_HYBRID ? hybrid_free(h, in, n, n_in, s) : free_impl(h, in, n, n_in, s);
+}
+static int batch_alloc(heap *h, const uint64_t *in, uint64_t *out, uint64_t n, const u64 *n_in, cudaStream_t s) {
+    return h->policy == HEAP_HYBRID ? hybrid_alloc(h, in, out, n, n_in, s) : alloc_impl(h, in, out, n, n_in, s);
+}
+
+// ---- CUDA-graph path ----
+// A batch is ~30-90 small launches whose host-side arguments depend only on the policy, the
+// capacities and the ping-pong state (every count is read from device memory), so one graph per
+// (op, ping-pong state) serves every n: its first node writes n to the device, a memcpy node
+// stages the caller's request words into the workspace, the captured batch runs on the staging
+// buffers with a device-side count, and (alloc) a memcpy node copies the results out.  Each call
+// only patches those three nodes and launches the graph: one launch instead of dozens.
+__global__ void k_set_req_n(DevCtr *ctr, u64 n) { ctr->req_n = n; }
+
+#define GRAPH_TRY(x)                                                                       \
+    do {                                                                                   \
+        cudaError_t _e = (x);                                                              \
+        if (_e != cudaSuccess) {                                                           \
+            if (getenv("HEAP_DEBUG")) fprintf(stderr, "libheap graph: %s: %s\n", #x, cudaGetErrorString(_e)); \
+            return HEAP_ECUDA;                                                             \
+        }                                                                                  \
+    } while (0)
+
+static bool use_graph(heap *h, cudaStream_t s) {
+    if (!h->graphs || h->prof_mask || (h->sub && h->sub->prof_mask)) return false;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return false;
+    return true;
+}
+
+static int graph_batch(heap *h, int op, const uint64_t *in, uint64_t *out, uint64_t n, cudaStream_t s) {
+    heap *sub = h->sub;
+    const int sc = sub ? sub->cur : 0;
+    heap::GSlot &g = h->gs[op][h->cur][sc];
+    DevCtr *ctr = h->ctr;
+    void *kargs[2] = {(void *)&ctr, (void *)&n};
+    cudaKernelNodeParams kp = {};
+    kp.func = (void *)k_set_req_n;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = kargs;
+    if (!g.exec) {
+        if (!h->cap) CUDA_TRY(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+        const int cur0 = h->cur;
+        const u64 l0 = h->launches, ls0 = sub ? sub->launches : 0;
+        cudaGraph_t body = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+        const uint64_t *gin = (const uint64_t *)h->gin;
+        int rc = op == 0 ? batch_free(h, gin, h->max_batch, &ctr->req_n, h->cap)
+                         : batch_alloc(h, gin, (uint64_t *)h->gout, h->max_batch, &ctr->req_n, h->cap);
+        cudaError_t e = cudaStreamEndCapture(h->cap, &body);
+        g.cur_after = h->cur;
+        g.subcur_after = sub ? sub->cur : 0;
+        g.nlaunch = (h->launches - l0) + (sub ? sub->launches - ls0 : 0) + 1;
+        h->cur = cur0;                                 // nothing ran yet: restore the host state
+        h->launches = l0;
+        if (sub) { sub->cur = sc; sub->launches = ls0; }
+        if (rc != HEAP_OK || e != cudaSuccess) {
+            if (getenv("HEAP_DEBUG")) fprintf(stderr, "libheap graph: capture rc %d: %s\n", rc, cudaGetErrorString(e));
+            if (body) cudaGraphDestroy(body);
+            cudaGetLastError();
+            return rc ? rc : HEAP_ECUDA;
+        }
+        cudaGraph_t G = nullptr;
+        cudaGraphNode_t child = nullptr;
+        GRAPH_TRY(cudaGraphCreate(&G, 0));
+        GRAPH_TRY(cudaGraphAddKernelNode(&g.set_n, G, nullptr, 0, &kp));
+        GRAPH_TRY(cudaGraphAddMemcpyNode1D(&g.cin, G, &g.set_n, 1, h->gin, in, n * 8, cudaMemcpyDefault));
+        GRAPH_TRY(cudaGraphAddChildGraphNode(&child, G, &g.cin, 1, body));
+        if (op == 1) GRAPH_TRY(cudaGraphAddMemcpyNode1D(&g.cout, G, &child, 1, out, h->gout, n * 8, cudaMemcpyDefault));
+        cudaGraphExec_t ex = nullptr;
+        GRAPH_TRY(cudaGraphInstantiate(&ex, G, 0));
+        g.exec = ex;
+        g.graph = G;
+        cudaGraphDestroy(body);
+    } else {
+        GRAPH_TRY(cudaGraphExecKernelNodeSetParams(g.exec, g.set_n, &kp));
+        GRAPH_TRY(cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.cin, h->gin, in, n * 8, cudaMemcpyDefault));
+        if (op == 1) GRAPH_TRY(cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.cout, out, h->gout, n * 8, cudaMemcpyDefault));
+    }
+    GRAPH_TRY(cudaGraphLaunch(g.exec, s));
+    h->cur = g.cur_after;
+    if (sub) sub->cur = g.subcur_after;
+    h->launches += g.nlaunch;
+    return HEAP_OK;
+}
+
 // ---- HEAP_HYBRID (pool.cuh): pools in front of the TLSF heap `sub` ----
-static int hybrid_free(heap *h, const uint64_t *d_offsets, uint64_t n, cudaStream_t s) {
+static int hybrid_free(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *n_in, cudaStream_t s) {
     const pool::Geom &G = h->L.geo;
     pool::Ctr *P = h->pctr;
     TAG(h, HEAP_TAG_CLASSIFY);
-    LAUNCH(h, pool::k_free, h->G, 256, 0, s, (const u64 *)d_offsets, n, G, h->bits, h->sbcnt, P, h->flags, h->toff);
+    LAUNCH(h, pool::k_free, h->G, 256, 0, s, (const u64 *)d_offsets, n, n_in, G, h->bits, h->sbcnt, P, h->flags, h->toff);
     TAG(h, HEAP_TAG_SCAN);
     scan(h, h->flags, h->pos, &P->nreq, &P->n_tl, s);
     TAG(h, HEAP_TAG_COMPACT);
@@ -742,12 +862,12 @@ static int hybrid_free(heap *h, const uint64_t *d_offsets, uint64_t n, cudaStrea
     return free_impl(h->sub, (const uint64_t *)h->tsz, n, &P->n_tl, s);
 }
 
-static int hybrid_alloc(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, cudaStream_t s) {
+static int hybrid_alloc(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, const u64 *n_in, cudaStream_t s) {
     const pool::Geom &G = h->L.geo;
     pool::Ctr *P = h->pctr;
     // 1. pool class per request, stable counting sort by class (request order within a class)
     TAG(h, HEAP_TAG_ALLOC_PREP);
-    LAUNCH(h, pool::k_keys, h->G, 256, 0, s, (const u64 *)d_sizes, n, G, h->kA, h->vA, P);
+    LAUNCH(h, pool::k_keys, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, G, h->kA, h->vA, P);
     TAG(h, HEAP_TAG_SORT);
     int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &P->nreq, 4, s);
     u32 *sk = rb ? h->kB : h->kA, *sv = rb ? h->vB : h->vA;
@@ -777,15 +897,21 @@ extern "C" {
 int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_stream_t sp) {
     if (!h || n > h->max_batch || (n && !d_offsets)) return HEAP_EINVAL;
     if (n == 0) return HEAP_OK;
-    if (h->policy == HEAP_HYBRID) return hybrid_free(h, d_offsets, n, (cudaStream_t)sp);
-    return free_impl(h, d_offsets, n, nullptr, (cudaStream_t)sp);
+    if (use_graph(h, (cudaStream_t)sp)) return graph_batch(h, 0, d_offsets, nullptr, n, (cudaStream_t)sp);
+    return batch_free(h, d_offsets, n, nullptr, (cudaStream_t)sp);
 }
 
 int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, heap_stream_t sp) {
     if (!h || n > h->max_batch || (n && (!d_sizes || !d_out))) return HEAP_EINVAL;
     if (n == 0) return HEAP_OK;
-    if (h->policy == HEAP_HYBRID) return hybrid_alloc(h, d_sizes, d_out, n, (cudaStream_t)sp);
-    return alloc_impl(h, d_sizes, d_out, n, nullptr, (cudaStream_t)sp);
+    if (use_graph(h, (cudaStream_t)sp)) return graph_batch(h, 1, d_sizes, d_out, n, (cudaStream_t)sp);
+    return batch_alloc(h, d_sizes, d_out, n, nullptr, (cudaStream_t)sp);
+}
+
+int heap_set_graphs(heap_t *h, int enable) {
+    if (!h) return HEAP_EINVAL;
+    h->graphs = enable ? 1 : 0;
+    return HEAP_OK;
 }
 
 static u64 meta_bytes(const heap *h) { return (u64)h->L.total; }

@@ -78,9 +78,10 @@ __global__ void k_init(Geom G, u32 *bits, u32 *sbcnt, Ctr *c) {
 
 // ---- free batch: classify every copy against the batch-start state; pool frees set their bit
 // (atomicOr: exactly one copy of an allocated slot sees it clear); the rest go to the TLSF heap
-__global__ void __launch_bounds__(256) k_free(const u64 *__restrict__ offs, u64 n, Geom G, u32 *bits, u32 *sbcnt,
-                                              Ctr *c, u32 *__restrict__ flags, u64 *__restrict__ toff) {
+__global__ void __launch_bounds__(256) k_free(const u64 *__restrict__ offs, u64 n, const u64 *n_in, Geom G, u32 *bits,
+                                              u32 *sbcnt, Ctr *c, u32 *__restrict__ flags, u64 *__restrict__ toff) {
     __shared__ u64 s_cnt[5 + 2 * MAXJ];      // null, ok, invalid, double, live_b, pfree[J]
+    if (n_in) n = *n_in;
     for (int t = threadIdx.x; t < 5 + 2 * MAXJ; t += blockDim.x) s_cnt[t] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) c->nreq = n;
     __syncthreads();
@@ -135,8 +136,9 @@ __global__ void __launch_bounds__(256) k_free(const u64 *__restrict__ offs, u64 
 
 // ---- alloc batch ----
 // key = pool class j for 0 < s < PAGE (smallest pool whose objects hold s), J for the TLSF heap
-__global__ void k_keys(const u64 *__restrict__ sizes, u64 n, Geom G, u32 *__restrict__ key, u32 *__restrict__ val,
-                       Ctr *c) {
+__global__ void k_keys(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, Geom G, u32 *__restrict__ key,
+                       u32 *__restrict__ val, Ctr *c) {
+    if (n_in) n = *n_in;
     if (blockIdx.x == 0 && threadIdx.x == 0) c->nreq = n;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u64 s = sizes[i];

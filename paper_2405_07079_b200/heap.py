@@ -97,6 +97,10 @@ def heap_launch_count(h) -> int:
     return int(lib().heap_launch_count(h))
 
 
+def heap_set_graphs(h, enable: bool) -> None:
+    check("heap_set_graphs", lib().heap_set_graphs(h, 1 if enable else 0))
+
+
 def heap_profile_enable(h, tag_mask: int) -> None:
     check("heap_profile_enable", lib().heap_profile_enable(h, tag_mask))
 
@@ -170,6 +174,9 @@ class Heap:
 
     def launch_count(self) -> int:
         return heap_launch_count(self._h)
+
+    def set_graphs(self, enable: bool) -> None:
+        heap_set_graphs(self._h, enable)
 
     def profile(self, tag_mask: int) -> None:
         heap_profile_enable(self._h, tag_mask)

@@ -24,9 +24,10 @@ COUNTERS = ("live_bytes", "free_bytes", "n_live", "n_free", "largest_free", "hig
 class Gpu:
     """numpy-in / numpy-out adapter over the product binding (same interface as OracleL)."""
 
-    def __init__(self, arena, align, policy, max_live, max_batch):
+    def __init__(self, arena, align, policy, max_live, max_batch, graphs=True):
         from paper_2405_07079_b200 import Heap
         self.h = Heap(arena, align, policy, max_live, max_batch)
+        self.h.set_graphs(graphs)
 
     def free_batch(self, offs):
         a = np.ascontiguousarray(np.asarray(offs, dtype=np.uint64))
@@ -59,9 +60,9 @@ def compare_state(g, o, ctx=""):
 
 
 def run_parity(cfg, max_live, max_batch, total_ops=None, every_batch_state=False, max_batches=None,
-               batch=None):
+               batch=None, graphs=True):
     t = tg.Trace(cfg, total_ops=total_ops, batch=batch)
-    g = Gpu(cfg.arena_bytes, cfg.align, cfg.policy, max_live, max_batch)
+    g = Gpu(cfg.arena_bytes, cfg.align, cfg.policy, max_live, max_batch, graphs)
     o = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
     im = IdMap(1 << 16)
     for bi, (fids, sizes, first) in enumerate(t):
@@ -271,3 +272,26 @@ def test_hybrid_config5_shape():
     assert gs["error_flags"] == 0
     for k in COUNTERS:
         assert gs[k] == os_[k], k
+
+
+@pytest.mark.parametrize("pol", [tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.BUDDY, tg.SEGFIT_LIFO, tg.HYBRID])
+def test_direct_launch_path(pol):
+    """The same batches with batch graphs disabled (direct launches, the path tracing uses), and
+    a heap switching between the two paths mid-trace."""
+    kind = 1 if pol == tg.BUDDY else 0
+    sizes = (6, 16) if pol == tg.BUDDY else (4, 14)
+    cfg = tg.custom(pol, 1 << 22, 16, 500, rho=(2, 5), total_ops=8000, sizes=sizes, size_kind=kind, idx=70 + pol)
+    run_parity(cfg, max_live=1 << 15, max_batch=500, graphs=False)
+    t = tg.Trace(cfg)
+    g = Gpu(cfg.arena_bytes, cfg.align, pol, 1 << 15, 500)
+    o = OracleL(cfg.arena_bytes, cfg.align, pol)
+    im = IdMap(1 << 14)
+    for bi, (fids, sz, first) in enumerate(t):
+        g.h.set_graphs(bi % 3 != 1)
+        offs = im.offsets(fids)
+        g.free_batch(offs)
+        o.free_batch(offs)
+        go = g.alloc_batch(sz)
+        assert np.array_equal(go, o.alloc_batch(sz)), bi
+        im.record(first, go)
+    compare_state(g, o, "mixed paths")
