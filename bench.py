@@ -249,15 +249,19 @@ def run_ours(args, cfg, rank, world, local_rank):
             dist.all_gather_into_tensor(stats_all, stats_dev)
 
     # ---------------- device-resident run ----------------
-    def device_run(policy):
+    def device_run(policy, profile):
+        """W warm-up + K timed steps on a fresh heap.  profile=False: the production path (batch
+        graphs), timed for `value`; profile=True: direct launches bracketed by per-tag events
+        (heap_profile_*), used only for the kernel shares and the roofline."""
         h = Heap(cfg.arena_bytes, cfg.align, policy, max_live, cfg.batch, device=dev)
         idmap = torch.full((n_alloc_total,), -1, dtype=torch.int64, device=dev)
         outbuf = torch.empty(cfg.batch, dtype=torch.int64, device=dev)
         for b in dev_batches[:args.warmup]:
             run_device(h, idmap, outbuf, b)
         torch.cuda.synchronize()
-        h.profile((1 << NTAGS) - 1)
-        h.profile_read()
+        if profile:
+            h.profile((1 << NTAGS) - 1)
+            h.profile_read()
         l0 = h.launch_count()
         sampler = ClockSampler(local_rank)
         sampler.start()
@@ -276,7 +280,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
         clocks = sampler.stop()
         launches = h.launch_count() - l0
-        prof = h.profile_read()
+        prof = h.profile_read() if profile else None
         h.profile(0)
         step_ms = [a.elapsed_time(e) for a, e in ev]
         t_ms = sum(step_ms)
@@ -287,9 +291,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         return dict(value=ops_all / (t_max / 1e3), t_ms=t_ms, t_max=t_max, step_ms=step_ms, prof=prof,
                     launches=launches, st=st, clocks=clocks)
 
-    R = device_run(cfg.policy)
-    value, t_ms, t_max, step_ms, prof, launches, st, clocks = (R[k] for k in (
-        "value", "t_ms", "t_max", "step_ms", "prof", "launches", "st", "clocks"))
+    R = device_run(cfg.policy, False)
+    value, t_ms, t_max, step_ms, launches, st, clocks = (R[k] for k in (
+        "value", "t_ms", "t_max", "step_ms", "launches", "st", "clocks"))
+    RP = device_run(cfg.policy, True)
+    prof, t_ms_prof = RP["prof"], RP["t_ms"]
 
     # ---------------- e2e through the C ABI with host buffers ----------------
     e2e = None
@@ -348,15 +354,17 @@ def run_ours(args, cfg, rank, world, local_rank):
                  "peak_source": peak_src, "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_s * 1e3},
                 shares)
 
-    roof, shares = roofline(prof, t_ms, TAG_BYTES)
+    roof, shares = roofline(prof, t_ms_prof, TAG_BYTES)
 
     # ---------------- the same trace on the §5.3 hybrid (pools below a page + TLSF) ----------------
     hyb = None
     if not args.no_hybrid and cfg.policy != tg.HYBRID:
-        H = device_run(tg.HYBRID)
-        hroof, hshares = roofline(H["prof"], H["t_ms"], TAG_BYTES_HYBRID)
+        H = device_run(tg.HYBRID, False)
+        HP = device_run(tg.HYBRID, True)
+        hroof, hshares = roofline(HP["prof"], HP["t_ms"], TAG_BYTES_HYBRID)
         hyb = {"policy": "hybrid", "value": H["value"], "unit": UNIT, "ms_per_step": H["t_max"] / args.steps,
                "gpu_launches": H["launches"], "roofline": hroof, "kernel_shares": hshares,
+               "ms_per_step_profiled": HP["t_max"] / args.steps,
                "heap": {"n_live": H["st"]["n_live"], "allocs_failed": H["st"]["allocs_failed"],
                         "error_flags": H["st"]["error_flags"]},
                "note": "same trace and timing protocol; every request of this workload is below a page, "
