@@ -22,6 +22,7 @@ import numpy as np
 
 HEAP_NULL = (1 << 64) - 1
 FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY = 1, 2, 3, 4, 5
+NEXT_FIT = 8
 
 
 def cls_of(u: int, L: int) -> int:
@@ -65,6 +66,7 @@ class OracleB:
                 s += 1 << t
         self.counts = dict(allocs_ok=0, allocs_failed=0, frees_ok=0, frees_invalid=0,
                            frees_double=0, frees_null=0)
+        self.rover = 0       # NEXT_FIT (reading C27): only allocations move it
 
     # ---- derived free blocks ----
     def runs(self):
@@ -95,6 +97,9 @@ class OracleB:
         blocks = self.blocks()
         if self.policy == FIRST_FIT:
             cand = [(s, s, z) for s, z in blocks if z >= r]
+        elif self.policy == NEXT_FIT:
+            # key (wrapped, start): blocks at or after the rover first, then from address 0
+            cand = [((s < self.rover, s), s, z) for s, z in blocks if z >= r]
         elif self.policy == BEST_FIT:
             cand = [((z, s), s, z) for s, z in blocks if z >= r]
         elif self.policy in (SEGFIT, TLSF):
@@ -107,6 +112,7 @@ class OracleB:
         _, s, _ = min(cand)
         self.bits[s:s + r] = False
         self.live[s] = r
+        self.rover = s + r
         return s
 
     def alloc_batch(self, sizes):

@@ -26,6 +26,10 @@
  *       SEGFIT_LIFO the paper's segregated fit verbatim: power-of-two bins used as stacks —
  *                  alloc pops the head (newest push) of the first nonempty bin >= ceil(log2 r),
  *                  every free / remainder is pushed at the head of its bin (Alg. 4/5)
+ *       NEXT_FIT   first fit resumed at a rover ("each traversal of the free list
+ *                  resumes from the last position"): the first block with start >= rover and
+ *                  size >= r, else (wrap) the first from the lowest address; after a carve the
+ *                  rover is the end of the allocation (reading C27)
  *       HYBRID     §5.3's hybrid: requests below a page (0 < s < 4096 B) go
  *                  to object pools managed by bitmasks (§3.2) — pool j holds
  *                  objects of align*2^j bytes, an allocation takes the pool's lowest free slot
@@ -50,7 +54,7 @@
 namespace {
 
 const uint64_t HEAP_NULL = ~0ull;
-enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6, HYBRID = 7 };
+enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6, HYBRID = 7, NEXT_FIT = 8 };
 const uint64_t PAGE = 4096;   /* "allocations smaller than a page (<4kB)" */
 
 /* floor(log2 u) for u >= 1, written as a plain loop */
@@ -94,6 +98,7 @@ struct Heap {
     std::set<std::tuple<uint64_t, uint64_t, uint64_t>> lifo_index;
     std::map<uint64_t, uint64_t> stamp_of;                 /* start -> push stamp */
     uint64_t clock = 0;
+    uint64_t rover = 0;                                   /* NEXT_FIT: where the next scan starts */
     std::vector<std::set<uint64_t>> bfree;                /* BUDDY: free starts per order */
     int K = 0;                                            /* BUDDY: max order */
     Counters c;
@@ -197,6 +202,15 @@ struct Heap {
                 if (kv.second >= r) return take(kv.first, r);
             return HEAP_NULL;
         }
+        if (policy == NEXT_FIT) {
+            /* scan from the rover to the end of the list, then from the start up to the rover */
+            auto at = freeb.lower_bound(rover);
+            for (auto it = at; it != freeb.end(); ++it)
+                if (it->second >= r) { rover = it->first + r; return take(it->first, r); }
+            for (auto it = freeb.begin(); it != at; ++it)
+                if (it->second >= r) { rover = it->first + r; return take(it->first, r); }
+            return HEAP_NULL;
+        }
         if (policy == BEST_FIT) {
             /* Alg. 3: scan the whole free list, keep the smallest fitting block; exact match
              * ends the scan.  Ties go to the lowest address (reading C3). */
@@ -245,7 +259,7 @@ extern "C" {
 
 void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
     if (align == 0 || (align & (align - 1)) || arena_bytes == 0 || arena_bytes % align) return nullptr;
-    if (policy < FIRST_FIT || policy > HYBRID) return nullptr;
+    if (policy < FIRST_FIT || policy > NEXT_FIT) return nullptr;
     if (policy == HYBRID) {
         /* reading C26: pool classes align*2^j <= PAGE; the first half of the arena is split
          * evenly between the pools, each share rounded down to a whole number of pages */

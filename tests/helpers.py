@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HEAP_NULL = (1 << 64) - 1
-POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6, "HYBRID": 7}
+POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6, "HYBRID": 7, "NEXT": 8}
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 

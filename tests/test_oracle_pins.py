@@ -24,7 +24,7 @@ from oracle.oracle_b import OracleB, OracleBHybrid, OracleBLifo, cls_lo, cls_of,
 from tests.helpers import HEAP_NULL, IdMap, check_invariants, hybrid_layout, parse_golden, replay
 
 FIT_POLICIES = [1, 2, 3, 4]
-ALL_POLICIES = [1, 2, 3, 4, 5, 6]
+ALL_POLICIES = [1, 2, 3, 4, 5, 6, 8]
 
 
 def run_case(H, case):
