@@ -64,7 +64,7 @@ enum heap_policy {
                            bins as stacks — an alloc pops the head (most recent
                            push) of the first nonempty bin >= ceil(log2 r); frees
                            and split remainders are pushed at the head      Alg. 4/5 */
-    HEAP_HYBRID = 7     /* §5.3 hybrid: requests of 0 < s < 4096 B
+    HEAP_HYBRID = 7,    /* §5.3 hybrid: requests of 0 < s < 4096 B
                            take the LOWEST free slot of a bitmask object pool
                            (§3.2) of align*2^j-byte objects, the
                            smallest that holds s; a full pool and every other
@@ -76,6 +76,10 @@ enum heap_policy {
                            plus TLSF free blocks; largest_free is the TLSF heap's.
                            heap_export lists pool runs / objects, then TLSF blocks.
                            max_live_blocks bounds the TLSF heap's live blocks only. */
+    HEAP_NEXT_FIT = 8   /* first fit resumed at a rover: the first
+                           block with start >= rover and size >= r, else the first
+                           from address 0; the rover is the end of the last
+                           allocation; frees leave it alone (C27) */
 };
 
 #define HEAP_NULL UINT64_MAX /* failed alloc; no-op in a free batch (offset 0 is valid, C18) */

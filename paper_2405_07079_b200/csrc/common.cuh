@@ -40,6 +40,7 @@ struct DevCtr {
     u64 eng[16];        // alloc engine diagnostics (engine_tlsf.cuh)
     u64 lifo_clock;     // SEGFIT_LIFO logical push clock (fits.cuh)
     u64 req_n;          // request count of a graph-launched batch (heap.cu graph path)
+    u64 rover;          // NEXT_FIT: unit address where the next search starts (reading C27)
 };
 
 enum { ERR_CAP_LIVE = 1, ERR_TABLE_FULL = 2, ERR_CAP_FREE = 4, ERR_ENGINE = 8 };

@@ -325,9 +325,14 @@ __global__ void k_ff_level(const u64 *__restrict__ below, u64 *__restrict__ abov
 
 constexpr int FF_MAX_LEVELS = 8;
 
+// NEXT_FIT (rover != nullptr, reading C27): the search starts at the first piece whose start is
+// >= the rover — walk up from that leaf checking only later siblings, descend into the first
+// subtree holding a fit — and wraps to the plain first-fit search from piece 0 when nothing at
+// or after the rover fits.  Pieces only shrink from their low end during the phase, so after a
+// carve of piece f the rover (its new start) is again at index f.
 __global__ void __launch_bounds__(32) k_ff_engine(u64 *tree, const u64 *__restrict__ lvl_off, int nlev,
                                                   u64 *fs, const u64 *F_dev, const u64 *__restrict__ r, u64 n,
-                                                  const u64 *n_in, u64 *__restrict__ out_u) {
+                                                  const u64 *n_in, u64 *__restrict__ out_u, u64 *rover) {
     const u32 lane = lane_id();
     if (n_in) n = *n_in;
     u64 sz[FF_MAX_LEVELS];
@@ -336,20 +341,71 @@ __global__ void __launch_bounds__(32) k_ff_engine(u64 *tree, const u64 *__restri
     for (int l = 1; l < nlev; l++) sz[l] = (sz[l - 1] + 31) >> 5;
     int top = 0;
     while (top + 1 < nlev && sz[top] > 32) top++;
+    u64 f0 = 0;                  // rover as a piece index
+    bool moved = false;
+    if (rover) {
+        const u64 R = *rover;
+        u64 lo = 0, hi = F;      // first piece with start >= R
+        while (hi - lo > 32) {
+            const u64 step = (hi - lo + 31) >> 5;
+            u64 idx = lo + (u64)(lane + 1) * step - 1;
+            if (idx >= hi) idx = hi - 1;
+            const u32 b = __ballot_sync(FULLMASK, fs[idx] >= R);
+            if (!b) { lo = hi; break; }
+            const u32 fl = __ffs(b) - 1;
+            const u64 nlo = lo + (u64)fl * step, nhi = lo + (u64)(fl + 1) * step;
+            lo = nlo;
+            hi = nhi < hi ? nhi : hi;
+        }
+        if (lo < hi) {
+            const u32 b = __ballot_sync(FULLMASK, lo + lane < hi && fs[lo + lane] >= R);
+            lo = b ? lo + __ffs(b) - 1 : hi;
+        }
+        f0 = lo;
+    }
     for (u64 i = 0; i < n; i++) {
         u64 ri = r[i];
         if (ri == 0 || F == 0) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
-        u64 j = 0;     // node index at the current level (level top has one node: 0)
-        bool fail = false;
-        for (int l = top; l >= 0; l--) {
-            u64 idx = j * 32 + lane;
-            u64 v = idx < sz[l] ? tree[lvl_off[l] + idx] : 0;
+        u64 f = ~0ull;
+        if (rover && f0 < F) {
+            // leaves of f0's group at or after f0
+            u64 g = f0 >> 5, idx = g * 32 + lane;
+            u64 v = (idx < sz[0] && idx >= f0) ? tree[lvl_off[0] + idx] : 0;
             u32 b = __ballot_sync(FULLMASK, v >= ri);
-            if (!b) { fail = true; break; }
-            j = j * 32 + __ffs(b) - 1;
+            if (b) f = g * 32 + __ffs(b) - 1;
+            u64 node = g;
+            for (int l = 1; l <= top && f == ~0ull; l++) {
+                g = node >> 5;
+                idx = g * 32 + lane;
+                v = (idx < sz[l] && idx > node) ? tree[lvl_off[l] + idx] : 0;
+                b = __ballot_sync(FULLMASK, v >= ri);
+                if (b) {
+                    u64 j = g * 32 + __ffs(b) - 1;
+                    for (int ll = l - 1; ll >= 0; ll--) {
+                        idx = j * 32 + lane;
+                        v = idx < sz[ll] ? tree[lvl_off[ll] + idx] : 0;
+                        j = j * 32 + __ffs(__ballot_sync(FULLMASK, v >= ri)) - 1;
+                    }
+                    f = j;
+                }
+                node = g;
+            }
         }
-        if (fail) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
-        u64 f = j;
+        if (f == ~0ull) {        // first fit from piece 0 (also the wrap-around of next fit)
+            u64 j = 0;           // node index at the current level (level top has one node: 0)
+            bool fail = false;
+            for (int l = top; l >= 0; l--) {
+                u64 idx = j * 32 + lane;
+                u64 v = idx < sz[l] ? tree[lvl_off[l] + idx] : 0;
+                u32 b = __ballot_sync(FULLMASK, v >= ri);
+                if (!b) { fail = true; break; }
+                j = j * 32 + __ffs(b) - 1;
+            }
+            if (fail) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+            f = j;
+        }
+        f0 = f;
+        moved = true;
         if (lane == 0) {
             u64 s = fs[f];
             out_u[i] = s;
@@ -368,6 +424,7 @@ __global__ void __launch_bounds__(32) k_ff_engine(u64 *tree, const u64 *__restri
             node = p;
         }
     }
+    if (rover && moved && lane == 0) *rover = fs[f0];   // the end of the last allocation
 }
 
 // -------------------------------------------------------------------- BEST FIT ----

@@ -46,7 +46,7 @@ struct Layout {
 
 bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, Layout *Lo) {
     if (align == 0 || (align & (align - 1)) || arena == 0 || arena % align) return false;
-    if (policy < HEAP_FIRST_FIT || policy > HEAP_HYBRID) return false;
+    if (policy < HEAP_FIRST_FIT || policy > HEAP_NEXT_FIT) return false;
     if (max_live == 0 || max_batch == 0 || max_batch >= (1ull << 31) || max_live >= (1ull << 30)) return false;
     Layout &L = *Lo;
     memset(&L, 0, sizeof(L));
@@ -173,7 +173,7 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.o_bk0 = take(L.cap_f * 8);          // (class, stamp) sort keys
         L.o_bk1 = take(L.cap_f * 8);
     }
-    if (policy == HEAP_FIRST_FIT) {
+    if (policy == HEAP_FIRST_FIT || policy == HEAP_NEXT_FIT) {
         L.o_tree = take(L.ff_tree * 8);
         L.o_lvl = take(fits::FF_MAX_LEVELS * 8);
     }
@@ -563,7 +563,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     cudaStream_t st = (cudaStream_t)s;
     LAUNCH(h, k_init, h->G, 256, 0, st, h->ctr, h->tbl, L.tcap, h->fs[0], h->fe[0], L.A_u,
            policy == HEAP_BUDDY ? 1 : 0, L.K);
-    if (policy == HEAP_FIRST_FIT) {
+    if (policy == HEAP_FIRST_FIT || policy == HEAP_NEXT_FIT) {
         u64 offs[fits::FF_MAX_LEVELS] = {0};
         u64 n = L.cap_f, o = 0;
         for (int l = 0; l < L.nlev && l < fits::FF_MAX_LEVELS; l++) { offs[l] = o; o += n; n = (n + 31) / 32; }
@@ -714,7 +714,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, tlsfw::k_bitheap_clear, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->slot, h->bm,
                L.bm_w0, L.bm_w1, L.bm_w2, L.NC, L.L);
-    } else if (h->policy == HEAP_FIRST_FIT) {
+    } else if (h->policy == HEAP_FIRST_FIT || h->policy == HEAP_NEXT_FIT) {
         u64 offs[fits::FF_MAX_LEVELS] = {0};
         u64 m = L.cap_f, o = 0;
         for (int l = 0; l < L.nlev; l++) { offs[l] = o; o += m; m = (m + 31) / 32; }
@@ -723,7 +723,8 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         for (int l = 1; l < L.nlev; l++)
             LAUNCH(h, fits::k_ff_level, h->G, 256, 0, s, h->tree + offs[l - 1], h->tree + offs[l], &C->F, l);
         TAG(h, HEAP_TAG_ENGINE);
-        LAUNCH(h, fits::k_ff_engine, 1, 32, 0, s, h->tree, h->lvl, L.nlev, h->fs[cur], &C->F, h->r, n, n_in, h->out);
+        LAUNCH(h, fits::k_ff_engine, 1, 32, 0, s, h->tree, h->lvl, L.nlev, h->fs[cur], &C->F, h->r, n, n_in, h->out,
+               h->policy == HEAP_NEXT_FIT ? &C->rover : (u64 *)nullptr);
     } else {   // BEST_FIT
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_bf_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.FB, h->bk[0]);

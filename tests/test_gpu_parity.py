@@ -104,6 +104,9 @@ SMALL = [
     (tg.HYBRID, 1 << 18, 16, 48, 3000, (4, 14), (1, 3), 0),              # §5.3 pools + TLSF
     (tg.HYBRID, 1 << 22, 16, 3000, 40000, (4, 14), (2, 5), 0),
     (tg.HYBRID, 1 << 24, 64, 5000, 60000, (4, 13), (1, 2), 0),
+    (tg.NEXT_FIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2), 0),           # first fit from a rover
+    (tg.NEXT_FIT, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
+    (tg.NEXT_FIT, 1 << 28, 16, 4096, 120000, (4, 20), (1, 2), 0),       # config-2 shaped
 ]
 
 
@@ -145,7 +148,7 @@ def test_config5_first_batches():
 def test_edge_cases():
     """Empty batches, NULL / interior / unaligned / out-of-range / duplicate frees,
     zero and oversize requests, OOM in a tiny arena, the last unit of a 2^32-unit arena."""
-    for pol in (1, 2, 3, 4, 5, 6, 7):
+    for pol in (1, 2, 3, 4, 5, 6, 7, 8):
         arena, align = 1 << 12, 16
         g = Gpu(arena, align, pol, 256, 64)
         o = OracleL(arena, align, pol)
@@ -274,7 +277,7 @@ def test_hybrid_config5_shape():
         assert gs[k] == os_[k], k
 
 
-@pytest.mark.parametrize("pol", [tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.BUDDY, tg.SEGFIT_LIFO, tg.HYBRID])
+@pytest.mark.parametrize("pol", [tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.BUDDY, tg.SEGFIT_LIFO, tg.HYBRID, tg.NEXT_FIT])
 def test_direct_launch_path(pol):
     """The same batches with batch graphs disabled (direct launches, the path tracing uses), and
     a heap switching between the two paths mid-trace."""
