@@ -1,4 +1,5 @@
-"""Dev tool: device-time throughput of every BASELINE config (a few batches each) vs the oracle."""
+"""Dev tool: device-time throughput of every BASELINE config (a few batches each) vs the oracle.
+Arguments: config ids, optionally "c:p" to run config c's trace under policy p."""
 import os
 import sys
 import time
@@ -6,14 +7,20 @@ import time
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import tracegen as tg  # noqa: E402
 from oracle import OracleL  # noqa: E402
 from paper_2405_07079_b200 import Heap  # noqa: E402
 
 NB = {1: 30, 2: 60, 3: 40, 4: 40, 5: 6}
-for c in [int(x) for x in (sys.argv[1:] or ["1", "2", "3", "4", "5"])]:
+for arg in (sys.argv[1:] or ["1", "2", "3", "4", "5"]):
+    c, _, pol = arg.partition(":")
+    c = int(c)
     cfg = tg.CONFIGS[c]
+    if pol:
+        cfg = tg.Config(cfg.idx, f"{cfg.name}-as-{tg.POLICY_NAME[int(pol)]}", int(pol), cfg.arena_bytes, cfg.align,
+                        cfg.model, cfg.batch, cfg.rho_num, cfg.rho_den, cfg.total_ops, cfg.size_kind, cfg.a, cfg.b,
+                        n_slots=cfg.n_slots, max_live=cfg.max_live)
     nb = NB[c]
     bs = list(tg.Trace(cfg, total_ops=cfg.batch * nb if cfg.model == 0 else None))[:nb]
     h = Heap(cfg.arena_bytes, cfg.align, cfg.policy, cfg.max_live, max(cfg.batch, 1000))

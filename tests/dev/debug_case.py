@@ -5,7 +5,7 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import tracegen as tg  # noqa: E402
 from oracle import OracleL  # noqa: E402
 from paper_2405_07079_b200 import Heap  # noqa: E402

@@ -1,6 +1,6 @@
 """Dev tool: sweep small SEGFIT_LIFO cases on the GPU against Oracle-L; for each failing case
 save (config, batch index, sizes, gpu out, oracle out) to gpurun_out/lifo_hunt/ for offline
-analysis.  Usage: python tools/lifo_hunt.py [max_cases]"""
+analysis.  Usage: PYTHONPATH=. python tests/dev/lifo_hunt.py [max_cases]"""
 import json
 import os
 import sys
@@ -8,7 +8,7 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import tracegen as tg  # noqa: E402
 from oracle import OracleL  # noqa: E402
 from paper_2405_07079_b200 import Heap  # noqa: E402
