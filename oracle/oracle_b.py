@@ -358,3 +358,71 @@ class OracleBHybrid:
         fp += [(int(s) + self.pool_end, int(z)) for s, z in sf]
         lp += [(int(s) + self.pool_end, int(z)) for s, z in sl]
         return (np.array(fp, dtype=np.uint64).reshape(-1, 2), np.array(lp, dtype=np.uint64).reshape(-1, 2))
+
+
+class OracleBDouble:
+    """Brute-force twin of Oracle-L's DOUBLE_BUDDY (reading C28): two OracleB
+    binary-buddy heaps (unit bitmaps, blocks derived on every call), the second counting in
+    units of 3*align.  The class choice is written from its definition: the smallest block of
+    either family {2^k} / {3 * 2^k} (units) that holds the request."""
+
+    def __init__(self, arena_bytes: int, align: int, policy: int = 9):
+        assert policy == 9
+        self.align, self.arena = align, arena_bytes
+        self.N3 = arena_bytes // (6 * align)
+        self.A_bytes = arena_bytes - 3 * align * self.N3
+        self.a = OracleB(self.A_bytes, align, BUDDY)
+        self.b = OracleB(self.N3, 1, BUDDY) if self.N3 else None
+        self.own = dict(frees_null=0, frees_invalid=0)
+
+    @property
+    def counts(self):
+        c = dict(self.a.counts)
+        if self.b:
+            for k, v in self.b.counts.items():
+                c[k] += v
+        for k, v in self.own.items():
+            c[k] += v
+        return c
+
+    @property
+    def live(self):
+        return [int(o) for o, _ in self.export()[1]]
+
+    def alloc_batch(self, sizes):
+        out = np.empty(len(sizes), dtype=np.uint64)
+        for i, s in enumerate(int(x) for x in sizes):
+            r = -(-s // self.align)
+            two = next(1 << k for k in range(80) if (1 << k) >= r)
+            three = next(3 << k for k in range(80) if (3 << k) >= r)
+            if s and r <= self.arena // self.align and self.b and three < two:
+                u = int(self.b.alloc_batch(np.array([three // 3], dtype=np.uint64))[0])
+                out[i] = HEAP_NULL if u == HEAP_NULL else self.A_bytes + u * 3 * self.align
+            else:
+                out[i] = self.a.alloc_batch(np.array([s], dtype=np.uint64))[0]
+        return out
+
+    def free_batch(self, offsets):
+        fa, fb = [], []
+        for o in (int(x) for x in offsets):
+            if o == HEAP_NULL:
+                self.own["frees_null"] += 1
+            elif o < self.A_bytes:
+                fa.append(o)
+            elif self.b is None or (o - self.A_bytes) % (3 * self.align):
+                self.own["frees_invalid"] += 1
+            else:
+                fb.append((o - self.A_bytes) // (3 * self.align))
+        self.a.free_batch(np.array(fa, dtype=np.uint64))
+        if self.b:
+            self.b.free_batch(np.array(fb, dtype=np.uint64))
+
+    def export(self):
+        fa, la = self.a.export()
+        fp, lp = [tuple(map(int, x)) for x in fa], [tuple(map(int, x)) for x in la]
+        if self.b:
+            fb, lb = self.b.export()
+            m = 3 * self.align
+            fp += [(self.A_bytes + int(s) * m, int(z) * m) for s, z in fb]
+            lp += [(self.A_bytes + int(s) * m, int(z) * m) for s, z in lb]
+        return (np.array(fp, dtype=np.uint64).reshape(-1, 2), np.array(lp, dtype=np.uint64).reshape(-1, 2))

@@ -30,6 +30,10 @@
  *                  resumes from the last position"): the first block with start >= rover and
  *                  size >= r, else (wrap) the first from the lowest address; after a carve the
  *                  rover is the end of the allocation (reading C27)
+ *       DOUBLE_BUDDY double buddies ("two heaps with staggered class sizes, e.g.
+ *                  2, 4, 8, ... and 3, 6, 12, ..."): a binary buddy heap of align-sized units on
+ *                  [0, A_bytes) and one of 3*align-sized units on [A_bytes, arena); a request
+ *                  goes to the heap whose class is smaller (no fallback; reading C28)
  *       HYBRID     §5.3's hybrid: requests below a page (0 < s < 4096 B) go
  *                  to object pools managed by bitmasks (§3.2) — pool j holds
  *                  objects of align*2^j bytes, an allocation takes the pool's lowest free slot
@@ -54,7 +58,8 @@
 namespace {
 
 const uint64_t HEAP_NULL = ~0ull;
-enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6, HYBRID = 7, NEXT_FIT = 8 };
+enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6, HYBRID = 7, NEXT_FIT = 8,
+       DOUBLE_BUDDY = 9 };
 const uint64_t PAGE = 4096;   /* "allocations smaller than a page (<4kB)" */
 
 /* floor(log2 u) for u >= 1, written as a plain loop */
@@ -111,7 +116,11 @@ struct Heap {
     std::vector<std::set<uint64_t>> freed;
     uint64_t pool_live_n = 0, pool_live_b = 0;
     Heap *sub = nullptr;
-    ~Heap() { delete sub; }
+    /* DOUBLE_BUDDY: heap `sub` (units of align on [0, A_bytes)) and `sub3` (units of 3*align on
+     * [A_bytes, arena)); sub3 is a plain buddy heap whose "bytes" are those 3*align units */
+    Heap *sub3 = nullptr;
+    uint64_t A_bytes = 0, N3 = 0;
+    ~Heap() { delete sub; delete sub3; }
 
     bool slot_free(int j, uint64_t t) const { return t >= fresh[j] || freed[j].count(t); }
     /* lowest free slot of pool j, or HEAP_NULL when the pool is full */
@@ -259,7 +268,21 @@ extern "C" {
 
 void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
     if (align == 0 || (align & (align - 1)) || arena_bytes == 0 || arena_bytes % align) return nullptr;
-    if (policy < FIRST_FIT || policy > NEXT_FIT) return nullptr;
+    if (policy < FIRST_FIT || policy > DOUBLE_BUDDY) return nullptr;
+    if (policy == DOUBLE_BUDDY) {
+        /* reading C28: the 3-unit heap gets floor(arena / (6 align)) units at the top of the
+         * arena, the binary heap everything below (at least half) */
+        Heap *h = new Heap();
+        h->policy = DOUBLE_BUDDY;
+        h->align = align;
+        h->arena_bytes = arena_bytes;
+        h->A_u = arena_bytes / align;
+        h->N3 = arena_bytes / (6 * align);
+        h->A_bytes = arena_bytes - 3 * align * h->N3;
+        h->sub = (Heap *)oracle_create(h->A_bytes, align, BUDDY);
+        h->sub3 = h->N3 ? (Heap *)oracle_create(h->N3, 1, BUDDY) : nullptr;
+        return h;
+    }
     if (policy == HYBRID) {
         /* reading C26: pool classes align*2^j <= PAGE; the first half of the arena is split
          * evenly between the pools, each share rounded down to a whole number of pages */
@@ -336,9 +359,26 @@ static void hybrid_free_batch(Heap *h, const uint64_t *offsets, uint64_t n) {
     oracle_free_batch(h->sub, sub_offs.data(), sub_offs.size());
 }
 
+/* DOUBLE_BUDDY frees: an offset below A_bytes is the binary heap's; above, it must be a whole
+ * number of 3*align units past A_bytes and is the 3-unit heap's unit index (else invalid) */
+static void double_free_batch(Heap *h, const uint64_t *offsets, uint64_t n) {
+    std::vector<uint64_t> a, b;
+    const uint64_t u3 = 3 * h->align;
+    for (uint64_t i = 0; i < n; i++) {
+        uint64_t o = offsets[i];
+        if (o == HEAP_NULL) { h->c.frees_null++; continue; }
+        if (o < h->A_bytes) { a.push_back(o); continue; }
+        if ((o - h->A_bytes) % u3 || !h->sub3) { h->c.frees_invalid++; continue; }
+        b.push_back((o - h->A_bytes) / u3);
+    }
+    oracle_free_batch(h->sub, a.data(), a.size());
+    if (h->sub3) oracle_free_batch(h->sub3, b.data(), b.size());
+}
+
 void oracle_free_batch(void *p, const uint64_t *offsets, uint64_t n) {
     Heap *h = (Heap *)p;
     if (h->policy == HYBRID) { hybrid_free_batch(h, offsets, n); return; }
+    if (h->policy == DOUBLE_BUDDY) { double_free_batch(h, offsets, n); return; }
     std::vector<uint64_t> v(offsets, offsets + n);
     std::sort(v.begin(), v.end());
     std::vector<uint64_t> to_free;
@@ -362,6 +402,27 @@ void oracle_free_batch(void *p, const uint64_t *offsets, uint64_t n) {
 
 void oracle_alloc_batch(void *p, const uint64_t *sizes, uint64_t n, uint64_t *out) {
     Heap *h = (Heap *)p;
+    if (h->policy == DOUBLE_BUDDY) {
+        /* r units -> binary class 2^ceil(log2 r) or 3-unit class 3 * 2^ceil(log2 ceil(r/3)),
+         * whichever is smaller (they are never equal); that heap alone serves it (C28) */
+        for (uint64_t i = 0; i < n; i++) {
+            uint64_t s = sizes[i];
+            uint64_t r = s / h->align + (s % h->align != 0);
+            uint64_t p2 = 1, q = (r + 2) / 3, p3 = 1;
+            while (p2 < r) p2 <<= 1;
+            while (p3 < q) p3 <<= 1;
+            uint64_t o = HEAP_NULL;
+            if (s != 0 && r <= h->A_u && h->sub3 && 3 * p3 < p2) {
+                uint64_t t = q, u = HEAP_NULL;
+                oracle_alloc_batch(h->sub3, &t, 1, &u);
+                o = (u == HEAP_NULL) ? HEAP_NULL : h->A_bytes + u * 3 * h->align;
+            } else {
+                oracle_alloc_batch(h->sub, &s, 1, &o);
+            }
+            out[i] = o;
+        }
+        return;
+    }
     if (h->policy == HYBRID) {
         /* request order; a sub-page request takes the lowest free slot of the smallest pool whose
          * objects hold it, else (pool full, or s >= PAGE, or s = 0) the TLSF heap serves it */
@@ -428,6 +489,19 @@ static std::vector<std::pair<uint64_t, uint64_t>> pool_runs(const Heap *h, int j
 
 void oracle_stats(void *p, uint64_t *o) {
     Heap *h = (Heap *)p;
+    if (h->policy == DOUBLE_BUDDY) {
+        uint64_t a[16], b[16] = {0};
+        oracle_stats(h->sub, a);
+        if (h->sub3) oracle_stats(h->sub3, b);
+        const uint64_t u3 = 3 * h->align;
+        uint64_t live = a[2] + b[2] * u3;
+        uint64_t hw = std::max(a[7], b[7] ? h->A_bytes + b[7] * u3 : 0);
+        uint64_t vals[16] = {h->arena_bytes, h->align, live, h->arena_bytes - live, a[4] + b[4], a[5] + b[5],
+                             std::max(a[6], b[6] * u3), hw, a[8] + b[8], a[9] + b[9], a[10] + b[10],
+                             a[11] + b[11] + h->c.frees_invalid, a[12] + b[12], a[13] + b[13] + h->c.frees_null, 0, 0};
+        memcpy(o, vals, sizeof(vals));
+        return;
+    }
     if (h->policy == HYBRID) {
         /* pools + TLSF heap; largest_free is the TLSF heap's (reading C26); counters add up */
         uint64_t sv[16];
@@ -466,6 +540,27 @@ void oracle_stats(void *p, uint64_t *o) {
 void oracle_export(void *p, uint64_t *free_pairs, uint64_t cap_free, uint64_t *live_pairs,
                    uint64_t cap_live, uint64_t *counts) {
     Heap *h = (Heap *)p;
+    if (h->policy == DOUBLE_BUDDY) {
+        /* the binary heap's blocks (below A_bytes), then the 3-unit heap's, in bytes */
+        std::vector<uint64_t> fp, lp;
+        const uint64_t u3 = 3 * h->align;
+        for (int part = 0; part < 2; part++) {
+            Heap *x = part ? h->sub3 : h->sub;
+            if (!x) continue;
+            uint64_t sc[2];
+            oracle_export(x, nullptr, 0, nullptr, 0, sc);
+            std::vector<uint64_t> sf(2 * sc[0] + 2), sl(2 * sc[1] + 2);
+            oracle_export(x, sf.data(), sc[0], sl.data(), sc[1], sc);
+            const uint64_t base = part ? h->A_bytes : 0, mul = part ? u3 : 1;
+            for (uint64_t k = 0; k < sc[0]; k++) { fp.push_back(base + sf[2 * k] * mul); fp.push_back(sf[2 * k + 1] * mul); }
+            for (uint64_t k = 0; k < sc[1]; k++) { lp.push_back(base + sl[2 * k] * mul); lp.push_back(sl[2 * k + 1] * mul); }
+        }
+        counts[0] = fp.size() / 2;
+        counts[1] = lp.size() / 2;
+        for (uint64_t k = 0; k < counts[0] && k < cap_free; k++) { free_pairs[2 * k] = fp[2 * k]; free_pairs[2 * k + 1] = fp[2 * k + 1]; }
+        for (uint64_t k = 0; k < counts[1] && k < cap_live; k++) { live_pairs[2 * k] = lp[2 * k]; live_pairs[2 * k + 1] = lp[2 * k + 1]; }
+        return;
+    }
     if (h->policy == HYBRID) {
         /* pool runs / objects first (they lie below pool_end), then the TLSF heap's, shifted */
         std::vector<uint64_t> fp, lp;

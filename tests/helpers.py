@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HEAP_NULL = (1 << 64) - 1
-POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6, "HYBRID": 7, "NEXT": 8}
+POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6, "HYBRID": 7, "NEXT": 8, "DOUBLE": 9}
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
@@ -55,6 +55,28 @@ def hybrid_layout(arena: int, align: int):
     share = arena // (2 * len(obj)) if obj else 0
     S = share - share % 4096
     return S, len(obj) * S, obj
+
+
+def double_layout(arena: int, align: int):
+    """(A_bytes, N3) of a DOUBLE_BUDDY heap, reading C28."""
+    n3 = arena // (6 * align)
+    return arena - 3 * align * n3, n3
+
+
+def check_double_invariants(free_pairs, live_pairs, arena: int, align: int):
+    """DOUBLE_BUDDY: each heap separately satisfies the buddy invariants in its own units."""
+    A_bytes, n3 = double_layout(arena, align)
+    fp = np.asarray(free_pairs, dtype=np.uint64).reshape(-1, 2)
+    lp = np.asarray(live_pairs, dtype=np.uint64).reshape(-1, 2)
+    lo_f, lo_l = fp[fp[:, 0] < A_bytes], lp[lp[:, 0] < A_bytes]
+    check_invariants(lo_f, lo_l, A_bytes, align, True)
+    if n3:
+        m = np.uint64(3 * align)
+        hi_f, hi_l = fp[fp[:, 0] >= A_bytes], lp[lp[:, 0] >= A_bytes]
+        assert np.all((hi_f[:, 0] - np.uint64(A_bytes)) % m == 0) and np.all(hi_f[:, 1] % m == 0)
+        assert np.all((hi_l[:, 0] - np.uint64(A_bytes)) % m == 0) and np.all(hi_l[:, 1] % m == 0)
+        to_u = lambda a: np.c_[(a[:, 0] - np.uint64(A_bytes)) // m, a[:, 1] // m]  # noqa: E731
+        check_invariants(to_u(hi_f), to_u(hi_l), n3, 1, True)
 
 
 def check_invariants(free_pairs, live_pairs, arena: int, align: int, buddy: bool, region_edges=()):

@@ -20,8 +20,9 @@ import tracegen as tg
 from oracle import OracleL, insert_class, search_class
 import copy
 
-from oracle.oracle_b import OracleB, OracleBHybrid, OracleBLifo, cls_lo, cls_of, search_cls
-from tests.helpers import HEAP_NULL, IdMap, check_invariants, hybrid_layout, parse_golden, replay
+from oracle.oracle_b import OracleB, OracleBDouble, OracleBHybrid, OracleBLifo, cls_lo, cls_of, search_cls
+from tests.helpers import (HEAP_NULL, IdMap, check_double_invariants, check_invariants, double_layout, hybrid_layout,
+                           parse_golden, replay)
 
 FIT_POLICIES = [1, 2, 3, 4]
 ALL_POLICIES = [1, 2, 3, 4, 5, 6, 8]
@@ -213,7 +214,10 @@ def _run_both(policy, arena, align, batch, ops, sizes, rho, idx, size_kind=0):
         fl, ll = hl.export()
         fb, lb = hb.export()
         assert np.array_equal(fl, fb) and np.array_equal(ll, lb), (policy, bi)
-        check_invariants(fl, ll, arena, align, policy == tg.BUDDY, _edges(policy, arena, align))
+        if policy == 9:
+            check_double_invariants(fl, ll, arena, align)
+        else:
+            check_invariants(fl, ll, arena, align, policy == tg.BUDDY, _edges(policy, arena, align))
     st = hl.stats()
     for k, v in hb.counts.items():
         assert st[k] == v, k
@@ -282,7 +286,7 @@ def test_exhaustive_tiny_heaps(policy):
 
 
 def _twin(policy):
-    return {6: OracleBLifo, 7: OracleBHybrid}.get(policy, OracleB)
+    return {6: OracleBLifo, 7: OracleBHybrid, 9: OracleBDouble}.get(policy, OracleB)
 
 
 def _edges(policy, arena, align):
@@ -450,3 +454,66 @@ def test_hybrid_exhaustive_tiny():
         assert st["live_bytes"] + st["free_bytes"] == arena
         n += 1
     assert n > 4000
+
+
+# ---------------- DOUBLE_BUDDY (two staggered buddy heaps; reading C28) ----------------
+
+@pytest.mark.parametrize("seed", range(4))
+def test_double_buddy_oracle_l_equals_oracle_b(seed):
+    _run_both(9, 6 * 1024 * 16, 16, 24, 1200, (4, 12), (1, 2) if seed % 2 else (2, 5), 110 + seed)
+
+
+def test_double_buddy_layout_classes_and_taxonomy():
+    """Layout (the 3-unit heap gets floor(arena / 6 align) units at the top), the class choice
+    (smaller of 2^a and 3 * 2^b units — never equal), frees at a non-multiple of 3*align past
+    A_bytes are invalid, and both heaps merge buddies back."""
+    assert double_layout(98304, 16) == (49152, 1024)
+    assert double_layout(1000, 16) == (1000 - 48 * 10, 10)
+    for r in range(1, 5000):
+        two = 1 << (r - 1).bit_length()
+        three = 3 * (1 << (-(-r // 3) - 1).bit_length())
+        assert two != three and max(two, three) >= r and min(two, three) >= r
+    for H in (OracleL, OracleBDouble):
+        h = H(98304, 16, 9)
+        a = [int(x) for x in h.alloc_batch([48, 16, 96])]
+        assert a == [49152, 32768, 49248], H               # 96 B = 6 units -> 3-unit class 6
+        h.free_batch(np.array([49152 + 16, 49152 + 48, 49152, 49152, HEAP_NULL, 32768], dtype=np.uint64))
+        c = h.stats() if H is OracleL else h.counts
+        assert (c["frees_ok"], c["frees_invalid"], c["frees_double"], c["frees_null"]) == (2, 1, 2, 1), (H, c)   # 49152+48 is a free 3-unit block start: double
+        fp, lp = h.export()
+        assert [tuple(int(v) for v in p) for p in lp] == [(49248, 96)]
+        check_double_invariants(fp, lp, 98304, 16)
+
+
+def test_double_buddy_exhaustive_tiny():
+    """Every sequence of <= 4 ops on a 12-unit heap (align 1: 3-unit heap of 2 units = [6, 12),
+    binary heap of 6 units = 4 @0 + 2 @4): allocs of 1..7 units, frees of any live block."""
+    arena = 12
+
+    def leaves(depth, seq, hb):
+        yield seq
+        if depth == 0:
+            return
+        for s in range(1, 8):
+            hb2 = copy.deepcopy(hb)
+            hb2.alloc_batch([s])
+            yield from leaves(depth - 1, seq + [("a", s)], hb2)
+        for o in hb.live:
+            hb2 = copy.deepcopy(hb)
+            hb2.free_batch([o])
+            yield from leaves(depth - 1, seq + [("f", o)], hb2)
+
+    n = 0
+    for seq in leaves(4, [], OracleBDouble(arena, 1)):
+        hl, hb = OracleL(arena, 1, 9), OracleBDouble(arena, 1)
+        for op, v in seq:
+            if op == "a":
+                assert int(hl.alloc_batch([v])[0]) == int(hb.alloc_batch([v])[0]), seq
+            else:
+                hl.free_batch([v])
+                hb.free_batch([v])
+        fl, ll = hl.export()
+        fb, lb = hb.export()
+        assert np.array_equal(fl, fb) and np.array_equal(ll, lb), seq
+        n += 1
+    assert n > 2000
