@@ -76,10 +76,18 @@ enum heap_policy {
                            plus TLSF free blocks; largest_free is the TLSF heap's.
                            heap_export lists pool runs / objects, then TLSF blocks.
                            max_live_blocks bounds the TLSF heap's live blocks only. */
-    HEAP_NEXT_FIT = 8   /* first fit resumed at a rover: the first
+    HEAP_NEXT_FIT = 8,  /* first fit resumed at a rover: the first
                            block with start >= rover and size >= r, else the first
                            from address 0; the rover is the end of the last
                            allocation; frees leave it alone (C27) */
+    HEAP_DOUBLE_BUDDY = 9 /* double buddies: a binary buddy heap of
+                           align-sized units on [0, A) and one of 3*align-sized units
+                           (blocks 3*2^k*align) on [A, arena) holding
+                           floor(arena / 6 align) units; a request of r units goes to
+                           the heap with the smaller class, 2^ceil(log2 r) or
+                           3*2^ceil(log2 ceil(r/3)) units, with no fallback
+                           (C28).  Offsets past A must be whole 3-units.
+                           max_live_blocks bounds each heap's live blocks. */
 };
 
 #define HEAP_NULL UINT64_MAX /* failed alloc; no-op in a free batch (offset 0 is valid, C18) */

@@ -16,6 +16,7 @@
 #include "fits.cuh"
 #include "engine_tlsf.cuh"
 #include "pool.cuh"
+#include "dbuddy.cuh"
 
 namespace {
 
@@ -42,16 +43,53 @@ struct Layout {
     pool::Geom geo;
     u64 o_pctr, o_bits, o_sbcnt, o_sbpre, o_tsz, o_tout, o_toff, o_tidx, o_coff, o_sstats, o_sub, sub_total;
     u64 o_gin, o_gout;   // graph path: staging of the request / result words
+    // HEAP_DOUBLE_BUDDY: the 3-unit heap's geometry and the split / merge buffers
+    u64 dbl_A, dbl_n3, o_dctr, o_ca, o_cb, o_ia, o_ib, o_ra, o_rb, o_sstats2, o_sub2, sub2_total;
 };
 
 bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, Layout *Lo) {
     if (align == 0 || (align & (align - 1)) || arena == 0 || arena % align) return false;
-    if (policy < HEAP_FIRST_FIT || policy > HEAP_NEXT_FIT) return false;
+    if (policy < HEAP_FIRST_FIT || policy > HEAP_DOUBLE_BUDDY) return false;
     if (max_live == 0 || max_batch == 0 || max_batch >= (1ull << 31) || max_live >= (1ull << 30)) return false;
     Layout &L = *Lo;
     memset(&L, 0, sizeof(L));
     L.A_u = arena / align;
     if (L.A_u > (1ull << 32)) return false;
+    if (policy == HEAP_DOUBLE_BUDDY) {
+        // reading C28 (dbuddy.cuh): the 3-unit heap gets floor(arena / 6 align) units at the top
+        L.dbl_n3 = arena / (6 * align);
+        L.dbl_A = arena - 3 * align * L.dbl_n3;
+        Layout la, lb;
+        if (!make_layout(L.dbl_A, align, HEAP_BUDDY, max_live, max_batch, &la)) return false;
+        if (L.dbl_n3 && !make_layout(L.dbl_n3, 1, HEAP_BUDDY, max_live, max_batch, &lb)) return false;
+        u64 o = 0;
+        auto take = [&](u64 bytes) { u64 r = o; o = align_up(o + bytes, 256); return r; };
+        L.o_ctr = take(sizeof(DevCtr));
+        L.o_stats = take(sizeof(heap_stats_t));
+        L.o_dctr = take(sizeof(dbl::Ctr));
+        L.o_flags = take(max_batch * 4 + 4);
+        L.o_pos = take(max_batch * 4 + 4);
+        L.o_kA = take(max_batch * 4 + 4);
+        L.o_kB = take(max_batch * 4 + 4);
+        L.o_tsum = take((prims::ntiles_of(max_batch) + 16) * 4);
+        L.o_tsz = take(max_batch * 8);
+        L.o_toff = take(max_batch * 8);
+        L.o_ca = take(max_batch * 8);
+        L.o_cb = take(max_batch * 8);
+        L.o_ia = take(max_batch * 4);
+        L.o_ib = take(max_batch * 4);
+        L.o_ra = take(max_batch * 8);
+        L.o_rb = take(max_batch * 8);
+        L.o_sstats = take(sizeof(heap_stats_t));
+        L.o_sstats2 = take(sizeof(heap_stats_t));
+        L.o_gin = take(max_batch * 8);
+        L.o_gout = take(max_batch * 8);
+        L.o_sub = take(la.total);
+        L.sub_total = la.total;
+        if (L.dbl_n3) { L.o_sub2 = take(lb.total); L.sub2_total = lb.total; }
+        L.total = o;
+        return true;
+    }
     if (policy == HEAP_HYBRID) {
         // reading C26 (pool.cuh): pools of align*2^j <= 4096 B objects share the first half of the
         // arena, each a whole number of pages; the TLSF heap covers the rest
@@ -222,7 +260,12 @@ struct heap {
     u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
     u64 *baddr, *bufA, *bufB, *promo, *fr;
     // HEAP_HYBRID
-    heap *sub;                                // the TLSF heap on [pool_end, arena)
+    heap *sub;                                // HYBRID: the TLSF heap on [pool_end, arena); DOUBLE: the binary heap
+    heap *sub2;                               // DOUBLE_BUDDY: the 3-unit heap (NULL if it has no units)
+    dbl::Ctr *dctr;
+    u64 *ca, *cb, *ra, *rb;
+    u32 *ia, *ib;
+    heap_stats_t *sstats2;
     pool::Ctr *pctr;
     u32 *bits, *sbcnt, *sbpre, *tidx, *coff;
     u64 *tsz, *tout, *toff;
@@ -232,7 +275,7 @@ struct heap {
         cudaGraphExec_t exec = nullptr;
         cudaGraph_t graph = nullptr;          // kept alive: the exec's node handles refer to it
         cudaGraphNode_t set_n = nullptr, cin = nullptr, cout = nullptr;
-        int cur_after = 0, subcur_after = 0;
+        int cur_after = 0, subcur_after = 0, sub2cur_after = 0;
         u64 nlaunch = 0;
     };
     int graphs;
@@ -501,6 +544,31 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     if (cudaFuncSetAttribute(buddy::k_alloc_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)buddy::ALLOC_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     void *w = d_workspace;
+    if (policy == HEAP_DOUBLE_BUDDY) {
+        cudaStream_t st = (cudaStream_t)s;
+        h->ctr = at<DevCtr>(w, L.o_ctr);
+        h->dstats = at<heap_stats_t>(w, L.o_stats);
+        h->dctr = at<dbl::Ctr>(w, L.o_dctr);
+        h->flags = at<u32>(w, L.o_flags); h->pos = at<u32>(w, L.o_pos);
+        h->kA = at<u32>(w, L.o_kA); h->kB = at<u32>(w, L.o_kB); h->tsum = at<u32>(w, L.o_tsum);
+        h->tsz = at<u64>(w, L.o_tsz); h->toff = at<u64>(w, L.o_toff);
+        h->ca = at<u64>(w, L.o_ca); h->cb = at<u64>(w, L.o_cb); h->ia = at<u32>(w, L.o_ia); h->ib = at<u32>(w, L.o_ib);
+        h->ra = at<u64>(w, L.o_ra); h->rb = at<u64>(w, L.o_rb);
+        h->sstats = at<heap_stats_t>(w, L.o_sstats); h->sstats2 = at<heap_stats_t>(w, L.o_sstats2);
+        h->gin = at<u64>(w, L.o_gin); h->gout = at<u64>(w, L.o_gout);
+        h->graphs = 1;
+        h->cur = 0; h->launches = 0; h->prof_mask = 0; h->tag = HEAP_TAG_MISC;
+        if (cudaMemsetAsync(h->ctr, 0, sizeof(DevCtr), st) != cudaSuccess ||
+            cudaMemsetAsync(h->dctr, 0, sizeof(dbl::Ctr), st) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+        int rc = heap_create(L.dbl_A, align, HEAP_BUDDY, max_live_blocks, max_batch, at<char>(w, L.o_sub), L.sub_total,
+                             s, &h->sub);
+        if (rc == HEAP_OK && L.dbl_n3)
+            rc = heap_create(L.dbl_n3, 1, HEAP_BUDDY, max_live_blocks, max_batch, at<char>(w, L.o_sub2), L.sub2_total, s,
+                             &h->sub2);
+        if (rc != HEAP_OK) { if (h->sub) heap_destroy(h->sub); delete h; return rc; }
+        *h_out = h;
+        return HEAP_OK;
+    }
     if (policy == HEAP_HYBRID) {
         cudaStream_t st = (cudaStream_t)s;
         h->ctr = at<DevCtr>(w, L.o_ctr);
@@ -577,6 +645,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
 int heap_destroy(heap_t *h) {
     if (!h) return HEAP_EINVAL;
     if (h->sub) heap_destroy(h->sub);
+    if (h->sub2) heap_destroy(h->sub2);
     for (auto &a : h->gs)
         for (auto &b : a)
             for (auto &g : b) {
@@ -590,7 +659,9 @@ int heap_destroy(heap_t *h) {
     return HEAP_OK;
 }
 
-uint64_t heap_launch_count(const heap_t *h) { return h ? h->launches + (h->sub ? h->sub->launches : 0) : 0; }
+uint64_t heap_launch_count(const heap_t *h) {
+    return h ? h->launches + (h->sub ? h->sub->launches : 0) + (h->sub2 ? h->sub2->launches : 0) : 0;
+}
 
 }  // extern "C"
 
@@ -760,10 +831,54 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
 static int hybrid_free(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *n_in, cudaStream_t s);
 static int hybrid_alloc(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, const u64 *n_in, cudaStream_t s);
 
+// ---- HEAP_DOUBLE_BUDDY (dbuddy.cuh): split a batch between the two buddy heaps ----
+static int double_free(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *n_in, cudaStream_t s) {
+    dbl::Ctr *D = h->dctr;
+    const int has3 = h->sub2 != nullptr;
+    TAG(h, HEAP_TAG_CLASSIFY);
+    LAUNCH(h, dbl::k_free_split, h->G, 256, 0, s, (const u64 *)d_offsets, n, n_in, h->L.dbl_A, 3 * h->align, has3,
+           h->flags, h->kA, h->tsz, h->toff, D);
+    TAG(h, HEAP_TAG_SCAN);
+    scan(h, h->flags, h->pos, &D->nreq, &D->nA, s);
+    scan(h, h->kA, h->kB, &D->nreq, &D->nB, s);
+    TAG(h, HEAP_TAG_COMPACT);
+    LAUNCH(h, dbl::k_compact_idx, h->G, 256, 0, s, h->tsz, h->flags, h->pos, &D->nreq, h->ca, (u32 *)nullptr);
+    LAUNCH(h, dbl::k_compact_idx, h->G, 256, 0, s, h->toff, h->kA, h->kB, &D->nreq, h->cb, (u32 *)nullptr);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    int rc = free_impl(h->sub, (const uint64_t *)h->ca, n, &D->nA, s);
+    if (rc == HEAP_OK && has3) rc = free_impl(h->sub2, (const uint64_t *)h->cb, n, &D->nB, s);
+    return rc;
+}
+
+static int double_alloc(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, const u64 *n_in, cudaStream_t s) {
+    dbl::Ctr *D = h->dctr;
+    const int has3 = h->sub2 != nullptr;
+    TAG(h, HEAP_TAG_ALLOC_PREP);
+    LAUNCH(h, dbl::k_alloc_split, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, h->arena / h->align, has3,
+           h->flags, h->kA, h->tsz, h->toff, D);
+    TAG(h, HEAP_TAG_SCAN);
+    scan(h, h->flags, h->pos, &D->nreq, &D->nA, s);
+    scan(h, h->kA, h->kB, &D->nreq, &D->nB, s);
+    TAG(h, HEAP_TAG_COMPACT);
+    LAUNCH(h, dbl::k_compact_idx, h->G, 256, 0, s, h->tsz, h->flags, h->pos, &D->nreq, h->ca, h->ia);
+    LAUNCH(h, dbl::k_compact_idx, h->G, 256, 0, s, h->toff, h->kA, h->kB, &D->nreq, h->cb, h->ib);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    int rc = alloc_impl(h->sub, (const uint64_t *)h->ca, (uint64_t *)h->ra, n, &D->nA, s);
+    if (rc == HEAP_OK && has3) rc = alloc_impl(h->sub2, (const uint64_t *)h->cb, (uint64_t *)h->rb, n, &D->nB, s);
+    if (rc != HEAP_OK) return rc;
+    TAG(h, HEAP_TAG_FINISH);
+    LAUNCH(h, dbl::k_scatter, h->G, 256, 0, s, h->ra, h->ia, &D->nA, 0ull, 1ull, (u64 *)d_out);
+    if (has3) LAUNCH(h, dbl::k_scatter, h->G, 256, 0, s, h->rb, h->ib, &D->nB, h->L.dbl_A, 3 * h->align, (u64 *)d_out);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    return HEAP_OK;
+}
+
 static int batch_free(heap *h, const uint64_t *in, uint64_t n, const u64 *n_in, cudaStream_t s) {
+    if (h->policy == HEAP_DOUBLE_BUDDY) return double_free(h, in, n, n_in, s);
     return h->policy == HEAP_HYBRID ? hybrid_free(h, in, n, n_in, s) : free_impl(h, in, n, n_in, s);
 }
 static int batch_alloc(heap *h, const uint64_t *in, uint64_t *out, uint64_t n, const u64 *n_in, cudaStream_t s) {
+    if (h->policy == HEAP_DOUBLE_BUDDY) return double_alloc(h, in, out, n, n_in, s);
     return h->policy == HEAP_HYBRID ? hybrid_alloc(h, in, out, n, n_in, s) : alloc_impl(h, in, out, n, n_in, s);
 }
 
@@ -786,7 +901,7 @@ __global__ void k_set_req_n(DevCtr *ctr, u64 n) { ctr->req_n = n; }
     } while (0)
 
 static bool use_graph(heap *h, cudaStream_t s) {
-    if (!h->graphs || h->prof_mask || (h->sub && h->sub->prof_mask)) return false;
+    if (!h->graphs || h->prof_mask || (h->sub && h->sub->prof_mask) || (h->sub2 && h->sub2->prof_mask)) return false;
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return false;
     return true;
@@ -806,7 +921,9 @@ static int graph_batch(heap *h, int op, const uint64_t *in, uint64_t *out, uint6
     if (!g.exec) {
         if (!h->cap) CUDA_TRY(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
         const int cur0 = h->cur;
-        const u64 l0 = h->launches, ls0 = sub ? sub->launches : 0;
+        heap *sub2 = h->sub2;
+        const int sc2 = sub2 ? sub2->cur : 0;
+        const u64 l0 = h->launches, ls0 = sub ? sub->launches : 0, ls2 = sub2 ? sub2->launches : 0;
         cudaGraph_t body = nullptr;
         CUDA_TRY(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
         const uint64_t *gin = (const uint64_t *)h->gin;
@@ -815,10 +932,12 @@ static int graph_batch(heap *h, int op, const uint64_t *in, uint64_t *out, uint6
         cudaError_t e = cudaStreamEndCapture(h->cap, &body);
         g.cur_after = h->cur;
         g.subcur_after = sub ? sub->cur : 0;
-        g.nlaunch = (h->launches - l0) + (sub ? sub->launches - ls0 : 0) + 1;
+        g.sub2cur_after = sub2 ? sub2->cur : 0;
+        g.nlaunch = (h->launches - l0) + (sub ? sub->launches - ls0 : 0) + (sub2 ? sub2->launches - ls2 : 0) + 1;
         h->cur = cur0;                                 // nothing ran yet: restore the host state
         h->launches = l0;
         if (sub) { sub->cur = sc; sub->launches = ls0; }
+        if (sub2) { sub2->cur = sc2; sub2->launches = ls2; }
         if (rc != HEAP_OK || e != cudaSuccess) {
             if (getenv("HEAP_DEBUG")) fprintf(stderr, "libheap graph: capture rc %d: %s\n", rc, cudaGetErrorString(e));
             if (body) cudaGraphDestroy(body);
@@ -845,6 +964,7 @@ static int graph_batch(heap *h, int op, const uint64_t *in, uint64_t *out, uint6
     GRAPH_TRY(cudaGraphLaunch(g.exec, s));
     h->cur = g.cur_after;
     if (sub) sub->cur = g.subcur_after;
+    if (h->sub2) h->sub2->cur = g.sub2cur_after;
     h->launches += g.nlaunch;
     return HEAP_OK;
 }
@@ -921,6 +1041,15 @@ int heap_stats_async(heap_t *h, heap_stats_t *d_out, heap_stream_t sp) {
     if (!h || !d_out) return HEAP_EINVAL;
     cudaStream_t s = (cudaStream_t)sp;
     TAG(h, HEAP_TAG_MISC);
+    if (h->policy == HEAP_DOUBLE_BUDDY) {
+        int rc = heap_stats_async(h->sub, h->sstats, sp);
+        if (rc == HEAP_OK && h->sub2) rc = heap_stats_async(h->sub2, h->sstats2, sp);
+        if (rc != HEAP_OK) return rc;
+        LAUNCH(h, dbl::k_stats, 1, 1, 0, s, h->sstats, h->sstats2, h->sub2 ? 1 : 0, h->dctr, h->arena, h->align,
+               h->L.dbl_A, meta_bytes(h), d_out);
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        return HEAP_OK;
+    }
     if (h->policy == HEAP_HYBRID) {
         int rc = heap_stats_async(h->sub, h->sstats, sp);
         if (rc != HEAP_OK) return rc;
@@ -952,6 +1081,26 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
     if (!h || !h_counts) return HEAP_EINVAL;
     cudaStream_t s = (cudaStream_t)sp;
     TAG(h, HEAP_TAG_MISC);
+    if (h->policy == HEAP_DOUBLE_BUDDY) {
+        // the binary heap's blocks (below A_bytes), then the 3-unit heap's converted to bytes
+        uint64_t ca[2] = {0, 0}, cb[2] = {0, 0};
+        int rc = heap_export(h->sub, d_free_pairs, cap_free, d_live_pairs, cap_live, ca, sp);
+        if (rc != HEAP_OK) return rc;
+        if (h->sub2) {
+            uint64_t *fp2 = (d_free_pairs && cap_free > ca[0]) ? d_free_pairs + 2 * ca[0] : nullptr;
+            uint64_t *lp2 = (d_live_pairs && cap_live > ca[1]) ? d_live_pairs + 2 * ca[1] : nullptr;
+            const u64 cf2 = fp2 ? cap_free - ca[0] : 0, cl2 = lp2 ? cap_live - ca[1] : 0;
+            rc = heap_export(h->sub2, fp2, cf2, lp2, cl2, cb, sp);
+            if (rc != HEAP_OK) return rc;
+            if (fp2) LAUNCH(h, dbl::k_pairs_to_bytes, h->G, 256, 0, s, (u64 *)fp2, std::min<u64>(cb[0], cf2), h->L.dbl_A, 3 * h->align);
+            if (lp2) LAUNCH(h, dbl::k_pairs_to_bytes, h->G, 256, 0, s, (u64 *)lp2, std::min<u64>(cb[1], cl2), h->L.dbl_A, 3 * h->align);
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        h_counts[0] = ca[0] + cb[0];
+        h_counts[1] = ca[1] + cb[1];
+        return HEAP_OK;
+    }
     if (h->policy == HEAP_HYBRID) {
         // pool runs / live objects first (below pool_end, address order), then the TLSF heap's
         const pool::Geom &G = h->L.geo;
@@ -1031,6 +1180,7 @@ int heap_profile_enable(heap_t *h, uint64_t tag_mask) {
     if (!h) return HEAP_EINVAL;
     h->prof_mask = tag_mask;
     if (h->sub) h->sub->prof_mask = tag_mask;
+    if (h->sub2) h->sub2->prof_mask = tag_mask;
     return HEAP_OK;
 }
 
@@ -1046,6 +1196,7 @@ int heap_profile_read(heap_t *h, double *h_ms, uint64_t *h_launches) {
         h->pool.push_back(r.b);
     }
     h->recs.clear();
+    if (h->sub2) { int rc = heap_profile_read(h->sub2, h_ms, h_launches); if (rc) return rc; }
     if (h->sub) return heap_profile_read(h->sub, h_ms, h_launches);
     return HEAP_OK;
 }

@@ -32,7 +32,10 @@ def test_workspace_bytes_and_argument_checks():
     assert L.heap_workspace_bytes(1 << 20, 16, 4, 1024, 1024) > 0
     assert L.heap_workspace_bytes(1 << 20, 24, 4, 1024, 1024) == 0      # align not a power of two
     assert L.heap_workspace_bytes((1 << 20) + 8, 16, 4, 1024, 1024) == 0  # arena not a multiple
-    assert L.heap_workspace_bytes(1 << 20, 16, 9, 1024, 1024) == 0       # bad policy
+    assert L.heap_workspace_bytes(1 << 20, 16, 10, 1024, 1024) == 0      # bad policy
+    assert L.heap_workspace_bytes(1 << 20, 16, 0, 1024, 1024) == 0
+    for pol in range(1, 10):
+        assert L.heap_workspace_bytes(1 << 20, 16, pol, 1024, 1024) > 0, pol
     assert L.heap_workspace_bytes((1 << 36) + (1 << 5), 16, 4, 1024, 1024) == 0  # > 2^32 units
     assert L.heap_workspace_bytes(1 << 36, 16, 4, 1024, 1024) > 0        # exactly 2^32 units
     h = ctypes.c_void_p()

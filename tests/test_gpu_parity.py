@@ -107,6 +107,9 @@ SMALL = [
     (tg.NEXT_FIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2), 0),           # first fit from a rover
     (tg.NEXT_FIT, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
     (tg.NEXT_FIT, 1 << 28, 16, 4096, 120000, (4, 20), (1, 2), 0),       # config-2 shaped
+    (tg.DOUBLE_BUDDY, 6 * 4096 * 16, 16, 24, 1500, (4, 12), (1, 2), 0),  # two staggered buddy heaps
+    (tg.DOUBLE_BUDDY, (1 << 24) + 4096, 64, 3000, 40000, (6, 16), (2, 5), 0),
+    (tg.DOUBLE_BUDDY, 1 << 30, 256, 20000, 200000, (8, 24), (1, 2), 0),
 ]
 
 
@@ -148,7 +151,7 @@ def test_config5_first_batches():
 def test_edge_cases():
     """Empty batches, NULL / interior / unaligned / out-of-range / duplicate frees,
     zero and oversize requests, OOM in a tiny arena, the last unit of a 2^32-unit arena."""
-    for pol in (1, 2, 3, 4, 5, 6, 7, 8):
+    for pol in (1, 2, 3, 4, 5, 6, 7, 8, 9):
         arena, align = 1 << 12, 16
         g = Gpu(arena, align, pol, 256, 64)
         o = OracleL(arena, align, pol)
@@ -277,7 +280,8 @@ def test_hybrid_config5_shape():
         assert gs[k] == os_[k], k
 
 
-@pytest.mark.parametrize("pol", [tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.BUDDY, tg.SEGFIT_LIFO, tg.HYBRID, tg.NEXT_FIT])
+@pytest.mark.parametrize("pol", [tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.BUDDY, tg.SEGFIT_LIFO, tg.HYBRID, tg.NEXT_FIT,
+                                 tg.DOUBLE_BUDDY])
 def test_direct_launch_path(pol):
     """The same batches with batch graphs disabled (direct launches, the path tracing uses), and
     a heap switching between the two paths mid-trace."""
