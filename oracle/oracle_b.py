@@ -23,6 +23,7 @@ import numpy as np
 HEAP_NULL = (1 << 64) - 1
 FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY = 1, 2, 3, 4, 5
 NEXT_FIT = 8
+PARTIAL = 0x100     # policy flag: partial (tail) deallocation (Alg. 2 :205-212)
 
 
 def cls_of(u: int, L: int) -> int:
@@ -50,10 +51,16 @@ def search_cls(u: int, L: int) -> int:
 class OracleB:
     def __init__(self, arena_bytes: int, align: int, policy: int):
         assert align > 0 and align & (align - 1) == 0 and arena_bytes % align == 0
+        self.partial = bool(policy & PARTIAL)
+        policy &= ~PARTIAL
+        assert not (self.partial and policy == BUDDY)
         self.align, self.policy = align, policy
         self.A = arena_bytes // align
         self.bits = np.ones(self.A, dtype=bool)
         self.live: dict[int, int] = {}
+        # owner[u] = start of the live block holding unit u, -1 if u is free (a per-unit map
+        # instead of Oracle-L's ordered search, so a partial free is located differently)
+        self.owner = np.full(self.A, -1, dtype=np.int64)
         self.L = 5 if policy == TLSF else 0
         self.roots = []
         if policy == BUDDY:
@@ -111,6 +118,7 @@ class OracleB:
             return None
         _, s, _ = min(cand)
         self.bits[s:s + r] = False
+        self.owner[s:s + r] = s
         self.live[s] = r
         self.rover = s + r
         return s
@@ -148,19 +156,25 @@ class OracleB:
                 self.counts["frees_invalid"] += 1
             else:
                 u = o // self.align
-                if u in self.live:
-                    if u in seen:
-                        self.counts["frees_double"] += 1
-                    else:
-                        seen.add(u)
-                        self.counts["frees_ok"] += 1
-                        to_free.append(u)
-                elif u in free_starts:
+                a = int(self.owner[u])
+                if u in free_starts:
+                    self.counts["frees_double"] += 1
+                elif a < 0 or (a != u and not self.partial):
+                    self.counts["frees_invalid"] += 1
+                elif a in seen:            # a copy, or a second offset inside one live block
                     self.counts["frees_double"] += 1
                 else:
-                    self.counts["frees_invalid"] += 1
-        for u in to_free:
-            self.bits[u:u + self.live.pop(u)] = True
+                    seen.add(a)
+                    self.counts["frees_ok"] += 1
+                    to_free.append((a, u))
+        for a, u in to_free:
+            end = a + self.live[a]
+            if u == a:
+                del self.live[a]
+            else:
+                self.live[a] = u - a      # the in-use block is shrunk
+            self.bits[u:end] = True
+            self.owner[u:end] = -1
 
     def export(self):
         fp = np.array([(s * self.align, z * self.align) for s, z in self.blocks()],

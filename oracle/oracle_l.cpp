@@ -43,6 +43,12 @@
  *   - batch driver (canonical order, BASELINE.json north_star): a free batch classifies every
  *     offset against the batch-start state, then frees the valid ones in ascending address
  *     order; an alloc batch serves requests in request order, HEAP_NULL on failure.
+ *   - partial (tail) deallocation, policy flag PARTIAL (0x100) on FIRST_FIT, BEST_FIT, SEGFIT,
+ *     TLSF and NEXT_FIT: "freeing the last 2kB of a 10kB block ... the in-use block will be shrunk"
+ *     (Alg. 2 :205-212 `search(used_list, addr)` then `it.size = addr - it.addr`):
+ *     an offset inside a live block frees from that offset to the block's end.  Per live block
+ *     of the batch-start state, the lowest offset of the batch inside it frees (the whole block
+ *     if it is the start); every other offset inside it is a double free (C29).
  * Everything is in units of `align` (reading C14).  Sizes of s bytes become
  * r = ceil(s / align) units; s = 0 or r > A_u fails (C17).
  */
@@ -60,6 +66,7 @@ namespace {
 const uint64_t HEAP_NULL = ~0ull;
 enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6, HYBRID = 7, NEXT_FIT = 8,
        DOUBLE_BUDDY = 9 };
+const int PARTIAL = 0x100;    /* policy flag: partial (tail) deallocation */
 const uint64_t PAGE = 4096;   /* "allocations smaller than a page (<4kB)" */
 
 /* floor(log2 u) for u >= 1, written as a plain loop */
@@ -94,6 +101,7 @@ struct Counters {
 
 struct Heap {
     int policy;
+    bool partial = false;                 /* PARTIAL flag: an interior offset frees the block's tail */
     int L;
     uint64_t align, A_u, arena_bytes;
     std::map<uint64_t, uint64_t> live;    /* start -> size (units): the block table */
@@ -169,17 +177,34 @@ struct Heap {
         uint64_t size = live[o];
         live.erase(o);
         if (policy == BUDDY) { buddy_free(o, size); return; }
-        uint64_t start = o, end = o + size;
+        free_range(o, o + size);
+    }
+    /* partial deallocation (Alg. 2 :205-212): the live block at a keeps [a, o), [o, end) is freed */
+    void free_tail(uint64_t a, uint64_t o) {
+        uint64_t end = a + live[a];
+        live[a] = o - a;                        /* it.size = addr - it.addr */
+        free_range(o, end);
+    }
+    /* insert [o, end) into the free list, merging with the free neighbours on both sides */
+    void free_range(uint64_t o, uint64_t end) {
+        uint64_t start = o;
         /* left: the free block whose end is o */
         auto it = freeb.lower_bound(o);
         if (it != freeb.begin()) {
             auto left = std::prev(it);
             if (left->first + left->second == o) { start = left->first; free_erase(left->first); }
         }
-        /* right: the free block starting at o + size */
+        /* right: the free block starting at end */
         auto right = freeb.find(end);
         if (right != freeb.end()) { end = right->first + right->second; free_erase(right->first); }
         free_insert(start, end - start);
+    }
+    /* the live block containing unit u (search(used_list, addr), Alg. 2 :205), or HEAP_NULL */
+    uint64_t containing_live(uint64_t u) const {
+        auto it = live.upper_bound(u);
+        if (it == live.begin()) return HEAP_NULL;
+        --it;
+        return (u < it->first + it->second) ? it->first : HEAP_NULL;
     }
 
     /* buddy merge: while the buddy a XOR 2^k is a free block of order k, merge */
@@ -268,7 +293,12 @@ extern "C" {
 
 void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
     if (align == 0 || (align & (align - 1)) || arena_bytes == 0 || arena_bytes % align) return nullptr;
+    const bool partial = (policy & PARTIAL) != 0;
+    policy &= ~PARTIAL;
     if (policy < FIRST_FIT || policy > DOUBLE_BUDDY) return nullptr;
+    /* partial frees need address coalescing: not for buddies or the object pools */
+    if (partial && (policy == BUDDY || policy == HYBRID || policy == DOUBLE_BUDDY || policy == SEGFIT_LIFO))
+        return nullptr;
     if (policy == DOUBLE_BUDDY) {
         /* reading C28: the 3-unit heap gets floor(arena / (6 align)) units at the top of the
          * arena, the binary heap everything below (at least half) */
@@ -304,6 +334,7 @@ void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
     }
     Heap *h = new Heap();
     h->policy = policy;
+    h->partial = partial;
     h->L = (policy == TLSF) ? 5 : 0;
     h->align = align;
     h->arena_bytes = arena_bytes;
@@ -381,23 +412,27 @@ void oracle_free_batch(void *p, const uint64_t *offsets, uint64_t n) {
     if (h->policy == DOUBLE_BUDDY) { double_free_batch(h, offsets, n); return; }
     std::vector<uint64_t> v(offsets, offsets + n);
     std::sort(v.begin(), v.end());
-    std::vector<uint64_t> to_free;
+    std::set<uint64_t> claimed;                          /* live blocks already freed from */
+    std::vector<std::pair<uint64_t, uint64_t>> to_free;  /* (block start, freed from) */
     for (uint64_t i = 0; i < n; i++) {
         uint64_t o = v[i];
-        bool dup = (i > 0 && v[i - 1] == o);
         if (o == HEAP_NULL) { h->c.frees_null++; continue; }
         if (o % h->align || o / h->align >= h->A_u) { h->c.frees_invalid++; continue; }
         uint64_t u = o / h->align;
-        if (h->live.count(u)) {
-            if (dup) h->c.frees_double++;
-            else { h->c.frees_ok++; to_free.push_back(u); }
-        } else if (h->is_free_start(u)) {
-            h->c.frees_double++;
-        } else {
-            h->c.frees_invalid++;
-        }
+        uint64_t a = HEAP_NULL;
+        if (h->live.count(u)) a = u;
+        else if (h->is_free_start(u)) { h->c.frees_double++; continue; }
+        else if (h->partial) a = h->containing_live(u);
+        if (a == HEAP_NULL) { h->c.frees_invalid++; continue; }
+        if (claimed.count(a)) { h->c.frees_double++; continue; }   /* a copy, or a higher offset */
+        claimed.insert(a);
+        h->c.frees_ok++;
+        to_free.push_back({a, u});
     }
-    for (uint64_t u : to_free) h->free_block(u);   /* ascending address order */
+    for (auto &f : to_free) {                       /* ascending address order */
+        if (f.first == f.second) h->free_block(f.first);
+        else h->free_tail(f.first, f.second);
+    }
 }
 
 void oracle_alloc_batch(void *p, const uint64_t *sizes, uint64_t n, uint64_t *out) {

@@ -11,6 +11,7 @@ import numpy as np
 
 HEAP_NULL = (1 << 64) - 1
 POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6, "HYBRID": 7, "NEXT": 8, "DOUBLE": 9}
+PARTIAL = 0x100      # policy flag: partial (tail) deallocation (include/heap.h HEAP_PARTIAL_FREE)
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
@@ -47,6 +48,49 @@ def replay(heap, trace, idmap: IdMap | None = None, on_batch=None, max_batches=N
         if on_batch is not None:
             on_batch(bi, offs, sizes, out)
     return idmap
+
+
+def replay_partial(heaps, cfg, seed: int, p_tail=0.5, p_extra=0.15, p_wild=0.05, on_batch=None):
+    """Drive ``heaps`` in lockstep with a tracegen trace whose frees are partly turned into
+    partial (tail) frees (policy flag PARTIAL).  Every input comes from the trace,
+    a seeded numpy generator and heaps[0] (the oracle) — never from the heap under test:
+    for a freed id of u units at offset o, with probability p_tail the offset becomes
+    o + d*align, d uniform in [1, u) (the id keeps its d-unit head, which the trace then never
+    frees: a leak, as a caller that shrinks a block and forgets it); extra offsets are added
+    inside the same block (a second offset: a double free) or anywhere in the arena (start,
+    interior or free memory).  Returns the per-batch outputs of heaps[0]."""
+    rng = np.random.default_rng(seed)
+    align, A_u = cfg.align, cfg.arena_bytes // cfg.align
+    idmap = IdMap(1 << 12)
+    units = {}
+    for bi, (fids, sizes, first) in enumerate(__import__("tracegen").Trace(cfg)):
+        offs = [int(x) for x in idmap.offsets(fids)]
+        extra = []
+        for j, fid in enumerate(int(x) for x in fids):
+            o = offs[j]
+            if o == HEAP_NULL:
+                continue
+            z = units.get(fid, 1)
+            x = rng.random()
+            if x < p_tail and z > 1:
+                d = 1 + int(rng.integers(z - 1))
+                offs[j] = o + d * align
+                if rng.random() < p_extra:
+                    extra.append(o + int(rng.integers(d, z)) * align)
+            elif x < p_tail + p_extra:
+                extra.append(o + int(rng.integers(z)) * align)
+            if rng.random() < p_wild:
+                extra.append(int(rng.integers(A_u)) * align)
+        batch = np.array(offs + extra, dtype=np.uint64)
+        outs = []
+        for h in heaps:
+            h.free_batch(batch)
+            outs.append(np.asarray(h.alloc_batch(sizes), dtype=np.uint64))
+        for k, sz in enumerate(int(x) for x in sizes):
+            units[first + k] = -(-sz // align)
+        idmap.record(first, outs[0])
+        if on_batch is not None:
+            on_batch(bi, batch, sizes, outs)
 
 
 def hybrid_layout(arena: int, align: int):
@@ -138,6 +182,8 @@ def parse_golden(name: str):
                 fl = None
             else:
                 fl = [tuple(int(v) for v in x.split(":")) for x in frees.split()]
-            cases.append(dict(policy=POLICY[pol], arena=int(arena), align=int(align),
+            pol, _, flag = pol.partition("+")
+            pid = POLICY[pol] | (PARTIAL if flag == "P" else 0)
+            cases.append(dict(policy=pid, arena=int(arena), align=int(align),
                               batches=batches, outs=outs, frees=fl, cite=cite.strip()))
     return cases

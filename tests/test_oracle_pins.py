@@ -21,8 +21,8 @@ from oracle import OracleL, insert_class, search_class
 import copy
 
 from oracle.oracle_b import OracleB, OracleBDouble, OracleBHybrid, OracleBLifo, cls_lo, cls_of, search_cls
-from tests.helpers import (HEAP_NULL, IdMap, check_double_invariants, check_invariants, double_layout, hybrid_layout,
-                           parse_golden, replay)
+from tests.helpers import (HEAP_NULL, PARTIAL, IdMap, check_double_invariants, check_invariants, double_layout,
+                           hybrid_layout, parse_golden, replay, replay_partial)
 
 FIT_POLICIES = [1, 2, 3, 4]
 ALL_POLICIES = [1, 2, 3, 4, 5, 6, 8]
@@ -517,3 +517,99 @@ def test_double_buddy_exhaustive_tiny():
         assert np.array_equal(fl, fb) and np.array_equal(ll, lb), seq
         n += 1
     assert n > 2000
+
+
+# ---------------- partial (tail) deallocation: policy flag PARTIAL ----------------
+
+PARTIAL_POLICIES = [1, 2, 3, 4, 8]
+
+
+def test_partial_free_classification():
+    """Reading C29 on a hand-built state: an interior offset of a live block frees its tail;
+    per live block the lowest offset of the batch wins, every other offset inside it (and a
+    copy of the winner) is a double free; an interior offset of FREE memory stays invalid; on a
+    heap without the flag an interior offset is invalid (C6)."""
+    for H in (OracleL, OracleB):
+        h = H(1024, 16, tg.FIRST_FIT | PARTIAL)
+        assert [int(x) for x in h.alloc_batch([64, 64, 64])] == [0, 64, 128]     # free [192, 1024)
+        h.free_batch(np.array([32, 48, 32, 64, 96, 512, 512 + 8, HEAP_NULL], dtype=np.uint64))
+        c = h.stats() if H is OracleL else h.counts
+        # 32 -> tail of block 0 (ok); 48, second 32 -> double; 64 -> whole block 1 (ok); 96 -> double;
+        # 512 -> interior of the free block [192, 1024): invalid; 520 unaligned: invalid
+        assert (c["frees_ok"], c["frees_double"], c["frees_invalid"], c["frees_null"]) == (2, 3, 2, 1), (H, c)
+        fp, lp = h.export()
+        assert [tuple(int(v) for v in p) for p in lp] == [(0, 32), (128, 64)]
+        assert [tuple(int(v) for v in p) for p in fp] == [(32, 96), (192, 832)]
+        g = H(1024, 16, tg.FIRST_FIT)
+        g.alloc_batch([64])
+        g.free_batch(np.array([32], dtype=np.uint64))
+        c = g.stats() if H is OracleL else g.counts
+        assert c["frees_invalid"] == 1 and c["frees_ok"] == 0
+
+
+def test_partial_tail_then_start_equals_whole_free():
+    """Freeing a block's tail and then its start (two batches) leaves the same state as freeing
+    the whole block at once: conservation of the block's bytes across the split (I2)."""
+    for policy in PARTIAL_POLICIES:
+        a, b = OracleL(1 << 14, 16, policy | PARTIAL), OracleL(1 << 14, 16, policy)
+        for h in (a, b):
+            h.alloc_batch([1000, 3000, 200])
+        a.free_batch(np.array([1008 + 1600], dtype=np.uint64))        # tail of the 3000-byte block
+        a.free_batch(np.array([1008], dtype=np.uint64))               # then its start
+        b.free_batch(np.array([1008], dtype=np.uint64))
+        for x, y in zip(a.export(), b.export()):
+            assert np.array_equal(x, y), policy
+
+
+@pytest.mark.parametrize("policy", PARTIAL_POLICIES)
+@pytest.mark.parametrize("seed", range(3))
+def test_partial_oracle_l_equals_oracle_b(policy, seed):
+    """Random traces with tail frees, second offsets and wild offsets: Oracle-L (ordered live-map
+    search) == Oracle-B (per-unit owner map over a bitmap) on every output, state and counter;
+    invariants I1-I4 after every batch."""
+    arena, align = 1 << 14, 16
+    cfg = tg.custom(policy, arena, align, 24, rho=(1, 2), total_ops=1200, sizes=(4, 10), idx=120 + seed)
+    hl, hb = OracleL(arena, align, policy | PARTIAL), OracleB(arena, align, policy | PARTIAL)
+
+    def check(bi, batch, sizes, outs):
+        assert np.array_equal(outs[0], outs[1]), (policy, bi)
+        fl, ll = hl.export()
+        fb, lb = hb.export()
+        assert np.array_equal(fl, fb) and np.array_equal(ll, lb), (policy, bi)
+        check_invariants(fl, ll, arena, align, False)
+
+    replay_partial([hl, hb], cfg, seed, on_batch=check)
+    st = hl.stats()
+    for k, v in hb.counts.items():
+        assert st[k] == v, k
+    assert st["frees_ok"] > 0 and st["frees_double"] > 0 and st["frees_invalid"] > 0
+
+
+@pytest.mark.parametrize("policy", PARTIAL_POLICIES)
+def test_partial_exhaustive_tiny_heaps(policy):
+    """Every sequence of 3 single-op batches over an 8-unit heap: alloc 1..8 units or free ANY
+    unit offset (live start, interior, free memory), Oracle-L == Oracle-B everywhere."""
+    A, pol = 8, policy | PARTIAL
+    n = 0
+    for seq in itertools.product([("a", s) for s in range(1, A + 1)] + [("f", o) for o in range(A)], repeat=3):
+        hl, hb = OracleL(A, 1, pol), OracleB(A, 1, pol)
+        for op, v in seq:
+            if op == "a":
+                assert int(hl.alloc_batch([v])[0]) == int(hb.alloc_batch([v])[0]), seq
+            else:
+                hl.free_batch([v])
+                hb.free_batch([v])
+        fl, ll = hl.export()
+        fb, lb = hb.export()
+        assert np.array_equal(fl, fb) and np.array_equal(ll, lb), seq
+        st = hl.stats()
+        assert all(st[k] == v for k, v in hb.counts.items()), seq
+        n += 1
+    assert n == 16 ** 3
+
+
+def test_partial_rejected_where_undefined():
+    """The flag needs address coalescing: buddies, pools and LIFO bins reject it."""
+    for policy in (tg.BUDDY, tg.HYBRID, tg.DOUBLE_BUDDY, tg.SEGFIT_LIFO):
+        with pytest.raises(ValueError):
+            OracleL(1 << 14, 16, policy | PARTIAL)
