@@ -29,7 +29,8 @@
  *     than the arena, or no candidate block) yields HEAP_NULL and changes nothing; a free
  *     of HEAP_NULL is a no-op; a free of anything that is not a live block start is
  *     skipped and counted (frees_invalid / frees_double).  Partial (interior) frees are
- *     not supported (C6).
+ *     opt-in per heap with the HEAP_PARTIAL_FREE policy flag (below); without it an interior
+ *     offset is invalid (C6).
  *   - Metadata capacity overflow inside a batch (more live blocks than max_live_blocks)
  *     cannot be reported synchronously: it sets error_flags and the next heap_stats()
  *     returns HEAP_ECAPACITY.  The heap state after such a batch is unspecified.
@@ -90,6 +91,18 @@ enum heap_policy {
                            max_live_blocks bounds each heap's live blocks. */
 };
 
+/* Policy flag (OR into policy): partial (tail) deallocation, "freeing the last 2kB of a 10kB
+ * block ... the in-use block will be shrunk" (Alg. 2 :205-212 searches the used
+ * list for the block CONTAINING the address).  Valid with HEAP_FIRST_FIT, HEAP_BEST_FIT,
+ * HEAP_SEGFIT, HEAP_TLSF and HEAP_NEXT_FIT (heap_create returns HEAP_EINVAL otherwise).  In a
+ * free batch an offset inside a live block frees from that offset to the block's end (the
+ * whole block when it is the start); per live block of the batch-start state the LOWEST such
+ * offset of the batch frees and every other offset inside the block (copies included) counts
+ * as frees_double; an offset in free memory that is not a free block's start stays
+ * frees_invalid (C29).  The shrunk block keeps its start; heap_export reports its
+ * new size.  Costs one bit per arena unit of workspace (a live-start bitmap with summaries). */
+#define HEAP_PARTIAL_FREE 0x100
+
 #define HEAP_NULL UINT64_MAX /* failed alloc; no-op in a free batch (offset 0 is valid, C18) */
 
 enum heap_error {
@@ -111,7 +124,9 @@ typedef struct heap_stats {
     uint64_t allocs_ok, allocs_failed; /* failed = OOM + zero size + oversize */
     uint64_t frees_ok, frees_invalid, frees_double, frees_null;
     uint64_t metadata_bytes;           /* device workspace bytes the heap occupies */
-    uint64_t error_flags;              /* bit 0: live-block capacity, bit 1: table full */
+    uint64_t error_flags;              /* bit 0: live-block capacity, bit 1: table full,
+                                          bit 2: free-array capacity, bit 3: engine watchdog,
+                                          bit 4: live-start bitmap and table disagree */
 } heap_stats_t;
 
 /* Bytes of device workspace heap_create needs for these capacities.

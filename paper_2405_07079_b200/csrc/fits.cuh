@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_free_lookup(const u32 *__restrict__ key
         bool in = idx < nk;
         u32 key = in ? keys[idx] : 0;
         bool first = in && (idx == 0 || keys[idx - 1] != key);
-        u64 s = table::lookup(slots, tmask, key, first, true, max_lines);
+        u64 s = table::lookup(slots, tmask, key, first, table::TOMB, max_lines);
         if (in && sub == 0) {
             u32 f = 0;
             if (first) {

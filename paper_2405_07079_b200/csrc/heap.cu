@@ -17,6 +17,7 @@
 #include "engine_tlsf.cuh"
 #include "pool.cuh"
 #include "dbuddy.cuh"
+#include "partial.cuh"
 
 namespace {
 
@@ -45,14 +46,25 @@ struct Layout {
     u64 o_gin, o_gout;   // graph path: staging of the request / result words
     // HEAP_DOUBLE_BUDDY: the 3-unit heap's geometry and the split / merge buffers
     u64 dbl_A, dbl_n3, o_dctr, o_ca, o_cb, o_ia, o_ib, o_ra, o_rb, o_sstats2, o_sub2, sub2_total;
+    // HEAP_PARTIAL_FREE: live-start bitmap (partial.cuh)
+    bool partial;
+    partial::Lbm lbm;
+    u64 o_lbm, lbm_words;
 };
 
 bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, Layout *Lo) {
     if (align == 0 || (align & (align - 1)) || arena == 0 || arena % align) return false;
+    const bool partial_free = (policy & HEAP_PARTIAL_FREE) != 0;
+    policy &= ~HEAP_PARTIAL_FREE;
     if (policy < HEAP_FIRST_FIT || policy > HEAP_DOUBLE_BUDDY) return false;
+    // partial frees need address coalescing (C29)
+    if (partial_free && policy != HEAP_FIRST_FIT && policy != HEAP_BEST_FIT && policy != HEAP_SEGFIT &&
+        policy != HEAP_TLSF && policy != HEAP_NEXT_FIT)
+        return false;
     if (max_live == 0 || max_batch == 0 || max_batch >= (1ull << 31) || max_live >= (1ull << 30)) return false;
     Layout &L = *Lo;
     memset(&L, 0, sizeof(L));
+    L.partial = partial_free;
     L.A_u = arena / align;
     if (L.A_u > (1ull << 32)) return false;
     if (policy == HEAP_DOUBLE_BUDDY) {
@@ -218,6 +230,10 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
     if (policy == HEAP_BEST_FIT) {
         L.o_bk0 = take(L.cap_f * 8);
         L.o_bk1 = take(L.cap_f * 8);
+    }
+    if (L.partial) {
+        L.lbm_words = partial::lbm_layout(L.A_u, &L.lbm);
+        L.o_lbm = take(L.lbm_words * 4);
     }
     if (policy == HEAP_BUDDY) {
         L.o_dtm = take(L.dpool * 4);
@@ -525,6 +541,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     if (workspace_bytes < L.total) return HEAP_ENOMEM;
     heap *h = new (std::nothrow) heap();
     if (!h) return HEAP_ENOMEM;
+    policy &= ~HEAP_PARTIAL_FREE;            // the flag lives in L.partial
     h->arena = arena_bytes; h->align = align; h->policy = policy;
     h->max_live = max_live_blocks; h->max_batch = max_batch;
     h->alog2 = ilog2(align);
@@ -624,6 +641,10 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->bufA = at<u64>(w, L.o_bufA); h->bufB = at<u64>(w, L.o_bufB); h->promo = at<u64>(w, L.o_promo);
         h->fr = at<u64>(w, L.o_fr); h->froff = at<u32>(w, L.o_froff); h->reqoff = at<u32>(w, L.o_reqoff);
     }
+    if (L.partial) {
+        h->L.lbm.w = at<u32>(w, L.o_lbm);      // all free: no live starts
+        if (cudaMemsetAsync(h->L.lbm.w, 0, L.lbm_words * 4, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    }
     h->cur = 0;
     h->launches = 0;
     h->prof_mask = 0;
@@ -688,9 +709,18 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
     u32 *keys = rb ? h->kA : h->kB;
     // 3. block-table lookup + delete; classify double / invalid
     TAG(h, HEAP_TAG_LOOKUP);
-    LAUNCH(h, fits::k_free_lookup, h->G, 256, 0, s, keys, &C->nk, h->tbl, L.tcap - 1, L.tcap / table::LINE,
-           bud ? nullptr : h->fs[cur], bud ? nullptr : &C->F, bud ? h->fs[cur] : nullptr, L.K,
-           h->flags, h->vs, h->ve, C);
+    if (L.partial) {
+        // containing-block resolution through the live-start bitmap, then the winners' table
+        // updates (tombstone or shrink) — partial.cuh, reading C29
+        LAUNCH(h, partial::k_resolve, h->G, 256, 0, s, keys, &C->nk, h->tbl, L.tcap - 1, L.tcap / table::LINE,
+               L.lbm, h->fs[cur], &C->F, h->vA, h->vB, h->vs, C);
+        LAUNCH(h, partial::k_apply, h->G, 256, 0, s, keys, &C->nk, h->vA, h->vB, h->vs, h->tbl, L.tcap - 1,
+               L.tcap / table::LINE, L.lbm, h->flags, h->vs, h->ve, C);
+    } else {
+        LAUNCH(h, fits::k_free_lookup, h->G, 256, 0, s, keys, &C->nk, h->tbl, L.tcap - 1, L.tcap / table::LINE,
+               bud ? nullptr : h->fs[cur], bud ? nullptr : &C->F, bud ? h->fs[cur] : nullptr, L.K,
+               h->flags, h->vs, h->ve, C);
+    }
     TAG(h, HEAP_TAG_SCAN);
     scan(h, h->flags, h->pos, &C->nk, &C->nv, s);
     TAG(h, HEAP_TAG_COMPACT);
@@ -822,6 +852,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
     TAG(h, HEAP_TAG_FINISH);
     LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, n_in, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
            L.tcap / table::LINE, C, h->max_live);
+    if (L.partial) LAUNCH(h, partial::k_set_bits, h->G, 256, 0, s, h->out, n, n_in, L.lbm);
     h->cur = nxt;
     maybe_rebuild(h, s);
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;

@@ -31,10 +31,11 @@ __device__ __forceinline__ u64 home_line(u64 key, u64 mask) {
     return (h & mask) & ~(u64)(LINE - 1);
 }
 
-// Tile-cooperative lookup (and optional delete).  All 32 lanes of the warp call it; lanes of
-// an inactive group pass active = false.  Returns the live slot value found (EMPTY if the key
-// is absent) on every lane of the group.
-__device__ u64 lookup(u64 *__restrict__ slots, u64 mask, u64 key, bool active, bool del, u64 max_lines) {
+// Tile-cooperative lookup (and optional replacement of the slot found: TOMB deletes, a packed
+// value updates the size; EMPTY leaves it).  All 32 lanes of the warp call it; lanes of an
+// inactive group pass active = false.  Returns the live slot value found (EMPTY if the key is
+// absent) on every lane of the group.
+__device__ u64 lookup(u64 *__restrict__ slots, u64 mask, u64 key, bool active, u64 repl, u64 max_lines) {
     const u32 lane = lane_id(), sub = lane & (TILE_LANES - 1), g = lane >> 3;
     const u32 gmask = 0xFFu << (g * 8);
     u64 line = active ? home_line(key, mask) : 0;
@@ -56,7 +57,7 @@ __device__ u64 lookup(u64 *__restrict__ slots, u64 mask, u64 key, bool active, b
             if (bm) {
                 if (lane == (u32)(__ffs(bm) - 1)) {
                     result = m0 ? v.x : v.y;
-                    if (del) slots[line + 2 * sub + (m0 ? 0 : 1)] = TOMB;
+                    if (repl != EMPTY) slots[line + 2 * sub + (m0 ? 0 : 1)] = repl;
                 }
                 done = true;
             } else if (be || p + 1 >= max_lines) {

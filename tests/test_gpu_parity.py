@@ -302,3 +302,72 @@ def test_direct_launch_path(pol):
         assert np.array_equal(go, o.alloc_batch(sz)), bi
         im.record(first, go)
     compare_state(g, o, "mixed paths")
+
+
+# ---------------- partial (tail) deallocation: HEAP_PARTIAL_FREE (reading C29) ----------------
+
+PARTIAL_CASES = [
+    # (policy, arena, align, batch, ops, sizes, rho)
+    (tg.FIRST_FIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2)),
+    (tg.BEST_FIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2)),
+    (tg.SEGFIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2)),
+    (tg.TLSF, 1 << 16, 16, 24, 1500, (4, 10), (1, 2)),
+    (tg.NEXT_FIT, 1 << 16, 16, 24, 1500, (4, 10), (1, 2)),
+    (tg.TLSF, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5)),
+    (tg.FIRST_FIT, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5)),
+    (tg.BEST_FIT, 1 << 26, 16, 4096, 60000, (4, 20), (1, 2)),          # config-2 shaped sizes
+    (tg.TLSF, (1 << 30) + 4096, 16, 65536, 400000, (4, 12), (2, 5)),   # config-3 shaped batches
+]
+
+
+@pytest.mark.parametrize("case", PARTIAL_CASES, ids=lambda c: f"p{c[0]}-A{c[1]}-B{c[3]}")
+def test_partial_free_parity(case):
+    """Traces whose frees are partly tail frees, second offsets inside a block and wild
+    offsets (tests/helpers.replay_partial): every output, the final state and all counters
+    equal Oracle-L; the state is compared after every batch on the small heaps."""
+    from tests.helpers import PARTIAL, replay_partial
+    pol, arena, align, batch, ops, sizes, rho = case
+    cfg = tg.custom(pol, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes, idx=140 + pol)
+    o = OracleL(arena, align, pol | PARTIAL)
+    g = Gpu(arena, align, pol | PARTIAL, max(1 << 15, 8 * batch), 3 * batch)
+
+    def check(bi, offs, sizes, outs):
+        if not np.array_equal(outs[0], outs[1]):
+            bad = np.flatnonzero(outs[0] != outs[1])
+            raise AssertionError(f"batch {bi}: {len(bad)} offsets differ, first at {bad[0]}")
+        if batch < 100:
+            compare_state(g, o, f"batch {bi}")
+
+    replay_partial([o, g], cfg, 7 + pol, on_batch=check)
+    compare_state(g, o, "end")
+    st = o.stats()
+    assert st["frees_ok"] > 0 and st["frees_double"] > 0 and st["frees_invalid"] > 0
+
+
+def test_partial_free_edges():
+    """The paper's 10 KiB example; several offsets inside one block (lowest wins, the rest are
+    double); start + interior of one block (whole free); interior of free memory (invalid);
+    empty and all-null batches; a predecessor search that climbs every bitmap level (a 2^31-unit
+    block in a 2^32-unit arena, tail freed near its end); a tail free of the last unit."""
+    from tests.helpers import PARTIAL
+    cases = [
+        (1 << 14, 16, [[10240]], [[8192]]),
+        (1 << 16, 16, [[1024, 1024, 4096]], [[1040, 1024 + 512, 1024 + 2032, 1040]]),
+        (1 << 16, 16, [[1024, 1024]], [[1024, 1024 + 16, 2048 + 512, 4096 + 32, 60000 * 16 // 16]]),
+        (1 << 16, 16, [[1024]], [[], [(1 << 64) - 1] * 5, [16, 32, 48]]),
+        (1 << 36, 16, [[1 << 35, 4096]], [[(1 << 35) - 16, (1 << 35) + 16]]),
+        (1 << 16, 16, [[64, 64]], [[48, 112]]),
+    ]
+    for pol in (tg.FIRST_FIT, tg.TLSF):
+        for arena, align, allocs, frees in cases:
+            o = OracleL(arena, align, pol | PARTIAL)
+            g = Gpu(arena, align, pol | PARTIAL, 1 << 12, 1 << 10)
+            for a in allocs:
+                assert np.array_equal(g.alloc_batch(a), o.alloc_batch(a))
+            for f in frees:
+                g.free_batch(f)
+                o.free_batch(f)
+                compare_state(g, o, f"{pol} {arena} {f}")
+            # the heap keeps working after the tail frees
+            assert np.array_equal(g.alloc_batch([16, 4096, 1 << 20]), o.alloc_batch([16, 4096, 1 << 20]))
+            compare_state(g, o, f"{pol} {arena} after")
