@@ -440,3 +440,98 @@ class OracleBDouble:
             fp += [(self.A_bytes + int(s) * m, int(z) * m) for s, z in fb]
             lp += [(self.A_bytes + int(s) * m, int(z) * m) for s, z in lb]
         return (np.array(fp, dtype=np.uint64).reshape(-1, 2), np.array(lp, dtype=np.uint64).reshape(-1, 2))
+
+
+class OracleBFib:
+    """Brute-force twin of Oracle-L's FIB_BUDDY (Fibonacci buddies; reading C30).
+
+    No free lists at all: a unit bitmap plus the live map.  The arena is cut greedily into
+    Fibonacci roots (largest first); a block of size F splits into its low part of the previous
+    Fibonacci size and its high part of the one before (2 = 1 + 1).  The free blocks are DERIVED
+    on every call as the maximal fully-free nodes of those split trees, so merging is implicit.
+    An alloc takes the smallest free node holding the request (ties: lowest address) and uses the
+    node of the request's size at its start (descending through low parts); a free sets bits."""
+
+    def __init__(self, arena_bytes: int, align: int, policy: int = 10):
+        assert policy == 10
+        self.align, self.A = align, arena_bytes // align
+        fib = [1]
+        if self.A >= 2:
+            fib.append(2)
+        while len(fib) >= 2 and fib[-1] + fib[-2] <= self.A:
+            fib.append(fib[-1] + fib[-2])
+        self.fib = fib
+        self.roots, s, rem = [], 0, self.A
+        while rem:
+            z = max(x for x in fib if x <= rem)
+            self.roots.append((s, z))
+            s, rem = s + z, rem - z
+        self.bits = np.ones(self.A, dtype=bool)
+        self.live: dict[int, int] = {}
+        self.counts = dict(allocs_ok=0, allocs_failed=0, frees_ok=0, frees_invalid=0,
+                           frees_double=0, frees_null=0)
+
+    def _children(self, s, z):
+        i = self.fib.index(z)
+        lo = self.fib[i - 1] if i >= 1 else None
+        if lo is None:
+            return []
+        hi = z - lo                      # 2 = 1 + 1, otherwise the Fibonacci number before lo
+        return [(s, lo), (s + lo, hi)]
+
+    def blocks(self):
+        out = []
+
+        def rec(s, z):
+            if self.bits[s:s + z].all():
+                out.append((s, z))
+            else:
+                for c in self._children(s, z):
+                    rec(*c)
+        for r in self.roots:
+            rec(*r)
+        return sorted(out)
+
+    def alloc_batch(self, sizes):
+        out = np.empty(len(sizes), dtype=np.uint64)
+        for i, sz in enumerate(int(x) for x in sizes):
+            r = -(-sz // self.align)
+            fits = [x for x in self.fib if x >= r]
+            cand = [(z, s) for s, z in self.blocks() if fits and z >= fits[0]] if sz else []
+            if not cand:
+                out[i] = HEAP_NULL
+                self.counts["allocs_failed"] += 1
+                continue
+            _, s = min(cand)
+            self.bits[s:s + fits[0]] = False
+            self.live[s] = fits[0]
+            out[i] = s * self.align
+            self.counts["allocs_ok"] += 1
+        return out
+
+    def free_batch(self, offsets):
+        free_starts = {s for s, _ in self.blocks()}
+        seen, to_free = set(), []
+        for o in sorted(int(x) for x in offsets):
+            if o == HEAP_NULL:
+                self.counts["frees_null"] += 1
+            elif o % self.align or o // self.align >= self.A:
+                self.counts["frees_invalid"] += 1
+            else:
+                u = o // self.align
+                if u in self.live and u not in seen:
+                    seen.add(u)
+                    self.counts["frees_ok"] += 1
+                    to_free.append(u)
+                elif u in self.live or u in free_starts:
+                    self.counts["frees_double"] += 1
+                else:
+                    self.counts["frees_invalid"] += 1
+        for u in to_free:
+            self.bits[u:u + self.live.pop(u)] = True
+
+    def export(self):
+        fp = np.array([(s * self.align, z * self.align) for s, z in self.blocks()], dtype=np.uint64).reshape(-1, 2)
+        lp = np.array(sorted((s * self.align, z * self.align) for s, z in self.live.items()),
+                      dtype=np.uint64).reshape(-1, 2)
+        return fp, lp

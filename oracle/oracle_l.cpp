@@ -34,6 +34,14 @@
  *                  2, 4, 8, ... and 3, 6, 12, ..."): a binary buddy heap of align-sized units on
  *                  [0, A_bytes) and one of 3*align-sized units on [A_bytes, arena); a request
  *                  goes to the heap whose class is smaller (no fallback; reading C28)
+ *       FIB_BUDDY  Fibonacci buddies ("every Fibonacci number is the sum of two other
+ *                  Fibonacci numbers, blocks can be split recursively"): classes S_0 = 1, S_1 = 2,
+ *                  S_k = S_{k-1} + S_{k-2} units; a class-k block splits into its low part of class
+ *                  k-1 and its high part of class k-2 (class 1: two class-0 halves); the arena is
+ *                  the greedy (Zeckendorf) sum of Fibonacci roots, largest first.  An alloc takes the
+ *                  smallest nonempty class >= the request's, lowest address, and splits keeping the
+ *                  low part ("the first is split further", :116); a free merges a block with its
+ *                  tree sibling while the sibling is free (reading C30)
  *       HYBRID     §5.3's hybrid: requests below a page (0 < s < 4096 B) go
  *                  to object pools managed by bitmasks (§3.2) — pool j holds
  *                  objects of align*2^j bytes, an allocation takes the pool's lowest free slot
@@ -65,7 +73,7 @@ namespace {
 
 const uint64_t HEAP_NULL = ~0ull;
 enum { FIRST_FIT = 1, BEST_FIT = 2, SEGFIT = 3, TLSF = 4, BUDDY = 5, SEGFIT_LIFO = 6, HYBRID = 7, NEXT_FIT = 8,
-       DOUBLE_BUDDY = 9 };
+       DOUBLE_BUDDY = 9, FIB_BUDDY = 10 };
 const int PARTIAL = 0x100;    /* policy flag: partial (tail) deallocation */
 const uint64_t PAGE = 4096;   /* "allocations smaller than a page (<4kB)" */
 
@@ -112,7 +120,9 @@ struct Heap {
     std::map<uint64_t, uint64_t> stamp_of;                 /* start -> push stamp */
     uint64_t clock = 0;
     uint64_t rover = 0;                                   /* NEXT_FIT: where the next scan starts */
-    std::vector<std::set<uint64_t>> bfree;                /* BUDDY: free starts per order */
+    std::vector<std::set<uint64_t>> bfree;                /* BUDDY / FIB_BUDDY: free starts per class */
+    std::vector<uint64_t> FS;                             /* FIB_BUDDY: class sizes S_k (units) */
+    std::vector<std::pair<uint64_t, int>> roots;          /* FIB_BUDDY: (start, class) of the roots */
     int K = 0;                                            /* BUDDY: max order */
     Counters c;
     /* HYBRID: J pools of S bytes each at [j*S, (j+1)*S), then the TLSF heap `sub` on
@@ -165,7 +175,7 @@ struct Heap {
     }
 
     bool is_free_start(uint64_t u) const {
-        if (policy == BUDDY) {
+        if (policy == BUDDY || policy == FIB_BUDDY) {
             for (const auto &st : bfree) if (st.count(u)) return true;
             return false;
         }
@@ -177,6 +187,7 @@ struct Heap {
         uint64_t size = live[o];
         live.erase(o);
         if (policy == BUDDY) { buddy_free(o, size); return; }
+        if (policy == FIB_BUDDY) { fib_free(o, size); return; }
         free_range(o, o + size);
     }
     /* partial deallocation (Alg. 2 :205-212): the live block at a keeps [a, o), [o, end) is freed */
@@ -219,6 +230,45 @@ struct Heap {
             k++;
         }
         bfree[k].insert(o);
+    }
+
+    /* ---- Fibonacci buddies (reading C30) ---- */
+    int fib_class_of_size(uint64_t z) const {              /* exact class of a block size */
+        for (int k = 0; k < (int)FS.size(); k++) if (FS[k] == z) return k;
+        return -1;
+    }
+    static int fib_left(int t) { return t - 1; }           /* low child's class */
+    static int fib_right(int t) { return t >= 2 ? t - 2 : 0; }   /* high child's class (class 1: 1 + 1) */
+    /* walk from the root holding a down to the node (a, k); returns false if (a, k) is a root,
+     * else the sibling (q, qk) and the parent (p, pk) */
+    bool fib_family(uint64_t a, int k, uint64_t *q, int *qk, uint64_t *p, int *pk) const {
+        for (const auto &r : roots) {
+            if (a < r.first || a >= r.first + FS[r.second]) continue;
+            uint64_t s = r.first;
+            int t = r.second;
+            bool has_parent = false;
+            while (!(s == a && t == k)) {
+                uint64_t mid = s + FS[fib_left(t)];
+                *p = s; *pk = t; has_parent = true;
+                if (a < mid) { *q = mid; *qk = fib_right(t); t = fib_left(t); }
+                else { *q = s; *qk = fib_left(t); s = mid; t = fib_right(t); }
+            }
+            return has_parent;
+        }
+        return false;
+    }
+    /* free: while the tree sibling is a free block, remove it and move up to the parent */
+    void fib_free(uint64_t a, uint64_t size) {
+        int k = fib_class_of_size(size);
+        for (;;) {
+            uint64_t q = 0, p = 0;
+            int qk = 0, pk = 0;
+            if (!fib_family(a, k, &q, &qk, &p, &pk) || !bfree[qk].count(q)) break;
+            bfree[qk].erase(q);
+            a = p;
+            k = pk;
+        }
+        bfree[k].insert(a);
     }
 
     /* ---- Alg. 1: allocate r units from the chosen free block (low-end split) ---- */
@@ -274,6 +324,19 @@ struct Heap {
             if (it == lifo_index.end()) return HEAP_NULL;
             return take(std::get<2>(*it), r);
         }
+        if (policy == FIB_BUDDY) {
+            /* r is already a class size S_j: the smallest nonempty class >= j, lowest address;
+             * split keeping the low part, the high parts stay free */
+            int j = fib_class_of_size(r);
+            int t = j;
+            while (t <= K && bfree[t].empty()) t++;
+            if (t > K) return HEAP_NULL;
+            uint64_t a = *bfree[t].begin();
+            bfree[t].erase(bfree[t].begin());
+            for (int u = t; u > j; u--) bfree[fib_right(u)].insert(a + FS[fib_left(u)]);
+            live[a] = r;
+            return a;
+        }
         /* BUDDY: r is already a power of two */
         int k = floor_log2(r);
         int j = k;
@@ -295,9 +358,10 @@ void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
     if (align == 0 || (align & (align - 1)) || arena_bytes == 0 || arena_bytes % align) return nullptr;
     const bool partial = (policy & PARTIAL) != 0;
     policy &= ~PARTIAL;
-    if (policy < FIRST_FIT || policy > DOUBLE_BUDDY) return nullptr;
+    if (policy < FIRST_FIT || policy > FIB_BUDDY) return nullptr;
     /* partial frees need address coalescing: not for buddies or the object pools */
-    if (partial && (policy == BUDDY || policy == HYBRID || policy == DOUBLE_BUDDY || policy == SEGFIT_LIFO))
+    if (partial && (policy == BUDDY || policy == HYBRID || policy == DOUBLE_BUDDY || policy == SEGFIT_LIFO ||
+                    policy == FIB_BUDDY))
         return nullptr;
     if (policy == DOUBLE_BUDDY) {
         /* reading C28: the 3-unit heap gets floor(arena / (6 align)) units at the top of the
@@ -339,6 +403,26 @@ void *oracle_create(uint64_t arena_bytes, uint64_t align, int policy) {
     h->align = align;
     h->arena_bytes = arena_bytes;
     h->A_u = arena_bytes / align;
+    if (policy == FIB_BUDDY) {
+        /* S_0 = 1, S_1 = 2, S_k = S_{k-1} + S_{k-2} up to the arena; roots: the greedy
+         * (Zeckendorf) decomposition of A_u, largest first, at increasing addresses */
+        h->FS.push_back(1);
+        if (h->A_u >= 2) h->FS.push_back(2);
+        while (h->FS.size() >= 2 && h->FS[h->FS.size() - 1] + h->FS[h->FS.size() - 2] <= h->A_u)
+            h->FS.push_back(h->FS[h->FS.size() - 1] + h->FS[h->FS.size() - 2]);
+        h->K = (int)h->FS.size() - 1;
+        h->bfree.assign(h->K + 1, std::set<uint64_t>());
+        uint64_t s = 0, rem = h->A_u;
+        while (rem) {
+            int t = h->K;
+            while (h->FS[t] > rem) t--;
+            h->roots.push_back({s, t});
+            h->bfree[t].insert(s);
+            s += h->FS[t];
+            rem -= h->FS[t];
+        }
+        return h;
+    }
     if (policy == BUDDY) {
         h->K = floor_log2(h->A_u);
         h->bfree.assign(h->K + 1, std::set<uint64_t>());
@@ -489,7 +573,12 @@ void oracle_alloc_batch(void *p, const uint64_t *sizes, uint64_t n, uint64_t *ou
         uint64_t r = s / h->align + (s % h->align != 0);     /* ceil(s / align) */
         uint64_t u = HEAP_NULL;
         if (s != 0 && r <= h->A_u) {
-            if (h->policy == BUDDY) {
+            if (h->policy == FIB_BUDDY) {
+                uint64_t z = HEAP_NULL;                          /* the smallest class holding r */
+                for (uint64_t x : h->FS) if (x >= r) { z = x; break; }
+                if (z != HEAP_NULL) u = h->alloc_units(z);
+                if (u != HEAP_NULL) r = z;
+            } else if (h->policy == BUDDY) {
                 uint64_t p2 = 1;
                 while (p2 < r) p2 <<= 1;                        /* round up to a power of two */
                 if (p2 <= h->A_u) u = h->alloc_units(p2);
@@ -554,11 +643,12 @@ void oracle_stats(void *p, uint64_t *o) {
     }
     uint64_t live_b = 0, free_b = 0, nfree = 0, largest = 0;
     for (const auto &kv : h->live) live_b += kv.second;
-    if (h->policy == BUDDY) {
+    if (h->policy == BUDDY || h->policy == FIB_BUDDY) {
         for (int k = 0; k <= h->K; k++) {
+            uint64_t z = (h->policy == BUDDY) ? (1ull << k) : h->FS[k];
             nfree += h->bfree[k].size();
-            free_b += (uint64_t)h->bfree[k].size() << k;
-            if (!h->bfree[k].empty()) largest = std::max<uint64_t>(largest, 1ull << k);
+            free_b += (uint64_t)h->bfree[k].size() * z;
+            if (!h->bfree[k].empty()) largest = std::max<uint64_t>(largest, z);
         }
     } else {
         for (const auto &kv : h->freeb) { free_b += kv.second; nfree++; largest = std::max(largest, kv.second); }
@@ -618,9 +708,10 @@ void oracle_export(void *p, uint64_t *free_pairs, uint64_t cap_free, uint64_t *l
         return;
     }
     uint64_t a = h->align, i = 0;
-    if (h->policy == BUDDY) {
+    if (h->policy == BUDDY || h->policy == FIB_BUDDY) {
         std::map<uint64_t, uint64_t> all;
-        for (int k = 0; k <= h->K; k++) for (uint64_t s : h->bfree[k]) all[s] = 1ull << k;
+        for (int k = 0; k <= h->K; k++)
+            for (uint64_t s : h->bfree[k]) all[s] = (h->policy == BUDDY) ? (1ull << k) : h->FS[k];
         for (const auto &kv : all) { if (i < cap_free) { free_pairs[2 * i] = kv.first * a; free_pairs[2 * i + 1] = kv.second * a; } i++; }
     } else {
         for (const auto &kv : h->freeb) { if (i < cap_free) { free_pairs[2 * i] = kv.first * a; free_pairs[2 * i + 1] = kv.second * a; } i++; }

@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HEAP_NULL = (1 << 64) - 1
-POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6, "HYBRID": 7, "NEXT": 8, "DOUBLE": 9}
+POLICY = {"FIRST": 1, "BEST": 2, "SEGFIT": 3, "TLSF": 4, "BUDDY": 5, "LIFO": 6, "HYBRID": 7, "NEXT": 8, "DOUBLE": 9, "FIB": 10}
 PARTIAL = 0x100      # policy flag: partial (tail) deallocation (include/heap.h HEAP_PARTIAL_FREE)
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -187,3 +187,48 @@ def parse_golden(name: str):
             cases.append(dict(policy=pid, arena=int(arena), align=int(align),
                               batches=batches, outs=outs, frees=fl, cite=cite.strip()))
     return cases
+
+
+def fib_roots(arena: int, align: int):
+    """(sizes, roots) of a FIB_BUDDY heap in units (reading C30): the Fibonacci sizes
+    1, 2, 3, 5, ... up to the arena and its greedy (Zeckendorf) root decomposition."""
+    A = arena // align
+    fib = [1] + ([2] if A >= 2 else [])
+    while len(fib) >= 2 and fib[-1] + fib[-2] <= A:
+        fib.append(fib[-1] + fib[-2])
+    roots, s, rem = [], 0, A
+    while rem:
+        z = max(x for x in fib if x <= rem)
+        roots.append((s, z))
+        s, rem = s + z, rem - z
+    return fib, roots
+
+
+def check_fib_invariants(free_pairs, live_pairs, arena: int, align: int):
+    """FIB_BUDDY: tiling (I1/I2), every block is a node of a root's Fibonacci split tree, and no
+    two free siblings coexist (I3: complete merging)."""
+    fp = np.asarray(free_pairs, dtype=np.uint64).reshape(-1, 2)
+    lp = np.asarray(live_pairs, dtype=np.uint64).reshape(-1, 2)
+    check_invariants(np.zeros((0, 2), np.uint64), np.concatenate([fp, lp]), arena, align, True)
+    fib, roots = fib_roots(arena, align)
+    nodes = {}
+
+    def rec(s, z, parent):
+        nodes[(s, z)] = parent
+        i = fib.index(z)
+        if i >= 1:
+            lo = fib[i - 1]
+            rec(s, lo, (s, z))
+            rec(s + lo, z - lo, (s, z))
+    if arena // align <= 1 << 14:
+        for r in roots:
+            rec(*r, None)
+        a = int(align)
+        free = {(int(s) // a, int(z) // a) for s, z in fp}
+        for blk in free | {(int(s) // a, int(z) // a) for s, z in lp}:
+            assert blk in nodes, f"block {blk} is not a tree node"
+        kids = {}
+        for blk in free:
+            if nodes[blk] is not None:
+                kids.setdefault(nodes[blk], []).append(blk)
+        assert all(len(v) < 2 for v in kids.values()), "two free siblings not merged"

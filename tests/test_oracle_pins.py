@@ -20,9 +20,9 @@ import tracegen as tg
 from oracle import OracleL, insert_class, search_class
 import copy
 
-from oracle.oracle_b import OracleB, OracleBDouble, OracleBHybrid, OracleBLifo, cls_lo, cls_of, search_cls
-from tests.helpers import (HEAP_NULL, PARTIAL, IdMap, check_double_invariants, check_invariants, double_layout,
-                           hybrid_layout, parse_golden, replay, replay_partial)
+from oracle.oracle_b import OracleB, OracleBDouble, OracleBFib, OracleBHybrid, OracleBLifo, cls_lo, cls_of, search_cls
+from tests.helpers import (HEAP_NULL, PARTIAL, IdMap, check_double_invariants, check_fib_invariants, check_invariants,
+                           double_layout, fib_roots, hybrid_layout, parse_golden, replay, replay_partial)
 
 FIT_POLICIES = [1, 2, 3, 4]
 ALL_POLICIES = [1, 2, 3, 4, 5, 6, 8]
@@ -216,6 +216,8 @@ def _run_both(policy, arena, align, batch, ops, sizes, rho, idx, size_kind=0):
         assert np.array_equal(fl, fb) and np.array_equal(ll, lb), (policy, bi)
         if policy == 9:
             check_double_invariants(fl, ll, arena, align)
+        elif policy == 10:
+            check_fib_invariants(fl, ll, arena, align)
         else:
             check_invariants(fl, ll, arena, align, policy == tg.BUDDY, _edges(policy, arena, align))
     st = hl.stats()
@@ -286,7 +288,7 @@ def test_exhaustive_tiny_heaps(policy):
 
 
 def _twin(policy):
-    return {6: OracleBLifo, 7: OracleBHybrid, 9: OracleBDouble}.get(policy, OracleB)
+    return {6: OracleBLifo, 7: OracleBHybrid, 9: OracleBDouble, 10: OracleBFib}.get(policy, OracleB)
 
 
 def _edges(policy, arena, align):
@@ -610,6 +612,84 @@ def test_partial_exhaustive_tiny_heaps(policy):
 
 def test_partial_rejected_where_undefined():
     """The flag needs address coalescing: buddies, pools and LIFO bins reject it."""
-    for policy in (tg.BUDDY, tg.HYBRID, tg.DOUBLE_BUDDY, tg.SEGFIT_LIFO):
+    for policy in (tg.BUDDY, tg.HYBRID, tg.DOUBLE_BUDDY, tg.SEGFIT_LIFO, tg.FIB_BUDDY):
         with pytest.raises(ValueError):
             OracleL(1 << 14, 16, policy | PARTIAL)
+
+
+# ---------------- Fibonacci buddies (PAPER.md:129, reading C30) ----------------
+
+def test_fib_roots_and_closed_forms():
+    """Zeckendorf roots (every positive integer is a sum of non-consecutive Fibonacci numbers);
+    a fresh Fibonacci-sized heap fed only 1-unit requests fills in address order (0, 1, 2, ...,
+    the low part is always split further) — several roots fill smallest root first — and
+    freeing everything restores the roots."""
+    for A in (1, 2, 3, 4, 7, 8, 12, 20, 21, 100, 1000, 4181):
+        fib, roots = fib_roots(A, 1)
+        sizes = [z for _, z in roots]
+        assert sum(sizes) == A and sizes == sorted(sizes, reverse=True)
+        assert all(fib.index(a) - fib.index(b) >= 2 for a, b in zip(sizes, sizes[1:]))   # non-consecutive
+        h = OracleL(A, 1, tg.FIB_BUDDY)
+        assert [tuple(int(v) for v in p) for p in h.export()[0]] == roots
+        out = h.alloc_batch([1] * A)
+        if len(roots) == 1:              # one root: the low part is always split further
+            assert [int(x) for x in out] == list(range(A)), A
+        else:                            # smaller roots are used first, each in address order
+            want = [u for s, z in sorted(roots, key=lambda r: r[1]) for u in range(s, s + z)]
+            assert [int(x) for x in out] == want, A
+        assert int(h.alloc_batch([1])[0]) == HEAP_NULL
+        h.free_batch(out)
+        assert [tuple(int(v) for v in p) for p in h.export()[0]] == roots
+
+
+def test_fib_requests_round_up_to_fibonacci_sizes():
+    """A request of r units takes a block of the smallest Fibonacci size >= r (live sizes), and
+    the split leaves exactly the high parts of the descended classes free."""
+    h = OracleL(89, 1, tg.FIB_BUDDY)
+    out = [int(x) for x in h.alloc_batch([4, 6, 9, 1])]
+    fp, lp = h.export()
+    assert sorted(int(z) for _, z in lp) == [1, 5, 8, 13]
+    # 89 -> 55|34 -> 34|21 -> 21|13 -> 13|8 -> 8|5 -> 5|3: the 5 at 0 leaves high parts 3@5, 5@8,
+    # 8@13, 13@21, 21@34, 34@55; 6 units take 8@13, 9 units 13@21, 1 unit splits 3@5 -> 2|1 -> 1|1
+    assert out == [0, 13, 21, 5]
+    assert [tuple(int(v) for v in p) for p in fp] == [(6, 1), (7, 1), (8, 5), (34, 21), (55, 34)]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fib_buddy_oracle_l_equals_oracle_b(seed):
+    _run_both(tg.FIB_BUDDY, 1 << 14, 16, 24, 1500, (4, 11), (2, 5) if seed % 2 else (1, 2), 90 + seed)
+
+
+def test_fib_buddy_exhaustive_tiny():
+    """Every sequence of <= 4 single-op batches over a 12-unit heap (roots 8 + 3 + 1): alloc 1..12
+    units or free any live block; Oracle-L == Oracle-B (derived maximal free tree nodes)."""
+    A = 12
+
+    def leaves(depth, seq, hb):
+        yield seq
+        if depth == 0:
+            return
+        for s in range(1, A + 1):
+            hb2 = copy.deepcopy(hb)
+            hb2.alloc_batch([s])
+            yield from leaves(depth - 1, seq + [("a", s)], hb2)
+        for o in list(hb.live):
+            hb2 = copy.deepcopy(hb)
+            hb2.free_batch([o])
+            yield from leaves(depth - 1, seq + [("f", o)], hb2)
+
+    n = 0
+    for seq in leaves(3, [], OracleBFib(A, 1)):
+        hl, hb = OracleL(A, 1, tg.FIB_BUDDY), OracleBFib(A, 1)
+        for op, v in seq:
+            if op == "a":
+                assert int(hl.alloc_batch([v])[0]) == int(hb.alloc_batch([v])[0]), seq
+            else:
+                hl.free_batch([v])
+                hb.free_batch([v])
+        fl, ll = hl.export()
+        fb, lb = hb.export()
+        assert np.array_equal(fl, fb) and np.array_equal(ll, lb), seq
+        check_fib_invariants(fl, ll, A, 1)
+        n += 1
+    assert n > 1000

@@ -30,8 +30,9 @@ _LIB = os.path.join(_HERE, "libtracegen.so")
 HEAP_NULL = (1 << 64) - 1
 
 # policy ids (numbers only; the meaning lives in include/heap.h and oracle/)
-FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY, SEGFIT_LIFO, HYBRID, NEXT_FIT, DOUBLE_BUDDY = 1, 2, 3, 4, 5, 6, 7, 8, 9
-POLICY_NAME = {1: "first_fit", 2: "best_fit", 3: "segfit", 4: "tlsf", 5: "buddy", 6: "segfit_lifo", 7: "hybrid", 8: "next_fit", 9: "double_buddy"}
+FIRST_FIT, BEST_FIT, SEGFIT, TLSF, BUDDY, SEGFIT_LIFO, HYBRID, NEXT_FIT, DOUBLE_BUDDY, FIB_BUDDY = range(1, 11)
+POLICY_NAME = {1: "first_fit", 2: "best_fit", 3: "segfit", 4: "tlsf", 5: "buddy", 6: "segfit_lifo", 7: "hybrid", 8: "next_fit", 9: "double_buddy",
+               10: "fib_buddy"}
 
 
 @dataclass(frozen=True)
