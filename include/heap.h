@@ -81,7 +81,7 @@ enum heap_policy {
                            block with start >= rover and size >= r, else the first
                            from address 0; the rover is the end of the last
                            allocation; frees leave it alone (C27) */
-    HEAP_DOUBLE_BUDDY = 9 /* double buddies: a binary buddy heap of
+    HEAP_DOUBLE_BUDDY = 9, /* double buddies: a binary buddy heap of
                            align-sized units on [0, A) and one of 3*align-sized units
                            (blocks 3*2^k*align) on [A, arena) holding
                            floor(arena / 6 align) units; a request of r units goes to
@@ -89,6 +89,17 @@ enum heap_policy {
                            3*2^ceil(log2 ceil(r/3)) units, with no fallback
                            (C28).  Offsets past A must be whole 3-units.
                            max_live_blocks bounds each heap's live blocks. */
+    HEAP_FIB_BUDDY = 10 /* Fibonacci buddies: block sizes 1, 2, 3, 5,
+                           8, ... units (S_k = S_{k-1} + S_{k-2}); a block splits into
+                           its low part of the previous size and its high part of the
+                           size before (2 = 1 + 1); the arena is the greedy
+                           (Zeckendorf) sum of Fibonacci roots.  A request of r units
+                           takes the smallest nonempty class whose size is >= r,
+                           lowest address, split keeping the low part; a free merges
+                           a block with its split-tree sibling while that is free
+                           (C30).  Per alloc batch at most 1024 split
+                           leftovers of one class may be created (else
+                           HEAP_ECAPACITY). */
 };
 
 /* Policy flag (OR into policy): partial (tail) deallocation, "freeing the last 2kB of a 10kB

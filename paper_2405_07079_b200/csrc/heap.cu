@@ -18,6 +18,7 @@
 #include "pool.cuh"
 #include "dbuddy.cuh"
 #include "partial.cuh"
+#include "fib.cuh"
 
 namespace {
 
@@ -46,6 +47,9 @@ struct Layout {
     u64 o_gin, o_gout;   // graph path: staging of the request / result words
     // HEAP_DOUBLE_BUDDY: the 3-unit heap's geometry and the split / merge buffers
     u64 dbl_A, dbl_n3, o_dctr, o_ca, o_cb, o_ia, o_ib, o_ra, o_rb, o_sstats2, o_sub2, sub2_total;
+    // HEAP_FIB_BUDDY: geometry, leftovers, level lists (fib.cuh)
+    fib::Geom fg;
+    u64 o_fgeom, o_flo, o_fbufL, o_frem, o_fscr;
     // HEAP_PARTIAL_FREE: live-start bitmap (partial.cuh)
     bool partial;
     partial::Lbm lbm;
@@ -56,7 +60,7 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
     if (align == 0 || (align & (align - 1)) || arena == 0 || arena % align) return false;
     const bool partial_free = (policy & HEAP_PARTIAL_FREE) != 0;
     policy &= ~HEAP_PARTIAL_FREE;
-    if (policy < HEAP_FIRST_FIT || policy > HEAP_DOUBLE_BUDDY) return false;
+    if (policy < HEAP_FIRST_FIT || policy > HEAP_FIB_BUDDY) return false;
     // partial frees need address coalescing (C29)
     if (partial_free && policy != HEAP_FIRST_FIT && policy != HEAP_BEST_FIT && policy != HEAP_SEGFIT &&
         policy != HEAP_TLSF && policy != HEAP_NEXT_FIT)
@@ -153,10 +157,15 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         return true;
     }
     L.K = ilog2(L.A_u);
+    const bool fibp = policy == HEAP_FIB_BUDDY;
+    if (fibp) {                               // Fibonacci classes (reading C30)
+        fib::make_geom(L.A_u, &L.fg);
+        L.K = (int)L.fg.K;
+    }
     L.L = (policy == HEAP_TLSF) ? 5 : 0;
     L.NC = (int)h_cls_insert(L.A_u, L.L) + 1;
     L.cap_f = max_live + 1;
-    if (policy == HEAP_BUDDY) L.cap_f = (max_live + 1) * 2 * (u64)(L.K + 1);
+    if (policy == HEAP_BUDDY || fibp) L.cap_f = (max_live + 1) * 2 * (u64)(L.K + 1);
     L.cap_m = L.cap_f + max_batch;
     L.tcap = next_pow2(2 * max_live);
     if (L.tcap < 1024) L.tcap = 1024;
@@ -180,7 +189,7 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
     L.o_tbl = take(L.tcap * 8);
     L.o_fs0 = take(L.cap_f * 8);
     L.o_fs1 = take(L.cap_f * 8);
-    if (policy != HEAP_BUDDY) { L.o_fe0 = take(L.cap_f * 8); L.o_fe1 = take(L.cap_f * 8); }
+    if (policy != HEAP_BUDDY && !fibp) { L.o_fe0 = take(L.cap_f * 8); L.o_fe1 = take(L.cap_f * 8); }
     L.o_kA = take(L.sort_cap * 4);
     L.o_kB = take(L.sort_cap * 4);
     L.o_vA = take(L.sort_cap * 4);
@@ -235,7 +244,14 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.lbm_words = partial::lbm_layout(L.A_u, &L.lbm);
         L.o_lbm = take(L.lbm_words * 4);
     }
-    if (policy == HEAP_BUDDY) {
+    if (fibp) {
+        L.o_fgeom = take(sizeof(fib::Geom));
+        L.o_flo = take((u64)(L.K + 1) * fib::LC * 8);
+        L.o_fbufL = take(2 * L.bud_cap * 8);  // every level list: <= 2 x (resident + freed) nodes
+        L.o_frem = take(2 * L.bud_cap * 4);
+        L.o_fscr = take(4 * (fib::MAXC + 2) * 8);
+    }
+    if (policy == HEAP_BUDDY || fibp) {
         L.o_dtm = take(L.dpool * 4);
         L.o_dsrc = take(L.dpool * 4);
         L.o_baddr = take(L.bpool * 8);
@@ -275,6 +291,9 @@ struct heap {
     u64 *bk[2];
     u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
     u64 *baddr, *bufA, *bufB, *promo, *fr;
+    fib::Geom *fgeom;                         // HEAP_FIB_BUDDY
+    u64 *flo, *fbufL, *fscr;
+    u32 *frem;
     // HEAP_HYBRID
     heap *sub;                                // HYBRID: the TLSF heap on [pool_end, arena); DOUBLE: the binary heap
     heap *sub2;                               // DOUBLE_BUDDY: the 3-unit heap (NULL if it has no units)
@@ -333,7 +352,9 @@ __global__ void k_init(DevCtr *ctr, u64 *tbl, u64 tcap, u64 *fs, u64 *fe, u64 A_
     for (u64 i = tid; i < tcap; i += nth) tbl[i] = table::EMPTY;
     if (tid == 0) {
         memset(ctr, 0, sizeof(DevCtr));
-        if (!buddy) {
+        if (buddy == 2) {
+            // HEAP_FIB_BUDDY: the root lists are written by fib::k_init_lists
+        } else if (!buddy) {
             fs[0] = 0;      // the heap itself is the one free block (Alg. 6)
             fe[0] = A_u;
             ctr->F = 1;
@@ -433,7 +454,8 @@ void maybe_rebuild(heap *h, cudaStream_t s) {
 
 // ---- statistics ----
 __global__ void __launch_bounds__(1024) k_stats(const DevCtr *ctr, const u64 *fs, const u64 *fe, int buddy, int K,
-                                                u64 arena, u64 align, int alog2, u64 meta, heap_stats_t *out) {
+                                                u64 arena, u64 align, int alog2, u64 meta, heap_stats_t *out,
+                                                const u64 *fibS) {
     __shared__ u64 sm[33];
     u64 nfree, fu = 0, big = 0;
     if (!buddy) {
@@ -454,9 +476,10 @@ __global__ void __launch_bounds__(1024) k_stats(const DevCtr *ctr, const u64 *fs
     } else {
         nfree = 0;
         for (int t = 0; t <= K; t++) {
+            const u64 z = fibS ? fibS[t] : (1ull << t);   // Fibonacci or power-of-two class size
             nfree += ctr->bud_cnt[t];
-            fu += ctr->bud_cnt[t] << t;
-            if (ctr->bud_cnt[t]) big = 1ull << t;
+            fu += ctr->bud_cnt[t] * z;
+            if (ctr->bud_cnt[t]) big = z;
         }
     }
     if (threadIdx.x == 0) {
@@ -496,11 +519,11 @@ __global__ void k_bud_keys(const u64 *list, const DevCtr *ctr, int K, u32 *key, 
     }
 }
 __global__ void k_export_pairs_u32(const u32 *key, const u32 *val, const u64 *n_dev, int alog2, int val_is_order,
-                                   u64 *pairs, u64 cap) {
+                                   u64 *pairs, u64 cap, const u64 *fibS = nullptr) {
     const u64 n = *n_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n && i < cap; i += (u64)gridDim.x * blockDim.x) {
         pairs[2 * i] = (u64)key[i] << alog2;
-        u64 z = val_is_order ? (1ull << val[i]) : ((u64)val[i] + 1);
+        u64 z = val_is_order ? (fibS ? fibS[val[i]] : (1ull << val[i])) : ((u64)val[i] + 1);
         pairs[2 * i + 1] = z << alog2;
     }
 }
@@ -635,7 +658,15 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         // the initial whole-heap block was pushed at time 0; pushes of batches start at 1
         if (cudaMemsetAsync(h->ft[0], 0, 4, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     }
-    if (policy == HEAP_BUDDY) {
+    if (policy == HEAP_FIB_BUDDY) {
+        h->fgeom = at<fib::Geom>(w, L.o_fgeom);
+        h->flo = at<u64>(w, L.o_flo); h->fbufL = at<u64>(w, L.o_fbufL); h->frem = at<u32>(w, L.o_frem);
+        h->fscr = at<u64>(w, L.o_fscr);
+        if (cudaMemcpyAsync(h->fgeom, &L.fg, sizeof(fib::Geom), cudaMemcpyHostToDevice, (cudaStream_t)s) != cudaSuccess ||
+            cudaFuncSetAttribute(fib::k_alloc_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)fib::eng_smem(L.fg.K)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    }
+    if (policy == HEAP_BUDDY || policy == HEAP_FIB_BUDDY) {
         h->dtm = at<u32>(w, L.o_dtm); h->dsrc = at<u32>(w, L.o_dsrc); h->baddr = at<u64>(w, L.o_baddr);
         h->btm = at<u32>(w, L.o_btm); h->bsrc = at<u32>(w, L.o_bsrc);
         h->bufA = at<u64>(w, L.o_bufA); h->bufB = at<u64>(w, L.o_bufB); h->promo = at<u64>(w, L.o_promo);
@@ -651,7 +682,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->tag = HEAP_TAG_MISC;
     cudaStream_t st = (cudaStream_t)s;
     LAUNCH(h, k_init, h->G, 256, 0, st, h->ctr, h->tbl, L.tcap, h->fs[0], h->fe[0], L.A_u,
-           policy == HEAP_BUDDY ? 1 : 0, L.K);
+           policy == HEAP_BUDDY ? 1 : (policy == HEAP_FIB_BUDDY ? 2 : 0), L.K);
+    if (policy == HEAP_FIB_BUDDY) LAUNCH(h, fib::k_init_lists, 1, 1, 0, st, h->ctr, h->fs[0], h->fgeom);
     if (policy == HEAP_FIRST_FIT || policy == HEAP_NEXT_FIT) {
         u64 offs[fits::FF_MAX_LEVELS] = {0};
         u64 n = L.cap_f, o = 0;
@@ -692,7 +724,8 @@ uint64_t heap_launch_count(const heap_t *h) {
 static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *n_in, cudaStream_t s) {
     const Layout &L = h->L;
     const int cur = h->cur, nxt = cur ^ 1;
-    const bool bud = h->policy == HEAP_BUDDY;
+    const bool fibp = h->policy == HEAP_FIB_BUDDY;
+    const bool bud = h->policy == HEAP_BUDDY || fibp;
     DevCtr *C = h->ctr;
     u64 *n_dev = &C->tmp[0];
     // 1. classify (null / unaligned / out of range) and compact the candidate keys
@@ -747,13 +780,18 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
     } else {
         // 4b. group freed blocks by order, 5b. level-by-level buddy merge
         TAG(h, HEAP_TAG_BUDDY_FREE);
-        LAUNCH(h, buddy::k_free_orders, h->G, 256, 0, s, h->vsc, h->vec, &C->nv, h->kA, h->vA);
+        if (fibp) LAUNCH(h, fib::k_free_classes, h->G, 256, 0, s, h->vsc, h->vec, &C->nv, h->fgeom, h->kA, h->vA);
+        else LAUNCH(h, buddy::k_free_orders, h->G, 256, 0, s, h->vsc, h->vec, &C->nv, h->kA, h->vA);
         int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->nv, 8, s);
         u32 *ok = r2 ? h->kB : h->kA, *ov = r2 ? h->vB : h->vA;
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, ok, &C->nv, L.K + 1, h->froff);
         LAUNCH(h, buddy::k_gather_u64, h->G, 256, 0, s, h->vsc, ov, &C->nv, h->fr);
-        LAUNCH(h, buddy::k_free_levels, 1, buddy::NT, buddy::FREE_SMEM, s, h->fs[cur], h->fs[nxt], h->fr, h->froff, h->bufA,
-               h->bufB, h->promo, L.K, C);
+        if (fibp)
+            LAUNCH(h, fib::k_free_levels, 1, fib::NT, 0, s, h->fs[cur], h->fs[nxt], h->fr, h->froff, h->fbufL, h->frem,
+                   h->promo, h->bufA, h->fgeom, C);
+        else
+            LAUNCH(h, buddy::k_free_levels, 1, buddy::NT, buddy::FREE_SMEM, s, h->fs[cur], h->fs[nxt], h->fr, h->froff,
+                   h->bufA, h->bufB, h->promo, L.K, C);
     }
     h->cur = nxt;
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
@@ -764,6 +802,23 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
     const Layout &L = h->L;
     const int cur = h->cur, nxt = cur ^ 1;
     DevCtr *C = h->ctr;
+    if (h->policy == HEAP_FIB_BUDDY) {
+        // one warp serves the requests in order (fib.cuh), then each class's list is rebuilt
+        TAG(h, HEAP_TAG_BUDDY_ALLOC);
+        u64 *fo = h->fscr, *lcnt = h->fscr + (fib::MAXC + 2), *noff = h->fscr + 2 * (fib::MAXC + 2);
+        LAUNCH(h, fib::k_alloc_engine, 1, 32, fib::eng_smem(L.fg.K), s, (const u64 *)d_sizes, n, n_in, h->alog2,
+               h->fs[cur], h->fgeom, C, h->out, h->r, fo, h->flo, lcnt, noff);
+        LAUNCH(h, fib::k_alloc_rebuild, L.K + 1, fib::NT, 0, s, h->fs[cur], h->fs[nxt], h->fgeom, C, fo, h->flo, lcnt,
+               noff);
+        LAUNCH(h, fib::k_alloc_commit, 1, 1, 0, s, C, h->fgeom, noff);
+        TAG(h, HEAP_TAG_FINISH);
+        LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, n_in, h->alog2, (u64 *)d_out,
+               h->tbl, L.tcap - 1, L.tcap / table::LINE, C, h->max_live);
+        h->cur = nxt;
+        maybe_rebuild(h, s);
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        return HEAP_OK;
+    }
     if (h->policy == HEAP_BUDDY) {
         TAG(h, HEAP_TAG_BUDDY_ALLOC);
         LAUNCH(h, buddy::k_alloc_orders, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, L.A_u, L.K, h->kA, h->vA, &C->tmp[0]);
@@ -1090,8 +1145,10 @@ int heap_stats_async(heap_t *h, heap_stats_t *d_out, heap_stream_t sp) {
         if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
         return HEAP_OK;
     }
-    LAUNCH(h, k_stats, 1, 1024, 0, s, h->ctr, h->fs[h->cur], h->fe[h->cur], h->policy == HEAP_BUDDY ? 1 : 0, h->L.K,
-           h->arena, h->align, h->alog2, meta_bytes(h), d_out);
+    LAUNCH(h, k_stats, 1, 1024, 0, s, h->ctr, h->fs[h->cur], h->fe[h->cur],
+           (h->policy == HEAP_BUDDY || h->policy == HEAP_FIB_BUDDY) ? 1 : 0, h->L.K,
+           h->arena, h->align, h->alog2, meta_bytes(h), d_out,
+           h->policy == HEAP_FIB_BUDDY ? (const u64 *)h->fgeom : (const u64 *)nullptr);
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
     return HEAP_OK;
 }
@@ -1169,7 +1226,7 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
     int alog = h->alog2;
     u64 counts[2] = {0, 0};
     // free blocks
-    if (h->policy != HEAP_BUDDY) {
+    if (h->policy != HEAP_BUDDY && h->policy != HEAP_FIB_BUDDY) {
         if (d_free_pairs && cap_free)
             LAUNCH(h, k_export_free, h->G, 256, 0, s, h->fs[h->cur], h->fe[h->cur], &C->F, alog, (u64 *)d_free_pairs, cap_free);
         CUDA_TRY(cudaMemcpyAsync(&counts[0], &C->F, 8, cudaMemcpyDeviceToHost, s));
@@ -1178,7 +1235,8 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
         int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->bud_total, 32, s);
         u32 *k = rb ? h->kB : h->kA, *v = rb ? h->vB : h->vA;
         if (d_free_pairs && cap_free)
-            LAUNCH(h, k_export_pairs_u32, h->G, 256, 0, s, k, v, &C->bud_total, alog, 1, (u64 *)d_free_pairs, cap_free);
+            LAUNCH(h, k_export_pairs_u32, h->G, 256, 0, s, k, v, &C->bud_total, alog, 1, (u64 *)d_free_pairs, cap_free,
+                   h->policy == HEAP_FIB_BUDDY ? (const u64 *)h->fgeom : (const u64 *)nullptr);
         CUDA_TRY(cudaMemcpyAsync(&counts[0], &C->bud_total, 8, cudaMemcpyDeviceToHost, s));
     }
     // live blocks: collect table slots, sort by key

@@ -14,11 +14,12 @@ from . import _native
 from ._native import HeapStats, check, lib
 
 HEAP_FIRST_FIT, HEAP_BEST_FIT, HEAP_SEGFIT, HEAP_TLSF, HEAP_BUDDY, HEAP_SEGFIT_LIFO, HEAP_HYBRID = 1, 2, 3, 4, 5, 6, 7
-HEAP_NEXT_FIT, HEAP_DOUBLE_BUDDY = 8, 9
+HEAP_NEXT_FIT, HEAP_DOUBLE_BUDDY, HEAP_FIB_BUDDY = 8, 9, 10
 HEAP_PARTIAL_FREE = 0x100   # policy flag: partial (tail) deallocation (include/heap.h)
 HEAP_NULL = (1 << 64) - 1
 HEAP_NULL_I64 = -1
-POLICY_NAMES = {1: "first_fit", 2: "best_fit", 3: "segfit", 4: "tlsf", 5: "buddy", 6: "segfit_lifo", 7: "hybrid", 8: "next_fit", 9: "double_buddy"}
+POLICY_NAMES = {1: "first_fit", 2: "best_fit", 3: "segfit", 4: "tlsf", 5: "buddy", 6: "segfit_lifo", 7: "hybrid", 8: "next_fit", 9: "double_buddy",
+                10: "fib_buddy"}
 
 
 def _stream_handle(stream) -> int:

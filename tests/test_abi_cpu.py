@@ -32,14 +32,14 @@ def test_workspace_bytes_and_argument_checks():
     assert L.heap_workspace_bytes(1 << 20, 16, 4, 1024, 1024) > 0
     assert L.heap_workspace_bytes(1 << 20, 24, 4, 1024, 1024) == 0      # align not a power of two
     assert L.heap_workspace_bytes((1 << 20) + 8, 16, 4, 1024, 1024) == 0  # arena not a multiple
-    assert L.heap_workspace_bytes(1 << 20, 16, 10, 1024, 1024) == 0      # bad policy
+    assert L.heap_workspace_bytes(1 << 20, 16, 11, 1024, 1024) == 0      # bad policy
     assert L.heap_workspace_bytes(1 << 20, 16, 0, 1024, 1024) == 0
-    for pol in range(1, 10):
+    for pol in range(1, 11):
         assert L.heap_workspace_bytes(1 << 20, 16, pol, 1024, 1024) > 0, pol
     for pol in (1, 2, 3, 4, 8):                                           # HEAP_PARTIAL_FREE flag
         assert L.heap_workspace_bytes(1 << 20, 16, pol | 0x100, 1024, 1024) > \
             L.heap_workspace_bytes(1 << 20, 16, pol, 1024, 1024), pol
-    for pol in (5, 6, 7, 9):                                              # needs address coalescing
+    for pol in (5, 6, 7, 9, 10):                                          # needs address coalescing
         assert L.heap_workspace_bytes(1 << 20, 16, pol | 0x100, 1024, 1024) == 0, pol
     assert L.heap_workspace_bytes(1 << 20, 16, 4 | 0x200, 1024, 1024) == 0  # unknown flag
     assert L.heap_workspace_bytes((1 << 36) + (1 << 5), 16, 4, 1024, 1024) == 0  # > 2^32 units

@@ -110,6 +110,9 @@ SMALL = [
     (tg.DOUBLE_BUDDY, 6 * 4096 * 16, 16, 24, 1500, (4, 12), (1, 2), 0),  # two staggered buddy heaps
     (tg.DOUBLE_BUDDY, (1 << 24) + 4096, 64, 3000, 40000, (6, 16), (2, 5), 0),
     (tg.DOUBLE_BUDDY, 1 << 30, 256, 20000, 200000, (8, 24), (1, 2), 0),
+    (tg.FIB_BUDDY, 1 << 16, 16, 24, 1500, (4, 10), (1, 2), 0),          # Fibonacci buddies
+    (tg.FIB_BUDDY, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5), 0),
+    (tg.FIB_BUDDY, (1 << 30) + 12345 * 256, 256, 20000, 200000, (8, 24), (1, 2), 0),   # several roots
 ]
 
 
@@ -371,3 +374,24 @@ def test_partial_free_edges():
             # the heap keeps working after the tail frees
             assert np.array_equal(g.alloc_batch([16, 4096, 1 << 20]), o.alloc_batch([16, 4096, 1 << 20]))
             compare_state(g, o, f"{pol} {arena} after")
+
+
+def test_fib_buddy_config4_shape_and_edges():
+    """Config 4's trace (2^34-byte arena, 256 B units: roots 2^26 units = 39088169 + 24157817 +
+    ... ; 64K-request batches of power-of-two sizes) on Fibonacci buddies, every batch exact; then
+    a fresh Fibonacci-sized heap fed 1-unit requests fills in address order and frees back to its
+    root; empty / all-null / double / invalid free batches."""
+    c4 = tg.CONFIGS[4]
+    cfg = tg.Config(c4.idx, "cfg4-as-fib", tg.FIB_BUDDY, c4.arena_bytes, c4.align, c4.model, c4.batch, c4.rho_num,
+                    c4.rho_den, c4.batch * 12, c4.size_kind, c4.a, c4.b, max_live=c4.max_live)
+    run_parity(cfg, c4.max_live, c4.batch)
+    A = 4181
+    g, o = Gpu(A * 16, 16, tg.FIB_BUDDY, 1 << 13, 1 << 13), OracleL(A * 16, 16, tg.FIB_BUDDY)
+    out = g.alloc_batch([16] * A)
+    assert np.array_equal(out, o.alloc_batch([16] * A))
+    assert np.array_equal(out, np.arange(A, dtype=np.uint64) * 16)
+    for batch in ([], [HEAP_NULL] * 3, [16, 16, 17, 1 << 40], out[::2], out[1::2]):
+        g.free_batch(batch)
+        o.free_batch(batch)
+        compare_state(g, o, f"fib edge {len(batch)}")
+    assert [tuple(int(v) for v in p) for p in g.export()[0]] == [(0, A * 16)]
