@@ -199,67 +199,29 @@ __global__ void __launch_bounds__(NT) k_free_levels(const u64 *__restrict__ old_
 }
 
 // ------------------------------------------------------------------ alloc phase ----
+// Engine state: class c is owned by lane c & 31 (c < 32: "half" 0, c >= 32: half 1), which keeps
+// in registers its batch-start window (next list index, end), its head-cache window, its leftover
+// window and the two candidate heads (batch-start head hb, leftover head lb).  A request reads the
+// two heads of its class with two shuffles; only the owner updates; the nonempty mask is uniform.
+// Shared memory holds the head caches and the sorted leftover arrays.
 struct EngSmem {
-    Geom g;
-    u64 ptr[MAXC], end[MAXC];          // unconsumed part of the batch-start list beyond the cache
-    u32 hh[MAXC], hn[MAXC];            // head cache window [hh, hn)
-    u32 lh[MAXC], lt[MAXC];            // leftover window [lh, lt)
-    u64 mask;
+    u64 S[MAXC];
     u32 hc[MAXC * HC];
     u32 lo[1];                         // (K+1) * LC leftovers follow (dynamic)
 };
 inline size_t eng_smem(u32 K) { return sizeof(EngSmem) + (size_t)(K + 1) * LC * 4; }
 
-__device__ __forceinline__ void eng_refill(EngSmem &S, const u64 *__restrict__ old_list, u32 t) {
-    const u32 lane = lane_id();
-    const u64 p = S.ptr[t], e = S.end[t];
-    const u32 m = (u32)min((u64)HC, e - p);
-    if (lane < m) S.hc[t * HC + lane] = (u32)old_list[p + lane];
-    __syncwarp();
-    if (lane == 0) { S.hh[t] = 0; S.hn[t] = m; S.ptr[t] = p + m; }
-    __syncwarp();
-}
+struct Cls {                           // one class's state, held by its owner lane
+    u64 ptr, end;                      // batch-start list: next index to cache, end
+    u32 hh, hn;                        // cache window [hh, hn) in S.hc
+    u32 lh, lt;                        // leftover window [lh, lt) in S.lo
+    u64 hb, lb;                        // current heads (NONE64 if none)
+};
 
-// sorted insertion of leftover x into class c (whole warp)
-__device__ __forceinline__ void eng_insert(EngSmem &S, u32 c, u32 x, DevCtr *ctr) {
-    const u32 lane = lane_id();
-    u32 *L = S.lo + (u64)c * LC;
-    u32 h = S.lh[c], t = S.lt[c];
-    if (t == (u32)LC) {
-        if (h == 0) {                            // capacity: flag it (sticky), drop the leftover
-            if (lane == 0) atomicOr(&ctr->error_flags, (u64)ERR_CAP_FREE);
-            return;
-        }
-        for (u32 k = 0; k < t - h; k += 32) {    // move the window down to 0 (ascending chunks)
-            const u32 i = k + lane;
-            const u32 v = (i < t - h) ? L[h + i] : 0;
-            __syncwarp();
-            if (i < t - h) L[i] = v;
-            __syncwarp();
-        }
-        t -= h;
-        h = 0;
-    }
-    u32 a = h, b = t;                            // first element >= x
-    while (a < b) {
-        const u32 mid = (a + b) >> 1;
-        if (L[mid] < x) a = mid + 1; else b = mid;
-    }
-    for (int top = (int)t - 1; top >= (int)a; top -= 32) {   // shift [a, t) up by one, top chunk first
-        const int i = top - (int)lane;
-        const u32 v = (i >= (int)a) ? L[i] : 0;
-        __syncwarp();
-        if (i >= (int)a) L[i + 1] = v;
-        __syncwarp();
-    }
-    if (lane == 0) {
-        L[a] = x;
-        S.lh[c] = h;
-        S.lt[c] = t + 1;
-        S.mask |= 1ull << c;
-    }
-    __syncwarp();
-}
+// C0 / C1 are two named register sets (classes lane, lane + 32); hf is warp-uniform, so these
+// selections compile to selects / uniform branches, never to local memory
+#define CSEL(f) (hf ? C1.f : C0.f)
+#define CWITH(hf_, body) do { if (hf_) { Cls &x = C1; body; } else { Cls &x = C0; body; } } while (0)
 
 // outputs: out_u[i] (units or FAIL), r[i] = S_j (units; 0 on failure); per class the first
 // unconsumed batch-start index (fo), the leftovers (lo_g, lcnt) and the new list offsets (noff)
@@ -273,77 +235,167 @@ __global__ void __launch_bounds__(32, 1) k_alloc_engine(const u64 *__restrict__ 
     EngSmem &S = *reinterpret_cast<EngSmem *>(smem_raw);
     if (n_in) n = *n_in;
     const u32 lane = lane_id();
-    if (lane == 0) S.g = *gp;
-    __syncwarp();
-    const u32 K = S.g.K;
-    for (u32 t = lane; t <= K; t += 32) {
-        S.ptr[t] = ctr->bud_off[t];
-        S.end[t] = ctr->bud_off[t + 1];
-        S.hh[t] = 0; S.hn[t] = 0; S.lh[t] = 0; S.lt[t] = 0;
+    const u32 K = gp->K;
+    for (u32 t = lane; t < (u32)MAXC; t += 32) S.S[t] = (t <= K) ? gp->S[t] : NONE64;
+    // owner state of classes lane and lane + 32; initial caches (one coalesced load per class)
+    Cls C0, C1;
+#pragma unroll
+    for (int hf = 0; hf < 2; hf++) {
+        const u32 c = lane + 32 * hf;
+        CWITH(hf, {
+            x.ptr = x.end = 0; x.hh = x.hn = x.lh = x.lt = 0; x.hb = x.lb = NONE64;
+            if (c <= K) { x.ptr = ctr->bud_off[c]; x.end = ctr->bud_off[c + 1]; }
+        });
+    }
+    for (u32 t = 0; t <= K; t++) {
+        const u32 hf = t >> 5;
+        const u64 p0 = __shfl_sync(FULLMASK, CSEL(ptr), t & 31), e0 = __shfl_sync(FULLMASK, CSEL(end), t & 31);
+        const u32 m = (u32)min((u64)HC, e0 - p0);
+        if (lane < m) S.hc[t * HC + lane] = (u32)old_list[p0 + lane];
     }
     __syncwarp();
-    u64 mk = 0;
-    for (u32 t = 0; t <= K; t++) if (S.end[t] > S.ptr[t]) mk |= 1ull << t;
-    if (lane == 0) S.mask = mk;
-    __syncwarp();
+    u64 mask = 0;
+#pragma unroll
+    for (int hf = 0; hf < 2; hf++) {
+        const u32 c = lane + 32 * hf;
+        CWITH(hf, {
+            if (c <= K) {
+                const u32 m = (u32)min((u64)HC, x.end - x.ptr);
+                x.hn = m;
+                x.ptr += m;
+                x.hb = m ? (u64)S.hc[c * HC] : NONE64;
+            }
+        });
+        const u32 bal = __ballot_sync(FULLMASK, CSEL(hb) != NONE64);
+        mask |= (u64)bal << (32 * hf);
+    }
+    const u64 S0 = S.S[lane], S1 = S.S[lane + 32 < (u32)MAXC ? lane + 32 : 0];
+    const bool v1 = lane + 32 <= K;
     const u64 amask = (1ull << alog2) - 1;
+    u64 n_ins = 0, n_shift = 0, n_ref = 0;
+    long long cyc_ins = 0;
+    const long long cyc0 = clock64();
     for (u64 base = 0; base < n; base += 32) {
         const u64 my = base + lane;
         const u64 mys = my < n ? sizes[my] : 0;
-        u64 res = buddy::FAIL, rz = 0;
+        u64 res = NONE64, rz = 0;
         const u32 cnt = (u32)min((u64)32, n - base);
         for (u32 q = 0; q < cnt; q++) {
             const u64 s = __shfl_sync(FULLMASK, mys, q);
             const u64 r = (s >> alog2) + ((s & amask) != 0);
-            const u32 j = (s == 0) ? K + 1 : class_of_req(S.g, r);
+            // smallest class holding r: count the class sizes below r
+            const u32 j = (s == 0) ? K + 1
+                                   : (u32)(__popc(__ballot_sync(FULLMASK, lane <= K && S0 < r)) +
+                                           __popc(__ballot_sync(FULLMASK, v1 && S1 < r)));
+            const u64 m = (j <= K) ? (mask & (~0ull << j)) : 0;
             u64 a = NONE64;
-            const u64 m = (j <= K) ? (S.mask & (~0ull << j)) : 0;
             if (m) {
-                const u32 t = (u32)(__ffsll((long long)m) - 1);
-                const u32 hh = S.hh[t], hn = S.hn[t];
-                if (hh == hn && S.ptr[t] < S.end[t]) eng_refill(S, old_list, t);
-                const u32 hh2 = S.hh[t], hn2 = S.hn[t];
-                const u64 hb = (hh2 < hn2) ? (u64)S.hc[t * HC + hh2] : NONE64;
-                const u32 lh = S.lh[t], lt = S.lt[t];
-                const u64 lb = (lh < lt) ? (u64)S.lo[(u64)t * LC + lh] : NONE64;
-                __syncwarp();
-                if (hb < lb) {
-                    a = hb;
-                    if (lane == 0) S.hh[t] = hh2 + 1;
-                } else {
-                    a = lb;
-                    if (lane == 0) S.lh[t] = lh + 1;
+                const u32 t = (u32)(__ffsll((long long)m) - 1), ow = t & 31, hf = t >> 5;
+                const u64 hb = __shfl_sync(FULLMASK, CSEL(hb), ow), lb = __shfl_sync(FULLMASK, CSEL(lb), ow);
+                const bool th = hb < lb;
+                a = th ? hb : lb;
+                bool need = false;
+                if (lane == ow) {                                 // pop, next head
+                    CWITH(hf, {
+                        if (th) {
+                            x.hh++;
+                            if (x.hh < x.hn) x.hb = S.hc[t * HC + x.hh];
+                            else { x.hb = NONE64; need = x.ptr < x.end; }
+                        } else {
+                            x.lh++;
+                            x.lb = (x.lh < x.lt) ? (u64)S.lo[(u64)t * LC + x.lh] : NONE64;
+                        }
+                    });
                 }
-                __syncwarp();
-                if (lane == 0 && S.hh[t] == S.hn[t] && S.ptr[t] == S.end[t] && S.lh[t] == S.lt[t])
-                    S.mask &= ~(1ull << t);
-                __syncwarp();
-                for (u32 u = t; u > j; u--) eng_insert(S, rcls(u), (u32)(a + S.g.S[u - 1]), ctr);
+                if (__shfl_sync(FULLMASK, (int)need, ow)) {        // refill the cache (whole warp)
+                    const u64 p0 = __shfl_sync(FULLMASK, CSEL(ptr), ow), e0 = __shfl_sync(FULLMASK, CSEL(end), ow);
+                    const u32 mm = (u32)min((u64)HC, e0 - p0);
+                    if (lane < mm) S.hc[t * HC + lane] = (u32)old_list[p0 + lane];
+                    __syncwarp();
+                    if (lane == ow) CWITH(hf, { x.hh = 0; x.hn = mm; x.ptr = p0 + mm; x.hb = S.hc[t * HC]; });
+                    n_ref++;
+                }
+                const bool ne = __shfl_sync(FULLMASK, (int)(CSEL(hb) != NONE64 || CSEL(lb) != NONE64), ow);
+                if (!ne) mask &= ~(1ull << t);
+                // split keeping the low part: the high parts (a + S_{u-1}, R(u)) stay free
+                const long long c0 = clock64();
+                for (u32 u = t; u > j; u--) {
+                    const u32 c = rcls(u), oc = c & 31, hc2 = c >> 5;
+                    const u32 xv = (u32)(a + S.S[u - 1]);
+                    u32 h = __shfl_sync(FULLMASK, hc2 ? C1.lh : C0.lh, oc), tt = __shfl_sync(FULLMASK, hc2 ? C1.lt : C0.lt, oc);
+                    u32 *L = S.lo + (u64)c * LC;
+                    n_ins++;
+                    if (tt == (u32)LC) {
+                        if (h == 0) {                            // capacity: flag (sticky), drop
+                            if (lane == 0) atomicOr(&ctr->error_flags, (u64)ERR_CAP_FREE);
+                            continue;
+                        }
+                        for (u32 k = 0; k < tt - h; k += 32) {   // move the window down to 0
+                            const u32 i = k + lane;
+                            const u32 v = (i < tt - h) ? L[h + i] : 0;
+                            __syncwarp();
+                            if (i < tt - h) L[i] = v;
+                            __syncwarp();
+                        }
+                        tt -= h;
+                        h = 0;
+                    }
+                    // insertion point: the tail (common), else a 32-way warp search
+                    u32 lo2 = h, hi2 = tt;
+                    if (tt == h || L[tt - 1] < xv) lo2 = tt;
+                    while (hi2 - lo2 > 1 && lo2 < tt) {
+                        const u32 seg = (hi2 - lo2 + 31) / 32;
+                        const u32 i = lo2 + lane * seg;
+                        const u32 k = __popc(__ballot_sync(FULLMASK, i < hi2 && L[i] < xv));
+                        if (k == 0) { hi2 = lo2; break; }
+                        lo2 = lo2 + (k - 1) * seg + 1;
+                        hi2 = min(hi2, lo2 - 1 + seg);
+                        if (seg == 1) { hi2 = lo2; break; }
+                    }
+                    if (lo2 < hi2 && L[lo2] < xv) lo2++;
+                    n_shift += tt - lo2;
+                    for (int top = (int)tt - 1; top >= (int)lo2; top -= 32) {   // shift [lo2, tt) up by one
+                        const int i = top - (int)lane;
+                        const u32 v = (i >= (int)lo2) ? L[i] : 0;
+                        __syncwarp();
+                        if (i >= (int)lo2) L[i + 1] = v;
+                        __syncwarp();
+                    }
+                    if (lane == 0) L[lo2] = xv;
+                    __syncwarp();
+                    if (lane == oc) CWITH(hc2, { x.lh = h; x.lt = tt + 1; x.lb = L[h]; });
+                    mask |= 1ull << c;
+                }
+                cyc_ins += clock64() - c0;
             }
             if (lane == q) {
                 res = a;
-                rz = (a == NONE64) ? 0 : S.g.S[j];
+                rz = (a == NONE64) ? 0 : S.S[j];
             }
         }
         if (my < n) { out_u[my] = (res == NONE64) ? buddy::FAIL : res; r_out[my] = rz; }
     }
     __syncwarp();
-    // leftovers to global, new offsets
+    if (lane == 0) {                 // diagnostics (heap_debug_counters)
+        ctr->eng[0] += clock64() - cyc0; ctr->eng[1] += cyc_ins; ctr->eng[3] += n_ins;
+        ctr->eng[4] += n_shift; ctr->eng[6] += n_ref;
+    }
+    // leftovers to global; per class first unconsumed list index, leftover count, new offsets
     for (u32 t = 0; t <= K; t++) {
-        const u32 lh = S.lh[t], lt = S.lt[t];
+        const u32 hf = t >> 5;
+        const u32 lh = __shfl_sync(FULLMASK, CSEL(lh), t & 31), lt = __shfl_sync(FULLMASK, CSEL(lt), t & 31);
         for (u32 k = lane; k < lt - lh; k += 32) lo_g[(u64)t * LC + k] = S.lo[(u64)t * LC + lh + k];
     }
-    if (lane == 0) {
-        u64 o = 0;
-        for (u32 t = 0; t <= K; t++) {
-            const u64 first = S.ptr[t] - (S.hn[t] - S.hh[t]);   // cached but unpopped entries stay in the list
-            fo[t] = first;
-            lcnt[t] = S.lt[t] - S.lh[t];
-            noff[t] = o;
-            o += (S.end[t] - first) + lcnt[t];
-        }
-        noff[K + 1] = o;
+    u64 o = 0;
+    for (u32 t = 0; t <= K; t++) {
+        const u32 hf = t >> 5;
+        const u64 f = __shfl_sync(FULLMASK, CSEL(ptr) - (CSEL(hn) - CSEL(hh)), t & 31);   // unpopped cache entries stay
+        const u64 c = __shfl_sync(FULLMASK, (u64)(CSEL(lt) - CSEL(lh)), t & 31);
+        const u64 e = __shfl_sync(FULLMASK, CSEL(end), t & 31);
+        if (lane == 0) { fo[t] = f; lcnt[t] = c; noff[t] = o; }
+        o += (e - f) + c;
     }
+    if (lane == 0) noff[K + 1] = o;
 }
 
 // one CTA per class: merge the unconsumed batch-start suffix with the leftovers

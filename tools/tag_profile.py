@@ -10,8 +10,11 @@ import tracegen as tg  # noqa: E402
 from paper_2405_07079_b200 import Heap  # noqa: E402
 from paper_2405_07079_b200._native import NTAGS  # noqa: E402
 
-c = int(sys.argv[1]); nb = int(sys.argv[2])
+c, _, pol = sys.argv[1].partition(":"); c = int(c); nb = int(sys.argv[2])   # "c" or "c:policy"
 cfg = tg.CONFIGS[c]
+if pol:
+    cfg = tg.Config(cfg.idx, cfg.name, int(pol), cfg.arena_bytes, cfg.align, cfg.model, cfg.batch, cfg.rho_num,
+                    cfg.rho_den, cfg.total_ops, cfg.size_kind, cfg.a, cfg.b, n_slots=cfg.n_slots, max_live=cfg.max_live)
 bs = list(tg.Trace(cfg, total_ops=cfg.batch * nb if cfg.model == 0 else None))[:nb]
 h = Heap(cfg.arena_bytes, cfg.align, cfg.policy, cfg.max_live, max(cfg.batch, 1000))
 idm = torch.full((sum(len(b[1]) for b in bs) + 1,), -1, dtype=torch.int64, device="cuda")
