@@ -284,7 +284,7 @@ def test_hybrid_config5_shape():
 
 
 @pytest.mark.parametrize("pol", [tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.BUDDY, tg.SEGFIT_LIFO, tg.HYBRID, tg.NEXT_FIT,
-                                 tg.DOUBLE_BUDDY])
+                                 tg.DOUBLE_BUDDY, tg.FIB_BUDDY, tg.TLSF | 0x100])
 def test_direct_launch_path(pol):
     """The same batches with batch graphs disabled (direct launches, the path tracing uses), and
     a heap switching between the two paths mid-trace."""
