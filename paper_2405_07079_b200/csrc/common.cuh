@@ -33,9 +33,10 @@ struct DevCtr {
     u64 n_hist;         // radix histogram length (256 * tiles)
     u64 nsort;          // element count for a sort
     u64 tmp[8];
-    // buddy: per-order counts of the current per-order free lists and their offsets
-    u64 bud_cnt[40];
-    u64 bud_off[41];
+    // buddy: per-order counts of the current per-order free lists and their offsets (binary
+    // buddies use K + 1 <= 33 orders, Fibonacci buddies K + 1 <= 46 classes: fib::MAXC = 48)
+    u64 bud_cnt[48];
+    u64 bud_off[49];
     u64 bud_total;
     u64 eng[16];        // alloc engine diagnostics (engine_tlsf.cuh)
     u64 lifo_clock;     // SEGFIT_LIFO logical push clock (fits.cuh)

@@ -36,6 +36,9 @@ constexpr int HC = 32;            // batch-start head cache per class (engine)
 constexpr int LC = 1024;          // leftover capacity per class per alloc batch (engine)
 constexpr u64 NONE64 = 0xFFFFFFFFFFFFFFFFull;
 
+static_assert(sizeof(((DevCtr *)0)->bud_off) / sizeof(u64) >= MAXC, "DevCtr::bud_off must hold K + 2 class offsets");
+static_assert(sizeof(((DevCtr *)0)->bud_cnt) / sizeof(u64) >= MAXC - 1, "DevCtr::bud_cnt must hold K + 1 counts");
+
 struct Geom {
     u64 S[MAXC];
     u64 rs[MAXC];      // root starts (increasing)

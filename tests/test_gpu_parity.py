@@ -395,3 +395,21 @@ def test_fib_buddy_config4_shape_and_edges():
         o.free_batch(batch)
         compare_state(g, o, f"fib edge {len(batch)}")
     assert [tuple(int(v) for v in p) for p in g.export()[0]] == [(0, A * 16)]
+
+
+def test_fib_buddy_arena_extremes():
+    """Fibonacci buddies at the arena extremes: 1, 2, 3 and 7 units (one or a few tiny roots; K = 0
+    for one unit) and 2^32 units (K = 45, the largest class table and engine shared memory), each
+    filled, partly freed and refilled against Oracle-L."""
+    for arena, align, sizes in ((16, 16, [16, 16]), (32, 16, [16, 16, 16]), (48, 16, [32, 16, 16]),
+                                (112, 16, [16, 48, 32, 16, 16]),
+                                (1 << 36, 16, [1 << 35, 16, 4096, 1 << 30, 3 << 20, 1 << 34, 16])):
+        g, o = Gpu(arena, align, tg.FIB_BUDDY, 1 << 10, 1 << 10), OracleL(arena, align, tg.FIB_BUDDY)
+        out = g.alloc_batch(sizes)
+        assert np.array_equal(out, o.alloc_batch(sizes)), arena
+        compare_state(g, o, f"fib {arena} filled")
+        g.free_batch(out[::2])
+        o.free_batch(out[::2])
+        compare_state(g, o, f"fib {arena} half freed")
+        assert np.array_equal(g.alloc_batch(sizes[::-1]), o.alloc_batch(sizes[::-1])), arena
+        compare_state(g, o, f"fib {arena} refilled")
