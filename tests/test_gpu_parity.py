@@ -154,7 +154,7 @@ def test_config5_first_batches():
 def test_edge_cases():
     """Empty batches, NULL / interior / unaligned / out-of-range / duplicate frees,
     zero and oversize requests, OOM in a tiny arena, the last unit of a 2^32-unit arena."""
-    for pol in (1, 2, 3, 4, 5, 6, 7, 8, 9):
+    for pol in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 1 | 0x100, 4 | 0x100):
         arena, align = 1 << 12, 16
         g = Gpu(arena, align, pol, 256, 64)
         o = OracleL(arena, align, pol)
@@ -413,3 +413,22 @@ def test_fib_buddy_arena_extremes():
         compare_state(g, o, f"fib {arena} half freed")
         assert np.array_equal(g.alloc_batch(sizes[::-1]), o.alloc_batch(sizes[::-1])), arena
         compare_state(g, o, f"fib {arena} refilled")
+
+
+@pytest.mark.parametrize("pol", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 1 | 0x100, 4 | 0x100])
+def test_arena_extremes_all_policies(pol):
+    """Every policy at the arena extremes: 1 unit, 3 units and 2^32 units (the largest arena the
+    32-bit unit keys allow): whole-arena, oversize, zero and minimum requests, free everything,
+    allocate again — every output, the state and the counters against Oracle-L."""
+    for arena in (16, 48, 1 << 36):
+        g, o = Gpu(arena, 16, pol, 256, 64), OracleL(arena, 16, pol)
+        sizes = np.array([16, arena, arena + 16, 0, 32, arena // 2, 16, 1 << 20], dtype=np.uint64)
+        go, oo = g.alloc_batch(sizes), o.alloc_batch(sizes)
+        assert np.array_equal(go, oo), (pol, arena)
+        compare_state(g, o, f"p{pol} {arena} alloc")
+        live = oo[oo != HEAP_NULL]
+        g.free_batch(live)
+        o.free_batch(live)
+        compare_state(g, o, f"p{pol} {arena} free all")
+        assert np.array_equal(g.alloc_batch(sizes[::-1].copy()), o.alloc_batch(sizes[::-1].copy())), (pol, arena)
+        compare_state(g, o, f"p{pol} {arena} realloc")
