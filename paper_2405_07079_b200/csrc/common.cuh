@@ -42,6 +42,10 @@ struct DevCtr {
     u64 lifo_clock;     // SEGFIT_LIFO logical push clock (fits.cuh)
     u64 req_n;          // request count of a graph-launched batch (heap.cu graph path)
     u64 rover;          // NEXT_FIT: unit address where the next search starts (reading C27)
+    u64 wild_n;         // TLSF/SEGFIT wilderness split: request count when active, else 0
+    u64 wild_start;     // the wilderness piece's start at the batch start (units)
+    u64 wild_total;     // units the batch took from it
+    u32 wild[2];        // {class Kw, piece f} of the wilderness, {NONE, NONE} when inactive
 };
 
 enum { ERR_CAP_LIVE = 1, ERR_TABLE_FULL = 2, ERR_CAP_FREE = 4, ERR_ENGINE = 8, ERR_LIVEMAP = 16 };

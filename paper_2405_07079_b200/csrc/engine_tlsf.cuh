@@ -47,6 +47,8 @@ constexpr u32 NONE = 0xFFFFFFFFu;
 constexpr u32 HEAPBIT = 0x80000000u;
 constexpr u32 SAME = 0xFFFFFFFEu; // block stays in its class after the carve
 constexpr u32 F_OK = 0, F_OVER = 1, F_MISS = 2;
+constexpr u64 NIL64 = ~0ull;
+constexpr u64 WILD = 0xFFFFFFFFFFFFFFFEull;   // result marker: served by the wilderness (k_wild_apply)
 
 struct Smem {
     u32 ptr[MAX_NC], endp[MAX_NC], cnt[MAX_NC], root[MAX_NC], slot[MAX_NC];
@@ -64,6 +66,8 @@ struct Smem {
     u32 lor[32 * 32];             // lane of rank q in the group led by lane l: lor[l*32+q]
     u64 res_s[32];
     u32 res_f[32], res_nk[32], res_flag[32], res_e[32];
+    u64 ch_i[32], ch_r[32];       // the chunk's requests (index, units), lane = time order
+    u32 ch_c[32];
 };
 
 // Overflow members of a class (remainders that arrived while its head cache was full) live in
@@ -329,9 +333,14 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                                                   const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
                                                   u64 *__restrict__ out_u, u32 *bm, u64 w0, u64 w1, u64 w2,
                                                   u32 *slot_map, int NC, int L, u64 *stats, Lifo lf,
-                                                  const u64 *n_in) {
+                                                  const u64 *n_in, const u32 *wild) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (n_in) n = *n_in;   // request count on the device (a hybrid heap's TLSF share)
+    // wilderness split (k_wild_setup): class Kw's single member is left out of the class state;
+    // a valid request finding no class >= its search class is marked WILD and served later by
+    // k_wild_apply's prefix sum.  Kw = NONE: every class is in the state (the plain engine).
+    const u32 Kw = wild ? wild[0] : NONE;
+    const bool wmode = Kw != NONE;
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const u32 lane = lane_id();
     const u64 nslots = (u64)NC;
@@ -340,6 +349,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     // ---- init: CSR ranges, head caches, bitmaps ----
     for (int k = lane; k < NC; k += 32) {
         u32 b = off[k], e = off[k + 1];
+        if ((u32)k == Kw) b = e;     // the wilderness is not a member of the class state
         S.slot[k] = NONE;
         S.ow_i[k] = NONE;
         S.cnt[k] = e - b;
@@ -380,21 +390,77 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             if (lane == 0 && stats) stats[2] = hp.broken ? 4 : 3;
             break;
         }
-        if (pos + 32 > rb_end) {                 // stage requests
-            rb_base = pos;
-            rb_end = pos + RB < n ? pos + RB : n;
-            for (u64 j = lane; j < rb_end - rb_base; j += 32) {
-                S.rbuf[j] = R[rb_base + j];
-                S.cbuf[j] = C[rb_base + j];
+        const u32 sw = S.sw;
+        u64 i = NIL64, ri = 0, scan_end = 0;
+        u32 ci = NONE, limit = 0;
+        bool act = false;
+        if (!wmode) {
+            if (pos + 32 > rb_end) {                 // stage requests
+                rb_base = pos;
+                rb_end = pos + RB < n ? pos + RB : n;
+                for (u64 j = lane; j < rb_end - rb_base; j += 32) {
+                    S.rbuf[j] = R[rb_base + j];
+                    S.cbuf[j] = C[rb_base + j];
+                }
+                __syncwarp();
+            }
+            i = pos + lane;
+            act = i < n;
+            ri = act ? S.rbuf[i - rb_base] : 0;
+            ci = act ? S.cbuf[i - rb_base] : NONE;
+            limit = (n - pos) < 32 ? (u32)(n - pos) : 32u;
+        } else {
+            // gather the next 32 candidates: requests whose search class is at most the highest
+            // nonempty class Mx.  The highest nonempty class only falls during the phase (pieces
+            // only shrink), so a request with c > Mx now finds nothing >= c at its own time
+            // either: it is WILD (valid) or fails; it is written here and never enters a chunk.
+            int Mx = -1;
+            if (sw) {
+                const u32 w = 31 - __clz(sw);
+                Mx = (int)(w * 32 + 31 - __clz(S.cw[w]));
+            }
+            u32 ncand = 0;
+            u64 sc = pos;
+            while (ncand < 32 && sc < n) {
+                if (sc < rb_base || sc + 32 > rb_end) {   // a retried chunk can start below
+                    __syncwarp();
+                    rb_base = sc;
+                    rb_end = sc + RB < n ? sc + RB : n;
+                    for (u64 j = lane; j < rb_end - rb_base; j += 32) {
+                        S.rbuf[j] = R[rb_base + j];
+                        S.cbuf[j] = C[rb_base + j];
+                    }
+                    __syncwarp();
+                }
+                const u64 j = sc + lane;
+                const bool v = j < n;
+                const u64 rj = v ? S.rbuf[j - rb_base] : 0;
+                const u32 cj = v ? S.cbuf[j - rb_base] : NONE;
+                const bool cand = v && rj != 0 && (int)cj <= Mx;
+                const u32 cmask = __ballot_sync(FULLMASK, cand);
+                const u32 nc = __popc(cmask);
+                const u32 take = min(nc, 32u - ncand);
+                const u32 rk = __popc(cmask & lanemask_lt());
+                if (cand && rk < take) { S.ch_i[ncand + rk] = j; S.ch_r[ncand + rk] = rj; S.ch_c[ncand + rk] = cj; }
+                // scanning stops at the first candidate not taken
+                u64 nsc = sc + 32 < n ? sc + 32 : n;
+                const u32 firstout = __ballot_sync(FULLMASK, cand && rk == take);
+                if (firstout) nsc = sc + __ffs(firstout) - 1;
+                if (v && !cand && j < nsc) out_u[j] = rj != 0 ? WILD : HEAP_NULL_U64;
+                ncand += take;
+                sc = nsc;
             }
             __syncwarp();
+            if (ncand == 0) { pos = sc; continue; }
+            act = lane < ncand;
+            if (act) { i = S.ch_i[lane]; ri = S.ch_r[lane]; ci = S.ch_c[lane]; }
+            limit = ncand;
+            scan_end = sc;
         }
+        __syncwarp();
+        S.ch_r[lane] = ri;
+        __syncwarp();
         t0 = clock64();
-        const u32 sw = S.sw;
-        const u64 i = pos + lane;
-        const bool act = i < n;
-        const u64 ri = act ? S.rbuf[i - rb_base] : 0;
-        const u32 ci = act ? S.cbuf[i - rb_base] : NONE;
         const bool fail0 = act && (ri == 0 || ci >= (u32)NC);
         u32 k = (act && !fail0) ? first_ge(S, sw, ci, NC) : NONE;
         u32 peers = 0, rank = 0, flag = F_OK, myf = 0, mynk = NONE, mye = 0;
@@ -478,7 +544,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                         cur_e = (u64)S.he[sl] + 1;
                         need = false;
                     }
-                    const u64 rq = S.rbuf[pos + lq - rb_base];
+                    const u64 rq = S.ch_r[lq];
                     S.res_flag[lq] = F_OK;
                     S.res_f[lq] = curf;
                     S.res_s[lq] = cur_s;
@@ -529,7 +595,6 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             if (act && !fail0 && lane > d && ci <= dk && ((((u64)dk) << 32) | (LIFO ? 0u : dfb)) < key) bad = true;
         }
         const u32 badm = __ballot_sync(FULLMASK, bad);
-        const u32 limit = (n - pos) < 32 ? (u32)(n - pos) : 32u;
         const u32 commit = badm ? (u32)(__ffs(badm) - 1) : limit;
 #ifdef ENGINE_DEBUG
         if (lane == 0 && n_iter < 8) printf("it %llu commit %u badm %x\n", n_iter, commit, badm);
@@ -546,7 +611,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         const u32 nxt = later ? (u32)(__ffs(later) - 1) : NONE;
         const bool last_on_block = mynk != SAME || nxt >= commit;
         if (cm) {
-            if (!part) out_u[i] = HEAP_NULL_U64;
+            if (!part) out_u[i] = (wmode && ri != 0) ? WILD : HEAP_NULL_U64;
             else {
                 out_u[i] = mys;
                 if (last_on_block) {
@@ -571,7 +636,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 // re-read from fs, never from the stale CSR copy
                 const u32 d = __ffs(st) - 1;
                 const u32 sl = k * H + ((b + left) & (H - 1));
-                S.hs[sl] = (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]);
+                S.hs[sl] = (u32)(S.res_s[d] + S.ch_r[d]);
                 S.hf[sl] |= HEAPBIT;
             }
             if (left) {                          // pop `left` members: advance the ring base
@@ -597,14 +662,16 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             while (mm) {
                 const u32 d = __ffs(mm) - 1;
                 mm &= mm - 1;
-                const u32 s2 = (u32)(S.res_s[d] + S.rbuf[pos + d - rb_base]);
+                const u32 s2 = (u32)(S.res_s[d] + S.ch_r[d]);
                 if constexpr (LIFO) arrive_lifo(S, lf, mynk, S.res_f[d], s2, S.res_e[d]);
                 else arrive(S, hp, mynk, S.res_f[d], s2, S.res_e[d]);
             }
         }
         __syncwarp();
         t_arr += clock64() - t0;
-        pos += commit;
+        if (!wmode) pos += commit;
+        else pos = commit < limit ? S.ch_i[commit] : scan_end;
+        __syncwarp();
     }
     if (slot_map)
         for (int k = lane; k < NC; k += 32) slot_map[k] = S.slot[k];   // for k_bitheap_clear
@@ -647,6 +714,84 @@ __global__ void k_bitheap_clear(const u64 *__restrict__ fs, const u64 *__restric
         l1[s * w1 + (f >> 10)] = 0;
         l2[s * w2 + (f >> 15)] = 0;
     }
+}
+
+// ---------------------------------------------------------------- wilderness split ----
+// Let K0 be the highest class with a member at the start of the alloc phase.  If (a) K0 has exactly
+// one member w, (b) w minus the units T of EVERY request of the batch is still in a class Kf above
+// every other member's class, and (c) every valid request's search class is <= Kf, then during
+// the phase (i) w's class stays above every other piece's (pieces only shrink), (ii) a request
+// takes w iff no other piece has class >= its search class (lowest (class, address) key among
+// classes >= c_i; w is the only candidate left and it fits by (c)), and (iii) taking w changes no
+// other class.  So the engine runs without w: a request that finds no class is marked WILD, and
+// the WILD requests take consecutive pieces of w's low end in request order — result = start(w) +
+// exclusive prefix sum of their units (Alg. 1 carve, applied one by one).
+__global__ void __launch_bounds__(1024) k_wild_setup(const u32 *__restrict__ off, const u32 *__restrict__ csr_f,
+                                                     const u64 *__restrict__ fs, const u64 *__restrict__ fe,
+                                                     const u64 *__restrict__ R, const u32 *__restrict__ Cq, u64 n,
+                                                     const u64 *n_in, int NC, int L, int enable, DevCtr *C) {
+    __shared__ u64 red[32];
+    __shared__ int kmax, kmax2;
+    __shared__ u32 cmax;
+    if (n_in) n = *n_in;
+    if (threadIdx.x == 0) { kmax = -1; kmax2 = -1; cmax = 0; }
+    __syncthreads();
+    u64 t = 0;
+    u32 cm = 0;
+    for (u64 i = threadIdx.x; i < n; i += blockDim.x) {
+        const u64 r = R[i];
+        t += r;
+        if (r) cm = max(cm, Cq[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        t += __shfl_xor_sync(FULLMASK, t, o);
+        cm = max(cm, __shfl_xor_sync(FULLMASK, cm, o));
+    }
+    if (lane_id() == 0) { red[threadIdx.x >> 5] = t; atomicMax(&cmax, cm); }
+    for (int k = threadIdx.x; k < NC; k += blockDim.x)
+        if (off[k + 1] > off[k]) atomicMax(&kmax, k);
+    __syncthreads();
+    for (int k = threadIdx.x; k < kmax; k += blockDim.x)
+        if (off[k + 1] > off[k]) atomicMax(&kmax2, k);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 T = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) T += red[w];
+        u32 K0 = NONE, fw = NONE;
+        const int k = kmax;
+        if (enable && k >= 0 && off[k + 1] - off[k] == 1) {
+            const u32 f = csr_f[off[k]];
+            const u64 z = fe[f] - fs[f];
+            if (z > T) {
+                const u32 Kf = cls_insert(z - T, L);
+                if ((int)Kf > kmax2 && cmax <= Kf) { K0 = (u32)k; fw = f; }
+            }
+        }
+        C->wild[0] = K0;
+        C->wild[1] = fw;
+        C->wild_n = (K0 != NONE) ? n : 0;
+        C->wild_start = (K0 != NONE) ? fs[fw] : 0;
+        if (K0 != NONE) C->eng[14]++;           // diagnostics: batches served with the split
+    }
+}
+
+// units of each WILD request (0 otherwise), for the prefix sum
+__global__ void k_wild_flags(const u64 *__restrict__ out_u, const u64 *__restrict__ R, const DevCtr *C,
+                             u32 *__restrict__ flags) {
+    const u64 n = C->wild_n;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        flags[i] = out_u[i] == WILD ? (u32)R[i] : 0u;
+}
+
+// WILD request i takes [start(w) + pre_i, + r_i); w keeps what is left
+__global__ void k_wild_apply(u64 *__restrict__ out_u, const u32 *__restrict__ pre, const DevCtr *C,
+                             u64 *__restrict__ fs) {
+    const u64 n = C->wild_n;
+    if (!n) return;
+    const u64 w0 = C->wild_start;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        if (out_u[i] == WILD) out_u[i] = w0 + pre[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) fs[C->wild[1]] = w0 + C->wild_total;
 }
 
 // class-sorted copies of (start, end - 1) for the CSR (one gather after the class sort)

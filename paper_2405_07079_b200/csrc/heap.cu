@@ -275,6 +275,7 @@ template <typename T> T *at(void *ws, u64 off) { return reinterpret_cast<T *>(st
 struct heap {
     u64 arena, align, max_live, max_batch;
     int policy, alog2, sms, G;
+    int wild_split;          // TLSF/SEGFIT wilderness split (engine_tlsf.cuh); env HEAP_WILD_SPLIT=0 disables
     Layout L;
     void *ws;
     size_t ws_bytes;
@@ -568,6 +569,10 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->arena = arena_bytes; h->align = align; h->policy = policy;
     h->max_live = max_live_blocks; h->max_batch = max_batch;
     h->alog2 = ilog2(align);
+    {
+        const char *ws = getenv("HEAP_WILD_SPLIT");
+        h->wild_split = (ws && ws[0] == '0') ? 0 : 1;
+    }
     h->L = L;
     h->ws = d_workspace; h->ws_bytes = workspace_bytes;
     int dev = 0, sms = 148;
@@ -853,7 +858,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         tlsfw::Csr csr{sv, h->cs, h->ce};
         tlsfw::Lifo lf{h->lnext, h->ft[cur], &C->lifo_clock};
         LAUNCH(h, tlsfw::k_engine<true>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
-               h->c, n, h->out, nullptr, 0ull, 0ull, 0ull, h->slot, L.NC, L.L, C->eng, lf, n_in);
+               h->c, n, h->out, nullptr, 0ull, 0ull, 0ull, h->slot, L.NC, L.L, C->eng, lf, n_in, (const u32 *)nullptr);
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, fits::k_clock_add, 1, 1, 0, s, C, n_in, (u64)n);
     } else if (cls) {
@@ -865,8 +870,14 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs, h->ce);
         TAG(h, HEAP_TAG_ENGINE);
         tlsfw::Csr csr{sv, h->cs, h->ce};
+        LAUNCH(h, tlsfw::k_wild_setup, 1, 1024, 0, s, h->off, sv, h->fs[cur], h->fe[cur], h->r, h->c, n, n_in, L.NC, L.L,
+               h->wild_split, C);
         LAUNCH(h, tlsfw::k_engine<false>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
-               h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{}, n_in);
+               h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{}, n_in,
+               (const u32 *)C->wild);
+        LAUNCH(h, tlsfw::k_wild_flags, h->G, 256, 0, s, h->out, h->r, C, h->flags);
+        scan(h, h->flags, h->pos, &C->wild_n, &C->wild_total, s);
+        LAUNCH(h, tlsfw::k_wild_apply, h->G, 256, 0, s, h->out, h->pos, C, h->fs[cur]);
         TAG(h, HEAP_TAG_INDEX);
         LAUNCH(h, tlsfw::k_bitheap_clear, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, h->slot, h->bm,
                L.bm_w0, L.bm_w1, L.bm_w2, L.NC, L.L);

@@ -124,6 +124,34 @@ def test_small_every_batch(case):
     run_parity(cfg, max_live=max(1 << 15, 8 * batch), max_batch=batch, every_batch_state=batch < 100)
 
 
+WILD_CASES = [
+    # (policy, arena, align, batch, ops, sizes, rho): TLSF / SEGFIT heaps whose top class holds one
+    # large piece (the wilderness) for most batches, plus small arenas where it does not
+    (tg.TLSF, 1 << 16, 16, 24, 1500, (4, 10), (1, 2)),
+    (tg.TLSF, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5)),
+    (tg.SEGFIT, 1 << 24, 16, 3000, 40000, (4, 14), (2, 5)),
+    (tg.TLSF, (1 << 30) + 4096, 16, 65536, 400000, (4, 12), (2, 5)),   # config-3 shaped batches
+    (tg.TLSF, 1 << 20, 16, 2000, 30000, (4, 11), (2, 5)),              # wilderness runs out
+]
+
+
+@pytest.mark.parametrize("split", [True, False], ids=["split", "plain"])
+@pytest.mark.parametrize("case", WILD_CASES, ids=lambda c: f"p{c[0]}-A{c[1]}-B{c[3]}")
+def test_wild_split_both_paths(case, split, monkeypatch):
+    """The TLSF/SEGFIT engine with and without the wilderness split (engine_tlsf.cuh
+    k_wild_setup): both bit-exact with Oracle-L; with the split on, the large cases must
+    actually have used it (diagnostic counter 14 = batches served with the split)."""
+    monkeypatch.setenv("HEAP_WILD_SPLIT", "1" if split else "0")
+    pol, arena, align, batch, ops, sizes, rho = case
+    cfg = tg.custom(pol, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes, idx=80 + pol)
+    g, _ = run_parity(cfg, max_live=max(1 << 15, 8 * batch), max_batch=batch, every_batch_state=batch < 100)
+    used = g.h.debug_counters()[14]
+    if not split:
+        assert used == 0
+    elif arena >= 1 << 24:
+        assert used > 0
+
+
 def test_config1_exact():
     cfg = tg.CONFIGS[1]
     run_parity(cfg, cfg.max_live, 1000, every_batch_state=True)
