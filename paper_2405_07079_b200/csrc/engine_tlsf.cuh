@@ -36,10 +36,13 @@
 namespace tlsfw {
 
 #ifndef REFILL_AT_DEF
-#define REFILL_AT_DEF 12
+#define REFILL_AT_DEF 6
 #endif
 
-constexpr int H = 16;             // head-cache depth per class
+#ifndef H_DEF
+#define H_DEF 8
+#endif
+constexpr int H = H_DEF;          // head-cache depth per class (power of two)
 constexpr int REFILL_AT = REFILL_AT_DEF;      // refill a class's cache when it holds fewer members
 constexpr int MAX_NC = 928;       // classes of 2^32 units at SL_LOG2 = 5 (fl <= 28)
 constexpr int RB = 512;           // request staging buffer
