@@ -45,6 +45,7 @@ struct DevCtr {
     u64 wild_n;         // TLSF/SEGFIT wilderness split: request count when active, else 0
     u64 wild_start;     // the wilderness piece's start at the batch start (units)
     u64 wild_total;     // units the batch took from it
+    u64 wild_acc[2];    // k_alloc_prep: units of all requests, max search class of a valid one
     u32 wild[2];        // {class Kw, piece f} of the wilderness, {NONE, NONE} when inactive
 };
 

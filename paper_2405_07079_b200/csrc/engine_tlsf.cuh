@@ -42,6 +42,17 @@ namespace tlsfw {
 #ifndef H_DEF
 #define H_DEF 8
 #endif
+// request staging and result stores are touched once: streaming hints keep them out of L1
+#ifndef ENGINE_STREAM
+#define ENGINE_STREAM 1
+#endif
+#if ENGINE_STREAM
+#define LDS_(p) __ldcs(p)
+#define STS_(p, v) __stcs((p), (v))
+#else
+#define LDS_(p) (*(p))
+#define STS_(p, v) (*(p) = (v))
+#endif
 constexpr int H = H_DEF;          // head-cache depth per class (power of two)
 constexpr int REFILL_AT = REFILL_AT_DEF;      // refill a class's cache when it holds fewer members
 constexpr int MAX_NC = 928;       // classes of 2^32 units at SL_LOG2 = 5 (fl <= 28)
@@ -402,8 +413,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 rb_base = pos;
                 rb_end = pos + RB < n ? pos + RB : n;
                 for (u64 j = lane; j < rb_end - rb_base; j += 32) {
-                    S.rbuf[j] = R[rb_base + j];
-                    S.cbuf[j] = C[rb_base + j];
+                    S.rbuf[j] = LDS_(&R[rb_base + j]);
+                    S.cbuf[j] = LDS_(&C[rb_base + j]);
                 }
                 __syncwarp();
             }
@@ -430,8 +441,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                     rb_base = sc;
                     rb_end = sc + RB < n ? sc + RB : n;
                     for (u64 j = lane; j < rb_end - rb_base; j += 32) {
-                        S.rbuf[j] = R[rb_base + j];
-                        S.cbuf[j] = C[rb_base + j];
+                        S.rbuf[j] = LDS_(&R[rb_base + j]);
+                        S.cbuf[j] = LDS_(&C[rb_base + j]);
                     }
                     __syncwarp();
                 }
@@ -449,7 +460,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 u64 nsc = sc + 32 < n ? sc + 32 : n;
                 const u32 firstout = __ballot_sync(FULLMASK, cand && rk == take);
                 if (firstout) nsc = sc + __ffs(firstout) - 1;
-                if (v && !cand && j < nsc) out_u[j] = rj != 0 ? WILD : HEAP_NULL_U64;
+                if (v && !cand && j < nsc) STS_(&out_u[j], rj != 0 ? WILD : HEAP_NULL_U64);
                 ncand += take;
                 sc = nsc;
             }
@@ -614,9 +625,9 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         const u32 nxt = later ? (u32)(__ffs(later) - 1) : NONE;
         const bool last_on_block = mynk != SAME || nxt >= commit;
         if (cm) {
-            if (!part) out_u[i] = (wmode && ri != 0) ? WILD : HEAP_NULL_U64;
+            if (!part) STS_(&out_u[i], (wmode && ri != 0) ? WILD : HEAP_NULL_U64);
             else {
-                out_u[i] = mys;
+                STS_(&out_u[i], mys);
                 if (last_on_block) {
                     fs[myf] = mys + ri;
                     if (LIFO && mynk != NONE) lf.stamp[myf] = (u32)(t_alloc + i);   // pushed remainder
@@ -729,37 +740,22 @@ __global__ void k_bitheap_clear(const u64 *__restrict__ fs, const u64 *__restric
 // other class.  So the engine runs without w: a request that finds no class is marked WILD, and
 // the WILD requests take consecutive pieces of w's low end in request order — result = start(w) +
 // exclusive prefix sum of their units (Alg. 1 carve, applied one by one).
-__global__ void __launch_bounds__(1024) k_wild_setup(const u32 *__restrict__ off, const u32 *__restrict__ csr_f,
-                                                     const u64 *__restrict__ fs, const u64 *__restrict__ fe,
-                                                     const u64 *__restrict__ R, const u32 *__restrict__ Cq, u64 n,
-                                                     const u64 *n_in, int NC, int L, int enable, DevCtr *C) {
-    __shared__ u64 red[32];
-    __shared__ int kmax, kmax2;
-    __shared__ u32 cmax;
+__global__ void __launch_bounds__(32) k_wild_setup(const u32 *__restrict__ off, const u32 *__restrict__ csr_f,
+                                                   const u64 *__restrict__ fs, const u64 *__restrict__ fe,
+                                                   u64 n, const u64 *n_in, int NC, int L, int enable, DevCtr *C) {
+    // T = C->wild_acc[0] (units of all requests), cmax = C->wild_acc[1] (k_alloc_prep)
     if (n_in) n = *n_in;
-    if (threadIdx.x == 0) { kmax = -1; kmax2 = -1; cmax = 0; }
-    __syncthreads();
-    u64 t = 0;
-    u32 cm = 0;
-    for (u64 i = threadIdx.x; i < n; i += blockDim.x) {
-        const u64 r = R[i];
-        t += r;
-        if (r) cm = max(cm, Cq[i]);
+    const u32 lane = lane_id();
+    int kmax = -1, kmax2 = -1;           // highest and second-highest class with members
+    for (int k = lane; k < NC; k += 32)
+        if (off[k + 1] > off[k]) { kmax2 = kmax; kmax = k; }
+    for (int o = 16; o > 0; o >>= 1) {   // merge (top, second) pairs across lanes
+        const int a = __shfl_xor_sync(FULLMASK, kmax, o), b = __shfl_xor_sync(FULLMASK, kmax2, o);
+        if (a > kmax) { kmax2 = max(kmax, b); kmax = a; }
+        else kmax2 = max(kmax2, a == kmax ? b : a);
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        t += __shfl_xor_sync(FULLMASK, t, o);
-        cm = max(cm, __shfl_xor_sync(FULLMASK, cm, o));
-    }
-    if (lane_id() == 0) { red[threadIdx.x >> 5] = t; atomicMax(&cmax, cm); }
-    for (int k = threadIdx.x; k < NC; k += blockDim.x)
-        if (off[k + 1] > off[k]) atomicMax(&kmax, k);
-    __syncthreads();
-    for (int k = threadIdx.x; k < kmax; k += blockDim.x)
-        if (off[k + 1] > off[k]) atomicMax(&kmax2, k);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        u64 T = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) T += red[w];
+    if (lane == 0) {
+        const u64 T = C->wild_acc[0], cmax = C->wild_acc[1];
         u32 K0 = NONE, fw = NONE;
         const int k = kmax;
         if (enable && k >= 0 && off[k + 1] - off[k] == 1) {

@@ -195,18 +195,37 @@ __global__ void k_u64_hi(const u64 *__restrict__ key, const u64 *n_dev, u32 *__r
 
 // ------------------------------------------------------------------ alloc phase ----
 // r = ceil(s / align) units (0 = fail: size 0 or larger than the arena), c = search class
+// acc (optional, zeroed before): acc[0] += sum of r, acc[1] = max search class of a valid request
 __global__ void k_alloc_prep(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2, u64 A_u, int L,
-                             int want_cls, u64 *__restrict__ r_out, u32 *__restrict__ c_out) {
+                             int want_cls, u64 *__restrict__ r_out, u32 *__restrict__ c_out, u64 *acc) {
     if (n_in) n = *n_in;
     const u64 amask = (1ull << alog2) - 1;
+    u64 t = 0, cm = 0;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         u64 s = sizes[i];
         u64 r = (s >> alog2) + ((s & amask) != 0);
         if (s == 0 || r > A_u) r = 0;
         r_out[i] = r;
-        if (want_cls) c_out[i] = r ? cls_search(r, L) : 0xFFFFFFFFu;
+        if (want_cls) {
+            const u32 c = r ? cls_search(r, L) : 0xFFFFFFFFu;
+            c_out[i] = c;
+            t += r;
+            if (r) cm = max(cm, (u64)c);
+        }
+    }
+    if (acc) {
+        for (int o = 16; o > 0; o >>= 1) {
+            t += __shfl_xor_sync(FULLMASK, t, o);
+            cm = max(cm, __shfl_xor_sync(FULLMASK, cm, o));
+        }
+        if (lane_id() == 0 && (t || cm)) {
+            atomicAdd(&acc[0], t);
+            atomicMax((unsigned long long *)&acc[1], (unsigned long long)cm);
+        }
     }
 }
+
+__global__ void k_zero2(u64 *p) { p[0] = 0; p[1] = 0; }
 
 // piece survives iff it still has units
 __global__ void k_piece_flags(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev,

@@ -843,7 +843,10 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
     const bool lifo = (h->policy == HEAP_SEGFIT_LIFO);
     const bool cls = (h->policy == HEAP_TLSF || h->policy == HEAP_SEGFIT || lifo);
     TAG(h, HEAP_TAG_ALLOC_PREP);
-    LAUNCH(h, fits::k_alloc_prep, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, L.A_u, L.L, cls ? 1 : 0, h->r, h->c);
+    const bool wild = cls && !lifo;          // the wilderness split needs the batch's totals
+    if (wild) LAUNCH(h, fits::k_zero2, 1, 1, 0, s, C->wild_acc);
+    LAUNCH(h, fits::k_alloc_prep, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, L.A_u, L.L, cls ? 1 : 0, h->r, h->c,
+           wild ? C->wild_acc : (u64 *)nullptr);
     if (lifo) {
         // class-major, newest-push-first CSR (the bins as the paper's stacks), then the engine
         TAG(h, HEAP_TAG_INDEX);
@@ -868,13 +871,14 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         u32 *sk = rb ? h->kB : h->kA, *sv = rb ? h->vB : h->vA;
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, sk, &C->F, L.NC, h->off);
         LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs, h->ce);
+        LAUNCH(h, tlsfw::k_wild_setup, 1, 32, 0, s, h->off, sv, h->fs[cur], h->fe[cur], n, n_in, L.NC, L.L,
+               h->wild_split, C);
         TAG(h, HEAP_TAG_ENGINE);
         tlsfw::Csr csr{sv, h->cs, h->ce};
-        LAUNCH(h, tlsfw::k_wild_setup, 1, 1024, 0, s, h->off, sv, h->fs[cur], h->fe[cur], h->r, h->c, n, n_in, L.NC, L.L,
-               h->wild_split, C);
         LAUNCH(h, tlsfw::k_engine<false>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
                h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{}, n_in,
                (const u32 *)C->wild);
+        TAG(h, HEAP_TAG_FINISH);
         LAUNCH(h, tlsfw::k_wild_flags, h->G, 256, 0, s, h->out, h->r, C, h->flags);
         scan(h, h->flags, h->pos, &C->wild_n, &C->wild_total, s);
         LAUNCH(h, tlsfw::k_wild_apply, h->G, 256, 0, s, h->out, h->pos, C, h->fs[cur]);
