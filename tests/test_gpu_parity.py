@@ -152,6 +152,41 @@ def test_wild_split_both_paths(case, split, monkeypatch):
         assert used > 0
 
 
+def test_wild_split_guards():
+    """The split's three conditions (engine_tlsf.cuh k_wild_setup) each switched off by a batch
+    built to violate it, and on for batches that satisfy them; zero-size and oversize requests
+    in a split batch (written as failures by the candidate gather).  Every batch must match
+    Oracle-L; diagnostic counter 14 counts the batches served with the split."""
+    U = 16
+    arena = 1 << 24                                    # 2^20 units
+    for pol in (tg.TLSF, tg.SEGFIT):
+        def step(g, o, frees, sizes, expect_split, ctx):
+            before = g.h.debug_counters()[14]
+            f = np.asarray(frees, dtype=np.uint64)
+            g.free_batch(f)
+            o.free_batch(f)
+            a = np.asarray(sizes, dtype=np.uint64)
+            go, oo = g.alloc_batch(a), o.alloc_batch(a)
+            assert np.array_equal(go, oo), (pol, ctx, go, oo)
+            compare_state(g, o, f"p{pol} {ctx}")
+            assert (g.h.debug_counters()[14] - before == 1) == expect_split, (pol, ctx)
+            return go
+
+        g, o = Gpu(arena, U, pol, 1024, 64), OracleL(arena, U, pol)
+        # the wilderness (one member) serves four blocks: on
+        blk = step(g, o, [], [100000 * U, U, 100000 * U, U], True, "fill")
+        # (b) two 100000-unit holes; requests large enough to pull the wilderness down to the
+        # holes' class: off
+        step(g, o, [blk[0], blk[2]], [250000 * U, 250000 * U, 250000 * U, 16], False, "b")
+        # (a) the top class now holds the wilderness and both holes: off
+        step(g, o, [], [16, 4096], False, "a")
+        g2, o2 = Gpu(arena, U, pol, 1024, 64), OracleL(arena, U, pol)
+        # (c) a request whose search class is above the wilderness's final class: off
+        step(g2, o2, [], [600000 * U, 300000 * U], False, "c")
+        # on, with zero-size and oversize requests among the candidates and the skipped ones
+        step(g2, o2, [], [16, 0, 48, arena * 4, 4096, 0, 32] * 5, True, "on+invalid")
+
+
 def test_config1_exact():
     cfg = tg.CONFIGS[1]
     run_parity(cfg, cfg.max_live, 1000, every_batch_state=True)
