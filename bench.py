@@ -426,8 +426,19 @@ def run_ours(args, cfg, rank, world, local_rank):
             "heap": {"n_live": st["n_live"], "n_free": st["n_free"], "allocs_failed": st["allocs_failed"],
                      "error_flags": st["error_flags"]},
             "step_ms": [round(x, 3) for x in step_ms],
+            "batch_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99))},
+            # SURVEY.md 8(d) payload model: 64 B per alloc, 88 B per free -> 73.6 B per op at 60/40
+            "payload_roofline": _payload_roofline(value),
         }
         print(json.dumps(line), flush=True)
+
+
+def _payload_roofline(ops_per_s):
+    bpo = 0.6 * 64 + 0.4 * 88
+    peak, src = measured_peak_hbm()
+    ach = ops_per_s * bpo / 1e9
+    return {"bytes_per_op": bpo, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_source": src}
 
 
 def main():
