@@ -258,26 +258,32 @@ def test_invariants_config3_prefix():
 
 
 def test_config5_full_size_properties():
-    """Config 5 at full size for 12 batches (the bench's launch configuration): the first two
-    batches exactly against the oracle, then properties that hold at any size — I1-I4 on the
-    exported state, conservation, counter consistency, and every returned offset of the last
-    batch is a live block of the rounded request size, pairwise disjoint."""
+    """Config 5 at full size for 13 batches — every batch bench.py warms up on (0..2) and times
+    (3..12 at the default --steps 10), in its launch configuration (batch graphs): every
+    returned offset of every batch exactly against the oracle and the final state, plus
+    properties that hold at any size — I1-I4 on the exported state, conservation, counter
+    consistency, and every returned offset of the last batch is a live block of the rounded
+    request size, pairwise disjoint."""
     cfg = tg.CONFIGS[5]
     g = Gpu(cfg.arena_bytes, cfg.align, cfg.policy, cfg.max_live, cfg.batch)
     o = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
-    im = IdMap(cfg.batch * 12)
+    nb = 13
+    im = IdMap(cfg.batch * nb)
     nreq = 0
     last = None
-    for bi, (fids, sizes, first) in enumerate(tg.Trace(cfg, total_ops=cfg.batch * 12)):
+    for bi, (fids, sizes, first) in enumerate(tg.Trace(cfg, total_ops=cfg.batch * nb)):
         offs = im.offsets(fids)
         g.free_batch(offs)
         go = g.alloc_batch(sizes)
-        if bi < 2:
-            o.free_batch(offs)
-            assert np.array_equal(go, o.alloc_batch(sizes)), bi
+        o.free_batch(offs)
+        oo = o.alloc_batch(sizes)
+        if not np.array_equal(go, oo):
+            bad = np.flatnonzero(go != oo)
+            raise AssertionError(f"config 5 batch {bi}: {len(bad)} offsets differ, first at {bad[0]}")
         im.record(first, go)
         nreq += len(sizes)
         last = (sizes, go)
+    compare_state(g, o, "config 5 after 13 batches")
     st = g.stats()
     assert st["error_flags"] == 0 and st["rc"] == 0
     assert st["allocs_ok"] + st["allocs_failed"] == nreq
