@@ -87,6 +87,8 @@ def aggregate(t_ms, ops, world, dev):
         return t_ms, ops
     import torch
     import torch.distributed as dist
+    if dist.get_backend() == "gloo":
+        dev = "cpu"
     tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     oo = torch.tensor([ops], dtype=torch.int64, device=dev)
@@ -100,6 +102,10 @@ def gather_stats(local, world):
         return local.view(1, -1)
     import torch
     import torch.distributed as dist
+    if dist.get_backend() == "gloo":            # CPU tests and the one-GPU dev mode
+        parts = [torch.empty_like(local.cpu()) for _ in range(world)]
+        dist.all_gather(parts, local.cpu())
+        return torch.stack(parts).to(local.device)
     out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, local)
     return out.view(world, -1)
@@ -236,6 +242,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stats_dev = torch.zeros(16, dtype=torch.int64, device=dev)
     stats_all = torch.zeros(16 * world, dtype=torch.int64, device=dev) if world > 1 else None
+    gloo = world > 1 and dist.get_backend() == "gloo"
 
     def run_device(h, idmap, outbuf, b, stream_stats=True):
         fids, sizes, first = b
@@ -246,7 +253,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         idmap[first:first + na] = out
         if world > 1 and stream_stats:
             heap_stats_async(h.handle, stats_dev)
-            dist.all_gather_into_tensor(stats_all, stats_dev)
+            if gloo:
+                stats_all.copy_(gather_stats(stats_dev, world).view(-1))
+            else:
+                dist.all_gather_into_tensor(stats_all, stats_dev)
 
     # ---------------- device-resident run ----------------
     def device_run(policy, profile):
@@ -447,6 +457,13 @@ def main():
     if args.dev_share_gpu:        # dev only: run every rank on GPU 0 (tests the N > 1 logic on one GPU)
         local_rank = 0
     cfg = tg.CONFIGS[args.config]
+    if args.impl == "reference":
+        # the reference arm is the CPU oracle: rank 0 alone runs it, no GPU and no process group
+        if rank == 0:
+            run_reference(args, cfg)
+        return
+    if args.dev_share_gpu:
+        args.dist_backend = "gloo"    # NCCL refuses two ranks on one GPU
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -455,11 +472,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(args.dist_backend)
-    if args.impl == "reference":
-        if rank == 0:
-            run_reference(args, cfg)
-    else:
-        run_ours(args, cfg, rank, world, local_rank)
+    run_ours(args, cfg, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
