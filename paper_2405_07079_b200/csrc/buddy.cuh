@@ -271,7 +271,6 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
                                                      u32 *dtm, u32 *dsrc, u64 *daddr, u64 *baddr,
                                                      u32 *btm, u32 *bsrc, u64 *__restrict__ out_u, int K,
                                                      DevCtr *ctr) {
-    __shared__ u32 sm[33];
     __shared__ u64 ooff[41];
     __shared__ u64 doff[42], boff[42];
     __shared__ u64 s_nb;
@@ -326,7 +325,6 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         __syncthreads();
     }
     // ---- top-down ----
-    u64 out_pos = 0;   // running offset of the new per-order lists (thread-uniform)
     __shared__ u64 s_left[41], s_cnt[41];
     for (int t = K; t >= 0; t--) {
         const u64 n_t = ooff[t + 1] - ooff[t];
@@ -368,7 +366,6 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         }
         __syncthreads();
     }
-    (void)out_pos;
     // ---- new per-order lists: surviving batch-start blocks, or the one leftover ----
     __shared__ u64 noff[42];
     if (threadIdx.x == 0) {

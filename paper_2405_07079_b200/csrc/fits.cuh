@@ -478,19 +478,10 @@ __device__ __forceinline__ u64 warp_lower_bound(const u64 *a, u64 lo, u64 hi, u6
     return b ? lo + __ffs(b) - 1 : hi;
 }
 
-template <bool SMEM>
-__global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
-                                                  const u64 *__restrict__ r, u64 n, const u64 *n_in,
-                                                  u64 *__restrict__ out_u) {
-    extern __shared__ u64 skeys[];
-    if (n_in) n = *n_in;
+// the flat engine: one sorted key array (shared or global memory), warp shift per request
+__device__ void bf_flat(u64 *keys, u64 nb, int FB, u64 *fs, const u64 *__restrict__ r, u64 n,
+                        u64 *__restrict__ out_u) {
     const u32 lane = lane_id();
-    u64 nb = *F_dev;
-    u64 *keys = SMEM ? skeys : gkeys;
-    if (SMEM) {
-        for (u64 i = lane; i < nb; i += 32) skeys[i] = gkeys[i];
-        __syncwarp();
-    }
     const u64 fmask = (1ull << FB) - 1;
     for (u64 i = 0; i < n; i++) {
         u64 ri = r[i];
@@ -531,6 +522,170 @@ __global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, 
         }
         __syncwarp();
     }
+}
+
+// The blocked engine: the same key order kept as a list of chunks of <= 32 keys (one per lane) in
+// shared memory, with the chunks' maxima in position order.  A request costs one 32-ary search over
+// the maxima, one ballot inside a chunk, and one-step shifts inside at most two chunks (delete the
+// chosen key, insert the carved piece's new key), instead of a shift across up to F keys.  Results
+// are those of bf_flat (same keys, same order).  Chunks only split (a full chunk into two of 16):
+// with phi = sum over chunks of max(0, count - 16), an insert raises phi by at most 1, a split
+// lowers it by 16, and phi starts at 8 per chunk, so there are at most nc0/2 + n/16 splits
+// (nc0 = ceil(F/BF_FILL)); batches that could exceed BF_NCH chunks use bf_flat on the global array.
+constexpr u32 BF_NCH = 640, BF_FILL = 24;
+struct BfSmem {
+    u64 K[BF_NCH * 32];     // chunk id c holds K[c*32 .. c*32 + cnt[c])
+    u64 mx[BF_NCH];         // largest key of the chunk at position i
+    unsigned short ord[BF_NCH], fl[BF_NCH];   // chunk id at position i; free chunk ids
+    unsigned char cnt[BF_NCH];
+    u32 nch, nfl;
+};
+
+__device__ __forceinline__ void bf_pos_insert(BfSmem &S, u32 i, u32 c, u64 m) {   // new position i
+    const u32 lane = lane_id();
+    for (int hi = (int)S.nch; hi > (int)i;) {            // shift [i, nch) right, top chunk first
+        const int lo = hi - 32 > (int)i ? hi - 32 : (int)i;
+        const int idx = lo + (int)lane;
+        unsigned short o = 0;
+        u64 v = 0;
+        if (idx < hi) { o = S.ord[idx]; v = S.mx[idx]; }
+        __syncwarp();
+        if (idx < hi) { S.ord[idx + 1] = o; S.mx[idx + 1] = v; }
+        __syncwarp();
+        hi = lo;
+    }
+    if (lane == 0) { S.ord[i] = (unsigned short)c; S.mx[i] = m; S.nch++; }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void bf_pos_remove(BfSmem &S, u32 i) {
+    const u32 lane = lane_id();
+    const u32 n = S.nch;
+    for (u32 lo = i + 1; lo < n; lo += 32) {
+        const u32 idx = lo + lane;
+        unsigned short o = 0;
+        u64 v = 0;
+        if (idx < n) { o = S.ord[idx]; v = S.mx[idx]; }
+        __syncwarp();
+        if (idx < n) { S.ord[idx - 1] = o; S.mx[idx - 1] = v; }
+        __syncwarp();
+    }
+    if (lane == 0) S.nch = n - 1;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
+                                                  const u64 *__restrict__ r, u64 n, const u64 *n_in,
+                                                  u64 *__restrict__ out_u) {
+    extern __shared__ __align__(16) unsigned char bf_raw[];
+    BfSmem &S = *reinterpret_cast<BfSmem *>(bf_raw);
+    if (n_in) n = *n_in;
+    const u32 lane = lane_id();
+    const u64 nb = *F_dev;
+    const u64 nc0_ = (nb + BF_FILL - 1) / BF_FILL;
+    if (nc0_ + (nc0_ + 1) / 2 + (n + 15) / 16 + 2 > BF_NCH) {   // could outgrow the chunk pool
+        bf_flat(gkeys, nb, FB, fs, r, n, out_u);
+        return;
+    }
+    // build: chunks of BF_FILL keys in order
+    const u32 nc0 = (u32)((nb + BF_FILL - 1) / BF_FILL);
+    for (u32 c = 0; c < nc0; c++) {
+        const u64 b = (u64)c * BF_FILL, e = min(b + BF_FILL, nb);
+        if (lane < e - b) S.K[c * 32 + lane] = gkeys[b + lane];
+        if (lane == 0) { S.cnt[c] = (unsigned char)(e - b); S.ord[c] = (unsigned short)c; S.mx[c] = gkeys[e - 1]; }
+    }
+    for (u32 c = nc0 + lane; c < BF_NCH; c += 32) S.fl[BF_NCH - 1 - c] = (unsigned short)c;   // pop from the end: lowest id first
+    if (lane == 0) { S.nch = nc0; S.nfl = BF_NCH - nc0; }
+    __syncwarp();
+    const u64 fmask = (1ull << FB) - 1;
+    u64 r_next = n ? r[0] : 0;                     // the next request's size, loaded one step ahead
+    for (u64 i = 0; i < n; i++) {
+        const u64 ri = r_next;
+        if (i + 1 < n) r_next = r[i + 1];
+        if (ri == 0) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+        const u64 target = ri << FB;
+        const u32 nch = S.nch;
+        const u32 p = (u32)warp_lower_bound(S.mx, 0, nch, target);
+        if (p >= nch) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+        u32 c = S.ord[p];
+        u32 m = S.cnt[c];
+        u64 v = lane < m ? S.K[c * 32 + lane] : ~0ull;
+        const u32 j = __ffs(__ballot_sync(FULLMASK, lane < m && v >= target)) - 1;   // exists: mx[p] >= target
+        const u64 key = __shfl_sync(FULLMASK, v, j);
+        const u64 z = key >> FB, f = key & fmask;
+        // the piece's start: its load overlaps the chunk updates below, the stores come last
+        const u64 s0 = lane == 0 ? fs[f] : 0;
+        // delete key j of chunk c (position p)
+        __syncwarp();
+        if (lane > j && lane < m) S.K[c * 32 + lane - 1] = v;
+        if (lane == 0) S.cnt[c] = (unsigned char)(m - 1);
+        __syncwarp();
+        if (m == 1) {
+            bf_pos_remove(S, p);
+            if (lane == 0) S.fl[S.nfl++] = (unsigned short)c;
+        } else if (j == m - 1) {
+            if (lane == 0) S.mx[p] = S.K[c * 32 + m - 2];
+        }
+        __syncwarp();
+        // insert the carved piece's new key
+        const u64 z2 = z - ri;
+        if (!z2) {
+            if (lane == 0) { out_u[i] = s0; fs[f] = s0 + ri; }
+            continue;
+        }
+        const u64 x = (z2 << FB) | f;
+        u32 q = S.nch ? (u32)warp_lower_bound(S.mx, 0, S.nch, x) : 0;
+        if (S.nch == 0) {
+            if (lane == 0) { const u32 c0 = S.fl[--S.nfl]; S.cnt[c0] = 0; S.ord[0] = (unsigned short)c0; S.mx[0] = 0; S.nch = 1; }
+            __syncwarp();
+        } else if (q == S.nch) {
+            q = S.nch - 1;                           // above every key: the last chunk
+        }
+        c = S.ord[q];
+        m = S.cnt[c];
+        if (m == 32) {                               // split: upper half to a new chunk at q + 1
+            u32 c2 = 0;
+            if (lane == 0) c2 = S.fl[--S.nfl];
+            c2 = __shfl_sync(FULLMASK, c2, 0);
+            const u64 w = S.K[c * 32 + lane];
+            if (lane >= 16) S.K[c2 * 32 + lane - 16] = w;
+            const u64 top = __shfl_sync(FULLMASK, w, 31), mid = __shfl_sync(FULLMASK, w, 15);
+            if (lane == 0) { S.cnt[c] = 16; S.cnt[c2] = 16; S.mx[q] = mid; }
+            __syncwarp();
+            bf_pos_insert(S, q + 1, c2, top);
+            if (x > mid) { q = q + 1; c = c2; }
+            m = 16;
+        }
+        v = lane < m ? S.K[c * 32 + lane] : 0;
+        const u32 at = __popc(__ballot_sync(FULLMASK, lane < m && v < x));
+        __syncwarp();
+        if (lane >= at && lane < m) S.K[c * 32 + lane + 1] = v;
+        if (lane == 0) {
+            S.K[c * 32 + at] = x;
+            S.cnt[c] = (unsigned char)(m + 1);
+            if (at == m) S.mx[q] = x;
+            out_u[i] = s0;
+            fs[f] = s0 + ri;
+        }
+        __syncwarp();
+    }
+}
+
+// the flat engine with the array in shared memory (small heaps) or global memory
+template <bool SMEM>
+__global__ void __launch_bounds__(32) k_bf_engine_flat(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
+                                                       const u64 *__restrict__ r, u64 n, const u64 *n_in,
+                                                       u64 *__restrict__ out_u) {
+    extern __shared__ u64 skeys[];
+    if (n_in) n = *n_in;
+    const u32 lane = lane_id();
+    const u64 nb = *F_dev;
+    u64 *keys = SMEM ? skeys : gkeys;
+    if (SMEM) {
+        for (u64 i = lane; i < nb; i += 32) skeys[i] = gkeys[i];
+        __syncwarp();
+    }
+    bf_flat(keys, nb, FB, fs, r, n, out_u);
 }
 
 }  // namespace fits

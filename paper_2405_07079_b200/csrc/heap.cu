@@ -276,6 +276,7 @@ struct heap {
     u64 arena, align, max_live, max_batch;
     int policy, alog2, sms, G;
     int wild_split;          // TLSF/SEGFIT wilderness split (engine_tlsf.cuh); env HEAP_WILD_SPLIT=0 disables
+    int bf_flat;             // BEST_FIT: the flat one-array engine instead of the blocked one (env HEAP_BF_FLAT=1)
     Layout L;
     void *ws;
     size_t ws_bytes;
@@ -572,6 +573,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     {
         const char *ws = getenv("HEAP_WILD_SPLIT");
         h->wild_split = (ws && ws[0] == '0') ? 0 : 1;
+        const char *bf = getenv("HEAP_BF_FLAT");
+        h->bf_flat = (bf && bf[0] == '1') ? 1 : 0;
     }
     h->L = L;
     h->ws = d_workspace; h->ws_bytes = workspace_bytes;
@@ -584,6 +587,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(tlsfw::k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(fits::k_bf_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(fits::BfSmem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_free_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)buddy::FREE_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_alloc_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -902,13 +907,18 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         int bits = 33 + L.FB;
         int rb = radix_sort<u64, false>(h, h->bk[0], h->bk[1], nullptr, nullptr, &C->F, bits, s);
         u64 *keys = h->bk[rb];
-        size_t smem = L.cap_f * 8;
         TAG(h, HEAP_TAG_ENGINE);
-        if (smem <= 200 * 1024) {
-            cudaFuncSetAttribute(fits::k_bf_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            LAUNCH(h, fits::k_bf_engine<true>, 1, 32, smem, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in, h->out);
+        if (h->bf_flat) {      // ablation (HEAP_BF_FLAT=1): the one-array engine
+            size_t smem = L.cap_f * 8;
+            if (smem <= 200 * 1024) {
+                cudaFuncSetAttribute(fits::k_bf_engine_flat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                LAUNCH(h, fits::k_bf_engine_flat<true>, 1, 32, smem, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in, h->out);
+            } else {
+                LAUNCH(h, fits::k_bf_engine_flat<false>, 1, 32, 0, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in, h->out);
+            }
         } else {
-            LAUNCH(h, fits::k_bf_engine<false>, 1, 32, 0, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in, h->out);
+            LAUNCH(h, fits::k_bf_engine, 1, 32, sizeof(fits::BfSmem), s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in,
+                   h->out);
         }
     }
     // compact the surviving pieces into the other buffer (address order is kept)
