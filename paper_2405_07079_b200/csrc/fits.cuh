@@ -543,7 +543,8 @@ struct BfSmem {
 
 __device__ __forceinline__ void bf_pos_insert(BfSmem &S, u32 i, u32 c, u64 m) {   // new position i
     const u32 lane = lane_id();
-    for (int hi = (int)S.nch; hi > (int)i;) {            // shift [i, nch) right, top chunk first
+    const int n0 = (int)S.nch;
+    for (int hi = n0; hi > (int)i;) {                    // shift [i, nch) right, top chunk first
         const int lo = hi - 32 > (int)i ? hi - 32 : (int)i;
         const int idx = lo + (int)lane;
         unsigned short o = 0;
@@ -554,7 +555,8 @@ __device__ __forceinline__ void bf_pos_insert(BfSmem &S, u32 i, u32 c, u64 m) { 
         __syncwarp();
         hi = lo;
     }
-    if (lane == 0) { S.ord[i] = (unsigned short)c; S.mx[i] = m; S.nch++; }
+    __syncwarp();                                        // every lane has read nch
+    if (lane == 0) { S.ord[i] = (unsigned short)c; S.mx[i] = m; S.nch = (u32)n0 + 1; }
     __syncwarp();
 }
 
@@ -570,6 +572,7 @@ __device__ __forceinline__ void bf_pos_remove(BfSmem &S, u32 i) {
         if (idx < n) { S.ord[idx - 1] = o; S.mx[idx - 1] = v; }
         __syncwarp();
     }
+    __syncwarp();
     if (lane == 0) S.nch = n - 1;
     __syncwarp();
 }
@@ -634,12 +637,14 @@ __global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, 
             continue;
         }
         const u64 x = (z2 << FB) | f;
-        u32 q = S.nch ? (u32)warp_lower_bound(S.mx, 0, S.nch, x) : 0;
-        if (S.nch == 0) {
+        const u32 nch1 = S.nch;
+        u32 q = nch1 ? (u32)warp_lower_bound(S.mx, 0, nch1, x) : 0;
+        __syncwarp();
+        if (nch1 == 0) {
             if (lane == 0) { const u32 c0 = S.fl[--S.nfl]; S.cnt[c0] = 0; S.ord[0] = (unsigned short)c0; S.mx[0] = 0; S.nch = 1; }
             __syncwarp();
-        } else if (q == S.nch) {
-            q = S.nch - 1;                           // above every key: the last chunk
+        } else if (q == nch1) {
+            q = nch1 - 1;                            // above every key: the last chunk
         }
         c = S.ord[q];
         m = S.cnt[c];
@@ -650,6 +655,7 @@ __global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, 
             const u64 w = S.K[c * 32 + lane];
             if (lane >= 16) S.K[c2 * 32 + lane - 16] = w;
             const u64 top = __shfl_sync(FULLMASK, w, 31), mid = __shfl_sync(FULLMASK, w, 15);
+            __syncwarp();                            // every lane has read cnt[c] and mx
             if (lane == 0) { S.cnt[c] = 16; S.cnt[c2] = 16; S.mx[q] = mid; }
             __syncwarp();
             bf_pos_insert(S, q + 1, c2, top);
