@@ -39,6 +39,9 @@ namespace tlsfw {
 #define REFILL_AT_DEF 6
 #endif
 
+#ifndef LIGHT_ROUNDS
+#define LIGHT_ROUNDS 3
+#endif
 #ifndef H_DEF
 #define H_DEF 8
 #endif
@@ -477,6 +480,20 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         t0 = clock64();
         const bool fail0 = act && (ri == 0 || ci >= (u32)NC);
         u32 k = (act && !fail0) ? first_ge(S, sw, ci, NC) : NONE;
+        // light pre-rounds (count model): a lane ranked at or past its class's member count is
+        // moved to the next nonempty class before the full round.  The model ignores head carves
+        // (a member serving several requests), so a moved lane is checked after the full round:
+        // if a class it skipped saw a head carve, the lane is dirty (see the dirty phase).
+        const u32 k0 = k;
+#pragma unroll 1
+        for (int it = 0; it < LIGHT_ROUNDS; it++) {
+            const bool pl = act && k != NONE;
+            const u32 pm = __match_any_sync(FULLMASK, pl ? k : (0x40000000u | lane));
+            const bool ov = pl && (u32)__popc(pm & lanemask_lt()) >= S.cnt[k];
+            if (!__any_sync(FULLMASK, ov)) break;
+            if (ov) k = first_ge(S, sw, k + 1, NC);
+        }
+        const u32 kpre = k;
         u32 peers = 0, rank = 0, flag = F_OK, myf = 0, mynk = NONE, mye = 0;
         u64 mys = 0;
         for (u32 round = 0;; round++) {
@@ -607,6 +624,15 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             const u32 dk = __shfl_sync(FULLMASK, mynk, d);
             const u32 dfb = __shfl_sync(FULLMASK, myf, d);
             if (act && !fail0 && lane > d && ci <= dk && ((((u64)dk) << 32) | (LIFO ? 0u : dfb)) < key) bad = true;
+        }
+        if (__any_sync(FULLMASK, act && kpre != k0)) {     // pre-moved lanes: skipped classes
+            u32 sm = __ballot_sync(FULLMASK, part && flag == F_OK && mynk == SAME);
+            while (sm) {
+                const u32 d = __ffs(sm) - 1;
+                sm &= sm - 1;
+                const u32 sk = __shfl_sync(FULLMASK, k, d);
+                if (act && kpre != k0 && k0 <= sk && sk < kpre) bad = true;
+            }
         }
         const u32 badm = __ballot_sync(FULLMASK, bad);
         const u32 commit = badm ? (u32)(__ffs(badm) - 1) : limit;
