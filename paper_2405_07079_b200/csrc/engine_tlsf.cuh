@@ -40,7 +40,7 @@ namespace tlsfw {
 #endif
 
 #ifndef LIGHT_ROUNDS
-#define LIGHT_ROUNDS 3
+#define LIGHT_ROUNDS 16
 #endif
 #ifndef H_DEF
 #define H_DEF 8
