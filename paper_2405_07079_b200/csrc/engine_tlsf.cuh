@@ -39,6 +39,12 @@ namespace tlsfw {
 #define REFILL_AT_DEF 6
 #endif
 
+#ifndef BITMAP_PLAIN
+#define BITMAP_PLAIN 1
+#endif
+#ifndef ENGINE_PF
+#define ENGINE_PF 1
+#endif
 #ifndef LIGHT_ROUNDS
 #define LIGHT_ROUNDS 16
 #endif
@@ -111,12 +117,41 @@ struct Heap {
     // add f to class k's overflow set whose current minimum is root; returns the new minimum
     __device__ __forceinline__ u32 insert(u32 k, u32 root, u32 f) {
         const u64 s = slot_of(k);
+#if BITMAP_PLAIN
+        // one warp owns these words (a class's slot is touched by one lane at a time, phases are
+        // separated by __syncwarp), so plain L1-cached read-modify-writes replace L2 atomics
+        // (a summary bit is set iff the word below it is nonzero, so a nonempty word's summary
+        // bits are already set)
+        if (ow_i[k] == (f >> 5)) {                 // the cached word holds the minimum: nonzero
+            ow_v[k] |= 1u << (f & 31);
+            l0[s * w0 + (f >> 5)] = ow_v[k];
+        } else {
+            u32 *p0 = &l0[s * w0 + (f >> 5)];
+            const u32 o0 = *p0;
+            *p0 = o0 | (1u << (f & 31));
+            if (!o0) {
+                u32 *p1 = &l1[s * w1 + (f >> 10)];
+                const u32 o1 = *p1;
+                *p1 = o1 | (1u << ((f >> 5) & 31));
+                if (!o1) l2[s * w2 + (f >> 15)] |= 1u << ((f >> 10) & 31);
+            }
+        }
+#else
         atomicOr(&l0[s * w0 + (f >> 5)], 1u << (f & 31));
         if (ow_i[k] == (f >> 5)) ow_v[k] |= 1u << (f & 31);   // keep the cached word coherent
         atomicOr(&l1[s * w1 + (f >> 10)], 1u << ((f >> 5) & 31));
         atomicOr(&l2[s * w2 + (f >> 15)], 1u << ((f >> 10) & 31));
+#endif
         return f < root ? f : root;
     }
+#if BITMAP_PLAIN
+    __device__ __forceinline__ static u32 and_fetch(u32 *p, u32 m) { const u32 v = *p & m; *p = v; return v; }
+#define BM_AND(p, m) and_fetch((p), (m))
+#define BM_LD(p) (*(p))
+#else
+#define BM_AND(p, m) (atomicAnd((p), (m)) & (m))
+#define BM_LD(p) __ldcg(p)
+#endif
     // remove the minimum h of class k's overflow set; returns the next minimum (NIL32 if empty)
     __device__ u32 extract(u32 k, u32 h) {
         const u64 s = slot[k];
@@ -129,40 +164,42 @@ struct Heap {
             ow_v[k] = rest;
             a0[w] = rest;
         } else {
-            rest = atomicAnd(&a0[w], ~(1u << (h & 31))) & ~(1u << (h & 31));
+            rest = BM_AND(&a0[w], ~(1u << (h & 31)));
             ow_i[k] = w;
             ow_v[k] = rest;
         }
         if (rest) return (w << 5) + __ffs(rest) - 1;          // bits below h are never set
         ow_i[k] = NONE;
         const u32 v = w >> 5;
-        rest = atomicAnd(&a1[v], ~(1u << (w & 31))) & ~(1u << (w & 31));
+        rest = BM_AND(&a1[v], ~(1u << (w & 31)));
         u32 ww;
         if (rest) ww = (v << 5) + __ffs(rest) - 1;
         else {
             const u32 x = v >> 5;
-            rest = atomicAnd(&a2[x], ~(1u << (v & 31))) & ~(1u << (v & 31));
+            rest = BM_AND(&a2[x], ~(1u << (v & 31)));
             u32 vv = NONE;
             if (rest) vv = (x << 5) + __ffs(rest) - 1;
             else {
                 for (u64 j = x + 1; j < w2; j++) {
                     visits++;
-                    const u32 t = __ldcg(&a2[j]);
+                    const u32 t = BM_LD(&a2[j]);
                     if (t) { vv = (u32)(j << 5) + __ffs(t) - 1; break; }
                 }
                 if (vv == NONE) return NIL32;
             }
-            const u32 t1 = __ldcg(&a1[vv]);
+            const u32 t1 = BM_LD(&a1[vv]);
             if (!t1) { broken = true; return NIL32; }
             ww = (vv << 5) + __ffs(t1) - 1;
         }
-        const u32 t0 = __ldcg(&a0[ww]);
+        const u32 t0 = BM_LD(&a0[ww]);
         if (!t0) { broken = true; return NIL32; }
         ow_i[k] = ww;
         ow_v[k] = t0;
         return (ww << 5) + __ffs(t0) - 1;
     }
 };
+
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 __device__ __forceinline__ u32 first_ge(const Smem &S, u32 sw, u32 c, int NC) {
     if (c >= (u32)NC) return NONE;
@@ -608,6 +645,17 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             if (over) { k = first_ge(S, sw, k + 1, NC); flag = F_OK; n_retarget++; }
         }
         if (act && k != NONE) { S.res_f[lane] = myf; S.res_s[lane] = mys; S.res_e[lane] = mye; }
+#if ENGINE_PF
+        // group leaders: the class's next CSR members and its overflow root's piece are what a
+        // refill after this chunk's pops reads; start pulling them into L1 now (the dirty check
+        // runs meanwhile)
+        if (act && k != NONE && rank == 0) {
+            const u32 pp = S.ptr[k];
+            if (pp < S.endp[k]) { prefetch_l1(&csr.f[pp]); prefetch_l1(&csr.s[pp]); prefetch_l1(&csr.e[pp]); }
+            const u32 rt = S.root[k];
+            if (rt != NIL32) { prefetch_l1(&fs[rt]); prefetch_l1(&fe[rt]); }
+        }
+#endif
         __syncwarp();
         t_spec += clock64() - t0;
         t0 = clock64();
@@ -684,10 +732,11 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 S.hn[k] = (unsigned char)(S.hn[k] - left);
                 S.cnt[k] -= left;
                 const long long tr0 = clock64();
+                const bool work = S.hn[k] < (u32)REFILL_AT && (S.ptr[k] < S.endp[k] || S.root[k] != NIL32);
                 if constexpr (LIFO) refill_lifo(S, lf, csr, fs, fe, k, n_delmin);
                 else refill(S, hp, csr, fs, fe, k, n_delmin);
                 t_refill += clock64() - tr0;
-                n_refill++;
+                n_refill += work;                // diagnostics: refills that loaded members
                 if (S.cnt[k] == 0) clear_bit(S, k);
             }
         }
