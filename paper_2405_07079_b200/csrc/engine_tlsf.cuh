@@ -42,9 +42,6 @@ namespace tlsfw {
 #ifndef BITMAP_PLAIN
 #define BITMAP_PLAIN 1
 #endif
-#ifndef ENGINE_PF
-#define ENGINE_PF 1
-#endif
 #ifndef LIGHT_ROUNDS
 #define LIGHT_ROUNDS 16
 #endif
@@ -198,8 +195,6 @@ struct Heap {
         return (ww << 5) + __ffs(t0) - 1;
     }
 };
-
-__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 __device__ __forceinline__ u32 first_ge(const Smem &S, u32 sw, u32 c, int NC) {
     if (c >= (u32)NC) return NONE;
@@ -645,17 +640,6 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             if (over) { k = first_ge(S, sw, k + 1, NC); flag = F_OK; n_retarget++; }
         }
         if (act && k != NONE) { S.res_f[lane] = myf; S.res_s[lane] = mys; S.res_e[lane] = mye; }
-#if ENGINE_PF
-        // group leaders: the class's next CSR members and its overflow root's piece are what a
-        // refill after this chunk's pops reads; start pulling them into L1 now (the dirty check
-        // runs meanwhile)
-        if (act && k != NONE && rank == 0) {
-            const u32 pp = S.ptr[k];
-            if (pp < S.endp[k]) { prefetch_l1(&csr.f[pp]); prefetch_l1(&csr.s[pp]); prefetch_l1(&csr.e[pp]); }
-            const u32 rt = S.root[k];
-            if (rt != NIL32) { prefetch_l1(&fs[rt]); prefetch_l1(&fe[rt]); }
-        }
-#endif
         __syncwarp();
         t_spec += clock64() - t0;
         t0 = clock64();
