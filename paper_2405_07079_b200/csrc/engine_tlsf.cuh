@@ -104,7 +104,7 @@ struct Heap {
     u32 *slot;               // smem: slot of class k (NONE = none yet)
     u32 *nslot;              // smem counter
     u32 *ow_i, *ow_v;        // smem: cached level-0 word (index, value) holding class k's minimum
-    u64 visits = 0;
+    u64 visits = 0, inserts = 0;
     bool broken = false;
     __device__ __forceinline__ u32 slot_of(u32 k) {
         u32 s = slot[k];
@@ -114,6 +114,7 @@ struct Heap {
     // add f to class k's overflow set whose current minimum is root; returns the new minimum
     __device__ __forceinline__ u32 insert(u32 k, u32 root, u32 f) {
         const u64 s = slot_of(k);
+        inserts++;
 #if BITMAP_PLAIN
         // one warp owns these words (a class's slot is touched by one lane at a time, phases are
         // separated by __syncwarp), so plain L1-cached read-modify-writes replace L2 atomics
@@ -749,7 +750,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     if (slot_map)
         for (int k = lane; k < NC; k += 32) slot_map[k] = S.slot[k];   // for k_bitheap_clear
     if (stats) {
-        u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits, nr = n_refill;
+        u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits, nr = n_refill, ins = hp.inserts;
         u64 tmax = (u64)t_refill;
         for (int o = 16; o > 0; o >>= 1) {
             nr += __shfl_xor_sync(FULLMASK, nr, o);
@@ -761,11 +762,12 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             t += __shfl_xor_sync(FULLMASK, t, o);
             q += __shfl_xor_sync(FULLMASK, q, o);
             dl += __shfl_xor_sync(FULLMASK, dl, o);
+            ins += __shfl_xor_sync(FULLMASK, ins, o);
         }
         if (lane == 0) {
             stats[0] += n_iter; stats[1] += t; stats[3] += n_rounds; stats[4] += q;
             stats[5] += t_spec; stats[6] += t_dirty; stats[7] += t_cls; stats[8] += t_arr; stats[9] += dl; stats[10] += vis; stats[11] += t_store;
-            stats[12] += nr; stats[13] += tmax;
+            stats[12] += nr; stats[13] += tmax; stats[15] += ins;
         }
     }
 }
