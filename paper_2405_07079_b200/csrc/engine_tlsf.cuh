@@ -539,8 +539,6 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             peers = __match_any_sync(FULLMASK, part ? k : (0x40000000u | lane));
             rank = __popc(peers & lanemask_lt());
             const u32 leader = __ffs(peers) - 1;
-            if (part) S.lor[leader * 32 + rank] = lane;
-            __syncwarp();
             // Two parallel patterns cover almost every group; mixed groups fall back to the
             // leader's sequential replay below.
             //  (A) one block per request: request of rank q takes cached member q, valid when
@@ -561,76 +559,87 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 nkA = zA ? cls_insert(zA, L) : NONE;
             }
             const bool okA = (__ballot_sync(FULLMASK, hasA && nkA == k && rank + 1 < npeer) & peers) == 0;
-            // segmented exclusive prefix of r over the group (Hillis-Steele over ranks)
-            u64 incl = part ? ri : 0;
-            // only groups that fail pattern A need the prefix (skip the scan when none does)
-            const u32 maxpeer = __reduce_max_sync(FULLMASK, (part && !okA) ? npeer : 0u);
-            for (u32 st = 1; st < maxpeer; st <<= 1) {
-                const u32 src = (part && rank >= st) ? S.lor[leader * 32 + rank - st] : lane;
-                const u64 t = __shfl_sync(FULLMASK, incl, src);
-                if (part && rank >= st) incl += t;
-            }
-            const u64 P = incl - (part ? ri : 0);
-            u64 s0 = 0, z0 = 0;
-            u32 f0 = 0;
-            if (part && nh) {
-                f0 = S.hf[slot0] & ~HEAPBIT;
-                s0 = S.hs[slot0];
-                z0 = (u64)S.he[slot0] + 1 - s0;
-            }
-            const bool covB = part && nh && (rank == 0 || (P < z0 && z0 - P >= cls_lo(k, L)));
-            const u32 uncov = __ballot_sync(FULLMASK, part && !covB);   // every lane must vote
-            const bool okB = !okA && (uncov & peers) == 0;
-            if (part && okA) {
-                if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = S.he[slotA]; }
-                else flag = (rank < nc) ? F_MISS : F_OVER;
-            } else if (part && okB) {
-                flag = F_OK; myf = f0; mys = s0 + P; mye = S.he[slot0];
-                const u64 z = z0 - P - ri;
-                const u32 nk = z ? cls_insert(z, L) : NONE;
-                mynk = (nk == k) ? SAME : nk;
-            }
-            const bool seq = part && !okA && !okB;
-            if (seq && rank == 0) {
-                // replay the group in time order (shared memory only)
-                n_qsteps += npeer;
-                u32 b = 0, curf = 0;
-                u64 cur_s = 0, cur_e = 0;
-                bool need = true;
-                u32 q = 0;
-                for (; q < npeer; q++) {
-                    const u32 lq = S.lor[lane * 32 + q];
-                    if (need) {
-                        if (b >= nh) break;
-                        const u32 sl = k * H + ((hb + b) & (H - 1));
-                        curf = S.hf[sl] & ~HEAPBIT;
-                        cur_s = S.hs[sl];
-                        cur_e = (u64)S.he[sl] + 1;
-                        need = false;
-                    }
-                    const u64 rq = S.ch_r[lq];
-                    S.res_flag[lq] = F_OK;
-                    S.res_f[lq] = curf;
-                    S.res_s[lq] = cur_s;
-                    S.res_e[lq] = (u32)(cur_e - 1);
-                    cur_s += rq;
-                    const u64 z = cur_e - cur_s;
-                    const u32 nk = z ? cls_insert(z, L) : NONE;
-                    if (nk == k) S.res_nk[lq] = SAME;
-                    else { S.res_nk[lq] = nk; b++; need = true; }
+            bool okB = false, seq = false;
+            if (__all_sync(FULLMASK, !part || okA)) {
+                // every group takes one member per request (the common case): no prefix, no replay
+                if (part) {
+                    if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = S.he[slotA]; }
+                    else flag = (rank < nc) ? F_MISS : F_OVER;
                 }
-                const u32 fl = (b < nc) ? F_MISS : F_OVER;
-                for (; q < npeer; q++) S.res_flag[S.lor[lane * 32 + q]] = fl;
+            } else {
+                if (part) S.lor[leader * 32 + rank] = lane;   // lane of rank q in the group
+                __syncwarp();
+                // segmented exclusive prefix of r over the group (Hillis-Steele over ranks)
+                u64 incl = part ? ri : 0;
+                // only groups that fail pattern A need the prefix (skip the scan when none does)
+                const u32 maxpeer = __reduce_max_sync(FULLMASK, (part && !okA) ? npeer : 0u);
+                for (u32 st = 1; st < maxpeer; st <<= 1) {
+                    const u32 src = (part && rank >= st) ? S.lor[leader * 32 + rank - st] : lane;
+                    const u64 t = __shfl_sync(FULLMASK, incl, src);
+                    if (part && rank >= st) incl += t;
+                }
+                const u64 P = incl - (part ? ri : 0);
+                u64 s0 = 0, z0 = 0;
+                u32 f0 = 0;
+                if (part && nh) {
+                    f0 = S.hf[slot0] & ~HEAPBIT;
+                    s0 = S.hs[slot0];
+                    z0 = (u64)S.he[slot0] + 1 - s0;
+                }
+                const bool covB = part && nh && (rank == 0 || (P < z0 && z0 - P >= cls_lo(k, L)));
+                const u32 uncov = __ballot_sync(FULLMASK, part && !covB);   // every lane must vote
+                okB = !okA && (uncov & peers) == 0;
+                if (part && okA) {
+                    if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = S.he[slotA]; }
+                    else flag = (rank < nc) ? F_MISS : F_OVER;
+                } else if (part && okB) {
+                    flag = F_OK; myf = f0; mys = s0 + P; mye = S.he[slot0];
+                    const u64 z = z0 - P - ri;
+                    const u32 nk = z ? cls_insert(z, L) : NONE;
+                    mynk = (nk == k) ? SAME : nk;
+                }
+                seq = part && !okA && !okB;
+                if (seq && rank == 0) {
+                    // replay the group in time order (shared memory only)
+                    n_qsteps += npeer;
+                    u32 b = 0, curf = 0;
+                    u64 cur_s = 0, cur_e = 0;
+                    bool need = true;
+                    u32 q = 0;
+                    for (; q < npeer; q++) {
+                        const u32 lq = S.lor[lane * 32 + q];
+                        if (need) {
+                            if (b >= nh) break;
+                            const u32 sl = k * H + ((hb + b) & (H - 1));
+                            curf = S.hf[sl] & ~HEAPBIT;
+                            cur_s = S.hs[sl];
+                            cur_e = (u64)S.he[sl] + 1;
+                            need = false;
+                        }
+                        const u64 rq = S.ch_r[lq];
+                        S.res_flag[lq] = F_OK;
+                        S.res_f[lq] = curf;
+                        S.res_s[lq] = cur_s;
+                        S.res_e[lq] = (u32)(cur_e - 1);
+                        cur_s += rq;
+                        const u64 z = cur_e - cur_s;
+                        const u32 nk = z ? cls_insert(z, L) : NONE;
+                        if (nk == k) S.res_nk[lq] = SAME;
+                        else { S.res_nk[lq] = nk; b++; need = true; }
+                    }
+                    const u32 fl = (b < nc) ? F_MISS : F_OVER;
+                    for (; q < npeer; q++) S.res_flag[S.lor[lane * 32 + q]] = fl;
+                }
+                __syncwarp();
+                if (seq) {
+                    flag = S.res_flag[lane];
+                    myf = S.res_f[lane];
+                    mys = S.res_s[lane];
+                    mynk = S.res_nk[lane];
+                    mye = S.res_e[lane];
+                }
+                __syncwarp();
             }
-            __syncwarp();
-            if (seq) {
-                flag = S.res_flag[lane];
-                myf = S.res_f[lane];
-                mys = S.res_s[lane];
-                mynk = S.res_nk[lane];
-                mye = S.res_e[lane];
-            }
-            __syncwarp();
             const bool over = part && flag == F_OVER;
 #ifdef ENGINE_DEBUG
             if (n_iter < 8)
