@@ -429,6 +429,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     }
     __syncwarp();
     u64 rb_base = 0, rb_end = 0;
+    u32 keep = 0;          // wilderness mode: candidates carried over from the previous chunk
+    u64 resume = 0;        // ... and where its gather stopped
     u64 n_iter = 0, n_retarget = 0, n_rounds = 0, n_qsteps = 0, n_refill = 0;
     long long t_refill = 0;
     long long t_spec = 0, t_dirty = 0, t_cls = 0, t_arr = 0, t_store = 0, t0;
@@ -469,8 +471,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 const u32 w = 31 - __clz(sw);
                 Mx = (int)(w * 32 + 31 - __clz(S.cw[w]));
             }
-            u32 ncand = 0;
-            u64 sc = pos;
+            u32 ncand = keep;                        // ch_*[0, keep) already hold candidates
+            u64 sc = keep ? resume : pos;
             while (ncand < 32 && sc < n) {
                 if (sc < rb_base || sc + 32 > rb_end) {   // a retried chunk can start below
                     __syncwarp();
@@ -752,8 +754,21 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         }
         __syncwarp();
         t_arr += clock64() - t0;
-        if (!wmode) pos += commit;
-        else pos = commit < limit ? S.ch_i[commit] : scan_end;
+        if (!wmode) {
+            pos += commit;
+        } else if (commit < limit) {                 // carry the uncommitted candidates over
+            keep = limit - commit;
+            u64 ci_ = 0, cr_ = 0;
+            u32 cc_ = 0;
+            if (lane < keep) { ci_ = S.ch_i[commit + lane]; cr_ = S.ch_r[commit + lane]; cc_ = S.ch_c[commit + lane]; }
+            __syncwarp();
+            if (lane < keep) { S.ch_i[lane] = ci_; S.ch_r[lane] = cr_; S.ch_c[lane] = cc_; }
+            resume = scan_end;
+            pos = __shfl_sync(FULLMASK, ci_, 0);
+        } else {
+            keep = 0;
+            pos = scan_end;
+        }
         __syncwarp();
     }
     if (slot_map)
