@@ -520,12 +520,15 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         // (a member serving several requests), so a moved lane is checked after the full round:
         // if a class it skipped saw a head carve, the lane is dirty (see the dirty phase).
         const u32 k0 = k;
+        u32 pm_fin = 0;                              // grouping of the final light round
+        bool have_pm = false;
 #pragma unroll 1
         for (int it = 0; it < LIGHT_ROUNDS; it++) {
             const bool pl = act && k != NONE;
+            const u32 ck = pl ? S.cnt[k] : 0u;       // issued before the match (independent)
             const u32 pm = __match_any_sync(FULLMASK, pl ? k : (0x40000000u | lane));
-            const bool ov = pl && (u32)__popc(pm & lanemask_lt()) >= S.cnt[k];
-            if (!__any_sync(FULLMASK, ov)) break;
+            const bool ov = pl && (u32)__popc(pm & lanemask_lt()) >= ck;
+            if (!__any_sync(FULLMASK, ov)) { pm_fin = pm; have_pm = true; break; }
             if (ov) k = first_ge(S, sw, k + 1, NC);
         }
         const u32 kpre = k;
@@ -538,7 +541,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 return;
             }
             const bool part = act && k != NONE;
-            peers = __match_any_sync(FULLMASK, part ? k : (0x40000000u | lane));
+            peers = (round == 0 && have_pm) ? pm_fin : __match_any_sync(FULLMASK, part ? k : (0x40000000u | lane));
             rank = __popc(peers & lanemask_lt());
             const u32 leader = __ffs(peers) - 1;
             // Two parallel patterns cover almost every group; mixed groups fall back to the
