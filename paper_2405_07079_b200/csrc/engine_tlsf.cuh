@@ -72,7 +72,10 @@ namespace tlsfw {
 constexpr int H = H_DEF;          // head-cache depth per class (power of two)
 constexpr int REFILL_AT = REFILL_AT_DEF;      // refill a class's cache when it holds fewer members
 constexpr int MAX_NC = 928;       // classes of 2^32 units at SL_LOG2 = 5 (fl <= 28)
-constexpr int RB = 512;           // request staging buffer
+#ifndef RB_DEF
+#define RB_DEF 512
+#endif
+constexpr int RB = RB_DEF;        // request staging buffer
 constexpr u32 NONE = 0xFFFFFFFFu;
 constexpr u32 HEAPBIT = 0x80000000u;
 constexpr u32 SAME = 0xFFFFFFFEu; // block stays in its class after the carve
