@@ -152,9 +152,10 @@ size_t heap_workspace_bytes(uint64_t arena_bytes, uint64_t align, int policy,
  * d_workspace (>= heap_workspace_bytes(...) bytes, 256-byte aligned) is caller-owned and
  * must outlive the heap; initialisation kernels are enqueued on s.  *h_out receives the
  * host handle (the only memory the library owns).
- * Environment: HEAP_WILD_SPLIT=0 (read here) turns off the TLSF/SEGFIT wilderness split — the
- * alloc engine then carries the top class's single member like any other piece; results are
- * identical either way (it exists for ablation and for testing both paths). */
+ * Environment (read here; for ablation and for testing both paths — results are identical either
+ * way): HEAP_WILD_SPLIT=0 turns off the TLSF/SEGFIT wilderness split (the alloc engine then
+ * carries the top class's single member like any other piece); HEAP_BF_FLAT=1 runs BEST_FIT on
+ * one flat sorted key array instead of the blocked chunk list. */
 int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_live_blocks,
                 uint64_t max_batch, void *d_workspace, size_t workspace_bytes,
                 heap_stream_t s, heap_t **h_out);
