@@ -273,6 +273,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             h.profile((1 << NTAGS) - 1)
             h.profile_read()
         l0 = h.launch_count()
+        dc0 = h.debug_counters()
         sampler = ClockSampler(local_rank)
         sampler.start()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -290,6 +291,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
         clocks = sampler.stop()
         launches = h.launch_count() - l0
+        dc = [a - b for a, b in zip(h.debug_counters(), dc0)]
         prof = h.profile_read() if profile else None
         h.profile(0)
         step_ms = [a.elapsed_time(e) for a, e in ev]
@@ -299,11 +301,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         del h
         torch.cuda.empty_cache()
         return dict(value=ops_all / (t_max / 1e3), t_ms=t_ms, t_max=t_max, step_ms=step_ms, prof=prof,
-                    launches=launches, st=st, clocks=clocks)
+                    launches=launches, st=st, clocks=clocks, dc=dc)
 
     R = device_run(cfg.policy, False)
     value, t_ms, t_max, step_ms, launches, st, clocks = (R[k] for k in (
         "value", "t_ms", "t_max", "step_ms", "launches", "st", "clocks"))
+    engine_chain = _engine_chain(R["dc"], sum(len(b[1]) for b in batches[args.warmup:]), cfg.policy)
     RP = device_run(cfg.policy, True)
     prof, t_ms_prof = RP["prof"], RP["t_ms"]
 
@@ -439,8 +442,24 @@ def run_ours(args, cfg, rank, world, local_rank):
             "batch_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99))},
             # SURVEY.md 8(d) payload model: 64 B per alloc, 88 B per free -> 73.6 B per op at 60/40
             "payload_roofline": _payload_roofline(value),
+            # the TLSF engine is one warp's dependent chain: its structure
+            "engine_chain": engine_chain,
         }
         print(json.dumps(line), flush=True)
+
+
+def _engine_chain(dc, n_alloc, policy):
+    """TLSF/SEGFIT alloc-engine structure over the timed steps, from heap_debug_counters
+    (engine_tlsf.cuh): chunks of 32 candidate requests, requests committed per chunk,
+    speculation rounds per chunk, and the engine's cycles per chunk by phase."""
+    if policy not in (tg.TLSF, tg.SEGFIT) or not dc or dc[0] == 0:
+        return None
+    ch = dc[0]
+    return {"allocs": n_alloc, "chunks": ch, "committed_per_chunk": n_alloc / ch,
+            "rounds_per_chunk": dc[3] / ch,
+            "cycles_per_chunk": {"speculation": dc[5] / ch, "dirty_check": dc[6] / ch,
+                                 "class_updates": dc[7] / ch, "arrivals": dc[8] / ch, "stores": dc[11] / ch},
+            "overflow_inserts": dc[15], "overflow_extractions": dc[9]}
 
 
 def _payload_roofline(ops_per_s):
