@@ -67,3 +67,20 @@ def test_two_rank_replicas_gather_and_aggregate():
             assert np.array_equal(gathered[r], locals_[r])      # gathered row r == rank r's stats
         assert t_max == float(world)                             # max over ranks
         assert ops_all == sum(x[5] for x in res)                 # sum over ranks
+
+
+def test_bench_line_helpers():
+    """bench.py's derived fields: the payload roofline (64 B per alloc, 88 B per
+    free, 73.6 B per op at the 60/40 mix) and the engine-chain summary of heap_debug_counters."""
+    pr = bench._payload_roofline(1e6)
+    assert abs(pr["bytes_per_op"] - 73.6) < 1e-9
+    assert abs(pr["achieved"] - 0.0736) < 1e-12
+    assert abs(pr["frac"] - pr["achieved"] / pr["peak"]) < 1e-15
+    dc = [0] * 16
+    dc[0], dc[3], dc[5], dc[6], dc[7], dc[8], dc[11], dc[9], dc[15] = 10, 10, 2000, 1000, 3000, 2500, 100, 7, 9
+    ec = bench._engine_chain(dc, 190, tg.TLSF)
+    assert ec["chunks"] == 10 and ec["committed_per_chunk"] == 19.0 and ec["rounds_per_chunk"] == 1.0
+    assert ec["cycles_per_chunk"]["class_updates"] == 300.0
+    assert ec["overflow_extractions"] == 7 and ec["overflow_inserts"] == 9
+    assert bench._engine_chain(dc, 190, tg.BUDDY) is None
+    assert bench._engine_chain([0] * 16, 190, tg.TLSF) is None
