@@ -272,8 +272,6 @@ __global__ void __launch_bounds__(32, 1) k_alloc_engine(const u64 *__restrict__ 
         const u32 bal = __ballot_sync(FULLMASK, CSEL(hb) != NONE64);
         mask |= (u64)bal << (32 * hf);
     }
-    const u64 S0 = S.S[lane], S1 = S.S[lane + 32 < (u32)MAXC ? lane + 32 : 0];
-    const bool v1 = lane + 32 <= K;
     const u64 amask = (1ull << alog2) - 1;
     u64 n_ins = 0, n_shift = 0, n_ref = 0;
     long long cyc_ins = 0;
@@ -283,13 +281,23 @@ __global__ void __launch_bounds__(32, 1) k_alloc_engine(const u64 *__restrict__ 
         const u64 mys = my < n ? sizes[my] : 0;
         u64 res = NONE64, rz = 0;
         const u32 cnt = (u32)min((u64)32, n - base);
+        // every lane classes its own request first (smallest class holding r = the number of
+        // class sizes below r, a binary search over the ascending S), then the requests are
+        // served one by one
+        u32 myj = K + 1;
+        {
+            const u64 myr = (mys >> alog2) + ((mys & amask) != 0);
+            if (mys != 0) {
+                u32 lo = 0, hi = K + 1;                  // first t with S[t] >= myr
+                while (lo < hi) {
+                    const u32 mid = (lo + hi) >> 1;
+                    if (S.S[mid] < myr) lo = mid + 1; else hi = mid;
+                }
+                myj = lo;
+            }
+        }
         for (u32 q = 0; q < cnt; q++) {
-            const u64 s = __shfl_sync(FULLMASK, mys, q);
-            const u64 r = (s >> alog2) + ((s & amask) != 0);
-            // smallest class holding r: count the class sizes below r
-            const u32 j = (s == 0) ? K + 1
-                                   : (u32)(__popc(__ballot_sync(FULLMASK, lane <= K && S0 < r)) +
-                                           __popc(__ballot_sync(FULLMASK, v1 && S1 < r)));
+            const u32 j = __shfl_sync(FULLMASK, myj, q);
             const u64 m = (j <= K) ? (mask & (~0ull << j)) : 0;
             u64 a = NONE64;
             if (m) {
