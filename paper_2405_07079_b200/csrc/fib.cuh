@@ -305,20 +305,22 @@ __global__ void __launch_bounds__(32, 1) k_alloc_engine(const u64 *__restrict__ 
                 const u64 hb = __shfl_sync(FULLMASK, CSEL(hb), ow), lb = __shfl_sync(FULLMASK, CSEL(lb), ow);
                 const bool th = hb < lb;
                 a = th ? hb : lb;
-                bool need = false;
+                int fl = 0;                                       // bit 0: refill needed, bit 1: nonempty
                 if (lane == ow) {                                 // pop, next head
                     CWITH(hf, {
                         if (th) {
                             x.hh++;
                             if (x.hh < x.hn) x.hb = S.hc[t * HC + x.hh];
-                            else { x.hb = NONE64; need = x.ptr < x.end; }
+                            else { x.hb = NONE64; fl = x.ptr < x.end; }
                         } else {
                             x.lh++;
                             x.lb = (x.lh < x.lt) ? (u64)S.lo[(u64)t * LC + x.lh] : NONE64;
                         }
+                        fl |= (x.hb != NONE64 || x.lb != NONE64) ? 2 : 0;
                     });
                 }
-                if (__shfl_sync(FULLMASK, (int)need, ow)) {        // refill the cache (whole warp)
+                fl = __shfl_sync(FULLMASK, fl, ow);               // (a refill leaves the class nonempty)
+                if (fl & 1) {                                     // refill the cache (whole warp)
                     const u64 p0 = __shfl_sync(FULLMASK, CSEL(ptr), ow), e0 = __shfl_sync(FULLMASK, CSEL(end), ow);
                     const u32 mm = (u32)min((u64)HC, e0 - p0);
                     if (lane < mm) S.hc[t * HC + lane] = (u32)old_list[p0 + lane];
@@ -326,8 +328,7 @@ __global__ void __launch_bounds__(32, 1) k_alloc_engine(const u64 *__restrict__ 
                     if (lane == ow) CWITH(hf, { x.hh = 0; x.hn = mm; x.ptr = p0 + mm; x.hb = S.hc[t * HC]; });
                     n_ref++;
                 }
-                const bool ne = __shfl_sync(FULLMASK, (int)(CSEL(hb) != NONE64 || CSEL(lb) != NONE64), ow);
-                if (!ne) mask &= ~(1ull << t);
+                if (!fl) mask &= ~(1ull << t);
                 // split keeping the low part: the high parts (a + S_{u-1}, R(u)) stay free
                 const long long c0 = clock64();
                 for (u32 u = t; u > j; u--) {
