@@ -302,13 +302,14 @@ __global__ void __launch_bounds__(32, 1) k_alloc_engine(const u64 *__restrict__ 
             u64 a = NONE64;
             if (m) {
                 const u32 t = (u32)(__ffsll((long long)m) - 1), ow = t & 31, hf = t >> 5;
-                const u64 hb = __shfl_sync(FULLMASK, CSEL(hb), ow), lb = __shfl_sync(FULLMASK, CSEL(lb), ow);
-                const bool th = hb < lb;
-                a = th ? hb : lb;
+                {
+                    const u64 hb0 = CSEL(hb), lb0 = CSEL(lb);  // the owner's two heads: one shuffle of the smaller
+                    a = __shfl_sync(FULLMASK, hb0 < lb0 ? hb0 : lb0, ow);
+                }
                 int fl = 0;                                       // bit 0: refill needed, bit 1: nonempty
                 if (lane == ow) {                                 // pop, next head
                     CWITH(hf, {
-                        if (th) {
+                        if (x.hb < x.lb) {
                             x.hh++;
                             if (x.hh < x.hn) x.hb = S.hc[t * HC + x.hh];
                             else { x.hb = NONE64; fl = x.ptr < x.end; }
