@@ -653,12 +653,14 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         bool bad = part && flag == F_MISS;
         const bool dropper = part && flag == F_OK && mynk != SAME && mynk != NONE;
         u32 dm = __ballot_sync(FULLMASK, dropper);
+        u32 samecls = 0;                     // droppers whose remainder joins my remainder's class
         while (dm) {
             const u32 d = __ffs(dm) - 1;
             dm &= dm - 1;
             const u32 dk = __shfl_sync(FULLMASK, mynk, d);
             const u32 dfb = __shfl_sync(FULLMASK, myf, d);
             if (act && !fail0 && lane > d && ci <= dk && ((((u64)dk) << 32) | (LIFO ? 0u : dfb)) < key) bad = true;
+            if (dropper && dk == mynk) samecls |= 1u << d;
         }
         if (__any_sync(FULLMASK, act && kpre != k0)) {     // pre-moved lanes: skipped classes
             u32 sm = __ballot_sync(FULLMASK, part && flag == F_OK && mynk == SAME);
@@ -732,8 +734,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         t0 = ENG_CLK();
         // ---- remainders join their new classes (grouped by class, time order) ----
         const bool cdrop = cm && dropper;
-        const u32 g = __match_any_sync(FULLMASK, cdrop ? mynk : (0x40000000u | lane));
-        if (cdrop && __popc(g & lanemask_lt()) == 0) {
+        const u32 g = samecls & (commit >= 32 ? FULLMASK : ((1u << commit) - 1u));   // committed ones
+        if (cdrop && (g & lanemask_lt()) == 0) {
             u32 mm = g;
             while (mm) {
                 const u32 d = __ffs(mm) - 1;
