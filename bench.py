@@ -21,6 +21,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -42,8 +43,11 @@ UNIT = "ops/s"
 #   unit "alloc": one alloc request; "free": one free request; "elem": one element of the
 #   tag's own array per launch (sort: keys+payload of a pass; merge/coalesce/compact: blocks)
 TAG_BYTES = {
-    "engine": ("alloc", 8 + 4 + 16 + 8 + 8),        # r, class in; block (start,end) in; start, out
-    "table_lookup": ("free", 4 + 8 + 8 + 16 + 4),   # key in; slot read + tombstone; (start,end) + flag out
+    # SURVEY.md 8(d)'s per-op payload model for the two phases' dominant kernels: an alloc moves
+    # size 8 + offset 8 + table slot 16 + chosen free entry 16 + remainder 16 = 64 B; a free moves
+    # offset 8 + slot read 16 + tombstone 16 + coalesced entry 16 + two neighbour reads 32 = 88 B
+    "engine": ("alloc", 64),
+    "table_lookup": ("free", 88),
     "finish": ("alloc", 8 + 8 + 8 + 8),             # r, offset in; bytes out; table slot write
     "alloc_prep": ("alloc", 8 + 8 + 4),             # size in; r, class out
     "classify": ("free", 8 + 4 + 4),                # offset in; key, flag out
@@ -72,6 +76,7 @@ def parse():
     p.add_argument("--driver-max-ops", type=int, default=2_000_000)
     p.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
     p.add_argument("--dev-share-gpu", action="store_true", help=argparse.SUPPRESS)
+    p.add_argument("--no-per-config", action="store_true", help="skip the configs 1-4 side measurements")
     p.add_argument("--no-hybrid", action="store_true",
                    help="skip the extra HEAP_HYBRID measurement on the same trace")
     return p.parse_args()
@@ -184,6 +189,52 @@ def ncu_traffic(tag):
         return None
 
 
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def oracle_replay(cfg, batches, warmup, gpu_outs=None, core=None):
+    """Oracle-L (1 host thread, pinned to `core` if given) over every batch of the trace: the
+    canonical free batch then the alloc batch, timed on batches warmup.. (the GPU's timed window),
+    and every returned offset compared with gpu_outs[bi] (the GPU's results, HEAP_NULL as -1)."""
+    from oracle import OracleL
+    if core is not None:
+        try:
+            os.sched_setaffinity(0, {core % (os.cpu_count() or 1)})
+        except (AttributeError, OSError):
+            pass
+    o = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
+    n_alloc = sum(len(b[1]) for b in batches) + 1
+    omap = np.full(n_alloc, (1 << 64) - 1, dtype=np.uint64)
+    t, ops, mism, checked = 0.0, 0, None, 0
+    for bi, (fids, sizes, first) in enumerate(batches):
+        offs = omap[fids.astype(np.int64)]
+        t0 = time.perf_counter()
+        o.free_batch(offs)
+        out = o.alloc_batch(sizes)
+        dt = time.perf_counter() - t0
+        if bi >= warmup:
+            t += dt
+            ops += len(fids) + len(sizes)
+        if gpu_outs is not None and bi < len(gpu_outs):
+            g = gpu_outs[bi].view(np.uint64)
+            if mism is None and not np.array_equal(g, out):
+                j = int(np.flatnonzero(g != out)[0])
+                mism = {"batch": bi, "request": j, "gpu": int(g[j]), "oracle": int(out[j])}
+            checked += 1
+        omap[first:first + len(sizes)] = out
+    return {"value": ops / t if t > 0 else None, "ops": ops, "seconds": t, "mismatch": mism,
+            "checked_batches": checked, "state": o.stats()}
+
+
 # --------------------------------------------------------------- reference ----
 def run_reference(args, cfg):
     from oracle import OracleL
@@ -222,7 +273,7 @@ def run_reference(args, cfg):
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
-    from paper_2405_07079_b200 import Heap, heap_stats_async
+    from paper_2405_07079_b200 import Heap, heap_stats_async, nccl_comm_init, nccl_unique_id
     from paper_2405_07079_b200._native import NTAGS
 
     torch.cuda.set_device(local_rank)
@@ -243,6 +294,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     stats_dev = torch.zeros(16, dtype=torch.int64, device=dev)
     stats_all = torch.zeros(16 * world, dtype=torch.int64, device=dev) if world > 1 else None
     gloo = world > 1 and dist.get_backend() == "gloo"
+    comm = None
+    if world > 1 and not gloo:
+        # the library's own NCCL communicator (heap_stats_allgather): rank 0's unique id travels
+        # over the process group once, outside any timed region
+        uid = torch.tensor(list(nccl_unique_id()) if rank == 0 else [0] * 128, dtype=torch.uint8, device=dev)
+        dist.broadcast(uid, 0)
+        comm = nccl_comm_init(world, bytes(uid.cpu().tolist()), rank)
 
     def run_device(h, idmap, outbuf, b, stream_stats=True):
         fids, sizes, first = b
@@ -252,22 +310,25 @@ def run_ours(args, cfg, rank, world, local_rank):
         out = h.alloc_batch(sizes, out=outbuf[:na])
         idmap[first:first + na] = out
         if world > 1 and stream_stats:
-            heap_stats_async(h.handle, stats_dev)
-            if gloo:
+            if gloo:      # CPU tests / one-GPU dev mode: NCCL cannot put two ranks on one GPU
+                heap_stats_async(h.handle, stats_dev)
                 stats_all.copy_(gather_stats(stats_dev, world).view(-1))
-            else:
-                dist.all_gather_into_tensor(stats_all, stats_dev)
+            else:         # heap_stats_allgather: ncclAllGather of the 128-byte records
+                h.stats_allgather(comm, stats_all.view(world, 16))
 
     # ---------------- device-resident run ----------------
-    def device_run(policy, profile):
+    def device_run(policy, profile, keep_outs=False):
         """W warm-up + K timed steps on a fresh heap.  profile=False: the production path (batch
         graphs), timed for `value`; profile=True: direct launches bracketed by per-tag events
         (heap_profile_*), used only for the kernel shares and the roofline."""
         h = Heap(cfg.arena_bytes, cfg.align, policy, max_live, cfg.batch, device=dev)
         idmap = torch.full((n_alloc_total,), -1, dtype=torch.int64, device=dev)
         outbuf = torch.empty(cfg.batch, dtype=torch.int64, device=dev)
+        outs = []
         for b in dev_batches[:args.warmup]:
             run_device(h, idmap, outbuf, b)
+            if keep_outs:
+                outs.append(outbuf[:b[1].numel()].cpu().numpy())
         torch.cuda.synchronize()
         if profile:
             h.profile((1 << NTAGS) - 1)
@@ -288,6 +349,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             ev[k][1].record()
             torch.cuda.synchronize()
             ops += b[0].numel() + b[1].numel()
+            if keep_outs:      # outside the timed region: the step's results, for the parity check
+                outs.append(outbuf[:b[1].numel()].cpu().numpy())
         torch.cuda.synchronize()
         clocks = sampler.stop()
         launches = h.launch_count() - l0
@@ -301,9 +364,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         del h
         torch.cuda.empty_cache()
         return dict(value=ops_all / (t_max / 1e3), t_ms=t_ms, t_max=t_max, step_ms=step_ms, prof=prof,
-                    launches=launches, st=st, clocks=clocks, dc=dc)
+                    launches=launches, st=st, clocks=clocks, dc=dc, outs=outs)
 
-    R = device_run(cfg.policy, False)
+    R = device_run(cfg.policy, False, keep_outs=True)
     value, t_ms, t_max, step_ms, launches, st, clocks = (R[k] for k in (
         "value", "t_ms", "t_max", "step_ms", "launches", "st", "clocks"))
     engine_chain = _engine_chain(R["dc"], sum(len(b[1]) for b in batches[args.warmup:]), cfg.policy)
@@ -397,27 +460,41 @@ def run_ours(args, cfg, rank, world, local_rank):
                            f"capped at {args.driver_max_ops} ops / 60 s")
             drv[name] = r
 
-    # ---------------- CPU oracle baseline (rank 0, N = 1) ----------------
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import OracleL
-        ns = args.cpu_sample_batches or min(len(batches), 8)
-        o = OracleL(cfg.arena_bytes, cfg.align, cfg.policy)
-        omap = np.full(n_alloc_total, (1 << 64) - 1, dtype=np.uint64)
-        c_t, c_ops = 0.0, 0
-        for fids, sizes, first in batches[:ns]:
-            offs = omap[fids.astype(np.int64)]
-            t0 = time.perf_counter()
-            o.free_batch(offs)
-            out = o.alloc_batch(sizes)
-            c_t += time.perf_counter() - t0
-            c_ops += len(fids) + len(sizes)
-            omap[first:first + len(sizes)] = out
-        cpu = {"value": c_ops / c_t, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"config {cfg.idx} batches 0..{ns - 1} ({c_ops} ops) replayed by Oracle-L on 1 host thread"}
+    # ---------------- CPU oracle: the same timed batches, and parity of every result ----------------
+    # Each rank replays its own trace with Oracle-L on its own host core (pinned), after the GPU
+    # runs; cpu_baseline = sum of ops / max time over ranks.  The oracle's outputs
+    # are compared with every offset the production run returned, warm-up and timed batches alike.
+    cpu, parity = None, None
+    if not args.no_cpu_baseline:
+        orc = oracle_replay(cfg, batches, args.warmup, R["outs"], core=local_rank if world > 1 else None)
+        c_s, c_ops = aggregate(orc["seconds"] * 1e3, orc["ops"], world, dev)
+        bad = orc["mismatch"] is not None
+        if world > 1:
+            import torch.distributed as dist
+            fl = torch.tensor([1 if bad else 0], dtype=torch.int64, device="cpu" if gloo else dev)
+            dist.all_reduce(fl)
+            bad = int(fl.item()) > 0
+        parity = {"checked": f"batches 0..{nb - 1} (warm-up and timed), every returned offset, every rank",
+                  "ok": not bad, "first_mismatch_rank0": orc["mismatch"]}
+        cpu = {"value": c_ops / (c_s / 1e3), "unit": UNIT, "cores": world, "kind": "oracle",
+               "sample": (f"config {cfg.idx} batches {args.warmup}..{nb - 1} ({c_ops} ops over {world} rank(s)) - "
+                          f"the GPU's timed batches - replayed by Oracle-L, 1 pinned host thread per rank"),
+               **cpu_info()}
 
+    # ---------------- the other configs: device vs oracle on the same batches ----------------
+    per_config = None
+    if rank == 0 and world == 1 and not args.no_per_config and cfg.idx == 5:
+        per_config = {}
+        for cid, nbc in ((1, 0), (2, 60), (3, 24), (4, 24)):
+            try:
+                per_config[tg.CONFIGS[cid].name] = run_config(tg.CONFIGS[cid], nbc, dev, flush)
+            except Exception as e:   # never lose the headline line over a side measurement
+                per_config[tg.CONFIGS[cid].name] = {"error": str(e)[:200]}
+
+    valid = st["error_flags"] == 0 and (parity is None or parity["ok"])
     if rank == 0:
         line = {
+            "valid": valid,
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64",
@@ -432,6 +509,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             "roofline": roof,
             "kernel_shares": shares,
             "cpu_baseline": cpu,
+            "parity": parity,
+            "per_config": per_config,
             "driver_baselines": drv,
             "hybrid_same_trace": hyb,
             "e2e": e2e,
@@ -446,6 +525,50 @@ def run_ours(args, cfg, rank, world, local_rank):
             "engine_chain": engine_chain,
         }
         print(json.dumps(line), flush=True)
+
+
+def run_config(cfg, nbatches, dev, flush, warmup=3):
+    """One BASELINE config as a side measurement (not the headline): W warm-up batches and the rest
+    timed on the device (batch graphs, CUDA events, L2 flushed between steps), the same batches
+    through Oracle-L on one host thread, every returned offset compared."""
+    import torch
+    from paper_2405_07079_b200 import Heap
+    batches = make_trace(cfg, 0, nbatches) if nbatches else [b for b in tg.Trace(cfg)]
+    warmup = min(warmup, len(batches) - 1)
+    n_alloc = sum(len(b[1]) for b in batches) + 1
+    h = Heap(cfg.arena_bytes, cfg.align, cfg.policy, cfg.max_live, max(max(len(b[1]), len(b[0])) for b in batches) or 1,
+             device=dev)
+    idmap = torch.full((n_alloc,), -1, dtype=torch.int64, device=dev)
+    outs, t_ms, ops = [], 0.0, 0
+    for bi, (f, s, first) in enumerate(batches):
+        fd = torch.from_numpy(f.astype(np.int64)).to(dev)
+        sd = torch.from_numpy(s.view(np.int64)).to(dev)
+        flush.fill_(bi & 255)
+        torch.cuda.synchronize()
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        h.free_batch(idmap[fd] if len(f) else fd)
+        out = h.alloc_batch(sd, out=idmap[first:first + len(s)])
+        e.record()
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+        if bi >= warmup:
+            t_ms += a.elapsed_time(e)
+            ops += len(f) + len(s)
+    st = h.stats()
+    del h
+    orc = oracle_replay(cfg, batches, warmup, outs)
+    dev_v = ops / (t_ms / 1e3)
+    n_free = sum(len(b[0]) for b in batches[warmup:])
+    n_al = sum(len(b[1]) for b in batches[warmup:])
+    peak, src = measured_peak_hbm()
+    pay = (64 * n_al + 88 * n_free) / (t_ms / 1e3) / 1e9
+    return {"policy": tg.POLICY_NAME.get(cfg.policy), "batches": f"{warmup}..{len(batches) - 1} timed of {len(batches)}",
+            "device_ops_s": dev_v, "ms_per_batch": t_ms / max(len(batches) - warmup, 1),
+            "oracle_ops_s": orc["value"], "vs_oracle": dev_v / orc["value"] if orc["value"] else None,
+            "parity_ok": orc["mismatch"] is None and st["error_flags"] == 0, "mismatch": orc["mismatch"],
+            "payload_roofline": {"achieved": pay, "peak": peak, "unit": "GB/s", "frac": pay / peak,
+                                 "peak_source": src, "bytes": "64 B/alloc + 88 B/free (SURVEY.md 8(d))"}}
 
 
 def _engine_chain(dc, n_alloc, policy):

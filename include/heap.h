@@ -50,6 +50,8 @@ extern "C" {
 typedef struct heap heap_t;
 /* ABI-compatible with cudaStream_t; declared opaquely so this header needs no CUDA headers */
 typedef struct CUstream_st *heap_stream_t;
+/* NCCL communicator handle, declared exactly as nccl.h does (so either header may come first) */
+typedef struct ncclComm *ncclComm_t;
 
 /* policies: which free block an alloc takes (lowest key wins; DESIGN.md §2 table) */
 enum heap_policy {
@@ -122,7 +124,8 @@ enum heap_error {
                             align, arena/align > 2^32, n > max_batch, NULL handle, ...) */
     HEAP_ENOMEM = -2,    /* workspace too small or host allocation failed */
     HEAP_ECAPACITY = -3, /* a batch overflowed a metadata capacity (sticky, see above) */
-    HEAP_ECUDA = -4      /* a CUDA call failed */
+    HEAP_ECUDA = -4,     /* a CUDA call failed */
+    HEAP_ENCCL = -5      /* an NCCL call failed (heap_stats_allgather, heap_nccl_*) */
 };
 
 /* 16 x u64 = 128 bytes; byte quantities unless noted */
@@ -179,6 +182,27 @@ int heap_stats_async(heap_t *h, heap_stats_t *d_out, heap_stream_t s);
 /* heap_stats_async + copy to h_out + stream synchronise.  Returns HEAP_ECAPACITY if a
  * capacity error flag is set (h_out is still filled). */
 int heap_stats(heap_t *h, heap_stats_t *h_out, heap_stream_t s);
+
+/* Multi-GPU statistics.  The paper's model is one host allocator
+ * per device heap (§1): heaps do not shard, so N GPUs run N independent heaps and
+ * the only cross-GPU traffic is their statistics.  heap_stats_allgather enqueues this rank's
+ * heap_stats_async into the heap's workspace and an ncclAllGather of the 128-byte records over
+ * comm, on stream s (no host synchronisation): d_all (device, nranks x 128 bytes) receives rank
+ * r's statistics at d_all[r].  Collective: every rank of comm must call it (with its own heap) in
+ * the same order.  Returns HEAP_EINVAL for NULL arguments, HEAP_ENCCL if NCCL fails. */
+int heap_stats_allgather(heap_t *h, ncclComm_t comm, heap_stats_t *d_all, heap_stream_t s);
+
+/* NCCL plumbing for callers without a communicator (the library links the image's NCCL 2.28):
+ *   heap_nccl_unique_id: 128 opaque bytes into h_id (rank 0 creates it and shares it, e.g. over
+ *     torch.distributed);
+ *   heap_nccl_comm_init: *h_comm = this rank's communicator of nranks (current CUDA device);
+ *   heap_nccl_comm_init_all: ndev communicators for devices h_devs[0..ndev) of this process
+ *     (single-process multi-GPU, no bootstrap network; ndev = 1 gives a 1-rank communicator);
+ *   heap_nccl_comm_destroy.  All return HEAP_OK or HEAP_ENCCL (HEAP_EINVAL for NULL pointers). */
+int heap_nccl_unique_id(uint8_t *h_id);
+int heap_nccl_comm_init(ncclComm_t *h_comm, int nranks, const uint8_t *h_id, int rank);
+int heap_nccl_comm_init_all(ncclComm_t *h_comms, int ndev, const int *h_devs);
+int heap_nccl_comm_destroy(ncclComm_t comm);
 
 /* Export the state for parity checks: free blocks and live blocks as (start, size) byte
  * pairs sorted by start, into device arrays of cap_free / cap_live pairs (2 x u64 each).

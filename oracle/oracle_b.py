@@ -71,9 +71,20 @@ class OracleB:
                     t -= 1
                 self.roots.append((s, t))
                 s += 1 << t
-        self.counts = dict(allocs_ok=0, allocs_failed=0, frees_ok=0, frees_invalid=0,
+        self._counts = dict(allocs_ok=0, allocs_failed=0, frees_ok=0, frees_invalid=0,
                            frees_double=0, frees_null=0)
         self.rover = 0       # NEXT_FIT (reading C27): only allocations move it
+        self.hw = 0          # max over successful allocations of its end (units)
+
+    @property
+    def counts(self):
+        """Outcome counters, plus the two size statistics of heap_stats_t derived here from the
+        bitmap: the largest derived free block and the high-water end (the largest end of any
+        allocation so far, the 'provisioned' extent of PAPER.md:518's fragmentation measure)."""
+        c = dict(self._counts)
+        c["largest_free"] = max((z for _, z in self.blocks()), default=0) * self.align
+        c["high_water_end"] = self.hw * self.align
+        return c
 
     # ---- derived free blocks ----
     def runs(self):
@@ -121,6 +132,7 @@ class OracleB:
         self.owner[s:s + r] = s
         self.live[s] = r
         self.rover = s + r
+        self.hw = max(self.hw, s + r)
         return s
 
     def alloc_batch(self, sizes):
@@ -139,10 +151,10 @@ class OracleB:
                     u = self.alloc_units(r)
             if u is None:
                 out[i] = HEAP_NULL
-                self.counts["allocs_failed"] += 1
+                self._counts["allocs_failed"] += 1
             else:
                 out[i] = u * self.align
-                self.counts["allocs_ok"] += 1
+                self._counts["allocs_ok"] += 1
         return out
 
     def free_batch(self, offsets):
@@ -151,21 +163,21 @@ class OracleB:
         to_free = []
         for o in sorted(int(x) for x in offsets):
             if o == HEAP_NULL:
-                self.counts["frees_null"] += 1
+                self._counts["frees_null"] += 1
             elif o % self.align or o // self.align >= self.A:
-                self.counts["frees_invalid"] += 1
+                self._counts["frees_invalid"] += 1
             else:
                 u = o // self.align
                 a = int(self.owner[u])
                 if u in free_starts:
-                    self.counts["frees_double"] += 1
+                    self._counts["frees_double"] += 1
                 elif a < 0 or (a != u and not self.partial):
-                    self.counts["frees_invalid"] += 1
+                    self._counts["frees_invalid"] += 1
                 elif a in seen:            # a copy, or a second offset inside one live block
-                    self.counts["frees_double"] += 1
+                    self._counts["frees_double"] += 1
                 else:
                     seen.add(a)
-                    self.counts["frees_ok"] += 1
+                    self._counts["frees_ok"] += 1
                     to_free.append((a, u))
         for a, u in to_free:
             end = a + self.live[a]
@@ -301,12 +313,16 @@ class OracleBHybrid:
         self.pools = [np.ones(self.S // o, dtype=bool) for o in self.obj]
         self.sub = OracleB(arena_bytes - self.pool_end, align, TLSF)
         self.own = dict(allocs_ok=0, frees_ok=0, frees_invalid=0, frees_double=0, frees_null=0)
+        self.pool_hw = 0
 
     @property
     def counts(self):
         c = dict(self.sub.counts)
         for k, v in self.own.items():
             c[k] = c.get(k, 0) + v
+        # largest_free is the TLSF heap's (reading C26); the high-water end spans pools and heap
+        sub_hw = c["high_water_end"]
+        c["high_water_end"] = max(self.pool_hw, sub_hw + self.pool_end if sub_hw else 0)
         return c
 
     @property
@@ -325,6 +341,7 @@ class OracleBHybrid:
                     self.pools[j][t] = False
                     out[i] = j * self.S + t * self.obj[j]
                     self.own["allocs_ok"] += 1
+                    self.pool_hw = max(self.pool_hw, int(out[i]) + self.obj[j])
                     continue
             o = int(self.sub.alloc_batch(np.array([s], dtype=np.uint64))[0])
             out[i] = HEAP_NULL if o == HEAP_NULL else o + self.pool_end
@@ -397,6 +414,7 @@ class OracleBDouble:
                 c[k] += v
         for k, v in self.own.items():
             c[k] += v
+        del c["largest_free"], c["high_water_end"]   # per-heap statistics: not additive
         return c
 
     @property

@@ -20,6 +20,14 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared"]
 
 
+def nccl_dirs():
+    """The image's NCCL (2.28, the copy torch loads): include and lib directories."""
+    import nvidia.nccl
+    base = os.path.dirname(nvidia.nccl.__file__) if getattr(nvidia.nccl, "__file__", None) \
+        else list(nvidia.nccl.__path__)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
 def sources():
     return [os.path.join(SRC_DIR, f) for f in sorted(os.listdir(SRC_DIR))
             if f.endswith((".cu", ".cuh"))] + [HEADER]
@@ -30,7 +38,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(p) for p in sources())
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH + ".tmp", os.path.join(SRC_DIR, "heap.cu")]
+    inc, libdir = nccl_dirs()
+    cmd = ["nvcc", *NVCC_FLAGS, "-I", inc, "-o", LIB_PATH + ".tmp", os.path.join(SRC_DIR, "heap.cu"),
+           "-L", libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath," + libdir]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
@@ -51,7 +61,8 @@ class HeapStats(ctypes.Structure):
 EXPORTS = ("heap_workspace_bytes", "heap_create", "heap_destroy", "heap_free_batch",
            "heap_alloc_batch", "heap_stats_async", "heap_stats", "heap_export",
            "heap_launch_count", "heap_set_graphs", "heap_profile_enable", "heap_profile_read", "heap_tag_name",
-           "heap_debug_counters", "heap_strerror")
+           "heap_debug_counters", "heap_stats_allgather", "heap_nccl_unique_id", "heap_nccl_comm_init",
+           "heap_nccl_comm_init_all", "heap_nccl_comm_destroy", "heap_strerror")
 NTAGS = 16
 
 _lib = None
@@ -95,6 +106,16 @@ def lib():
         L.heap_tag_name.argtypes = [i32]
         L.heap_strerror.restype = ctypes.c_char_p
         L.heap_strerror.argtypes = [i32]
+        L.heap_stats_allgather.restype = i32
+        L.heap_stats_allgather.argtypes = [vp, vp, vp, vp]
+        L.heap_nccl_unique_id.restype = i32
+        L.heap_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.heap_nccl_comm_init.restype = i32
+        L.heap_nccl_comm_init.argtypes = [ctypes.POINTER(vp), i32, ctypes.c_char_p, i32]
+        L.heap_nccl_comm_init_all.restype = i32
+        L.heap_nccl_comm_init_all.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(i32)]
+        L.heap_nccl_comm_destroy.restype = i32
+        L.heap_nccl_comm_destroy.argtypes = [vp]
         _lib = L
     return _lib
 

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <vector>
 #include "../../include/heap.h"
+#include <nccl.h>
 #include "common.cuh"
 #include "prims.cuh"
 #include "table.cuh"
@@ -682,8 +683,10 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->flo = at<u64>(w, L.o_flo); h->fbufL = at<u64>(w, L.o_fbufL); h->frem = at<u32>(w, L.o_frem);
         h->fscr = at<u64>(w, L.o_fscr);
         if (cudaMemcpyAsync(h->fgeom, &L.fg, sizeof(fib::Geom), cudaMemcpyHostToDevice, (cudaStream_t)s) != cudaSuccess ||
+            // the limit is per function and process-wide: always the largest any heap needs
+            // (K <= MAXC - 3 = 45), so a small heap never lowers it under a live larger one
             cudaFuncSetAttribute(fib::k_alloc_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)fib::eng_smem(L.fg.K)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+                                 (int)fib::eng_smem(fib::MAXC - 3)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     }
     if (policy == HEAP_BUDDY || policy == HEAP_FIB_BUDDY) {
         h->dtm = at<u32>(w, L.o_dtm); h->dsrc = at<u32>(w, L.o_dsrc); h->baddr = at<u64>(w, L.o_baddr);
@@ -1339,8 +1342,47 @@ const char *heap_tag_name(int tag) {
     return (tag >= 0 && tag < HEAP_NTAGS) ? names[tag] : "?";
 }
 
+int heap_stats_allgather(heap_t *h, ncclComm_t comm, heap_stats_t *d_all, heap_stream_t sp) {
+    if (!h || !comm || !d_all) return HEAP_EINVAL;
+    // this rank's record goes to the heap's own 128-byte stats slot in the workspace, then every
+    // rank's record to d_all[rank] (the only inter-GPU bytes of the path)
+    int rc = heap_stats_async(h, h->dstats, sp);
+    if (rc != HEAP_OK) return rc;
+    if (ncclAllGather(h->dstats, d_all, sizeof(heap_stats_t) / sizeof(uint64_t), ncclUint64, comm,
+                      (cudaStream_t)sp) != ncclSuccess)
+        return HEAP_ENCCL;
+    return HEAP_OK;
+}
+
+int heap_nccl_unique_id(uint8_t *h_id) {
+    if (!h_id) return HEAP_EINVAL;
+    ncclUniqueId id;
+    static_assert(sizeof(id.internal) == 128, "ncclUniqueId is 128 bytes");
+    if (ncclGetUniqueId(&id) != ncclSuccess) return HEAP_ENCCL;
+    memcpy(h_id, id.internal, sizeof(id.internal));
+    return HEAP_OK;
+}
+
+int heap_nccl_comm_init(ncclComm_t *h_comm, int nranks, const uint8_t *h_id, int rank) {
+    if (!h_comm || !h_id || nranks < 1 || rank < 0 || rank >= nranks) return HEAP_EINVAL;
+    ncclUniqueId id;
+    memcpy(id.internal, h_id, sizeof(id.internal));
+    return ncclCommInitRank(h_comm, nranks, id, rank) == ncclSuccess ? HEAP_OK : HEAP_ENCCL;
+}
+
+int heap_nccl_comm_init_all(ncclComm_t *h_comms, int ndev, const int *h_devs) {
+    if (!h_comms || ndev < 1) return HEAP_EINVAL;
+    return ncclCommInitAll(h_comms, ndev, h_devs) == ncclSuccess ? HEAP_OK : HEAP_ENCCL;
+}
+
+int heap_nccl_comm_destroy(ncclComm_t comm) {
+    if (!comm) return HEAP_EINVAL;
+    return ncclCommDestroy(comm) == ncclSuccess ? HEAP_OK : HEAP_ENCCL;
+}
+
 const char *heap_strerror(int code) {
     switch (code) {
+    case HEAP_ENCCL: return "NCCL error";
     case HEAP_OK: return "ok";
     case HEAP_EINVAL: return "invalid argument";
     case HEAP_ENOMEM: return "workspace too small / out of host memory";

@@ -75,6 +75,39 @@ def heap_stats_async(h, d_out: torch.Tensor, stream=None) -> None:
     check("heap_stats_async", lib().heap_stats_async(h, _dev_ptr(d_out, "d_out"), _stream_handle(stream)))
 
 
+def heap_stats_allgather(h, comm: int, d_all: torch.Tensor, stream=None) -> None:
+    """NCCL all-gather of every rank's 128-byte statistics into d_all (CUDA int64, nranks x 16)."""
+    check("heap_stats_allgather", lib().heap_stats_allgather(h, ctypes.c_void_p(comm), _dev_ptr(d_all, "d_all"),
+                                                             _stream_handle(stream)))
+
+
+def nccl_unique_id() -> bytes:
+    """128 opaque bytes identifying a new NCCL communicator (create on one rank, share)."""
+    buf = ctypes.create_string_buffer(128)
+    check("heap_nccl_unique_id", lib().heap_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_init(nranks: int, uid: bytes, rank: int) -> int:
+    """This rank's NCCL communicator (on the current CUDA device); returns the handle."""
+    comm = ctypes.c_void_p()
+    check("heap_nccl_comm_init", lib().heap_nccl_comm_init(ctypes.byref(comm), nranks, uid, rank))
+    return int(comm.value)
+
+
+def nccl_comm_init_all(devices) -> list:
+    """One communicator per device of this process (single-process multi-GPU)."""
+    n = len(devices)
+    comms = (ctypes.c_void_p * n)()
+    devs = (ctypes.c_int * n)(*devices)
+    check("heap_nccl_comm_init_all", lib().heap_nccl_comm_init_all(comms, n, devs))
+    return [int(c) for c in comms]
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    check("heap_nccl_comm_destroy", lib().heap_nccl_comm_destroy(ctypes.c_void_p(comm)))
+
+
 def heap_stats(h, stream=None) -> dict:
     st = HeapStats()
     rc = lib().heap_stats(h, ctypes.byref(st), _stream_handle(stream))
@@ -138,10 +171,17 @@ class Heap:
         nbytes = heap_workspace_bytes(arena_bytes, align, policy, max_live_blocks, max_batch)
         if nbytes == 0:
             raise ValueError("invalid heap arguments")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        self._h = heap_create(arena_bytes, align, policy, max_live_blocks, max_batch, self.workspace,
-                              stream)
+        # heap_create reads the current device (SM count, kernel attributes): make it ours
+        with torch.cuda.device(self.device):
+            self._h = heap_create(arena_bytes, align, policy, max_live_blocks, max_batch, self.workspace,
+                                  self._stream())
         self._out = torch.empty(max_batch, dtype=torch.int64, device=self.device)
+
+    def _stream(self):
+        return self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -160,20 +200,39 @@ class Heap:
         return self._h
 
     def free_batch(self, offsets: torch.Tensor) -> None:
-        heap_free_batch(self._h, offsets, self.stream)
+        with torch.cuda.device(self.device):
+            heap_free_batch(self._h, offsets, self._stream())
 
     def alloc_batch(self, sizes: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Serve a batch of sizes (bytes) in request order; returns the offsets (HEAP_NULL as -1).
+
+        Without ``out`` the result is a fresh tensor the caller owns.  With ``out`` (int64, at least
+        ``sizes.numel()`` elements) the offsets are written there and ``out[:n]`` is returned: the
+        zero-copy path for callers that manage their own result buffers."""
         n = sizes.numel()
-        if out is None:
-            out = self._out[:n]
-        heap_alloc_batch(self._h, sizes, out, self.stream)
-        return out
+        with torch.cuda.device(self.device):
+            if out is None:
+                heap_alloc_batch(self._h, sizes, self._out[:n], self._stream())
+                return self._out[:n].clone()
+            heap_alloc_batch(self._h, sizes, out[:n], self._stream())
+            return out[:n]
 
     def stats(self) -> dict:
-        return heap_stats(self._h, self.stream)
+        with torch.cuda.device(self.device):
+            return heap_stats(self._h, self._stream())
 
     def export(self):
-        return heap_export(self._h, self.stream)
+        with torch.cuda.device(self.device):
+            return heap_export(self._h, self._stream())
+
+    def stats_allgather(self, comm: int, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Every rank's statistics (int64 [nranks, 16], heap_stats_t field order) through NCCL;
+        collective over comm, asynchronous on the heap's stream."""
+        with torch.cuda.device(self.device):
+            if out is None:
+                raise ValueError("pass out = torch.empty((nranks, 16), dtype=torch.int64, device=heap.device)")
+            heap_stats_allgather(self._h, comm, out, self._stream())
+            return out
 
     def launch_count(self) -> int:
         return heap_launch_count(self._h)
@@ -189,5 +248,6 @@ class Heap:
 
     def debug_counters(self) -> list:
         out = (ctypes.c_uint64 * 16)()
-        check("heap_debug_counters", lib().heap_debug_counters(self._h, out, 16, _stream_handle(self.stream)))
+        with torch.cuda.device(self.device):
+            check("heap_debug_counters", lib().heap_debug_counters(self._h, out, 16, _stream_handle(self._stream())))
         return [int(x) for x in out]

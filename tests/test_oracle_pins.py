@@ -283,6 +283,8 @@ def test_exhaustive_tiny_heaps(policy):
         fl, ll = hl.export()
         fb, lb = hb.export()
         assert np.array_equal(fl, fb) and np.array_equal(ll, lb), seq
+        st = hl.stats()
+        assert all(st[k] == v for k, v in hb.counts.items()), seq   # incl. largest_free, high_water_end
         n += 1
     assert n > 1000
 
@@ -310,7 +312,7 @@ def _clone_b(h):
     c.__dict__.update(h.__dict__)
     c.bits = h.bits.copy()
     c.live = dict(h.live)
-    c.counts = dict(h.counts)
+    c._counts = dict(h._counts)
     return c
 
 
@@ -693,3 +695,50 @@ def test_fib_buddy_exhaustive_tiny():
         check_fib_invariants(fl, ll, A, 1)
         n += 1
     assert n > 1000
+
+
+def test_buddy_roots_closed_form():
+    """A buddy arena that is not a power of two starts as its binary digits, largest first at
+    increasing addresses (the greedy decomposition of reading C13 into maximal aligned powers of
+    two): A_u = sum 2^b_j (b_0 > b_1 > ...) gives free blocks
+    (sum_{i<j} 2^b_i, 2^b_j).  Written from the binary expansion, not from either oracle's loop."""
+    for A in list(range(1, 70)) + [96, 100, 1000, 4095, (1 << 20) + (1 << 7) + 3, (1 << 33) - 1]:
+        bits = [b for b in range(A.bit_length() - 1, -1, -1) if A >> b & 1]
+        want, s = [], 0
+        for b in bits:
+            want.append((s, 1 << b))
+            s += 1 << b
+        for H in ((OracleL, OracleB) if A < (1 << 21) else (OracleL,)):
+            fp, lp = H(A, 1, tg.BUDDY).export()
+            assert [tuple(int(v) for v in p) for p in fp] == want, (H.__name__, A)
+            assert len(lp) == 0
+        # the largest root is the largest free block; nothing allocated yet
+        st = OracleL(A, 1, tg.BUDDY).stats()
+        assert st["largest_free"] == 1 << bits[0] and st["high_water_end"] == 0 and st["n_free"] == len(bits)
+
+
+def test_size_statistics_closed_forms():
+    """largest_free and high_water_end (heap_stats_t) on hand-worked sequences, for both oracles:
+    a fresh heap's largest block is the arena; after allocations of r_0, r_1, ... the high-water
+    end is sum r_i (L3) and the largest free block the tail; a free below the top does not lower
+    the high-water end (it is the provisioned extent of PAPER.md:518, not the live extent)."""
+    for H in (OracleL, OracleB):
+        for pol in (tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.SEGFIT, tg.NEXT_FIT):
+            h = H(1024, 16, pol)
+            c = h.stats() if H is OracleL else h.counts
+            assert (c["largest_free"], c["high_water_end"]) == (1024, 0)
+            a = [int(x) for x in h.alloc_batch([100, 16, 300])]   # 112, 16, 304 bytes
+            assert a == [0, 112, 128], (H, pol)
+            c = h.stats() if H is OracleL else h.counts
+            assert (c["largest_free"], c["high_water_end"]) == (1024 - 432, 432), (H, pol)
+            h.free_batch(np.array([128], dtype=np.uint64))          # the top block: coalesces with the tail
+            c = h.stats() if H is OracleL else h.counts
+            assert (c["largest_free"], c["high_water_end"]) == (1024 - 128, 432), (H, pol)
+            h.free_batch(np.array([0], dtype=np.uint64))
+            c = h.stats() if H is OracleL else h.counts
+            assert (c["largest_free"], c["high_water_end"]) == (1024 - 128, 432), (H, pol)
+        h = H(1024, 16, tg.BUDDY)
+        a = [int(x) for x in h.alloc_batch([16, 100])]                # orders 16 B and 128 B
+        assert a == [0, 128]
+        c = h.stats() if H is OracleL else h.counts
+        assert (c["largest_free"], c["high_water_end"]) == (512, 256)
