@@ -121,7 +121,8 @@ struct Ovf {
     u64 *pse;               // (end-1) << 32 | start of every piece in some O_k (helper-owned)
 };
 
-__device__ __forceinline__ u32 ovf_slot(Smem &S, u32 k) {
+template <class SM>
+__device__ __forceinline__ u32 ovf_slot(SM &S, u32 k) {
     u32 s = S.slot[k];
     if (s == NONE) {
         if (lane_id() == 0) s = atomicAdd(&S.nslot, 1u);
@@ -133,7 +134,8 @@ __device__ __forceinline__ u32 ovf_slot(Smem &S, u32 k) {
 }
 
 // warp-uniform: f joins O_k
-__device__ void ovf_insert(Smem &S, const Ovf &O, u32 k, u32 f, u32 s, u32 e1) {
+template <class SM>
+__device__ void ovf_insert(SM &S, const Ovf &O, u32 k, u32 f, u32 s, u32 e1) {
     const u64 sl = ovf_slot(S, k);
     u32 *a0 = O.l0 + sl * O.w0, *a1 = O.l1 + sl * O.w1, *a2 = O.l2 + sl * O.w2;
     if (lane_id() == 0) {
@@ -153,7 +155,8 @@ __device__ void ovf_insert(Smem &S, const Ovf &O, u32 k, u32 f, u32 s, u32 e1) {
 
 // warp-uniform: remove O_k's minimum h; returns the new minimum (NONE if empty).  Every set bit is
 // above h (h is the minimum), so the search only looks upward.
-__device__ u32 ovf_extract(Smem &S, const Ovf &O, u32 k, u32 h, bool &broken) {
+template <class SM>
+__device__ u32 ovf_extract(SM &S, const Ovf &O, u32 k, u32 h, bool &broken) {
     const u64 sl = S.slot[k];
     u32 *a0 = O.l0 + sl * O.w0, *a1 = O.l1 + sl * O.w1, *a2 = O.l2 + sl * O.w2;
     const u32 lane = lane_id();
@@ -194,6 +197,77 @@ __device__ u32 ovf_extract(Smem &S, const Ovf &O, u32 k, u32 h, bool &broken) {
     const u32 t0 = a0[ww];
     if (!t0) { broken = true; return NONE; }
     return (ww << 5) + __ffs(t0) - 1;
+}
+
+// A helper warp: serves INS / REQ messages from its FIFO in order until STOP (the caller's shared
+// memory type SM provides the FIFOs, delivery slots, completion ring and the helper-owned class
+// state ptr / endp / root / slot).  At STOP it publishes its classes' overflow slots (slot_map).
+template <class SM, int NH>
+__device__ void helper_loop(SM &S, u32 hid, const Csr &csr, const Ovf O, int NC, u32 *slot_map, u64 *stats) {
+    const u32 lane = lane_id();
+    bool broken = false;
+    u64 nmsg = 0;
+    for (u32 head = 0;; head++) {
+        const u32 want = ((head / QD) + 1) & 0xFFFFFu;
+        uint4 m;
+        bool quit = false;
+        for (;;) {
+            m = ld_vol_v4(&S.q[hid][head & (QD - 1)]);
+            if ((m.x >> 12) == want) break;
+            if (ld_vol(&S.abort_)) { quit = true; break; }
+            __nanosleep(100);
+        }
+        if (quit) break;
+        if (lane == 0) st_vol(&S.qhead[hid], head + 1);
+        const u32 type = (m.x >> 10) & 3, k = m.x & 0x3FF;
+        if (type == M_STOP) {
+            // every message for this helper's classes is done: publish their overflow slots
+            if (slot_map)
+                for (u32 k = hid + lane * NH; k < (u32)NC; k += 32 * NH) slot_map[k] = S.slot[k];
+            break;
+        }
+        nmsg++;
+        if (type == M_INS) {
+            ovf_insert(S, O, k, m.y, m.z, m.w);
+        } else {   // M_REQ: the m.y smallest of the CSR suffix and O_k into slot m.z
+            const u32 want_n = m.y, slot = m.z;
+            const u32 p = S.ptr[k], e = S.endp[k];
+            u32 rt = S.root[k];
+            const u32 mc = min(want_n, e - p);
+            u32 cf = NONE, cs_ = 0, ce_ = 0;
+            if (lane < mc) { cf = csr.f[p + lane]; cs_ = csr.s[p + lane]; ce_ = csr.e[p + lane]; }
+            u32 got = 0, cp = 0;
+            u32 of = 0, os = 0, oe = 0;
+            while (got < want_n) {
+                const u32 fc = __shfl_sync(FULLMASK, cf, cp & 31);
+                const u32 sc = __shfl_sync(FULLMASK, cs_, cp & 31);
+                const u32 ec = __shfl_sync(FULLMASK, ce_, cp & 31);
+                const bool have_c = cp < mc;
+                if (rt != NONE && (!have_c || rt < fc)) {
+                    const u64 v = O.pse[rt];
+                    if (lane == got) { of = rt; os = (u32)v; oe = (u32)(v >> 32); }
+                    rt = ovf_extract(S, O, k, rt, broken);
+                } else if (have_c) {
+                    if (lane == got) { of = fc; os = sc; oe = ec; }
+                    cp++;
+                } else break;
+                got++;
+            }
+            if (lane < got) S.dl[slot][lane] = make_uint4(of, os, oe, 0);
+            if (lane == 0) { S.ptr[k] = p + cp; S.root[k] = rt; S.dn[slot] = got; }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                const u32 pos = atomicAdd(&S.ctail, 1u);
+                st_vol(&S.cq[pos & (CQ - 1)], slot | ((((pos / CQ) + 1) & 0xFFFFu) << 16));
+            }
+            __syncwarp();
+        }
+    }
+    if (stats && lane == 0) {
+        atomicAdd(&stats[10], nmsg);
+        if (broken) stats[2] = 4;
+    }
 }
 
 // ------------------------------------------------------------------ main side ----
@@ -558,72 +632,8 @@ k_seq_engine(Csr csr, const u32 *__restrict__ off, u64 *__restrict__ fs, const u
             __syncwarp();
         }
     } else if ((warp & 3) != 0) {
-        // ---- helper warp ----
-        const u32 hid = warp - 2 - (warp >> 2);      // 2,3,5,6,7,9,10,11,13,14,15 -> 0..10
-        Ovf O{bm, bm + (u64)NC * w0, bm + (u64)NC * (w0 + w1), w0, w1, w2, pse};
-        bool broken = false;
-        u64 nmsg = 0;
-        for (u32 head = 0;; head++) {
-            const u32 want = ((head / QD) + 1) & 0xFFFFFu;
-            uint4 m;
-            bool quit = false;
-            for (;;) {
-                m = ld_vol_v4(&S.q[hid][head & (QD - 1)]);
-                if ((m.x >> 12) == want) break;
-                if (ld_vol(&S.abort_)) { quit = true; break; }
-                __nanosleep(100);
-            }
-            if (quit) break;
-            if (lane == 0) st_vol(&S.qhead[hid], head + 1);
-            const u32 type = (m.x >> 10) & 3, k = m.x & 0x3FF;
-            if (type == M_STOP) {
-                // every message for this helper's classes is done: publish their overflow slots
-                if (slot_map)
-                    for (u32 k = hid + lane * NHELP; k < (u32)NC; k += 32 * NHELP) slot_map[k] = S.slot[k];
-                break;
-            }
-            nmsg++;
-            if (type == M_INS) {
-                ovf_insert(S, O, k, m.y, m.z, m.w);
-            } else {   // M_REQ: the m.y smallest of the CSR suffix and O_k into slot m.z
-                const u32 want_n = m.y, slot = m.z;
-                const u32 p = S.ptr[k], e = S.endp[k];
-                u32 rt = S.root[k];
-                const u32 mc = min(want_n, e - p);
-                u32 cf = NONE, cs_ = 0, ce_ = 0;
-                if (lane < mc) { cf = csr.f[p + lane]; cs_ = csr.s[p + lane]; ce_ = csr.e[p + lane]; }
-                u32 got = 0, cp = 0;
-                u32 of = 0, os = 0, oe = 0;
-                while (got < want_n) {
-                    const u32 fc = __shfl_sync(FULLMASK, cf, cp & 31);
-                    const u32 sc = __shfl_sync(FULLMASK, cs_, cp & 31);
-                    const u32 ec = __shfl_sync(FULLMASK, ce_, cp & 31);
-                    const bool have_c = cp < mc;
-                    if (rt != NONE && (!have_c || rt < fc)) {
-                        const u64 v = O.pse[rt];
-                        if (lane == got) { of = rt; os = (u32)v; oe = (u32)(v >> 32); }
-                        rt = ovf_extract(S, O, k, rt, broken);
-                    } else if (have_c) {
-                        if (lane == got) { of = fc; os = sc; oe = ec; }
-                        cp++;
-                    } else break;
-                    got++;
-                }
-                if (lane < got) S.dl[slot][lane] = make_uint4(of, os, oe, 0);
-                if (lane == 0) { S.ptr[k] = p + cp; S.root[k] = rt; S.dn[slot] = got; }
-                __syncwarp();
-                if (lane == 0) {
-                    __threadfence_block();
-                    const u32 pos = atomicAdd(&S.ctail, 1u);
-                    st_vol(&S.cq[pos & (CQ - 1)], slot | ((((pos / CQ) + 1) & 0xFFFFu) << 16));
-                }
-                __syncwarp();
-            }
-        }
-        if (stats && lane == 0) {
-            atomicAdd(&stats[10], nmsg);
-            if (broken) stats[2] = 4;
-        }
+        helper_loop<Smem, NHELP>(S, warp - 2 - (warp >> 2), csr, Ovf{bm, bm + (u64)NC * w0, bm + (u64)NC * (w0 + w1), w0, w1, w2, pse},
+                    NC, slot_map, stats);   // warps 2,3,5,6,7,9,10,11,13,14,15 -> helpers 0..10
     }
     // (no final barrier: main's lanes 1..31 left early; each helper published its slot_map entries)
 }

@@ -17,6 +17,7 @@
 #include "fits.cuh"
 #include "engine_tlsf.cuh"
 #include "engine_seq.cuh"
+#include "engine_tlsf_h.cuh"
 #include "pool.cuh"
 #include "dbuddy.cuh"
 #include "partial.cuh"
@@ -280,7 +281,9 @@ struct heap {
     int policy, alog2, sms, G;
     int wild_split;          // TLSF/SEGFIT wilderness split (engine_tlsf.cuh); env HEAP_WILD_SPLIT=0 disables
     int bf_flat;             // BEST_FIT: the flat one-array engine instead of the blocked one (env HEAP_BF_FLAT=1)
-    int seq_engine;          // TLSF/SEGFIT: engine_seq.cuh instead of the warp-chunk engine (env HEAP_ENGINE=seq; ablation)
+    int engine;              // TLSF/SEGFIT alloc engine: 0 warp-chunk (engine_tlsf.cuh, default); ablations:
+                             // 1 warp-chunk + helper warps (engine_tlsf_h.cuh; HEAP_ENGINE=helpers),
+                             // 2 sequential one-thread chain + helpers (engine_seq.cuh; HEAP_ENGINE=seq)
     Layout L;
     void *ws;
     size_t ws_bytes;
@@ -581,7 +584,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         const char *bf = getenv("HEAP_BF_FLAT");
         h->bf_flat = (bf && bf[0] == '1') ? 1 : 0;
         const char *en = getenv("HEAP_ENGINE");
-        h->seq_engine = (en && strcmp(en, "seq") == 0) ? 1 : 0;
+        h->engine = (en && strcmp(en, "helpers") == 0) ? 1 : (en && strcmp(en, "seq") == 0) ? 2 : 0;
     }
     h->L = L;
     h->ws = d_workspace; h->ws_bytes = workspace_bytes;
@@ -594,6 +597,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(tlsfw::k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(tlsfh::k_engine_h, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(tlsfh::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(tlsfs::k_seq_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(tlsfs::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(fits::k_bf_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -891,7 +896,12 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         LAUNCH(h, tlsfw::k_wild_setup, 1, 32, 0, s, h->off, sv, h->fs[cur], h->fe[cur], n, n_in, L.NC, L.L,
                h->wild_split, C);
         TAG(h, HEAP_TAG_ENGINE);
-        if (!h->seq_engine) {
+        if (h->engine == 1) {
+            tlsfw::Csr csr{sv, h->cs, h->ce};
+            LAUNCH(h, tlsfh::k_engine_h, 1, tlsfh::NWARP * 32, sizeof(tlsfh::Smem), s, csr, h->off, h->fs[cur], h->r,
+                   h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->pse, h->slot, L.NC, L.L, C->eng, n_in,
+                   (const u32 *)C->wild);
+        } else if (h->engine == 0) {
             tlsfw::Csr csr{sv, h->cs, h->ce};
             LAUNCH(h, tlsfw::k_engine<false>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
                    h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{}, n_in,

@@ -35,6 +35,12 @@ for bi, (f, s, first) in enumerate(tg.Trace(cfg, total_ops=cfg.batch * nb)):
     st = h.stats()
     na = len(s)
     cyc = d[5]
+    if os.environ.get("HEAP_ENGINE", "") != "seq":
+        ch = max(d[0], 1)
+        print(f"b{bi} na={na} engine={eng:.2f}ms chunks={d[0]} commit/chunk={na/ch:.1f} cyc/chunk spec={d[5]/ch:.0f} "
+              f"dirty={d[6]/ch:.0f} cls={d[7]/ch:.0f} arr={d[8]/ch:.0f} store={d[11]/ch:.0f} | req={d[9]} waits={d[12]} "
+              f"waitcyc/chunk={d[13]/ch:.0f} ins={d[15]} helper_msgs={d[10]} err={c[2]}", flush=True)
+        continue
     print(f"b{bi} na={na} F={st['n_free']} step={dt*1e3:.1f}ms engine={eng:.2f}ms cyc/req={cyc/max(na,1):.0f} "
           f"pops={d[0]} arr={d[1]} req={d[3]} ins={d[4]} waits={d[7]} waitcyc={d[6]} ({d[6]/max(cyc,1)*100:.1f}%) "
           f"merges={d[8]} gives={d[9]} helper_msgs={d[10]} err={c[2]} "
