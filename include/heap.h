@@ -236,7 +236,7 @@ enum heap_tag {
     HEAP_TAG_BUDDY_FREE = 12, HEAP_TAG_BUDDY_ALLOC = 13, HEAP_TAG_MISC = 14, HEAP_NTAGS = 16
 };
 int heap_profile_enable(heap_t *h, uint64_t tag_mask);
-/* Copy the alloc engine's cumulative diagnostic counters (n <= 16 u64: chunks, re-aimed
+/* Copy the alloc engine's cumulative diagnostic counters (n <= 32 u64: chunks, re-aimed
  * requests, invariant-failure flag, replay rounds, leader steps, cycle counts per engine
  * phase) to h_out.  Synchronises s.  For tuning and tests; values are implementation-defined. */
 int heap_debug_counters(heap_t *h, uint64_t *h_out, int n, heap_stream_t s);

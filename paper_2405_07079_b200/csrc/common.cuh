@@ -38,7 +38,7 @@ struct DevCtr {
     u64 bud_cnt[48];
     u64 bud_off[49];
     u64 bud_total;
-    u64 eng[16];        // alloc engine diagnostics (engine_tlsf.cuh)
+    u64 eng[32];        // alloc engine diagnostics (engine_tlsf.cuh)
     u64 lifo_clock;     // SEGFIT_LIFO logical push clock (fits.cuh)
     u64 req_n;          // request count of a graph-launched batch (heap.cu graph path)
     u64 rover;          // NEXT_FIT: unit address where the next search starts (reading C27)

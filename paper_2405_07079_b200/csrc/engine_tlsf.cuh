@@ -62,6 +62,7 @@ constexpr int MAX_NC = 928;       // classes of 2^32 units at SL_LOG2 = 5 (fl <=
 #define RB_DEF 512
 #endif
 constexpr int RB = RB_DEF;        // request staging buffer
+
 constexpr u32 NONE = 0xFFFFFFFFu;
 constexpr u32 HEAPBIT = 0x80000000u;
 constexpr u32 SAME = 0xFFFFFFFEu; // block stays in its class after the carve
@@ -73,9 +74,8 @@ struct Smem {
     u32 ptr[MAX_NC], endp[MAX_NC], cnt[MAX_NC], root[MAX_NC], slot[MAX_NC];
     u32 nslot;
     u32 ow_i[MAX_NC], ow_v[MAX_NC];   // cached overflow word per class (see Heap)
-    u32 hf[MAX_NC * H];           // cached member f (| HEAPBIT when it came from the heap)
-    u32 hs[MAX_NC * H];           // its current start (units)
-    u32 he[MAX_NC * H];           // its end - 1 (units; ends can be 2^32)
+    uint4 hc[MAX_NC * H];         // cached member {f (| HEAPBIT when it came from the overflow set),
+                                  //  current start, end - 1 (units; ends can be 2^32), 0}
     unsigned char hn[MAX_NC];
     unsigned char hb[MAX_NC];     // ring-buffer base of the cache (entry j at (hb + j) % H)
     u32 cw[32];
@@ -87,6 +87,8 @@ struct Smem {
     u32 res_f[32], res_nk[32], res_flag[32], res_e[32];
     u64 ch_i[32], ch_r[32];       // the chunk's requests (index, units), lane = time order
     u32 ch_c[32];
+    u64 dkey[32];                 // the chunk's droppers in time order: (drop class << 32 | f) ...
+    u32 dlane[32];                // ... and their lanes (the dirty check reads them as broadcasts)
 };
 
 // Overflow members of a class (remainders that arrived while its head cache was full) live in
@@ -206,52 +208,72 @@ __device__ __forceinline__ void clear_bit(Smem &S, u32 k) {
 }
 
 struct Csr {
-    const u32 *f;   // class-sorted f
-    const u32 *s;   // class-sorted batch-start start
-    const u32 *e;   // class-sorted end - 1
+    const uint4 *r4;   // class-sorted {f, batch-start start, end - 1, 0} (one 16-byte record per member)
 };
 
-// refill the head cache of class k from min(CSR[ptr], heap root)
-__device__ void refill(Smem &S, Heap &hp, const Csr &csr, const u64 *__restrict__ fs,
-                       const u64 *__restrict__ fe, u32 k, u64 &delmins) {
-    u32 n = S.hn[k];
-    u32 p = S.ptr[k], e = S.endp[k], rt = S.root[k];
-    if (n >= (u32)REFILL_AT || (p >= e && rt == NIL32)) return;
-    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
-    const u32 b = S.hb[k];                      // ring buffer: entry j lives at (b + j) % H
 #define RI(j) ((b + (j)) & (H - 1))
-    // 1) append the next CSR members (one round of independent loads, straight into smem)
-    const u32 m = min((u32)H - n, e - p);
+// Sorted insertion of v (key f) into class k's ring holding n < H entries: every entry is loaded
+// at once (independent loads), the position is a count of smaller keys, and the shift is a set of
+// predicated stores — no load-compare-store chain per step.
+__device__ __forceinline__ void ring_insert(uint4 *hc, u32 b, u32 n, uint4 v, u32 f) {
+    uint4 x[H];
 #pragma unroll
-    for (int j = 0; j < H; j++) {
-        if ((u32)j < m) {
-            hf[RI(n + j)] = csr.f[p + j];
-            hs[RI(n + j)] = csr.s[p + j];
-            he[RI(n + j)] = csr.e[p + j];
-        }
-    }
-    n += m;
-    p += m;
-    // 2) merge in overflow members smaller than the cache's tail (or filling it), evicting
-    //    CSR members back to the CSR range (they are its last consumed entries)
-    // (overflow pulls are serial atomics: pull only what correctness needs — members below the
-    //  tail — plus enough to get back to REFILL_AT)
-    while (rt != NIL32 && (n < (u32)REFILL_AT || rt < (hf[RI(n - 1)] & ~HEAPBIT))) {
-        // issue the extract's atomic and the member's data loads together (independent)
+    for (int j = 0; j < H - 1; j++) x[j] = hc[RI(j)];
+    u32 pos = 0;
+#pragma unroll
+    for (int j = 0; j < H - 1; j++) pos += ((u32)j < n && (x[j].x & ~HEAPBIT) < f) ? 1u : 0u;
+#pragma unroll
+    for (int j = H - 1; j >= 1; j--)
+        if ((u32)j <= n && (u32)j > pos) hc[RI(j)] = x[j - 1];
+    hc[RI(pos)] = v;
+}
+
+// Refill of class k's head cache from min(CSR[ptr], overflow root), in two passes that the warp
+// runs converged (every leader's CSR part, then every leader's overflow part).
+// Pass 1: append the next CSR members.  Returns whether the cache needed members (below
+// REFILL_AT); pass 2 runs only then.
+__device__ __forceinline__ bool refill_csr(Smem &S, const Csr &csr, u32 k) {
+    const u32 n = S.hn[k];
+    if (n >= (u32)REFILL_AT) return false;
+    const u32 p = S.ptr[k], e = S.endp[k];
+    if (p >= e) return true;
+    uint4 *hc = &S.hc[k * H];
+    const u32 b = S.hb[k];                      // ring buffer: entry j lives at (b + j) % H
+    const u32 m = min((u32)H - n, e - p);
+    uint4 v[H];
+#pragma unroll
+    for (int j = 0; j < H; j++)
+        if ((u32)j < m) v[j] = csr.r4[p + j];   // one round of independent 16-byte loads
+#pragma unroll
+    for (int j = 0; j < H; j++)
+        if ((u32)j < m) hc[RI(n + j)] = v[j];
+    S.hn[k] = (unsigned char)(n + m);
+    S.ptr[k] = p + m;
+    return true;
+}
+// Pass 2: merge in overflow members smaller than the cache's tail (or filling it to REFILL_AT),
+// evicting CSR members back to the CSR range (they are its last consumed entries).  Overflow pulls
+// are serial: pull only what correctness needs — members below the tail — plus enough to get back
+// to REFILL_AT.
+__device__ void refill_ovf(Smem &S, Heap &hp, const u64 *__restrict__ fs, const u64 *__restrict__ fe, u32 k,
+                           u64 &delmins) {
+    u32 rt = S.root[k];
+    if (rt == NIL32) return;
+    u32 n = S.hn[k];
+    u32 p = S.ptr[k];
+    uint4 *hc = &S.hc[k * H];
+    const u32 b = S.hb[k];
+    while (rt != NIL32 && (n < (u32)REFILL_AT || rt < (hc[RI(n - 1)].x & ~HEAPBIT))) {
+        // issue the extract's accesses and the member's data loads together (independent)
         u32 nxt = hp.extract(k, rt);
         const u32 s0 = (u32)fs[rt], e0 = (u32)(fe[rt] - 1);
         if (n == (u32)H) {                       // evict the tail (it is > rt)
-            const u32 ev = hf[RI(H - 1)];
+            const u32 ev = hc[RI(H - 1)].x;
             if (ev & HEAPBIT) nxt = hp.insert(k, nxt, ev & ~HEAPBIT);
             else p--;
             n--;
         }
-        u32 j = n;
-        while (j > 0 && (hf[RI(j - 1)] & ~HEAPBIT) > rt) {
-            hf[RI(j)] = hf[RI(j - 1)]; hs[RI(j)] = hs[RI(j - 1)]; he[RI(j)] = he[RI(j - 1)];
-            j--;
-        }
-        hf[RI(j)] = rt | HEAPBIT; hs[RI(j)] = s0; he[RI(j)] = e0;
+        ring_insert(hc, b, n, make_uint4(rt | HEAPBIT, s0, e0, 0u), rt);
         n++;
         rt = nxt;
         delmins++;
@@ -260,35 +282,31 @@ __device__ void refill(Smem &S, Heap &hp, const Csr &csr, const u64 *__restrict_
     S.ptr[k] = p;
     S.root[k] = rt;
 }
+__device__ __forceinline__ void refill(Smem &S, Heap &hp, const Csr &csr, const u64 *__restrict__ fs,
+                                       const u64 *__restrict__ fe, u32 k, u64 &delmins) {
+    if (refill_csr(S, csr, k)) refill_ovf(S, hp, fs, fe, k, delmins);
+}
 
 // a remainder piece f = [s, e1 + 1) joins class k
 __device__ void arrive(Smem &S, Heap &hp, u32 k, u32 f, u32 s, u32 e1) {
     const u32 before = S.cnt[k]++;
     if (before == 0) set_bit(S, k);
     u32 n = S.hn[k];
-    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    uint4 *hc = &S.hc[k * H];
     const u32 b = S.hb[k];
     // the cache must stay "the n smallest members": f enters it if it is below the cache's
     // tail, or if every member is cached (nothing outside could be smaller)
-    if ((n > 0 && f < (hf[RI(n - 1)] & ~HEAPBIT)) || (n < (u32)H && before == n)) {
-        u32 j;
+    const u32 tail = n > 0 ? (hc[RI(n - 1)].x & ~HEAPBIT) : 0u;
+    if ((n > 0 && f < tail) || (n < (u32)H && before == n)) {
         if (n == (u32)H) {      // evict the largest cached member
-            u32 ev = hf[RI(H - 1)];
-            if (ev & HEAPBIT) {
-                S.root[k] = hp.insert(k, S.root[k], ev & ~HEAPBIT);
-            } else {
-                S.ptr[k]--;     // the largest cached CSR member is CSR[ptr-1]
-            }
-            j = H - 1;
+            const u32 ev = hc[RI(H - 1)].x;
+            if (ev & HEAPBIT) S.root[k] = hp.insert(k, S.root[k], ev & ~HEAPBIT);
+            else S.ptr[k]--;    // the largest cached CSR member is CSR[ptr-1]
+            n = H - 1;
         } else {
-            j = n;
             S.hn[k] = (unsigned char)(n + 1);
         }
-        while (j > 0 && (hf[RI(j - 1)] & ~HEAPBIT) > f) {
-            hf[RI(j)] = hf[RI(j - 1)]; hs[RI(j)] = hs[RI(j - 1)]; he[RI(j)] = he[RI(j - 1)];
-            j--;
-        }
-        hf[RI(j)] = f | HEAPBIT; hs[RI(j)] = s; he[RI(j)] = e1;
+        ring_insert(hc, b, n, make_uint4(f | HEAPBIT, s, e1, 0u), f);
     } else {
         S.root[k] = hp.insert(k, S.root[k], f);
     }
@@ -313,13 +331,11 @@ __device__ void refill_lifo(Smem &S, const Lifo &lf, const Csr &csr, const u64 *
     u32 n = S.hn[k];
     u32 p = S.ptr[k], e = S.endp[k], rt = S.root[k];
     if (n >= (u32)REFILL_AT || (p >= e && rt == NIL32)) return;
-    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    uint4 *hc = &S.hc[k * H];
     const u32 b = S.hb[k];
     while (rt != NIL32 && n < (u32)REFILL_AT) {         // spilled remainders first (newer)
         const u32 nx = lf.next[rt];
-        hf[RI(n)] = rt | HEAPBIT;
-        hs[RI(n)] = (u32)fs[rt];
-        he[RI(n)] = (u32)(fe[rt] - 1);
+        hc[RI(n)] = make_uint4(rt | HEAPBIT, (u32)fs[rt], (u32)(fe[rt] - 1), 0u);
         n++;
         rt = nx;
         pops++;
@@ -328,11 +344,7 @@ __device__ void refill_lifo(Smem &S, const Lifo &lf, const Csr &csr, const u64 *
         const u32 m = min((u32)H - n, e - p);
 #pragma unroll
         for (int j = 0; j < H; j++) {
-            if ((u32)j < m) {
-                hf[RI(n + j)] = csr.f[p + j];
-                hs[RI(n + j)] = csr.s[p + j];
-                he[RI(n + j)] = csr.e[p + j];
-            }
+            if ((u32)j < m) hc[RI(n + j)] = csr.r4[p + j];
         }
         n += m;
         p += m;
@@ -347,9 +359,9 @@ __device__ void arrive_lifo(Smem &S, const Lifo &lf, u32 k, u32 f, u32 s, u32 e1
     if (S.cnt[k]++ == 0) set_bit(S, k);
     u32 n = S.hn[k];
     u32 b = S.hb[k];
-    u32 *hf = &S.hf[k * H], *hs = &S.hs[k * H], *he = &S.he[k * H];
+    uint4 *hc = &S.hc[k * H];
     if (n == (u32)H) {                                   // evict the oldest cached member
-        const u32 ev = hf[RI(H - 1)];
+        const u32 ev = hc[RI(H - 1)].x;
         if (ev & HEAPBIT) {
             const u32 x = ev & ~HEAPBIT;
             lf.next[x] = S.root[k];
@@ -361,7 +373,7 @@ __device__ void arrive_lifo(Smem &S, const Lifo &lf, u32 k, u32 f, u32 s, u32 e1
     }
     b = (b - 1) & (H - 1);
     S.hb[k] = (unsigned char)b;
-    hf[RI(0)] = f | HEAPBIT; hs[RI(0)] = s; he[RI(0)] = e1;
+    hc[RI(0)] = make_uint4(f | HEAPBIT, s, e1, 0u);
     S.hn[k] = (unsigned char)(n + 1);
 }
 
@@ -422,6 +434,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     u64 n_iter = 0, n_retarget = 0, n_rounds = 0, n_qsteps = 0, n_refill = 0;
     long long t_refill = 0;
     long long t_spec = 0, t_dirty = 0, t_cls = 0, t_arr = 0, t_store = 0, t0;
+    long long t_pop = 0, t_rcsr = 0, t_rovf = 0;   // class-update sub-phases (warp-level)
     u64 pos = 0;
     while (pos < n) {
         n_iter++;
@@ -545,10 +558,13 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             const bool hasA = part && rank < nh;
             u32 fA = 0, nkA = NONE;
             u64 sA = 0;
+            u32 eA = 0;
             if (hasA) {
-                fA = S.hf[slotA] & ~HEAPBIT;
-                sA = S.hs[slotA];
-                const u64 zA = (u64)S.he[slotA] + 1 - sA - ri;
+                const uint4 mA = S.hc[slotA];
+                fA = mA.x & ~HEAPBIT;
+                sA = mA.y;
+                eA = mA.z;
+                const u64 zA = (u64)eA + 1 - sA - ri;
                 nkA = zA ? cls_insert(zA, L) : NONE;
             }
             const bool okA = (__ballot_sync(FULLMASK, hasA && nkA == k && rank + 1 < npeer) & peers) == 0;
@@ -556,7 +572,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             if (__all_sync(FULLMASK, !part || okA)) {
                 // every group takes one member per request (the common case): no prefix, no replay
                 if (part) {
-                    if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = S.he[slotA]; }
+                    if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = eA; }
                     else flag = (rank < nc) ? F_MISS : F_OVER;
                 }
             } else {
@@ -573,20 +589,22 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 }
                 const u64 P = incl - (part ? ri : 0);
                 u64 s0 = 0, z0 = 0;
-                u32 f0 = 0;
+                u32 f0 = 0, e0 = 0;
                 if (part && nh) {
-                    f0 = S.hf[slot0] & ~HEAPBIT;
-                    s0 = S.hs[slot0];
-                    z0 = (u64)S.he[slot0] + 1 - s0;
+                    const uint4 m0 = S.hc[slot0];
+                    f0 = m0.x & ~HEAPBIT;
+                    s0 = m0.y;
+                    e0 = m0.z;
+                    z0 = (u64)e0 + 1 - s0;
                 }
                 const bool covB = part && nh && (rank == 0 || (P < z0 && z0 - P >= cls_lo(k, L)));
                 const u32 uncov = __ballot_sync(FULLMASK, part && !covB);   // every lane must vote
                 okB = !okA && (uncov & peers) == 0;
                 if (part && okA) {
-                    if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = S.he[slotA]; }
+                    if (hasA) { flag = F_OK; myf = fA; mys = sA; mynk = (nkA == k) ? SAME : nkA; mye = eA; }
                     else flag = (rank < nc) ? F_MISS : F_OVER;
                 } else if (part && okB) {
-                    flag = F_OK; myf = f0; mys = s0 + P; mye = S.he[slot0];
+                    flag = F_OK; myf = f0; mys = s0 + P; mye = e0;
                     const u64 z = z0 - P - ri;
                     const u32 nk = z ? cls_insert(z, L) : NONE;
                     mynk = (nk == k) ? SAME : nk;
@@ -604,9 +622,10 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                         if (need) {
                             if (b >= nh) break;
                             const u32 sl = k * H + ((hb + b) & (H - 1));
-                            curf = S.hf[sl] & ~HEAPBIT;
-                            cur_s = S.hs[sl];
-                            cur_e = (u64)S.he[sl] + 1;
+                            const uint4 mq = S.hc[sl];
+                            curf = mq.x & ~HEAPBIT;
+                            cur_s = mq.y;
+                            cur_e = (u64)mq.z + 1;
                             need = false;
                         }
                         const u64 rq = S.ch_r[lq];
@@ -652,15 +671,28 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         const u64 key = part ? (((u64)k << 32) | (LIFO ? 1u : myf)) : ~0ull;
         bool bad = part && flag == F_MISS;
         const bool dropper = part && flag == F_OK && mynk != SAME && mynk != NONE;
-        u32 dm = __ballot_sync(FULLMASK, dropper);
+        // The droppers are compacted into shared memory in time order, and every lane scans the list
+        // with broadcast loads: the loads are independent, so the scan pipelines instead of walking
+        // the dropper mask with a find-first-set and two shuffles per dropper.
+        const u32 dm = __ballot_sync(FULLMASK, dropper);
+        const u32 nd = __popc(dm);
+        if (dropper) {
+            const u32 q = __popc(dm & lanemask_lt());
+            S.dkey[q] = (((u64)mynk) << 32) | (LIFO ? 0u : myf);
+            S.dlane[q] = lane;
+        }
+        __syncwarp();
         u32 samecls = 0;                     // droppers whose remainder joins my remainder's class
-        while (dm) {
-            const u32 d = __ffs(dm) - 1;
-            dm &= dm - 1;
-            const u32 dk = __shfl_sync(FULLMASK, mynk, d);
-            const u32 dfb = __shfl_sync(FULLMASK, myf, d);
-            if (act && !fail0 && lane > d && ci <= dk && ((((u64)dk) << 32) | (LIFO ? 0u : dfb)) < key) bad = true;
-            if (dropper && dk == mynk) samecls |= 1u << d;
+        {
+            const bool chk = act && !fail0;
+            const u64 clo = ((u64)ci) << 32;         // a drop class >= ci  <=>  dkey >= clo
+#pragma unroll 4
+            for (u32 q = 0; q < nd; q++) {
+                const u64 dk = S.dkey[q];
+                const u32 dl = S.dlane[q];
+                if (chk && lane > dl && dk >= clo && dk < key) bad = true;
+                if (dropper && (u32)(dk >> 32) == mynk) samecls |= 1u << dl;
+            }
         }
         if (__any_sync(FULLMASK, act && kpre != k0)) {     // pre-moved lanes: skipped classes
             u32 sm = __ballot_sync(FULLMASK, part && flag == F_OK && mynk == SAME);
@@ -702,6 +734,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         t_store += ENG_CLK() - t0;
         const u32 leftm = __ballot_sync(FULLMASK, cm && part && mynk != SAME);
         const u32 staym = __ballot_sync(FULLMASK, cm && part && mynk == SAME && last_on_block);
+        bool rf = false;                         // this leader's class lost members: refill
         if (cm && part && rank == 0) {
             const u32 left = __popc(leftm & peers);
             const u32 st = staym & peers;        // the surviving head was carved: new start
@@ -713,22 +746,32 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 // re-read from fs, never from the stale CSR copy
                 const u32 d = __ffs(st) - 1;
                 const u32 sl = k * H + ((b + left) & (H - 1));
-                S.hs[sl] = (u32)(S.res_s[d] + S.ch_r[d]);
-                S.hf[sl] |= HEAPBIT;
+                S.hc[sl].y = (u32)(S.res_s[d] + S.ch_r[d]);
+                S.hc[sl].x |= HEAPBIT;
             }
             if (left) {                          // pop `left` members: advance the ring base
                 S.hb[k] = (unsigned char)((b + left) & (H - 1));
                 S.hn[k] = (unsigned char)(S.hn[k] - left);
                 S.cnt[k] -= left;
-                const long long tr0 = ENG_CLK();
-                const bool work = S.hn[k] < (u32)REFILL_AT && (S.ptr[k] < S.endp[k] || S.root[k] != NIL32);
-                if constexpr (LIFO) refill_lifo(S, lf, csr, fs, fe, k, n_delmin);
-                else refill(S, hp, csr, fs, fe, k, n_delmin);
-                t_refill += ENG_CLK() - tr0;
-                n_refill += work;                // diagnostics: refills that loaded members
-                if (S.cnt[k] == 0) clear_bit(S, k);
+                rf = true;
             }
         }
+        if constexpr (LIFO) {
+            if (rf) refill_lifo(S, lf, csr, fs, fe, k, n_delmin);
+        } else {
+            // the leaders' refills run converged: every CSR part, then every overflow part
+            __syncwarp();
+            const long long ta = ENG_CLK();
+            const bool rf2 = rf && refill_csr(S, csr, k);
+            __syncwarp();
+            const long long tb = ENG_CLK();
+            if (rf2) refill_ovf(S, hp, fs, fe, k, n_delmin);
+            __syncwarp();
+            const long long tc = ENG_CLK();
+            t_pop += ta - t0; t_rcsr += tb - ta; t_rovf += tc - tb;
+            n_refill += rf2;                     // diagnostics: refills that needed members
+        }
+        if (rf && S.cnt[k] == 0) clear_bit(S, k);
         __syncwarp();
         t_cls += ENG_CLK() - t0;
         t0 = ENG_CLK();
@@ -785,6 +828,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             stats[0] += n_iter; stats[1] += t; stats[3] += n_rounds; stats[4] += q;
             stats[5] += t_spec; stats[6] += t_dirty; stats[7] += t_cls; stats[8] += t_arr; stats[9] += dl; stats[10] += vis; stats[11] += t_store;
             stats[12] += nr; stats[13] += tmax; stats[15] += ins;
+            stats[16] += t_pop; stats[17] += t_rcsr; stats[18] += t_rovf;
         }
     }
 }
@@ -871,14 +915,13 @@ __global__ void k_wild_apply(u64 *__restrict__ out_u, const u32 *__restrict__ pr
     if (blockIdx.x == 0 && threadIdx.x == 0) fs[C->wild[1]] = w0 + C->wild_total;
 }
 
-// class-sorted copies of (start, end - 1) for the CSR (one gather after the class sort)
+// class-sorted records {f, start, end - 1, 0} for the CSR (one gather after the class sort)
 __global__ void k_csr_data(const u32 *__restrict__ csr_f, const u64 *__restrict__ fs, const u64 *__restrict__ fe,
-                           const u64 *F_dev, u32 *__restrict__ cs, u32 *__restrict__ ce) {
+                           const u64 *F_dev, uint4 *__restrict__ r4) {
     const u64 F = *F_dev;
     for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < F; p += (u64)gridDim.x * blockDim.x) {
-        u32 f = csr_f[p];
-        cs[p] = (u32)fs[f];
-        ce[p] = (u32)(fe[f] - 1);
+        const u32 f = csr_f[p];
+        r4[p] = make_uint4(f, (u32)fs[f], (u32)(fe[f] - 1), 0u);
     }
 }
 

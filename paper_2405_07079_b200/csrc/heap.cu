@@ -16,8 +16,6 @@
 #include "buddy.cuh"
 #include "fits.cuh"
 #include "engine_tlsf.cuh"
-#include "engine_seq.cuh"
-#include "engine_tlsf_h.cuh"
 #include "pool.cuh"
 #include "dbuddy.cuh"
 #include "partial.cuh"
@@ -42,7 +40,7 @@ struct Layout {
     // offsets
     u64 o_ctr, o_stats, o_tbl, o_fs0, o_fs1, o_fe0, o_fe1, o_kA, o_kB, o_vA, o_vB, o_flags, o_pos,
         o_hist, o_tsum, o_vs, o_ve, o_vsc, o_vec, o_ms, o_me, o_r, o_c, o_out, o_off, o_child,
-        o_sib, o_cs, o_ce, o_bm, o_slot, o_pse, bm_w0, bm_w1, bm_w2, bm_bytes, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
+        o_sib, o_cs, o_bm, o_slot, bm_w0, bm_w1, bm_w2, bm_bytes, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
         o_promo, o_fr, o_froff, o_reqoff, o_ft0, o_ft1, o_vt, o_mt, o_lnext, total;
     // HEAP_HYBRID: pool geometry and arrays, then the TLSF heap's own workspace at o_sub
     pool::Geom geo;
@@ -214,8 +212,7 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
     L.o_gout = take(max_batch * 8);
     L.o_off = take((fits::MAX_NC + 8) * 4);
     if (policy == HEAP_TLSF || policy == HEAP_SEGFIT) {
-        L.o_cs = take(L.cap_f * 4);
-        L.o_ce = take(L.cap_f * 4);
+        L.o_cs = take(L.cap_f * 16);          // CSR records {f, start, end - 1, 0} (engine_tlsf.cuh)
         // overflow bitmaps: one three-level slot per class (engine_tlsf.cuh)
         L.bm_w0 = (L.cap_f + 31) / 32;
         L.bm_w1 = (L.bm_w0 + 31) / 32;
@@ -223,11 +220,9 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.bm_bytes = (u64)L.NC * (L.bm_w0 + L.bm_w1 + L.bm_w2) * 4;
         L.o_bm = take(L.bm_bytes);
         L.o_slot = take(tlsfw::MAX_NC * 4);
-        L.o_pse = take(L.cap_f * 8);          // engine_seq.cuh: (end-1, start) of overflow members
     }
     if (policy == HEAP_SEGFIT_LIFO) {
-        L.o_cs = take(L.cap_f * 4);
-        L.o_ce = take(L.cap_f * 4);
+        L.o_cs = take(L.cap_f * 16);
         L.o_ft0 = take(L.cap_f * 4);          // push stamps of the free pieces (double buffer)
         L.o_ft1 = take(L.cap_f * 4);
         L.o_vt = take(max_batch * 4);         // stamps of this batch's frees
@@ -281,9 +276,6 @@ struct heap {
     int policy, alog2, sms, G;
     int wild_split;          // TLSF/SEGFIT wilderness split (engine_tlsf.cuh); env HEAP_WILD_SPLIT=0 disables
     int bf_flat;             // BEST_FIT: the flat one-array engine instead of the blocked one (env HEAP_BF_FLAT=1)
-    int engine;              // TLSF/SEGFIT alloc engine: 0 warp-chunk (engine_tlsf.cuh, default); ablations:
-                             // 1 warp-chunk + helper warps (engine_tlsf_h.cuh; HEAP_ENGINE=helpers),
-                             // 2 sequential one-thread chain + helpers (engine_seq.cuh; HEAP_ENGINE=seq)
     Layout L;
     void *ws;
     size_t ws_bytes;
@@ -294,8 +286,8 @@ struct heap {
     u64 *tbl, *fs[2], *fe[2];
     u32 *kA, *kB, *vA, *vB, *flags, *pos, *hist, *tsum;
     u64 *vs, *ve, *vsc, *vec, *ms, *me, *r, *out;
-    u32 *c, *off, *child, *sib, *cs, *ce, *bm, *slot;
-    u64 *pse;
+    u32 *c, *off, *child, *sib, *bm, *slot;
+    uint4 *cs;
     u32 *ft[2], *vt, *mt, *lnext;             // SEGFIT_LIFO stamps and spill links
     u64 *tree, *lvl;
     u64 *bk[2];
@@ -583,8 +575,6 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->wild_split = (ws && ws[0] == '0') ? 0 : 1;
         const char *bf = getenv("HEAP_BF_FLAT");
         h->bf_flat = (bf && bf[0] == '1') ? 1 : 0;
-        const char *en = getenv("HEAP_ENGINE");
-        h->engine = (en && strcmp(en, "helpers") == 0) ? 1 : (en && strcmp(en, "seq") == 0) ? 2 : 0;
     }
     h->L = L;
     h->ws = d_workspace; h->ws_bytes = workspace_bytes;
@@ -597,10 +587,6 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(tlsfw::k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
-    if (cudaFuncSetAttribute(tlsfh::k_engine_h, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(tlsfh::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
-    if (cudaFuncSetAttribute(tlsfs::k_seq_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(tlsfs::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(fits::k_bf_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(fits::BfSmem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_free_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -671,9 +657,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->off = at<u32>(w, L.o_off);
     h->gin = at<u64>(w, L.o_gin); h->gout = at<u64>(w, L.o_gout);
     h->graphs = 1;
-    h->cs = L.o_cs ? at<u32>(w, L.o_cs) : nullptr; h->ce = L.o_ce ? at<u32>(w, L.o_ce) : nullptr;
+    h->cs = L.o_cs ? at<uint4>(w, L.o_cs) : nullptr;
     h->bm = L.o_bm ? at<u32>(w, L.o_bm) : nullptr; h->slot = L.o_slot ? at<u32>(w, L.o_slot) : nullptr;
-    h->pse = L.o_pse ? at<u64>(w, L.o_pse) : nullptr;
     if (h->bm && cudaMemsetAsync(h->bm, 0, L.bm_bytes, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     h->tree = L.o_tree ? at<u64>(w, L.o_tree) : nullptr; h->lvl = L.o_lvl ? at<u64>(w, L.o_lvl) : nullptr;
     h->bk[0] = L.o_bk0 ? at<u64>(w, L.o_bk0) : nullptr; h->bk[1] = L.o_bk1 ? at<u64>(w, L.o_bk1) : nullptr;
@@ -878,9 +863,9 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         u32 *sv = rb ? h->vB : h->vA;
         LAUNCH(h, fits::k_u64_hi, h->G, 256, 0, s, sk, &C->F, h->kA);
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kA, &C->F, L.NC, h->off);
-        LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs, h->ce);
+        LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs);
         TAG(h, HEAP_TAG_ENGINE);
-        tlsfw::Csr csr{sv, h->cs, h->ce};
+        tlsfw::Csr csr{h->cs};
         tlsfw::Lifo lf{h->lnext, h->ft[cur], &C->lifo_clock};
         LAUNCH(h, tlsfw::k_engine<true>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
                h->c, n, h->out, nullptr, 0ull, 0ull, 0ull, h->slot, L.NC, L.L, C->eng, lf, n_in, (const u32 *)nullptr);
@@ -892,24 +877,14 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->F, ilog2((u64)L.NC) + 1, s);
         u32 *sk = rb ? h->kB : h->kA, *sv = rb ? h->vB : h->vA;
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, sk, &C->F, L.NC, h->off);
-        LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs, h->ce);
+        LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs);
         LAUNCH(h, tlsfw::k_wild_setup, 1, 32, 0, s, h->off, sv, h->fs[cur], h->fe[cur], n, n_in, L.NC, L.L,
                h->wild_split, C);
         TAG(h, HEAP_TAG_ENGINE);
-        if (h->engine == 1) {
-            tlsfw::Csr csr{sv, h->cs, h->ce};
-            LAUNCH(h, tlsfh::k_engine_h, 1, tlsfh::NWARP * 32, sizeof(tlsfh::Smem), s, csr, h->off, h->fs[cur], h->r,
-                   h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->pse, h->slot, L.NC, L.L, C->eng, n_in,
-                   (const u32 *)C->wild);
-        } else if (h->engine == 0) {
-            tlsfw::Csr csr{sv, h->cs, h->ce};
+        {
+            tlsfw::Csr csr{h->cs};
             LAUNCH(h, tlsfw::k_engine<false>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
                    h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{}, n_in,
-                   (const u32 *)C->wild);
-        } else {
-            tlsfs::Csr csr{sv, h->cs, h->ce};
-            LAUNCH(h, tlsfs::k_seq_engine, 1, tlsfs::NWARP * 32, sizeof(tlsfs::Smem), s, csr, h->off, h->fs[cur], h->r,
-                   h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->pse, h->slot, L.NC, L.L, C->eng, n_in,
                    (const u32 *)C->wild);
         }
         TAG(h, HEAP_TAG_FINISH);
@@ -1312,7 +1287,7 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
 }
 
 int heap_debug_counters(heap_t *h, uint64_t *h_out, int n, heap_stream_t sp) {
-    if (!h || !h_out || n < 0 || n > 16) return HEAP_EINVAL;
+    if (!h || !h_out || n < 0 || n > 32) return HEAP_EINVAL;
     cudaStream_t s = (cudaStream_t)sp;
     CUDA_TRY(cudaMemcpyAsync(h_out, (h->sub ? h->sub : h)->ctr->eng, n * sizeof(u64), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));

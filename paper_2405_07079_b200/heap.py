@@ -247,7 +247,7 @@ class Heap:
         return heap_profile_read(self._h)
 
     def debug_counters(self) -> list:
-        out = (ctypes.c_uint64 * 16)()
+        out = (ctypes.c_uint64 * 32)()
         with torch.cuda.device(self.device):
-            check("heap_debug_counters", lib().heap_debug_counters(self._h, out, 16, _stream_handle(self._stream())))
+            check("heap_debug_counters", lib().heap_debug_counters(self._h, out, 32, _stream_handle(self._stream())))
         return [int(x) for x in out]
