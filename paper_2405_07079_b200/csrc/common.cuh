@@ -47,6 +47,13 @@ struct DevCtr {
     u64 wild_total;     // units the batch took from it
     u64 wild_acc[2];    // k_alloc_prep: units of all requests, max search class of a valid one
     u32 wild[2];        // {class Kw, piece f} of the wilderness, {NONE, NONE} when inactive
+    // single-pass sort / scan control (prims.cuh; zero at creation, self-resetting)
+    u32 os_tile[8];     // onesweep radix sort: dynamic tile counter per pass
+    u32 os_epoch;       // bumped once per sort call (tags the lookback flags)
+    u32 os_done;        // histogram kernel: CTAs finished
+    u32 sc_tile, sc_done, sc_epoch, sc_pad;   // single-pass scan: tile counter, CTAs done, epoch
+    u32 os_gh[8][256];  // digit histograms of the current sort (zeroed again by the last CTA)
+    u32 os_gbase[8][256];   // their exclusive scans: first output position of each digit
 };
 
 enum { ERR_CAP_LIVE = 1, ERR_TABLE_FULL = 2, ERR_CAP_FREE = 4, ERR_ENGINE = 8, ERR_LIVEMAP = 16 };

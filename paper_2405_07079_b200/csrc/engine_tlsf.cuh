@@ -57,6 +57,10 @@ namespace tlsfw {
 #endif
 constexpr int H = H_DEF;          // head-cache depth per class (power of two)
 constexpr int REFILL_AT = REFILL_AT_DEF;      // refill a class's cache when it holds fewer members
+#ifndef FILL_TO_DEF
+#define FILL_TO_DEF H_DEF
+#endif
+constexpr int FILL_TO = FILL_TO_DEF;          // a refill appends CSR members up to this many cached
 constexpr int MAX_NC = 928;       // classes of 2^32 units at SL_LOG2 = 5 (fl <= 28)
 #ifndef RB_DEF
 #define RB_DEF 512
@@ -239,7 +243,7 @@ __device__ __forceinline__ bool refill_csr(Smem &S, const Csr &csr, u32 k) {
     if (p >= e) return true;
     uint4 *hc = &S.hc[k * H];
     const u32 b = S.hb[k];                      // ring buffer: entry j lives at (b + j) % H
-    const u32 m = min((u32)H - n, e - p);
+    const u32 m = min((u32)FILL_TO - n, e - p);
     uint4 v[H];
 #pragma unroll
     for (int j = 0; j < H; j++)

@@ -142,7 +142,7 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.o_vB = take(max_batch * 4);
         L.o_flags = take(scan_cap * 4);
         L.o_pos = take(scan_cap * 4);
-        L.o_hist = take((256 * prims::ntiles_of(max_batch) + 16) * 4);
+        L.o_hist = take((256 * prims::ntiles_of(max_batch) + 512) * 4);
         L.o_tsum = take((prims::ntiles_of(scan_cap) + 16) * 4);
         L.o_tsz = take(max_batch * 8);
         L.o_tout = take(max_batch * 8);
@@ -171,7 +171,7 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
     L.tcap = next_pow2(2 * max_live);
     if (L.tcap < 1024) L.tcap = 1024;
     L.sort_cap = std::max(std::max(max_batch, L.cap_f), max_live) + 16;
-    L.hist_cap = 256 * prims::ntiles_of(L.sort_cap) + 16;
+    L.hist_cap = 256 * prims::ntiles_of(L.sort_cap) + 512;   // u64 lookback words of the onesweep tiles
     L.scan_cap = std::max(std::max(L.cap_m, L.sort_cap), L.hist_cap);
     L.scan_cap = std::max(L.scan_cap, L.tcap);
     L.FB = ilog2(L.cap_f) + 1;
@@ -386,26 +386,25 @@ __global__ void k_init(DevCtr *ctr, u64 *tbl, u64 tcap, u64 *fs, u64 *fe, u64 A_
 // radix sort of *n_dev keys (ping-pong); returns the buffer index (0 = a, 1 = b) holding the result
 template <typename K, bool HV>
 int radix_sort(heap *h, K *ka, K *kb, u32 *va, u32 *vb, const u64 *n_dev, int bits, cudaStream_t s) {
-    int passes = (bits + 7) / 8;
+    // onesweep (prims.cuh): one histogram launch for every pass, then one launch per pass
+    const int passes = (bits + 7) / 8;
+    u64 *flags = reinterpret_cast<u64 *>(h->hist);
+    LAUNCH(h, prims::k_os_hist<K>, h->sms, prims::OS_NT, 0, s, ka, n_dev, passes, h->ctr);
     K *kin = ka, *kout = kb;
     u32 *vin = va, *vout = vb;
     for (int p = 0; p < passes; p++) {
-        LAUNCH(h, prims::k_rs_hist<K>, h->G, prims::NT, 0, s, kin, n_dev, 8 * p, h->hist, &h->ctr->n_hist);
-        LAUNCH(h, prims::k_scan_reduce, h->G, prims::NT, 0, s, h->hist, &h->ctr->n_hist, h->tsum);
-        LAUNCH(h, prims::k_scan_tiles, 1, 1024, 0, s, h->tsum, &h->ctr->n_hist, &h->ctr->scan_total);
-        LAUNCH(h, prims::k_scan_down, h->G, prims::NT, 0, s, h->hist, h->hist, &h->ctr->n_hist, h->tsum);
-        LAUNCH(h, (prims::k_rs_scatter<K, HV>), h->G, prims::NT, 0, s, kin, vin, kout, vout, n_dev, 8 * p, h->hist);
+        LAUNCH(h, (prims::k_os_scatter<K, HV>), h->G, prims::OS_NT, (prims::os_smem<K, HV>()), s, kin, vin, kout,
+               vout, n_dev, p, flags, h->ctr);
         K *tk = kin; kin = kout; kout = tk;
         u32 *tv = vin; vin = vout; vout = tv;
     }
     return passes & 1;
 }
 
-// exclusive scan of u32 in[*n_dev] into out, grand total into *total
+// exclusive scan of u32 in[*n_dev] into out, grand total into *total (single pass, prims.cuh)
 void scan(heap *h, const u32 *in, u32 *out, const u64 *n_dev, u64 *total, cudaStream_t s) {
-    LAUNCH(h, prims::k_scan_reduce, h->G, prims::NT, 0, s, in, n_dev, h->tsum);
-    LAUNCH(h, prims::k_scan_tiles, 1, 1024, 0, s, h->tsum, n_dev, total);
-    LAUNCH(h, prims::k_scan_down, h->G, prims::NT, 0, s, in, out, n_dev, h->tsum);
+    LAUNCH(h, prims::k_scan_1p, h->G, prims::OS_NT, 0, s, in, out, n_dev, total, reinterpret_cast<u64 *>(h->tsum),
+           h->ctr);
 }
 
 __global__ void k_set_F(DevCtr *ctr) {
@@ -587,6 +586,14 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(tlsfw::k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(prims::k_os_scatter<u32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)prims::os_smem<u32, false>()) != cudaSuccess ||
+        cudaFuncSetAttribute(prims::k_os_scatter<u32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)prims::os_smem<u32, true>()) != cudaSuccess ||
+        cudaFuncSetAttribute(prims::k_os_scatter<u64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)prims::os_smem<u64, false>()) != cudaSuccess ||
+        cudaFuncSetAttribute(prims::k_os_scatter<u64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)prims::os_smem<u64, true>()) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(fits::k_bf_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(fits::BfSmem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_free_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -609,7 +616,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->graphs = 1;
         h->cur = 0; h->launches = 0; h->prof_mask = 0; h->tag = HEAP_TAG_MISC;
         if (cudaMemsetAsync(h->ctr, 0, sizeof(DevCtr), st) != cudaSuccess ||
-            cudaMemsetAsync(h->dctr, 0, sizeof(dbl::Ctr), st) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+            cudaMemsetAsync(h->dctr, 0, sizeof(dbl::Ctr), st) != cudaSuccess ||
+            cudaMemsetAsync(h->tsum, 0, (prims::ntiles_of(max_batch) + 16) * 4, st) != cudaSuccess) { delete h; return HEAP_ECUDA; }
         int rc = heap_create(L.dbl_A, align, HEAP_BUDDY, max_live_blocks, max_batch, at<char>(w, L.o_sub), L.sub_total,
                              s, &h->sub);
         if (rc == HEAP_OK && L.dbl_n3)
@@ -634,7 +642,9 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->graphs = 1;
         h->cur = 0; h->launches = 0; h->prof_mask = 0; h->tag = HEAP_TAG_MISC;
         if (cudaMemsetAsync(h->ctr, 0, sizeof(DevCtr), st) != cudaSuccess ||
-            cudaMemsetAsync(h->pctr, 0, sizeof(pool::Ctr), st) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+            cudaMemsetAsync(h->pctr, 0, sizeof(pool::Ctr), st) != cudaSuccess ||
+            cudaMemsetAsync(h->hist, 0, L.o_tsum - L.o_hist, st) != cudaSuccess ||
+            cudaMemsetAsync(h->tsum, 0, L.o_tsz - L.o_tsum, st) != cudaSuccess) { delete h; return HEAP_ECUDA; }
         LAUNCH(h, pool::k_init, h->G, 256, 0, st, L.geo, h->bits, h->sbcnt, h->pctr);
         int rc = heap_create(arena_bytes - L.geo.pool_end, align, HEAP_TLSF, max_live_blocks, max_batch,
                              at<char>(w, L.o_sub), L.sub_total, s, &h->sub);
@@ -660,6 +670,12 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->cs = L.o_cs ? at<uint4>(w, L.o_cs) : nullptr;
     h->bm = L.o_bm ? at<u32>(w, L.o_bm) : nullptr; h->slot = L.o_slot ? at<u32>(w, L.o_slot) : nullptr;
     if (h->bm && cudaMemsetAsync(h->bm, 0, L.bm_bytes, (cudaStream_t)s) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    // lookback words of the single-pass sort / scan: never-published (epoch tags start above 0)
+    if (cudaMemsetAsync(h->hist, 0, L.hist_cap * 4, (cudaStream_t)s) != cudaSuccess ||
+        cudaMemsetAsync(h->tsum, 0, (prims::ntiles_of(L.scan_cap) + 16) * 4, (cudaStream_t)s) != cudaSuccess) {
+        delete h;
+        return HEAP_ECUDA;
+    }
     h->tree = L.o_tree ? at<u64>(w, L.o_tree) : nullptr; h->lvl = L.o_lvl ? at<u64>(w, L.o_lvl) : nullptr;
     h->bk[0] = L.o_bk0 ? at<u64>(w, L.o_bk0) : nullptr; h->bk[1] = L.o_bk1 ? at<u64>(w, L.o_bk1) : nullptr;
     if (policy == HEAP_SEGFIT_LIFO) {

@@ -1,2 +1,3 @@
-for v in t_pf0 t_u4; do echo "== $v"; HEAP_DEV_LIB=libheap_$v.so timeout 300 python tools/engine_probe.py 5 12 2>&1 | tail -3; done > gpurun_out/probe_u4.txt 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "small_every_batch or wild or config3 or edge or config5_first or direct or lifo" > gpurun_out/pytest_u4.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_u4.log
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_os.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_os.log
+for c in 1 2 3 4; do echo "== cfg $c"; timeout 300 python tools/tag_profile.py $c 12 2>&1 | tail -14; done > gpurun_out/tags_os.txt 2>&1
+timeout 300 python tests/dev/bench_all.py 1 2 3 4 > gpurun_out/bench_os.txt 2>&1
