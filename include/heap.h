@@ -233,7 +233,8 @@ enum heap_tag {
     HEAP_TAG_CLASSIFY = 0, HEAP_TAG_SCAN = 1, HEAP_TAG_SORT = 2, HEAP_TAG_LOOKUP = 3,
     HEAP_TAG_COMPACT = 4, HEAP_TAG_MERGE = 5, HEAP_TAG_COALESCE = 6, HEAP_TAG_ALLOC_PREP = 7,
     HEAP_TAG_INDEX = 8, HEAP_TAG_ENGINE = 9, HEAP_TAG_FINISH = 10, HEAP_TAG_REBUILD = 11,
-    HEAP_TAG_BUDDY_FREE = 12, HEAP_TAG_BUDDY_ALLOC = 13, HEAP_TAG_MISC = 14, HEAP_NTAGS = 16
+    HEAP_TAG_BUDDY_FREE = 12, HEAP_TAG_BUDDY_ALLOC = 13, HEAP_TAG_MISC = 14,
+    HEAP_TAG_MICRO = 15, HEAP_NTAGS = 16
 };
 int heap_profile_enable(heap_t *h, uint64_t tag_mask);
 /* Copy the alloc engine's cumulative diagnostic counters (n <= 32 u64: chunks, re-aimed

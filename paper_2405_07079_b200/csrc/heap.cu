@@ -12,6 +12,7 @@
 #include <nccl.h>
 #include "common.cuh"
 #include "prims.cuh"
+#include "micro.cuh"
 #include "table.cuh"
 #include "buddy.cuh"
 #include "fits.cuh"
@@ -276,6 +277,7 @@ struct heap {
     int policy, alog2, sms, G;
     int wild_split;          // TLSF/SEGFIT wilderness split (engine_tlsf.cuh); env HEAP_WILD_SPLIT=0 disables
     int bf_flat;             // BEST_FIT: the flat one-array engine instead of the blocked one (env HEAP_BF_FLAT=1)
+    int micro;               // small heap: each batch is one single-CTA launch (micro.cuh); env HEAP_MICRO=0 disables
     Layout L;
     void *ws;
     size_t ws_bytes;
@@ -574,6 +576,11 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->wild_split = (ws && ws[0] == '0') ? 0 : 1;
         const char *bf = getenv("HEAP_BF_FLAT");
         h->bf_flat = (bf && bf[0] == '1') ? 1 : 0;
+        const char *mi = getenv("HEAP_MICRO");
+        const bool fitp = policy == HEAP_FIRST_FIT || policy == HEAP_NEXT_FIT || policy == HEAP_BEST_FIT ||
+                          policy == HEAP_SEGFIT || policy == HEAP_TLSF;
+        h->micro = (fitp && !L.partial && max_live_blocks + 1 <= micro::MICRO_F && L.A_u <= 0xFFFFFFFFull &&
+                    max_batch <= micro::MICRO_N && !(mi && mi[0] == '0')) ? 1 : 0;
     }
     h->L = L;
     h->ws = d_workspace; h->ws_bytes = workspace_bytes;
@@ -594,6 +601,16 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
                              (int)prims::os_smem<u64, false>()) != cudaSuccess ||
         cudaFuncSetAttribute(prims::k_os_scatter<u64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)prims::os_smem<u64, true>()) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(micro::k_micro_free, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::FREE_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(micro::k_micro_alloc<micro::P_FF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::ALLOC_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(micro::k_micro_alloc<micro::P_NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::ALLOC_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(micro::k_micro_alloc<micro::P_BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::ALLOC_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(micro::k_micro_alloc<micro::P_CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::ALLOC_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(fits::k_bf_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(fits::BfSmem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_free_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -756,6 +773,15 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
     const bool bud = h->policy == HEAP_BUDDY || fibp;
     DevCtr *C = h->ctr;
     u64 *n_dev = &C->tmp[0];
+    if (h->micro) {          // small heap: the whole free batch in one single-CTA launch (micro.cuh)
+        TAG(h, HEAP_TAG_MICRO);
+        LAUNCH(h, micro::k_micro_free, 1, micro::MT, micro::FREE_SMEM, s, (const u64 *)d_offsets, n, n_in, h->alog2,
+               L.A_u, h->fs[cur], h->fe[cur], h->fs[nxt], h->fe[nxt], h->tbl, L.tcap - 1, L.tcap / table::LINE,
+               L.cap_f, C);
+        h->cur = nxt;
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        return HEAP_OK;
+    }
     // 1. classify (null / unaligned / out of range) and compact the candidate keys
     TAG(h, HEAP_TAG_CLASSIFY);
     LAUNCH(h, fits::k_free_classify, h->G, prims::NT, 0, s, (const u64 *)d_offsets, n, n_in, h->alog2, L.A_u, h->kA, h->flags, n_dev, C);
@@ -860,6 +886,23 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
                h->tbl, L.tcap - 1, L.tcap / table::LINE, C, h->max_live);
         h->cur = nxt;
         maybe_rebuild(h, s);
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        return HEAP_OK;
+    }
+    if (h->micro) {          // small heap: the whole alloc batch in one single-CTA launch (micro.cuh)
+        TAG(h, HEAP_TAG_MICRO);
+#define MICRO_ALLOC(P)                                                                                          \
+    LAUNCH(h, micro::k_micro_alloc<P>, 1, micro::MT, micro::ALLOC_SMEM, s, (const u64 *)d_sizes, n, n_in, h->alog2, \
+           L.A_u, L.L, h->fs[cur], h->fe[cur], h->fs[nxt], h->fe[nxt], (u64 *)d_out, h->tbl, L.tcap - 1,             \
+           L.tcap / table::LINE, L.tcap, h->ms, C, h->max_live)
+        switch (h->policy) {
+            case HEAP_FIRST_FIT: MICRO_ALLOC(micro::P_FF); break;
+            case HEAP_NEXT_FIT: MICRO_ALLOC(micro::P_NF); break;
+            case HEAP_BEST_FIT: MICRO_ALLOC(micro::P_BF); break;
+            default: MICRO_ALLOC(micro::P_CLS); break;
+        }
+#undef MICRO_ALLOC
+        h->cur = nxt;
         if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
         return HEAP_OK;
     }
@@ -1339,7 +1382,7 @@ const char *heap_tag_name(int tag) {
     static const char *names[HEAP_NTAGS] = {"classify", "scan", "sort", "table_lookup", "compact", "merge",
                                             "coalesce", "alloc_prep", "index_build", "engine", "finish",
                                             "table_rebuild", "buddy_free_levels", "buddy_alloc_levels",
-                                            "misc", "unused"};
+                                            "misc", "micro"};
     return (tag >= 0 && tag < HEAP_NTAGS) ? names[tag] : "?";
 }
 

@@ -173,11 +173,13 @@ def test_best_fit_engines(case, flat, monkeypatch):
     run_parity(cfg, max_live=max(1 << 15, 8 * batch), max_batch=batch, every_batch_state=batch < 100)
 
 
-def test_wild_split_guards():
+def test_wild_split_guards(monkeypatch):
     """The split's three conditions (engine_tlsf.cuh k_wild_setup) each switched off by a batch
     built to violate it, and on for batches that satisfy them; zero-size and oversize requests
     in a split batch (written as failures by the candidate gather).  Every batch must match
-    Oracle-L; diagnostic counter 14 counts the batches served with the split."""
+    Oracle-L; diagnostic counter 14 counts the batches served with the split.  (The heaps are
+    small enough for the single-launch path, which has no split: the general path is forced.)"""
+    monkeypatch.setenv("HEAP_MICRO", "0")
     U = 16
     arena = 1 << 24                                    # 2^20 units
     for pol in (tg.TLSF, tg.SEGFIT):
@@ -235,9 +237,12 @@ def test_config5_first_batches():
     run_parity(cfg, cfg.max_live, cfg.batch, max_batches=3)
 
 
-def test_edge_cases():
+@pytest.mark.parametrize("micro", ["1", "0"], ids=["micro", "general"])
+def test_edge_cases(micro, monkeypatch):
     """Empty batches, NULL / interior / unaligned / out-of-range / duplicate frees,
-    zero and oversize requests, OOM in a tiny arena, the last unit of a 2^32-unit arena."""
+    zero and oversize requests, OOM in a tiny arena, the last unit of a 2^32-unit arena — on the
+    single-launch small-heap path (micro.cuh) and on the general path."""
+    monkeypatch.setenv("HEAP_MICRO", micro)
     for pol in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 1 | 0x100, 4 | 0x100):
         arena, align = 1 << 12, 16
         g = Gpu(arena, align, pol, 256, 64)
@@ -265,10 +270,39 @@ def test_edge_cases():
     compare_state(g, o, "2^32 units")
 
 
-def test_table_rebuild_under_churn():
-    """Small live capacity with heavy churn forces tombstone purges of the block table."""
+@pytest.mark.parametrize("micro", ["1", "0"], ids=["micro", "general"])
+def test_table_rebuild_under_churn(micro, monkeypatch):
+    """Small live capacity with heavy churn forces tombstone purges of the block table (in the
+    micro kernel's own purge, and in the general path's rebuild launches)."""
+    monkeypatch.setenv("HEAP_MICRO", micro)
     cfg = tg.custom(tg.TLSF, 1 << 22, 16, 256, rho=(1, 2), total_ops=60000, sizes=(4, 10), idx=77)
     run_parity(cfg, max_live=600, max_batch=256)
+
+
+MICRO_CASES = [
+    # (arena, align, batch, ops, sizes, rho): heaps small enough for the single-launch path
+    # (max_live 4096 -> at most 4097 free pieces), live blocks kept below the capacity
+    (1 << 16, 16, 24, 1500, (4, 10), (1, 2)),
+    (1 << 22, 16, 1000, 40000, (4, 14), (1, 2)),
+    (1 << 20, 16, 500, 10000, (4, 12), (2, 5)),
+    (1 << 18, 16, 3000, 30000, (4, 9), (1, 2)),          # the arena fills: failed requests
+    ((1 << 22) + 48, 16, 700, 14000, (4, 13), (1, 2)),   # non power-of-two arena
+    (1 << 21, 64, 256, 8000, (6, 12), (1, 2)),           # align 64
+]
+
+
+@pytest.mark.parametrize("micro", ["1", "0"], ids=["micro", "general"])
+@pytest.mark.parametrize("pol", [tg.FIRST_FIT, tg.NEXT_FIT, tg.BEST_FIT, tg.SEGFIT, tg.TLSF],
+                         ids=lambda p: tg.POLICY_NAME[p])
+@pytest.mark.parametrize("case", MICRO_CASES, ids=lambda c: f"A{c[0]}-B{c[2]}")
+def test_micro_and_general_paths(case, pol, micro, monkeypatch):
+    """The small-heap path (micro.cuh: one single-CTA launch per free batch and per alloc batch,
+    brute-force exact argmin engine) and the general path, each bit-exact with Oracle-L on every
+    batch, state compared after every batch (the two interleave through the same state)."""
+    monkeypatch.setenv("HEAP_MICRO", micro)
+    arena, align, batch, ops, sizes, rho = case
+    cfg = tg.custom(pol, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes, idx=40 + pol)
+    run_parity(cfg, max_live=4096, max_batch=batch, every_batch_state=True)
 
 
 def test_invariants_config3_prefix():
