@@ -287,11 +287,11 @@ __global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r,
 
 // ---------------------------------------------------------------- TLSF / SEGFIT ----
 // Per batch the free blocks are grouped by their class (stable radix sort of (class, f)),
-// giving each class an address-ordered array consumed as a prefix.  A block whose carved
-// remainder drops to a lower class k' joins k' through a per-class pairing heap keyed by f
-// (a block can be in only one class at a time, so child/sibling arrays indexed by f
-// suffice).  Class emptiness is kept in two-level bitmaps (one u32 word per first level, 32
-// second-level classes = one word), searched with ffs.
+// giving each class an address-ordered CSR range consumed as a prefix (engine_tlsf.cuh reads it
+// as 16-byte records).  A block whose carved remainder drops to a lower class k' joins k' in the
+// engine's shared-memory head cache or, past the cache, in k''s overflow bitmap over f (a block
+// is in one class at a time).  Class emptiness is kept in two-level bitmaps (one u32 word per
+// first level, 32 second-level classes = one word), searched with ffs.
 __global__ void k_cls_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev, int L,
                            u32 *__restrict__ key, u32 *__restrict__ val) {
     const u64 F = *F_dev;

@@ -38,6 +38,9 @@ __device__ __forceinline__ u64 lb_load(const u64 *p) {
 }
 // Decoupled lookback for one value: publish `agg` for tile t, return the sum of all tiles before t,
 // publish the inclusive sum.  flags: one word per tile (stride apart); tag = epoch of this call.
+// The predecessors' words are read LB_W at a time (independent loads in flight), newest first, so a
+// walk back over many tiles that published only their aggregate takes 1/LB_W of the round trips.
+constexpr int LB_W = 8;
 __device__ __forceinline__ u32 lookback(u64 *flags, u64 stride, u64 t, u32 tag, u32 agg) {
     const u64 hi = (u64)tag << 32;
     if (t == 0) {
@@ -46,13 +49,21 @@ __device__ __forceinline__ u32 lookback(u64 *flags, u64 stride, u64 t, u32 tag, 
     }
     lb_store(flags + t * stride, hi | ((u64)LB_AGG << 30) | agg);
     u32 prefix = 0;
-    for (u64 tt = t - 1;;) {
-        const u64 v = lb_load(flags + tt * stride);
-        const u32 st = (u32)(v >> 30) & 3u;
-        if ((u32)(v >> 32) != tag || st == 0) continue;       // not published yet (spin)
-        prefix += (u32)v & 0x3FFFFFFFu;
-        if (st == LB_INC) break;
-        tt--;
+    u64 tt = t;                                   // tiles [tt, t) are summed into prefix
+    for (;;) {
+        u64 v[LB_W];
+#pragma unroll
+        for (int j = 0; j < LB_W; j++) v[j] = (tt > (u64)j) ? lb_load(flags + (tt - 1 - j) * stride) : 0ull;
+        bool done = false;
+        int j = 0;
+        for (; j < LB_W && tt > (u64)j; j++) {
+            const u32 st = (u32)(v[j] >> 30) & 3u;
+            if ((u32)(v[j] >> 32) != tag || st == 0) break;     // not published yet: re-read from here
+            prefix += (u32)v[j] & 0x3FFFFFFFu;
+            if (st == LB_INC) { done = true; break; }
+        }
+        if (done) break;
+        tt -= (u64)j;                             // j words consumed (all aggregates)
     }
     lb_store(flags + t * stride, hi | ((u64)LB_INC << 30) | (prefix + agg));
     return prefix;
