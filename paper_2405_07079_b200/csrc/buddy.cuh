@@ -134,6 +134,7 @@ __device__ u64 cta_compact(u64 n, Keep keep, Emit emit, u32 *sm) {
 __global__ void __launch_bounds__(NT) k_free_levels(const u64 *__restrict__ old_list, u64 *__restrict__ new_list,
                                                     const u64 *__restrict__ fr, const u32 *__restrict__ fr_off,
                                                     u64 *bufA, u64 *bufB, u64 *promo, int K, DevCtr *ctr) {
+    PDL_ENTRY();
     __shared__ u32 sm[33];
     __shared__ u64 ooff[41];
     __shared__ u64 s_np, s_out;
@@ -227,9 +228,106 @@ __global__ void __launch_bounds__(NT) k_free_levels(const u64 *__restrict__ old_
     }
 }
 
+// ------------------------------------------------ free phase, parallel form (default) ----
+// The buddy free set is the set of maximal free nodes of the buddy trees (lemma L2): every node
+// whose whole span is free and whose parent's is not.  Inside a maximal run of free space [x, y)
+// those nodes are exactly the greedy decomposition — at x the largest 2^s with x % 2^s == 0 and
+// x + 2^s <= y, repeat — and it never crosses a root boundary (the roots are the binary digits of
+// the arena, largest first, so each root start is a multiple of twice its size and every later
+// root is smaller).  So the merge that k_free_levels does level by level (27 dependent levels at
+// config 4) is computed in one pass of independent steps: old blocks in address order (radix sort
+// of the per-order lists), merged with the freed blocks, coalesced into maximal runs (the fits
+// path's kernels), each run decomposed, the result grouped by order (stable one-pass sort).
+__device__ __forceinline__ int bud_step(u64 x, u64 y) {   // order of the greedy block at x in [x, y)
+    const int a = x ? __ffsll((long long)x) - 1 : 63;
+    const int b = 63 - __clzll(y - x);
+    return a < b ? a : b;
+}
+// old per-order lists -> (start key, index) for the address sort
+__global__ void k_bud_keys(const u64 *__restrict__ list, const DevCtr *ctr, u32 *__restrict__ key,
+                           u32 *__restrict__ val) {
+    PDL_ENTRY();
+    const u64 n = ctr->bud_total;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        key[i] = (u32)list[i];
+        val[i] = (u32)i;
+    }
+}
+// sorted indices -> (start, end) in address order
+__global__ void k_bud_unpack(const u64 *__restrict__ list, const u32 *__restrict__ idx, const DevCtr *ctr, int K,
+                             u64 *__restrict__ os, u64 *__restrict__ oe) {
+    PDL_ENTRY();
+    __shared__ u64 off[42];
+    if (threadIdx.x <= (unsigned)K + 1) off[threadIdx.x] = ctr->bud_off[threadIdx.x];
+    __syncthreads();
+    const u64 n = ctr->bud_total;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u32 p = idx[i];
+        int lo = 0, hi = K;                 // order t: off[t] <= p < off[t + 1]
+        while (lo < hi) { const int m = (lo + hi + 1) >> 1; if (off[m] <= p) lo = m; else hi = m - 1; }
+        const u64 a = list[p];
+        os[i] = a;
+        oe[i] = a + (1ull << lo);
+    }
+}
+// blocks of each maximal run's greedy decomposition
+__global__ void k_bud_count(const u64 *__restrict__ rs, const u64 *__restrict__ re, const u64 *R_dev,
+                            u32 *__restrict__ cnt) {
+    PDL_ENTRY();
+    const u64 R = *R_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += (u64)gridDim.x * blockDim.x) {
+        u64 x = rs[i];
+        const u64 y = re[i];
+        u32 c = 0;
+        while (x < y) { x += 1ull << bud_step(x, y); c++; }
+        cnt[i] = c;
+    }
+}
+// write the decomposition in address order: start (units) and the order as the sort key
+__global__ void k_bud_write(const u64 *__restrict__ rs, const u64 *__restrict__ re, const u64 *R_dev,
+                            const u32 *__restrict__ pos, u64 *__restrict__ ostart, u32 *__restrict__ okey,
+                            u32 *__restrict__ oval, u64 cap, DevCtr *ctr) {
+    PDL_ENTRY();
+    const u64 R = *R_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += (u64)gridDim.x * blockDim.x) {
+        u64 x = rs[i];
+        const u64 y = re[i];
+        u64 o = pos[i];
+        while (x < y) {
+            const int t = bud_step(x, y);
+            if (o < cap) { ostart[o] = x; okey[o] = (u32)t; oval[o] = (u32)o; }
+            else atomicOr(&ctr->error_flags, (u64)ERR_CAP_FREE);
+            x += 1ull << t;
+            o++;
+        }
+    }
+}
+// order-grouped (stable: address order inside an order) -> the new per-order lists
+__global__ void k_bud_lists(const u32 *__restrict__ idx, const u64 *n_dev, const u64 *__restrict__ start,
+                            u64 *__restrict__ out) {
+    PDL_ENTRY();
+    const u64 n = *n_dev;
+    for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (u64)gridDim.x * blockDim.x)
+        out[p] = start[idx[p]];
+}
+__global__ void k_bud_offsets(const u32 *__restrict__ key, const u64 *n_dev, int K, DevCtr *ctr) {
+    PDL_ENTRY();
+    const u64 n = *n_dev;
+    const int t = threadIdx.x;
+    if (t <= K + 1) {
+        u64 lo = 0, hi = n;                 // first position with order >= t
+        while (lo < hi) { const u64 m = (lo + hi) >> 1; if (key[m] < (u32)t) lo = m + 1; else hi = m; }
+        ctr->bud_off[t] = lo;
+    }
+    __syncthreads();
+    if (t <= K) ctr->bud_cnt[t] = ctr->bud_off[t + 1] - ctr->bud_off[t];
+    if (t == 0) ctr->bud_total = n;
+}
+
 // freed (start, end) -> sort key = order, payload = index
 __global__ void k_free_orders(const u64 *__restrict__ vs, const u64 *__restrict__ ve, const u64 *nv_dev,
                               u32 *__restrict__ key, u32 *__restrict__ val) {
+    PDL_ENTRY();
     const u64 nv = *nv_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (u64)gridDim.x * blockDim.x) {
         key[i] = (u32)flog2(ve[i] - vs[i]);
@@ -238,6 +336,7 @@ __global__ void k_free_orders(const u64 *__restrict__ vs, const u64 *__restrict_
 }
 __global__ void k_gather_u64(const u64 *__restrict__ src, const u32 *__restrict__ idx, const u64 *n_dev,
                              u64 *__restrict__ dst) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         dst[i] = src[idx[i]];
@@ -247,6 +346,7 @@ __global__ void k_gather_u64(const u64 *__restrict__ src, const u32 *__restrict_
 // r -> order key (K+1 = fail bucket)
 __global__ void k_alloc_orders(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2, u64 A_u, int K,
                                u32 *__restrict__ key, u32 *__restrict__ val, u64 *n_dev) {
+    PDL_ENTRY();
     if (n_in) n = *n_in;
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
     const u64 amask = (1ull << alog2) - 1;
@@ -271,6 +371,7 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
                                                      u32 *dtm, u32 *dsrc, u64 *daddr, u64 *baddr,
                                                      u32 *btm, u32 *bsrc, u64 *__restrict__ out_u, int K,
                                                      DevCtr *ctr) {
+    PDL_ENTRY();
     __shared__ u64 ooff[41];
     __shared__ u64 doff[42], boff[42];
     __shared__ u64 s_nb;
@@ -394,6 +495,7 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
 
 // buddy results: order -> units = 2^k; reuse fits::k_alloc_finish by materialising r
 __global__ void k_alloc_r(const u32 *__restrict__ key_by_req, u64 n, const u64 *n_in, int K, u64 *__restrict__ r) {
+    PDL_ENTRY();
     if (n_in) n = *n_in;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         u32 k = key_by_req[i];

@@ -58,6 +58,17 @@ struct DevCtr {
 
 enum { ERR_CAP_LIVE = 1, ERR_TABLE_FULL = 2, ERR_CAP_FREE = 4, ERR_ENGINE = 8, ERR_LIVEMAP = 16 };
 
+// Programmatic dependent launch (heap.cu LAUNCH): every kernel lets the next kernel of the stream
+// be scheduled as soon as all of its own CTAs have started, then waits until the previous kernel
+// has completed and its memory is visible before touching anything.  Consecutive launches of a
+// batch thus overlap their launch latency, never their data (griddepcontrol.wait is a full
+// completion wait; without the launch attribute both instructions are no-ops).
+#define PDL_ENTRY()                                                          \
+    do {                                                                     \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");     \
+        asm volatile("griddepcontrol.wait;" ::: "memory");                  \
+    } while (0)
+
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ u32 lanemask_lt() {
     u32 m;

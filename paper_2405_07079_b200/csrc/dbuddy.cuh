@@ -23,6 +23,7 @@ struct Ctr {
 __global__ void k_free_split(const u64 *__restrict__ offs, u64 n, const u64 *n_in, u64 A_bytes, u64 u3, int has3,
                              u32 *__restrict__ fa, u32 *__restrict__ fb, u64 *__restrict__ va, u64 *__restrict__ vb,
                              Ctr *c) {
+    PDL_ENTRY();
     if (n_in) n = *n_in;
     if (blockIdx.x == 0 && threadIdx.x == 0) c->nreq = n;
     u64 nnull = 0, ninv = 0;
@@ -48,6 +49,7 @@ __global__ void k_free_split(const u64 *__restrict__ offs, u64 n, const u64 *n_i
 __global__ void k_alloc_split(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2, u64 A_u, int has3,
                               u32 *__restrict__ fa, u32 *__restrict__ fb, u64 *__restrict__ va, u64 *__restrict__ vb,
                               Ctr *c) {
+    PDL_ENTRY();
     if (n_in) n = *n_in;
     if (blockIdx.x == 0 && threadIdx.x == 0) c->nreq = n;
     const u64 amask = (1ull << alog2) - 1;
@@ -70,6 +72,7 @@ __global__ void k_alloc_split(const u64 *__restrict__ sizes, u64 n, const u64 *n
 
 __global__ void k_compact_idx(const u64 *__restrict__ v, const u32 *__restrict__ flags, const u32 *__restrict__ pos,
                               const u64 *n_dev, u64 *__restrict__ out, u32 *__restrict__ idx) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         if (flags[i]) { out[pos[i]] = v[i]; if (idx) idx[pos[i]] = (u32)i; }
@@ -77,6 +80,7 @@ __global__ void k_compact_idx(const u64 *__restrict__ v, const u32 *__restrict__
 
 __global__ void k_scatter(const u64 *__restrict__ res, const u32 *__restrict__ idx, const u64 *n_dev, u64 base,
                           u64 mul, u64 *__restrict__ out) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (u64)gridDim.x * blockDim.x) {
         const u64 o = res[k];
@@ -86,6 +90,7 @@ __global__ void k_scatter(const u64 *__restrict__ res, const u32 *__restrict__ i
 
 // export of the 3-unit heap: (unit, units) -> bytes past A_bytes
 __global__ void k_pairs_to_bytes(u64 *pairs, u64 n, u64 base, u64 mul) {
+    PDL_ENTRY();
     for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (u64)gridDim.x * blockDim.x) {
         pairs[2 * k] = base + pairs[2 * k] * mul;
         pairs[2 * k + 1] *= mul;
@@ -95,6 +100,7 @@ __global__ void k_pairs_to_bytes(u64 *pairs, u64 n, u64 base, u64 mul) {
 // heap_stats of the pair (reading C28): sums; sizes of the 3-unit heap scaled to bytes
 __global__ void k_stats(const heap_stats_t *a, const heap_stats_t *b, int has3, const Ctr *c, u64 arena, u64 align,
                         u64 A_bytes, u64 meta, heap_stats_t *out) {
+    PDL_ENTRY();
     const u64 u3 = 3 * align;
     heap_stats_t z = {};
     const heap_stats_t *bb = has3 ? b : &z;

@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                                                   u64 *__restrict__ out_u, u32 *bm, u64 w0, u64 w1, u64 w2,
                                                   u32 *slot_map, int NC, int L, u64 *stats, Lifo lf,
                                                   const u64 *n_in, const u32 *wild) {
+    PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (n_in) n = *n_in;   // request count on the device (a hybrid heap's TLSF share)
     // wilderness split (k_wild_setup): class Kw's single member is left out of the class state;
@@ -842,6 +843,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
 __global__ void k_bitheap_clear(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev,
                                 const u32 *__restrict__ slot_map, u32 *bm, u64 w0, u64 w1, u64 w2, int NC,
                                 int L) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     const u64 nslots = (u64)NC;
     u32 *l0 = bm, *l1 = bm + nslots * w0, *l2 = bm + nslots * (w0 + w1);
@@ -869,6 +871,7 @@ __global__ void k_bitheap_clear(const u64 *__restrict__ fs, const u64 *__restric
 __global__ void __launch_bounds__(32) k_wild_setup(const u32 *__restrict__ off, const u32 *__restrict__ csr_f,
                                                    const u64 *__restrict__ fs, const u64 *__restrict__ fe,
                                                    u64 n, const u64 *n_in, int NC, int L, int enable, DevCtr *C) {
+    PDL_ENTRY();
     // T = C->wild_acc[0] (units of all requests), cmax = C->wild_acc[1] (k_alloc_prep)
     if (n_in) n = *n_in;
     const u32 lane = lane_id();
@@ -903,6 +906,7 @@ __global__ void __launch_bounds__(32) k_wild_setup(const u32 *__restrict__ off, 
 // units of each WILD request (0 otherwise), for the prefix sum
 __global__ void k_wild_flags(const u64 *__restrict__ out_u, const u64 *__restrict__ R, const DevCtr *C,
                              u32 *__restrict__ flags) {
+    PDL_ENTRY();
     const u64 n = C->wild_n;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         flags[i] = out_u[i] == WILD ? (u32)R[i] : 0u;
@@ -911,6 +915,7 @@ __global__ void k_wild_flags(const u64 *__restrict__ out_u, const u64 *__restric
 // WILD request i takes [start(w) + pre_i, + r_i); w keeps what is left
 __global__ void k_wild_apply(u64 *__restrict__ out_u, const u32 *__restrict__ pre, const DevCtr *C,
                              u64 *__restrict__ fs) {
+    PDL_ENTRY();
     const u64 n = C->wild_n;
     if (!n) return;
     const u64 w0 = C->wild_start;
@@ -922,6 +927,7 @@ __global__ void k_wild_apply(u64 *__restrict__ out_u, const u32 *__restrict__ pr
 // class-sorted records {f, start, end - 1, 0} for the CSR (one gather after the class sort)
 __global__ void k_csr_data(const u32 *__restrict__ csr_f, const u64 *__restrict__ fs, const u64 *__restrict__ fe,
                            const u64 *F_dev, uint4 *__restrict__ r4) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < F; p += (u64)gridDim.x * blockDim.x) {
         const u32 f = csr_f[p];

@@ -98,6 +98,7 @@ __device__ __forceinline__ u32 class_of_req(const Geom &g, u64 r) {
 // freed (start, end) -> key = class of its size (sizes are exact class sizes), payload = index
 __global__ void k_free_classes(const u64 *__restrict__ vs, const u64 *__restrict__ ve, const u64 *nv_dev,
                                const Geom *__restrict__ gp, u32 *__restrict__ key, u32 *__restrict__ val) {
+    PDL_ENTRY();
     __shared__ Geom g;
     if (threadIdx.x == 0) g = *gp;
     __syncthreads();
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(NT) k_free_levels(const u64 *__restrict__ old_
                                                     const u64 *__restrict__ fr, const u32 *__restrict__ fr_off,
                                                     u64 *bufL, u32 *rem, u64 *promo, u64 *tmp,
                                                     const Geom *__restrict__ gp, DevCtr *ctr) {
+    PDL_ENTRY();
     __shared__ Geom g;
     __shared__ u32 sm[33];
     __shared__ u64 ooff[MAXC + 1], loff[MAXC + 1], lcnt[MAXC + 1];
@@ -234,6 +236,7 @@ __global__ void __launch_bounds__(32, 1) k_alloc_engine(const u64 *__restrict__ 
                                                         u64 *__restrict__ out_u, u64 *__restrict__ r_out,
                                                         u64 *__restrict__ fo, u64 *__restrict__ lo_g,
                                                         u64 *__restrict__ lcnt, u64 *__restrict__ noff) {
+    PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     EngSmem &S = *reinterpret_cast<EngSmem *>(smem_raw);
     if (n_in) n = *n_in;
@@ -416,6 +419,7 @@ __global__ void __launch_bounds__(NT) k_alloc_rebuild(const u64 *__restrict__ ol
                                                       const Geom *__restrict__ gp, const DevCtr *ctr,
                                                       const u64 *__restrict__ fo, const u64 *__restrict__ lo_g,
                                                       const u64 *__restrict__ lcnt, const u64 *__restrict__ noff) {
+    PDL_ENTRY();
     const u32 t = blockIdx.x;
     if (t > gp->K) return;
     const u64 first = fo[t], end = ctr->bud_off[t + 1];
@@ -423,6 +427,7 @@ __global__ void __launch_bounds__(NT) k_alloc_rebuild(const u64 *__restrict__ ol
 }
 
 __global__ void k_alloc_commit(DevCtr *ctr, const Geom *__restrict__ gp, const u64 *__restrict__ noff) {
+    PDL_ENTRY();
     const u32 K = gp->K;
     for (u32 t = 0; t <= K; t++) {
         ctr->bud_off[t] = noff[t];
@@ -434,6 +439,7 @@ __global__ void k_alloc_commit(DevCtr *ctr, const Geom *__restrict__ gp, const u
 
 // initial lists: one root per class at most (Zeckendorf roots have distinct classes)
 __global__ void k_init_lists(DevCtr *ctr, u64 *list, const Geom *__restrict__ gp) {
+    PDL_ENTRY();
     const u32 K = gp->K;
     u64 o = 0;
     for (u32 t = 0; t <= K; t++) {

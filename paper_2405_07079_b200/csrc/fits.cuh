@@ -30,6 +30,7 @@ namespace fits {
 __global__ void k_free_classify(const u64 *__restrict__ offs, u64 n, const u64 *n_in, int alog2, u64 A_u,
                                 u32 *__restrict__ keys, u32 *__restrict__ flags, u64 *n_dev,
                                 DevCtr *ctr) {
+    PDL_ENTRY();
     __shared__ u64 sm[33];
     if (n_in) n = *n_in;   // count on the device (a hybrid heap's TLSF share)
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
@@ -60,6 +61,7 @@ __global__ void k_free_classify(const u64 *__restrict__ offs, u64 n, const u64 *
 template <typename T>
 __global__ void k_compact(const T *__restrict__ in, const u32 *__restrict__ flags,
                           const u32 *__restrict__ pos, const u64 *n_dev, T *__restrict__ out) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         if (flags[i]) out[pos[i]] = in[i];
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(256) k_free_lookup(const u32 *__restrict__ key
                                                      const u64 *__restrict__ bud_list, int K,
                                                      u32 *__restrict__ vflag, u64 *__restrict__ vs,
                                                      u64 *__restrict__ ve, DevCtr *ctr) {
+    PDL_ENTRY();
     __shared__ u64 sm[33];
     const u64 nk = *nk_dev, F = F_dev ? *F_dev : 0;
     const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
@@ -129,6 +132,7 @@ __global__ void __launch_bounds__(256) k_free_lookup(const u32 *__restrict__ key
 // head flag: element i starts a new maximal run unless the previous block ends where it starts
 __global__ void k_coal_flags(const u64 *__restrict__ ms, const u64 *__restrict__ me, const u64 *M_dev,
                              u32 *__restrict__ head) {
+    PDL_ENTRY();
     const u64 M = *M_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (u64)gridDim.x * blockDim.x)
         head[i] = (i == 0 || me[i - 1] != ms[i]) ? 1u : 0u;
@@ -138,6 +142,7 @@ __global__ void k_coal_flags(const u64 *__restrict__ ms, const u64 *__restrict__
 __global__ void k_coal_write(const u64 *__restrict__ ms, const u64 *__restrict__ me, const u64 *M_dev,
                              const u32 *__restrict__ head, const u32 *__restrict__ pos,
                              u64 *__restrict__ os, u64 *__restrict__ oe, u64 cap, DevCtr *ctr) {
+    PDL_ENTRY();
     const u64 M = *M_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (u64)gridDim.x * blockDim.x) {
         u32 h = head[i];
@@ -154,11 +159,13 @@ __global__ void k_coal_write(const u64 *__restrict__ ms, const u64 *__restrict__
 // on a logical clock ctr->lifo_clock: the valid frees of a batch are pushed in ascending address
 // order (clock + rank), an alloc's remainder at clock + request index.
 __global__ void k_free_stamps(const u64 *nv_dev, const DevCtr *ctr, u32 *__restrict__ vstamp) {
+    PDL_ENTRY();
     const u64 nv = *nv_dev, t0 = ctr->lifo_clock;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (u64)gridDim.x * blockDim.x)
         vstamp[i] = (u32)(t0 + i);
 }
 __global__ void k_clock_add(DevCtr *ctr, const u64 *n_dev, u64 n_host) {
+    PDL_ENTRY();
     ctr->lifo_clock += n_dev ? *n_dev : n_host;
     if (ctr->lifo_clock >= 0xFFFFFFF0ull) ctr->error_flags |= ERR_CAP_LIVE;   // u32 stamps exhausted
 }
@@ -166,6 +173,7 @@ __global__ void k_clock_add(DevCtr *ctr, const u64 *n_dev, u64 n_host) {
 // (freed stamps exceed every resident stamp); heads wrote their own stamp, the rest max into it
 __global__ void k_coal_stamp(const u32 *__restrict__ mt, const u64 *M_dev, const u32 *__restrict__ head,
                              const u32 *__restrict__ pos, u32 *__restrict__ ot, u64 cap) {
+    PDL_ENTRY();
     const u64 M = *M_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (u64)gridDim.x * blockDim.x) {
         const u64 run = pos[i] + head[i] - 1;
@@ -174,6 +182,7 @@ __global__ void k_coal_stamp(const u32 *__restrict__ mt, const u64 *M_dev, const
 }
 __global__ void k_coal_stamp_head(const u32 *__restrict__ mt, const u64 *M_dev, const u32 *__restrict__ head,
                                   const u32 *__restrict__ pos, u32 *__restrict__ ot, u64 cap) {
+    PDL_ENTRY();
     const u64 M = *M_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (u64)gridDim.x * blockDim.x)
         if (head[i] && pos[i] < cap) ot[pos[i]] = mt[i];
@@ -181,6 +190,7 @@ __global__ void k_coal_stamp_head(const u32 *__restrict__ mt, const u64 *M_dev, 
 // CSR key for SEGFIT_LIFO pieces: class major, newest push first
 __global__ void k_lifo_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u32 *__restrict__ ft,
                             const u64 *F_dev, u64 *__restrict__ key, u32 *__restrict__ val) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x) {
         key[i] = ((u64)cls_insert(fe[i] - fs[i], 0) << 32) | (u64)(~ft[i]);
@@ -188,6 +198,7 @@ __global__ void k_lifo_keys(const u64 *__restrict__ fs, const u64 *__restrict__ 
     }
 }
 __global__ void k_u64_hi(const u64 *__restrict__ key, const u64 *n_dev, u32 *__restrict__ out) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         out[i] = (u32)(key[i] >> 32);
@@ -198,6 +209,7 @@ __global__ void k_u64_hi(const u64 *__restrict__ key, const u64 *n_dev, u32 *__r
 // acc (optional, zeroed before): acc[0] += sum of r, acc[1] = max search class of a valid request
 __global__ void k_alloc_prep(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2, u64 A_u, int L,
                              int want_cls, u64 *__restrict__ r_out, u32 *__restrict__ c_out, u64 *acc) {
+    PDL_ENTRY();
     if (n_in) n = *n_in;
     const u64 amask = (1ull << alog2) - 1;
     u64 t = 0, cm = 0;
@@ -225,11 +237,13 @@ __global__ void k_alloc_prep(const u64 *__restrict__ sizes, u64 n, const u64 *n_
     }
 }
 
-__global__ void k_zero2(u64 *p) { p[0] = 0; p[1] = 0; }
+__global__ void k_zero2(u64 *p) {
+    PDL_ENTRY(); p[0] = 0; p[1] = 0; }
 
 // piece survives iff it still has units
 __global__ void k_piece_flags(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev,
                               u32 *__restrict__ flags) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x)
         flags[i] = fs[i] < fe[i] ? 1u : 0u;
@@ -240,6 +254,7 @@ __global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r,
                                                       u64 n, const u64 *n_in, int alog2, u64 *__restrict__ out_bytes,
                                                       u64 *__restrict__ slots, u64 tmask, u64 max_lines,
                                                       DevCtr *ctr, u64 max_live) {
+    PDL_ENTRY();
     __shared__ u64 sm[33];
     if (n_in) n = *n_in;
     const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
@@ -294,6 +309,7 @@ __global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r,
 // first level, 32 second-level classes = one word), searched with ffs.
 __global__ void k_cls_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev, int L,
                            u32 *__restrict__ key, u32 *__restrict__ val) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x) {
         key[i] = cls_insert(fe[i] - fs[i], L);
@@ -303,6 +319,7 @@ __global__ void k_cls_keys(const u64 *__restrict__ fs, const u64 *__restrict__ f
 
 // off[k] = first position in the class-sorted order whose class >= k, for k = 0..NC
 __global__ void k_cls_off(const u32 *__restrict__ key, const u64 *F_dev, int NC, u32 *__restrict__ off) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x, nth = (u64)gridDim.x * blockDim.x;
     if (F == 0) {
@@ -324,12 +341,14 @@ constexpr int MAX_NC = 1024;   // class-offset array bound (TLSF classes of 2^32
 // Level l has ceil(F / 32^l) entries; levels are stored back to back at lvl_off[l].
 __global__ void k_ff_leaves(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev,
                             u64 *__restrict__ lv0) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x)
         lv0[i] = fe[i] - fs[i];
 }
 
 __global__ void k_ff_level(const u64 *__restrict__ below, u64 *__restrict__ above, const u64 *F_dev, int l) {
+    PDL_ENTRY();
     u64 nb = *F_dev;
     for (int i = 1; i < l; i++) nb = (nb + 31) >> 5;
     const u64 na = (nb + 31) >> 5;
@@ -352,6 +371,7 @@ constexpr int FF_MAX_LEVELS = 8;
 __global__ void __launch_bounds__(32) k_ff_engine(u64 *tree, const u64 *__restrict__ lvl_off, int nlev,
                                                   u64 *fs, const u64 *F_dev, const u64 *__restrict__ r, u64 n,
                                                   const u64 *n_in, u64 *__restrict__ out_u, u64 *rover) {
+    PDL_ENTRY();
     const u32 lane = lane_id();
     if (n_in) n = *n_in;
     u64 sz[FF_MAX_LEVELS];
@@ -453,6 +473,7 @@ __global__ void __launch_bounds__(32) k_ff_engine(u64 *tree, const u64 *__restri
 // The array lives in shared memory when it fits, otherwise in global memory.
 __global__ void k_bf_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev, int FB,
                           u64 *__restrict__ key) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x)
         key[i] = ((fe[i] - fs[i]) << FB) | i;
@@ -580,6 +601,7 @@ __device__ __forceinline__ void bf_pos_remove(BfSmem &S, u32 i) {
 __global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
                                                   const u64 *__restrict__ r, u64 n, const u64 *n_in,
                                                   u64 *__restrict__ out_u) {
+    PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char bf_raw[];
     BfSmem &S = *reinterpret_cast<BfSmem *>(bf_raw);
     if (n_in) n = *n_in;
@@ -682,6 +704,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(32) k_bf_engine_flat(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
                                                        const u64 *__restrict__ r, u64 n, const u64 *n_in,
                                                        u64 *__restrict__ out_u) {
+    PDL_ENTRY();
     extern __shared__ u64 skeys[];
     if (n_in) n = *n_in;
     const u32 lane = lane_id();

@@ -278,6 +278,8 @@ struct heap {
     int wild_split;          // TLSF/SEGFIT wilderness split (engine_tlsf.cuh); env HEAP_WILD_SPLIT=0 disables
     int bf_flat;             // BEST_FIT: the flat one-array engine instead of the blocked one (env HEAP_BF_FLAT=1)
     int micro;               // small heap: each batch is one single-CTA launch (micro.cuh); env HEAP_MICRO=0 disables
+    int pdl;                 // programmatic dependent launches (env HEAP_PDL=0 disables)
+    int bud_levels;          // BUDDY free phase: the level-by-level kernel instead of the parallel form (env HEAP_BUDDY_LEVELS=1)
     Layout L;
     void *ws;
     size_t ws_bytes;
@@ -338,12 +340,30 @@ cudaEvent_t prof_event(heap *h) {
 }
 }  // namespace
 
+// programmatic dependent launch (common.cuh PDL_ENTRY): the launch attribute lets this kernel be
+// scheduled while the previous one drains; the kernel itself waits for its completion
+template <typename... P, typename... A>
+static void launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
+
 #define LAUNCH(h, kern, grid, block, smem, stream, ...)                                   \
     do {                                                                                  \
         bool _p = ((h)->prof_mask >> (h)->tag) & 1;                                       \
         heap::Rec _r{(h)->tag, nullptr, nullptr};                                         \
         if (_p) { _r.a = prof_event(h); _r.b = prof_event(h); cudaEventRecord(_r.a, (cudaStream_t)(stream)); } \
-        kern<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__);             \
+        if ((h)->pdl) launch_pdl((kern), (grid), (block), (smem), (cudaStream_t)(stream), __VA_ARGS__); \
+        else kern<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__);        \
         if (_p) { cudaEventRecord(_r.b, (cudaStream_t)(stream)); (h)->recs.push_back(_r); } \
         (h)->launches++;                                                                  \
     } while (0)
@@ -352,6 +372,7 @@ cudaEvent_t prof_event(heap *h) {
 namespace {
 
 __global__ void k_init(DevCtr *ctr, u64 *tbl, u64 tcap, u64 *fs, u64 *fe, u64 A_u, int buddy, int K) {
+    PDL_ENTRY();
     const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x, nth = (u64)gridDim.x * blockDim.x;
     for (u64 i = tid; i < tcap; i += nth) tbl[i] = table::EMPTY;
     if (tid == 0) {
@@ -410,16 +431,19 @@ void scan(heap *h, const u32 *in, u32 *out, const u64 *n_dev, u64 *total, cudaSt
 }
 
 __global__ void k_set_F(DevCtr *ctr) {
+    PDL_ENTRY();
     ctr->F = ctr->tmp[1];
     if (ctr->eng[2]) ctr->error_flags |= ERR_ENGINE;   // engine watchdog fired: results invalid
 }
 
 // ---- table rebuild (tombstone purge), each kernel a no-op unless the flag is set ----
 __global__ void k_rb_check(DevCtr *ctr, u64 thresh) {
+    PDL_ENTRY();
     ctr->tmp[4] = (ctr->tbl_used > thresh) ? 1 : 0;
     ctr->tmp[5] = 0;
 }
 __global__ void k_rb_collect(DevCtr *ctr, const u64 *tbl, u64 tcap, u64 *scratch) {
+    PDL_ENTRY();
     if (!ctr->tmp[4]) return;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x) {
         u64 v = tbl[i];
@@ -427,11 +451,13 @@ __global__ void k_rb_collect(DevCtr *ctr, const u64 *tbl, u64 tcap, u64 *scratch
     }
 }
 __global__ void k_rb_clear(const DevCtr *ctr, u64 *tbl, u64 tcap) {
+    PDL_ENTRY();
     if (!ctr->tmp[4]) return;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
         tbl[i] = table::EMPTY;
 }
 __global__ void k_rb_insert(DevCtr *ctr, u64 *tbl, u64 tmask, u64 max_lines, const u64 *scratch) {
+    PDL_ENTRY();
     if (!ctr->tmp[4]) return;
     const u64 n = ctr->tmp[5];
     const u32 g = lane_id() >> 3;
@@ -459,6 +485,7 @@ void maybe_rebuild(heap *h, cudaStream_t s) {
 __global__ void __launch_bounds__(1024) k_stats(const DevCtr *ctr, const u64 *fs, const u64 *fe, int buddy, int K,
                                                 u64 arena, u64 align, int alog2, u64 meta, heap_stats_t *out,
                                                 const u64 *fibS) {
+    PDL_ENTRY();
     __shared__ u64 sm[33];
     u64 nfree, fu = 0, big = 0;
     if (!buddy) {
@@ -507,6 +534,7 @@ __global__ void __launch_bounds__(1024) k_stats(const DevCtr *ctr, const u64 *fs
 
 // ---- export ----
 __global__ void k_export_free(const u64 *fs, const u64 *fe, const u64 *F_dev, int alog2, u64 *pairs, u64 cap) {
+    PDL_ENTRY();
     const u64 F = *F_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F && i < cap; i += (u64)gridDim.x * blockDim.x) {
         pairs[2 * i] = fs[i] << alog2;
@@ -514,6 +542,7 @@ __global__ void k_export_free(const u64 *fs, const u64 *fe, const u64 *F_dev, in
     }
 }
 __global__ void k_bud_keys(const u64 *list, const DevCtr *ctr, int K, u32 *key, u32 *val) {
+    PDL_ENTRY();
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < ctr->bud_total; i += (u64)gridDim.x * blockDim.x) {
         int t = 0;
         while (t < K && ctr->bud_off[t + 1] <= i) t++;
@@ -523,6 +552,7 @@ __global__ void k_bud_keys(const u64 *list, const DevCtr *ctr, int K, u32 *key, 
 }
 __global__ void k_export_pairs_u32(const u32 *key, const u32 *val, const u64 *n_dev, int alog2, int val_is_order,
                                    u64 *pairs, u64 cap, const u64 *fibS = nullptr) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n && i < cap; i += (u64)gridDim.x * blockDim.x) {
         pairs[2 * i] = (u64)key[i] << alog2;
@@ -531,11 +561,13 @@ __global__ void k_export_pairs_u32(const u32 *key, const u32 *val, const u64 *n_
     }
 }
 __global__ void k_tbl_flags(const u64 *tbl, u64 tcap, u32 *flags) {
+    PDL_ENTRY();
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
         flags[i] = table::is_live(tbl[i]) ? 1u : 0u;
 }
 __global__ void k_tbl_compact(const u64 *tbl, u64 tcap, const u32 *flags, const u32 *pos, u32 *key, u32 *val,
                               u64 cap) {
+    PDL_ENTRY();
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
         if (flags[i] && pos[i] < cap) {
             u64 v = tbl[i];
@@ -543,8 +575,10 @@ __global__ void k_tbl_compact(const u64 *tbl, u64 tcap, const u32 *flags, const 
             val[pos[i]] = (u32)(v & 0xFFFFFFFFull);
         }
 }
-__global__ void k_set_u64(u64 *p, u64 v) { *p = v; }
-__global__ void k_clamp(const u64 *in, u64 *out, u64 cap) { *out = *in < cap ? *in : cap; }
+__global__ void k_set_u64(u64 *p, u64 v) {
+    PDL_ENTRY(); *p = v; }
+__global__ void k_clamp(const u64 *in, u64 *out, u64 cap) {
+    PDL_ENTRY(); *out = *in < cap ? *in : cap; }
 
 }  // namespace
 
@@ -576,6 +610,10 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->wild_split = (ws && ws[0] == '0') ? 0 : 1;
         const char *bf = getenv("HEAP_BF_FLAT");
         h->bf_flat = (bf && bf[0] == '1') ? 1 : 0;
+        const char *pd = getenv("HEAP_PDL");
+        h->pdl = (pd && pd[0] == '0') ? 0 : 1;
+        const char *bl = getenv("HEAP_BUDDY_LEVELS");
+        h->bud_levels = (bl && bl[0] == '1') ? 1 : 0;
         const char *mi = getenv("HEAP_MICRO");
         const bool fitp = policy == HEAP_FIRST_FIT || policy == HEAP_NEXT_FIT || policy == HEAP_BEST_FIT ||
                           policy == HEAP_SEGFIT || policy == HEAP_TLSF;
@@ -834,6 +872,30 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
     } else {
         // 4b. group freed blocks by order, 5b. level-by-level buddy merge
         TAG(h, HEAP_TAG_BUDDY_FREE);
+        if (!fibp && !h->bud_levels) {
+            // parallel form (buddy.cuh): old blocks in address order, merged with the freed ones,
+            // coalesced into maximal runs, each run's greedy decomposition grouped by order
+            const int abits = ilog2(L.A_u - 1 > 0 ? L.A_u - 1 : 1) + 1;
+            LAUNCH(h, buddy::k_bud_keys, h->G, 256, 0, s, h->fs[cur], C, h->kA, h->vA);
+            const int r1 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->bud_total, abits, s);
+            LAUNCH(h, buddy::k_bud_unpack, h->G, 256, 0, s, h->fs[cur], r1 ? h->vB : h->vA, C, L.K, h->bufA, h->bufB);
+            LAUNCH(h, prims::k_merge, h->G, prims::NT, 0, s, h->bufA, h->bufB, &C->bud_total, h->vsc, h->vec, &C->nv,
+                   h->ms, h->me, &C->M, (const u32 *)nullptr, (const u32 *)nullptr, (u32 *)nullptr);
+            LAUNCH(h, fits::k_coal_flags, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags);
+            scan(h, h->flags, h->pos, &C->M, &C->tmp[2], s);
+            LAUNCH(h, fits::k_coal_write, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags, h->pos, h->bufA, h->bufB,
+                   L.bud_cap, C);
+            LAUNCH(h, buddy::k_bud_count, h->G, 256, 0, s, h->bufA, h->bufB, &C->tmp[2], h->flags);
+            scan(h, h->flags, h->pos, &C->tmp[2], &C->tmp[3], s);
+            LAUNCH(h, buddy::k_bud_write, h->G, 256, 0, s, h->bufA, h->bufB, &C->tmp[2], h->pos, h->promo, h->kA,
+                   h->vA, L.cap_f, C);
+            const int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[3], 8, s);
+            LAUNCH(h, buddy::k_bud_lists, h->G, 256, 0, s, r2 ? h->vB : h->vA, &C->tmp[3], h->promo, h->fs[nxt]);
+            LAUNCH(h, buddy::k_bud_offsets, 1, 64, 0, s, r2 ? h->kB : h->kA, &C->tmp[3], L.K, C);
+            h->cur = nxt;
+            if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+            return HEAP_OK;
+        }
         if (fibp) LAUNCH(h, fib::k_free_classes, h->G, 256, 0, s, h->vsc, h->vec, &C->nv, h->fgeom, h->kA, h->vA);
         else LAUNCH(h, buddy::k_free_orders, h->G, 256, 0, s, h->vsc, h->vec, &C->nv, h->kA, h->vA);
         int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->nv, 8, s);
@@ -1063,7 +1125,8 @@ static int batch_alloc(heap *h, const uint64_t *in, uint64_t *out, uint64_t n, c
 // stages the caller's request words into the workspace, the captured batch runs on the staging
 // buffers with a device-side count, and (alloc) a memcpy node copies the results out.  Each call
 // only patches those three nodes and launches the graph: one launch instead of dozens.
-__global__ void k_set_req_n(DevCtr *ctr, u64 n) { ctr->req_n = n; }
+__global__ void k_set_req_n(DevCtr *ctr, u64 n) {
+    PDL_ENTRY(); ctr->req_n = n; }
 
 #define GRAPH_TRY(x)                                                                       \
     do {                                                                                   \
@@ -1336,7 +1399,8 @@ int heap_export(heap_t *h, uint64_t *d_free_pairs, uint64_t cap_free, uint64_t *
     int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[3], 32, s);
     u32 *k = rb ? h->kB : h->kA, *v = rb ? h->vB : h->vA;
     if (d_live_pairs && cap_live)
-        LAUNCH(h, k_export_pairs_u32, h->G, 256, 0, s, k, v, &C->tmp[3], alog, 0, (u64 *)d_live_pairs, cap_live);
+        LAUNCH(h, k_export_pairs_u32, h->G, 256, 0, s, k, v, &C->tmp[3], alog, 0, (u64 *)d_live_pairs, cap_live,
+               (const u64 *)nullptr);
     CUDA_TRY(cudaMemcpyAsync(&counts[1], &C->tmp[7], 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(MT, 1) k_micro_free(const u64 *__restrict__ of
                                                       const u64 *__restrict__ fe_in, u64 *__restrict__ fs_out,
                                                       u64 *__restrict__ fe_out, u64 *__restrict__ tbl, u64 tmask,
                                                       u64 max_lines, u64 cap_f, DevCtr *ctr) {
+    PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char dyn[];
     u32 *ps = reinterpret_cast<u32 *>(dyn);          // free array (units), F entries
     u32 *pe = ps + MICRO_F;
@@ -280,6 +281,7 @@ __global__ void __launch_bounds__(MT, 1) k_micro_alloc(const u64 *__restrict__ s
                                                        u64 *__restrict__ fe_out, u64 *__restrict__ out_bytes,
                                                        u64 *__restrict__ tbl, u64 tmask, u64 max_lines, u64 tcap,
                                                        u64 *__restrict__ scratch, DevCtr *ctr, u64 max_live) {
+    PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char dyn[];
     u32 *rr = reinterpret_cast<u32 *>(dyn);          // request units (0: fails)
     u32 *res = rr + MICRO_N;                         // result (unit offset) or NONE

@@ -73,6 +73,7 @@ __device__ __forceinline__ u32 pred(const Lbm &b, u64 x) {
 
 // set the live-start bit of every successful allocation (alloc phase: sets only)
 __global__ void k_set_bits(const u64 *__restrict__ out_u, u64 n, const u64 *n_in, Lbm b) {
+    PDL_ENTRY();
     if (n_in) n = *n_in;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         u64 p = out_u[i];
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(256) k_resolve(const u32 *__restrict__ keys, c
                                                  const u64 *__restrict__ fstart, const u64 *F_dev,
                                                  u32 *__restrict__ kind, u32 *__restrict__ own,
                                                  u64 *__restrict__ endu, DevCtr *ctr) {
+    PDL_ENTRY();
     const u64 nk = *nk_dev, F = *F_dev;
     const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(256) k_apply(const u32 *__restrict__ keys, con
                                                const u64 *endu, u64 *__restrict__ slots, u64 tmask,
                                                u64 max_lines, Lbm b, u32 *__restrict__ vflag, u64 *vs,
                                                u64 *__restrict__ ve, DevCtr *ctr) {
+    PDL_ENTRY();
     __shared__ u64 sm[33];
     const u64 nk = *nk_dev;
     const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;

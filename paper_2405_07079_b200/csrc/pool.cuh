@@ -62,6 +62,7 @@ __device__ __forceinline__ u32 valid_mask(const Geom &G, int j, u64 w) {
 
 // every slot free, superblock counts, per-pool free counts
 __global__ void k_init(Geom G, u32 *bits, u32 *sbcnt, Ctr *c) {
+    PDL_ENTRY();
     const u64 nth = (u64)gridDim.x * blockDim.x;
     for (u64 w = (u64)blockIdx.x * blockDim.x + threadIdx.x; w < G.nwords; w += nth) {   // nwords % 32 == 0
         const u32 m = valid_mask(G, pool_of_word(G, w), w);
@@ -80,6 +81,7 @@ __global__ void k_init(Geom G, u32 *bits, u32 *sbcnt, Ctr *c) {
 // (atomicOr: exactly one copy of an allocated slot sees it clear); the rest go to the TLSF heap
 __global__ void __launch_bounds__(256) k_free(const u64 *__restrict__ offs, u64 n, const u64 *n_in, Geom G, u32 *bits,
                                               u32 *sbcnt, Ctr *c, u32 *__restrict__ flags, u64 *__restrict__ toff) {
+    PDL_ENTRY();
     __shared__ u64 s_cnt[5 + 2 * MAXJ];      // null, ok, invalid, double, live_b, pfree[J]
     if (n_in) n = *n_in;
     for (int t = threadIdx.x; t < 5 + 2 * MAXJ; t += blockDim.x) s_cnt[t] = 0;
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(256) k_free(const u64 *__restrict__ offs, u64 
 // key = pool class j for 0 < s < PAGE (smallest pool whose objects hold s), J for the TLSF heap
 __global__ void k_keys(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, Geom G, u32 *__restrict__ key,
                        u32 *__restrict__ val, Ctr *c) {
+    PDL_ENTRY();
     if (n_in) n = *n_in;
     if (blockIdx.x == 0 && threadIdx.x == 0) c->nreq = n;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
@@ -154,6 +157,7 @@ __global__ void k_keys(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, Ge
 
 // how many requests each pool serves: min(requests of class j, free slots of pool j)
 __global__ void k_take(const u32 *__restrict__ coff, Geom G, Ctr *c) {
+    PDL_ENTRY();
     u64 ok = 0, lb = 0;
     for (int j = 0; j < G.J; j++) {
         const u64 m = coff[j + 1] - coff[j];
@@ -173,6 +177,7 @@ __global__ void k_take(const u32 *__restrict__ coff, Geom G, Ctr *c) {
 __global__ void __launch_bounds__(256) k_select(Geom G, u32 *bits, u32 *sbcnt, const u32 *__restrict__ sbpre,
                                                 const u32 *__restrict__ coff, const u32 *__restrict__ sval,
                                                 Ctr *c, u64 *__restrict__ out) {
+    PDL_ENTRY();
     const u32 lane = lane_id();
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
     u64 hw = 0;
@@ -211,6 +216,7 @@ __global__ void __launch_bounds__(256) k_select(Geom G, u32 *bits, u32 *sbcnt, c
 // requests the pools do not serve, flagged by request index (class J, or rank past the take)
 __global__ void k_tl_flags(const u32 *__restrict__ skey, const u32 *__restrict__ sval, const u32 *__restrict__ coff,
                            const u64 *n_dev, Geom G, const Ctr *c, u32 *__restrict__ flags) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (u64)gridDim.x * blockDim.x) {
         const u32 k = skey[p];
@@ -220,6 +226,7 @@ __global__ void k_tl_flags(const u32 *__restrict__ skey, const u32 *__restrict__
 // compact the TLSF share of the requests (request order kept) with their request index
 __global__ void k_tl_compact(const u64 *__restrict__ sizes, const u32 *__restrict__ flags, const u32 *__restrict__ pos,
                              const u64 *n_dev, u64 *__restrict__ tsz, u32 *__restrict__ tidx) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         if (flags[i]) { tsz[pos[i]] = sizes[i]; tidx[pos[i]] = (u32)i; }
@@ -227,6 +234,7 @@ __global__ void k_tl_compact(const u64 *__restrict__ sizes, const u32 *__restric
 // TLSF results back to request order, shifted by the pools' extent
 __global__ void k_tl_scatter(const u64 *__restrict__ tout, const u32 *__restrict__ tidx, const u64 *n_dev, u64 base,
                              u64 *__restrict__ out) {
+    PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (u64)gridDim.x * blockDim.x) {
         const u64 o = tout[k];
@@ -248,6 +256,7 @@ __device__ __forceinline__ void word_marks(const Geom &G, const u32 *bits, u64 w
 }
 // per-word counts (runs, live slots) for the scans; grand totals into c->runs / c->nlive_out
 __global__ void k_marks(Geom G, const u32 *bits, u32 *__restrict__ nrun, u32 *__restrict__ nlive, Ctr *c) {
+    PDL_ENTRY();
     u64 r = 0, l = 0;
     for (u64 w = (u64)blockIdx.x * blockDim.x + threadIdx.x; w < G.nwords; w += (u64)gridDim.x * blockDim.x) {
         u32 st, en, lv;
@@ -263,6 +272,7 @@ __global__ void k_marks(Geom G, const u32 *bits, u32 *__restrict__ nrun, u32 *__
 // export: run k -> (start, end) then (start, size); live slot -> (offset, object size)
 __global__ void k_emit(Geom G, const u32 *bits, const u32 *__restrict__ prun, const u32 *__restrict__ plive,
                        u64 *fpairs, u64 cap_f, u64 *lpairs, u64 cap_l) {
+    PDL_ENTRY();
     for (u64 w = (u64)blockIdx.x * blockDim.x + threadIdx.x; w < G.nwords; w += (u64)gridDim.x * blockDim.x) {
         u32 st, en, lv;
         word_marks(G, bits, w, st, en, lv);
@@ -283,10 +293,12 @@ __global__ void k_emit(Geom G, const u32 *bits, const u32 *__restrict__ prun, co
     }
 }
 __global__ void k_end_to_size(u64 *fpairs, u64 n) {
+    PDL_ENTRY();
     for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (u64)gridDim.x * blockDim.x)
         fpairs[2 * k + 1] -= fpairs[2 * k];
 }
 __global__ void k_shift_pairs(u64 *pairs, u64 n, u64 base) {
+    PDL_ENTRY();
     for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (u64)gridDim.x * blockDim.x)
         pairs[2 * k] += base;
 }
@@ -294,6 +306,7 @@ __global__ void k_shift_pairs(u64 *pairs, u64 n, u64 base) {
 // TLSF heap's; the pools' free runs count as free blocks)
 __global__ void k_stats(const heap_stats_t *sub, const Ctr *c, Geom G, u64 arena, u64 align, u64 meta,
                         heap_stats_t *out) {
+    PDL_ENTRY();
     const u64 live = c->live_b + sub->live_bytes;
     out->arena_bytes = arena;
     out->align = align;

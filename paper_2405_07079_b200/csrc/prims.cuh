@@ -72,6 +72,7 @@ __device__ __forceinline__ u32 lookback(u64 *flags, u64 stride, u64 t, u32 tag, 
 template <typename K>
 __global__ void __launch_bounds__(OS_NT) k_os_hist(const K *__restrict__ keys, const u64 *n_dev, int passes,
                                                    DevCtr *ctr) {
+    PDL_ENTRY();
     __shared__ u32 h[8][256];
     __shared__ u32 s_last, sm[33];
     const u64 n = *n_dev;
@@ -106,6 +107,7 @@ template <typename K, bool HV>
 __global__ void __launch_bounds__(OS_NT) k_os_scatter(const K *__restrict__ kin, const u32 *__restrict__ vin,
                                                       K *__restrict__ kout, u32 *__restrict__ vout,
                                                       const u64 *n_dev, int pass, u64 *flags, DevCtr *ctr) {
+    PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char os_dyn[];   // os_smem<K, HV>() bytes
     K *ks = reinterpret_cast<K *>(os_dyn);
     u32 *vs = reinterpret_cast<u32 *>(os_dyn + OS_TILE * sizeof(K));
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(OS_NT) k_os_scatter(const K *__restrict__ kin,
 // tile counter and bumps the epoch for the next call.  in == out is allowed.
 __global__ void __launch_bounds__(OS_NT) k_scan_1p(const u32 *in, u32 *out, const u64 *n_dev, u64 *total,
                                                    u64 *flags, DevCtr *ctr) {
+    PDL_ENTRY();
     __shared__ u32 sm[33];
     __shared__ u32 s_tile, s_pre;
     const u64 n = *n_dev, nt = os_ntiles(n);
@@ -227,6 +230,7 @@ __global__ void __launch_bounds__(NT) k_merge(const u64 *__restrict__ as, const 
                                               u64 *__restrict__ os, u64 *__restrict__ oe, u64 *total,
                                               const u32 *__restrict__ at = nullptr,
                                               const u32 *__restrict__ bt = nullptr, u32 *__restrict__ ot = nullptr) {
+    PDL_ENTRY();
     // at/bt/ot: optional per-block payload merged alongside (push stamps of SEGFIT_LIFO)
     const u64 na = *na_dev, nb = *nb_dev, n = na + nb;
     if (blockIdx.x == 0 && threadIdx.x == 0 && total) *total = n;

@@ -305,6 +305,29 @@ def test_micro_and_general_paths(case, pol, micro, monkeypatch):
     run_parity(cfg, max_live=4096, max_batch=batch, every_batch_state=True)
 
 
+BUDDY_CASES = [
+    # (policy, arena, align, batch, ops, sizes, rho)
+    (tg.BUDDY, 1 << 16, 16, 24, 1500, (0, 8), (1, 2)),
+    (tg.BUDDY, 1 << 24, 64, 3000, 40000, (6, 16), (1, 2)),
+    (tg.BUDDY, (1 << 20) + (1 << 14) + 256, 256, 700, 9000, (8, 18), (1, 2)),   # several roots
+    (tg.BUDDY, (1 << 30) + (1 << 23) + (1 << 12), 256, 8192, 120000, (8, 24), (1, 2)),
+    (tg.DOUBLE_BUDDY, (1 << 24) + 4096, 64, 3000, 40000, (6, 16), (2, 5)),
+]
+
+
+@pytest.mark.parametrize("levels", ["0", "1"], ids=["parallel", "levels"])
+@pytest.mark.parametrize("case", BUDDY_CASES, ids=lambda c: f"p{c[0]}-A{c[1]}-B{c[3]}")
+def test_buddy_free_forms(case, levels, monkeypatch):
+    """Binary-buddy free phase in its parallel form (runs of free space decomposed greedily into
+    maximal aligned blocks, buddy.cuh k_bud_*) and in the level-by-level form (k_free_levels):
+    both bit-exact with Oracle-L, state compared after every batch."""
+    monkeypatch.setenv("HEAP_BUDDY_LEVELS", levels)
+    pol, arena, align, batch, ops, sizes, rho = case
+    kind = 1 if pol == tg.BUDDY else 0
+    cfg = tg.custom(pol, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes, size_kind=kind, idx=20 + pol)
+    run_parity(cfg, max_live=max(1 << 15, 8 * batch), max_batch=batch, every_batch_state=True)
+
+
 def test_invariants_config3_prefix():
     cfg = tg.CONFIGS[3]
     g, _ = run_parity(cfg, cfg.max_live, cfg.batch, max_batches=10)
