@@ -374,21 +374,30 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
     PDL_ENTRY();
     __shared__ u64 ooff[41];
     __shared__ u64 doff[42], boff[42];
-    __shared__ u64 s_nb;
+    __shared__ u32 ro[42];
     if (threadIdx.x <= (unsigned)K + 1) ooff[threadIdx.x] = ctr->bud_off[threadIdx.x];
-    if (threadIdx.x == 0) { doff[0] = 0; boff[0] = 0; s_nb = 0; }
+    if (threadIdx.x <= (unsigned)K + 2) ro[threadIdx.x] = req_off[threadIdx.x];
     __syncthreads();
     // requests of the fail bucket
-    for (u64 i = req_off[K + 1] + threadIdx.x; i < req_off[K + 2]; i += NT) out_u[req[i]] = FAIL;
+    for (u64 i = ro[K + 1] + threadIdx.x; i < ro[K + 2]; i += NT) out_u[req[i]] = FAIL;
     // ---- bottom-up ----
+    // The level scalars (borrows in, demand / borrow offsets) are uniform: every thread keeps them
+    // in registers, so a level costs two barriers (staged inputs, merged demands) and a level with
+    // no demand none.
+    u64 nb = 0, dacc = 0, bacc = 0;
     for (int t = 0; t <= K; t++) {
         const u64 n_t = ooff[t + 1] - ooff[t];
-        const u64 nr = req_off[t + 1] - req_off[t];
-        const u32 *rq = req + req_off[t];
-        const u64 nb = s_nb;        // borrows from t-1 (already in btm/bsrc)
-        u32 *Dt = dtm + doff[t], *Ds = dsrc + doff[t];
-        // direct requests: time = request index, src = request index
-        // merge (rq, rq) with (btm, bsrc); staged in shared memory when the level fits
+        const u64 nr = ro[t + 1] - ro[t];
+        const u64 nd = nr + nb;
+        const u64 x = nd > n_t ? nd - n_t : 0;
+        const u64 nbor = (t < K) ? (x + 1) / 2 : 0;
+        if (threadIdx.x == 0) { doff[t] = dacc; boff[t] = bacc; }
+        if (nd == 0) { nb = 0; continue; }
+        const u32 *rq = req + ro[t];
+        u32 *Dt = dtm + dacc, *Ds = dsrc + dacc;
+        // direct requests: time = request index, src = request index; merged by time with the
+        // borrows from t-1 (btm, bsrc); staged in shared memory when the level fits, and then the
+        // merge itself writes the borrows to t+1: borrow j carries the time of demand n_t + 2j
         if (nr + 2 * nb <= (u64)ALLOC_CAP) {
             extern __shared__ u32 astage[];
             u32 *sr = astage, *st = astage + nr, *ss = astage + nr + nb;
@@ -396,41 +405,64 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
             cta_copy(st, btm, nb);
             cta_copy(ss, bsrc, nb);
             __syncthreads();
-            cta_merge_tm(sr, sr, nr, st, ss, nb, Dt, Ds);
+            const u64 per = (nd + NT - 1) / NT;
+            const u64 diag = (u64)threadIdx.x * per;
+            if (diag < nd) {
+                u64 lo = diag > nb ? diag - nb : 0, hi = diag < nr ? diag : nr;
+                while (lo < hi) {
+                    const u64 mid = (lo + hi) >> 1;
+                    if (sr[mid] <= st[diag - mid - 1]) lo = mid + 1; else hi = mid;
+                }
+                u64 i = lo, j = diag - lo;
+                for (u64 k = 0; k < per && diag + k < nd; k++) {
+                    const u64 o = diag + k;
+                    const bool ta = (j >= nb) || (i < nr && sr[i] <= st[j]);
+                    const u32 tm = ta ? sr[i] : st[j];
+                    const u32 sc = ta ? sr[i] : ss[j];
+                    if (ta) i++; else j++;
+                    Dt[o] = tm;
+                    Ds[o] = sc;
+                    if (o >= n_t && !((o - n_t) & 1)) {
+                        const u64 bj = (o - n_t) >> 1;
+                        if (bj < nbor) { btm[bj] = tm; bsrc[bj] = (u32)bj | BORROW; }
+                    }
+                }
+            }
+            __syncthreads();
         } else {
             cta_merge_tm(rq, rq, nr, btm, bsrc, nb, Dt, Ds);
-        }
-        __syncthreads();
-        const u64 nd = nr + nb;
-        const u64 x = nd > n_t ? nd - n_t : 0;
-        const u64 nbor = (t < K) ? (x + 1) / 2 : 0;
-        for (u64 base = 0; base < nbor; base += 8 * NT) {
-            u32 v[8];
+            __syncthreads();
+            for (u64 base = 0; base < nbor; base += 8 * NT) {
+                u32 v[8];
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const u64 j = base + (u64)k * NT + threadIdx.x;
-                v[k] = j < nbor ? Dt[n_t + 2 * j] : 0u;
-            }
+                for (int k = 0; k < 8; k++) {
+                    const u64 j = base + (u64)k * NT + threadIdx.x;
+                    v[k] = j < nbor ? Dt[n_t + 2 * j] : 0u;
+                }
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const u64 j = base + (u64)k * NT + threadIdx.x;
-                if (j < nbor) { btm[j] = v[k]; bsrc[j] = (u32)j | BORROW; }
+                for (int k = 0; k < 8; k++) {
+                    const u64 j = base + (u64)k * NT + threadIdx.x;
+                    if (j < nbor) { btm[j] = v[k]; bsrc[j] = (u32)j | BORROW; }
+                }
             }
+            __syncthreads();
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            doff[t + 1] = doff[t] + nd;
-            boff[t + 1] = boff[t] + nbor;
-            s_nb = nbor;
-        }
-        __syncthreads();
+        dacc += nd;
+        bacc += nbor;
+        nb = nbor;
     }
+    if (threadIdx.x == 0) { doff[K + 1] = dacc; boff[K + 1] = bacc; }
+    __syncthreads();
     // ---- top-down ----
     __shared__ u64 s_left[41], s_cnt[41];
     for (int t = K; t >= 0; t--) {
         const u64 n_t = ooff[t + 1] - ooff[t];
-        const u64 *blk = old_list + ooff[t];
         const u64 nd = doff[t + 1] - doff[t];
+        if (nd == 0) {                      // no demand: the level keeps its blocks, nothing moves
+            if (threadIdx.x == 0) { s_left[t] = FAIL; s_cnt[t] = n_t; }
+            continue;
+        }
+        const u64 *blk = old_list + ooff[t];
         const u32 *Ds = dsrc + doff[t];
         const u64 *bad = baddr + boff[t];   // borrows of order t (served by t+1)
         const u64 nbor = boff[t + 1] - boff[t];
@@ -467,6 +499,7 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         }
         __syncthreads();
     }
+    __syncthreads();
     // ---- new per-order lists: surviving batch-start blocks, or the one leftover ----
     __shared__ u64 noff[42];
     if (threadIdx.x == 0) {
