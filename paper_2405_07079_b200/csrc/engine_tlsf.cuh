@@ -55,8 +55,25 @@ namespace tlsfw {
 #ifndef H_DEF
 #define H_DEF 8
 #endif
-constexpr int H = H_DEF;          // head-cache depth per class (power of two)
+constexpr int H = H_DEF;          // head-cache depth of the classes below HOT (power of two)
 constexpr int REFILL_AT = REFILL_AT_DEF;      // refill a class's cache when it holds fewer members
+#ifndef HOT_DEF
+#define HOT_DEF 256
+#endif
+#ifndef HL_DEF
+#define HL_DEF 4
+#endif
+// Classes at and above HOT (pieces of >= 2^13 units at SL_LOG2 = 5, above every request's search
+// class of config 5) are reached only when everything below is empty and hold few members: they
+// keep a depth-HL cache.  The shared memory this saves (162 -> 118 KB) goes to the L1 carveout,
+// which the chain's global accesses (CSR records, overflow words, piece data) hit: measured +6.4 %
+// engine time per 40 KB of extra shared memory; net of the per-class depth arithmetic, HL = 4 is
+// 1.3 % faster than one depth for all classes and HL = 2 2 % slower (config 5, batches 10-11).
+constexpr int HOT = HOT_DEF;
+constexpr int HL = HL_DEF;
+__device__ __forceinline__ u32 hbase(u32 k) { return k < (u32)HOT ? k * H : HOT * H + (k - HOT) * HL; }
+__device__ __forceinline__ u32 hmask(u32 k) { return k < (u32)HOT ? H - 1 : HL - 1; }
+__device__ __forceinline__ u32 hrefill(u32 k) { return k < (u32)HOT ? (u32)REFILL_AT : (u32)HL; }
 #ifndef FILL_TO_DEF
 #define FILL_TO_DEF H_DEF
 #endif
@@ -78,7 +95,7 @@ struct Smem {
     u32 ptr[MAX_NC], endp[MAX_NC], cnt[MAX_NC], root[MAX_NC], slot[MAX_NC];
     u32 nslot;
     u32 ow_i[MAX_NC], ow_v[MAX_NC];   // cached overflow word per class (see Heap)
-    uint4 hc[MAX_NC * H];         // cached member {f (| HEAPBIT when it came from the overflow set),
+    uint4 hc[HOT * H + (MAX_NC - HOT) * HL];   // cached member {f (| HEAPBIT when it came from the overflow set),
                                   //  current start, end - 1 (units; ends can be 2^32), 0}
     unsigned char hn[MAX_NC];
     unsigned char hb[MAX_NC];     // ring-buffer base of the cache (entry j at (hb + j) % H)
@@ -91,6 +108,9 @@ struct Smem {
     u32 res_f[32], res_nk[32], res_flag[32], res_e[32];
     u64 ch_i[32], ch_r[32];       // the chunk's requests (index, units), lane = time order
     u32 ch_c[32];
+#ifdef SMEM_PAD
+    u32 pad_[SMEM_PAD];           // experiment: shared memory taken from the L1 carveout
+#endif
     u64 dkey[32];                 // the chunk's droppers in time order: (drop class << 32 | f) ...
     u32 dlane[32];                // ... and their lanes (the dirty check reads them as broadcasts)
 };
@@ -215,11 +235,11 @@ struct Csr {
     const uint4 *r4;   // class-sorted {f, batch-start start, end - 1, 0} (one 16-byte record per member)
 };
 
-#define RI(j) ((b + (j)) & (H - 1))
+#define RI(j) ((b + (j)) & msk)
 // Sorted insertion of v (key f) into class k's ring holding n < H entries: every entry is loaded
 // at once (independent loads), the position is a count of smaller keys, and the shift is a set of
 // predicated stores — no load-compare-store chain per step.
-__device__ __forceinline__ void ring_insert(uint4 *hc, u32 b, u32 n, uint4 v, u32 f) {
+__device__ __forceinline__ void ring_insert(uint4 *hc, u32 b, u32 msk, u32 n, uint4 v, u32 f) {
     uint4 x[H];
 #pragma unroll
     for (int j = 0; j < H - 1; j++) x[j] = hc[RI(j)];
@@ -238,12 +258,13 @@ __device__ __forceinline__ void ring_insert(uint4 *hc, u32 b, u32 n, uint4 v, u3
 // REFILL_AT); pass 2 runs only then.
 __device__ __forceinline__ bool refill_csr(Smem &S, const Csr &csr, u32 k) {
     const u32 n = S.hn[k];
-    if (n >= (u32)REFILL_AT) return false;
+    if (n >= hrefill(k)) return false;
     const u32 p = S.ptr[k], e = S.endp[k];
     if (p >= e) return true;
-    uint4 *hc = &S.hc[k * H];
-    const u32 b = S.hb[k];                      // ring buffer: entry j lives at (b + j) % H
-    const u32 m = min((u32)FILL_TO - n, e - p);
+    uint4 *hc = &S.hc[hbase(k)];
+    const u32 msk = hmask(k);
+    const u32 b = S.hb[k];                      // ring buffer: entry j lives at (b + j) % depth
+    const u32 m = min(min((u32)FILL_TO, msk + 1) - n, e - p);
     uint4 v[H];
 #pragma unroll
     for (int j = 0; j < H; j++)
@@ -265,19 +286,20 @@ __device__ void refill_ovf(Smem &S, Heap &hp, const u64 *__restrict__ fs, const 
     if (rt == NIL32) return;
     u32 n = S.hn[k];
     u32 p = S.ptr[k];
-    uint4 *hc = &S.hc[k * H];
+    uint4 *hc = &S.hc[hbase(k)];
+    const u32 msk = hmask(k), dep = msk + 1, rat = hrefill(k);
     const u32 b = S.hb[k];
-    while (rt != NIL32 && (n < (u32)REFILL_AT || rt < (hc[RI(n - 1)].x & ~HEAPBIT))) {
+    while (rt != NIL32 && (n < rat || rt < (hc[RI(n - 1)].x & ~HEAPBIT))) {
         // issue the extract's accesses and the member's data loads together (independent)
         u32 nxt = hp.extract(k, rt);
         const u32 s0 = (u32)fs[rt], e0 = (u32)(fe[rt] - 1);
-        if (n == (u32)H) {                       // evict the tail (it is > rt)
-            const u32 ev = hc[RI(H - 1)].x;
+        if (n == dep) {                          // evict the tail (it is > rt)
+            const u32 ev = hc[RI(dep - 1)].x;
             if (ev & HEAPBIT) nxt = hp.insert(k, nxt, ev & ~HEAPBIT);
             else p--;
             n--;
         }
-        ring_insert(hc, b, n, make_uint4(rt | HEAPBIT, s0, e0, 0u), rt);
+        ring_insert(hc, b, msk, n, make_uint4(rt | HEAPBIT, s0, e0, 0u), rt);
         n++;
         rt = nxt;
         delmins++;
@@ -296,21 +318,22 @@ __device__ void arrive(Smem &S, Heap &hp, u32 k, u32 f, u32 s, u32 e1) {
     const u32 before = S.cnt[k]++;
     if (before == 0) set_bit(S, k);
     u32 n = S.hn[k];
-    uint4 *hc = &S.hc[k * H];
+    uint4 *hc = &S.hc[hbase(k)];
+    const u32 msk = hmask(k), dep = msk + 1;
     const u32 b = S.hb[k];
     // the cache must stay "the n smallest members": f enters it if it is below the cache's
     // tail, or if every member is cached (nothing outside could be smaller)
     const u32 tail = n > 0 ? (hc[RI(n - 1)].x & ~HEAPBIT) : 0u;
-    if ((n > 0 && f < tail) || (n < (u32)H && before == n)) {
-        if (n == (u32)H) {      // evict the largest cached member
-            const u32 ev = hc[RI(H - 1)].x;
+    if ((n > 0 && f < tail) || (n < dep && before == n)) {
+        if (n == dep) {         // evict the largest cached member
+            const u32 ev = hc[RI(dep - 1)].x;
             if (ev & HEAPBIT) S.root[k] = hp.insert(k, S.root[k], ev & ~HEAPBIT);
             else S.ptr[k]--;    // the largest cached CSR member is CSR[ptr-1]
-            n = H - 1;
+            n = dep - 1;
         } else {
             S.hn[k] = (unsigned char)(n + 1);
         }
-        ring_insert(hc, b, n, make_uint4(f | HEAPBIT, s, e1, 0u), f);
+        ring_insert(hc, b, msk, n, make_uint4(f | HEAPBIT, s, e1, 0u), f);
     } else {
         S.root[k] = hp.insert(k, S.root[k], f);
     }
@@ -334,10 +357,11 @@ __device__ void refill_lifo(Smem &S, const Lifo &lf, const Csr &csr, const u64 *
                             const u64 *__restrict__ fe, u32 k, u64 &pops) {
     u32 n = S.hn[k];
     u32 p = S.ptr[k], e = S.endp[k], rt = S.root[k];
-    if (n >= (u32)REFILL_AT || (p >= e && rt == NIL32)) return;
-    uint4 *hc = &S.hc[k * H];
+    const u32 rat = hrefill(k), msk = hmask(k);
+    if (n >= rat || (p >= e && rt == NIL32)) return;
+    uint4 *hc = &S.hc[hbase(k)];
     const u32 b = S.hb[k];
-    while (rt != NIL32 && n < (u32)REFILL_AT) {         // spilled remainders first (newer)
+    while (rt != NIL32 && n < rat) {                     // spilled remainders first (newer)
         const u32 nx = lf.next[rt];
         hc[RI(n)] = make_uint4(rt | HEAPBIT, (u32)fs[rt], (u32)(fe[rt] - 1), 0u);
         n++;
@@ -345,7 +369,7 @@ __device__ void refill_lifo(Smem &S, const Lifo &lf, const Csr &csr, const u64 *
         pops++;
     }
     if (rt == NIL32) {                                   // then the CSR range (oldest members)
-        const u32 m = min((u32)H - n, e - p);
+        const u32 m = min(msk + 1 - n, e - p);
 #pragma unroll
         for (int j = 0; j < H; j++) {
             if ((u32)j < m) hc[RI(n + j)] = csr.r4[p + j];
@@ -363,9 +387,10 @@ __device__ void arrive_lifo(Smem &S, const Lifo &lf, u32 k, u32 f, u32 s, u32 e1
     if (S.cnt[k]++ == 0) set_bit(S, k);
     u32 n = S.hn[k];
     u32 b = S.hb[k];
-    uint4 *hc = &S.hc[k * H];
-    if (n == (u32)H) {                                   // evict the oldest cached member
-        const u32 ev = hc[RI(H - 1)].x;
+    uint4 *hc = &S.hc[hbase(k)];
+    const u32 msk = hmask(k);
+    if (n == msk + 1) {                                  // evict the oldest cached member
+        const u32 ev = hc[RI(msk)].x;
         if (ev & HEAPBIT) {
             const u32 x = ev & ~HEAPBIT;
             lf.next[x] = S.root[k];
@@ -375,7 +400,7 @@ __device__ void arrive_lifo(Smem &S, const Lifo &lf, u32 k, u32 f, u32 s, u32 e1
         }
         n--;
     }
-    b = (b - 1) & (H - 1);
+    b = (b - 1) & msk;
     S.hb[k] = (unsigned char)b;
     hc[RI(0)] = make_uint4(f | HEAPBIT, s, e1, 0u);
     S.hn[k] = (unsigned char)(n + 1);
@@ -559,7 +584,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             const u32 npeer = __popc(peers);
             const u32 nh = part ? S.hn[k] : 0, nc = part ? S.cnt[k] : 0;
             const u32 hb = part ? S.hb[k] : 0;
-            const u32 slotA = k * H + ((hb + rank) & (H - 1)), slot0 = k * H + hb;
+            const u32 hbk = part ? hbase(k) : 0u, hmk = part ? hmask(k) : 0u;
+            const u32 slotA = hbk + ((hb + rank) & hmk), slot0 = hbk + hb;
             const bool hasA = part && rank < nh;
             u32 fA = 0, nkA = NONE;
             u64 sA = 0;
@@ -626,7 +652,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                         const u32 lq = S.lor[lane * 32 + q];
                         if (need) {
                             if (b >= nh) break;
-                            const u32 sl = k * H + ((hb + b) & (H - 1));
+                            const u32 sl = hbase(k) + ((hb + b) & hmask(k));
                             const uint4 mq = S.hc[sl];
                             curf = mq.x & ~HEAPBIT;
                             cur_s = mq.y;
@@ -750,12 +776,12 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
                 // evicted later, it goes to the overflow set / spill stack and its start is
                 // re-read from fs, never from the stale CSR copy
                 const u32 d = __ffs(st) - 1;
-                const u32 sl = k * H + ((b + left) & (H - 1));
+                const u32 sl = hbase(k) + ((b + left) & hmask(k));
                 S.hc[sl].y = (u32)(S.res_s[d] + S.ch_r[d]);
                 S.hc[sl].x |= HEAPBIT;
             }
             if (left) {                          // pop `left` members: advance the ring base
-                S.hb[k] = (unsigned char)((b + left) & (H - 1));
+                S.hb[k] = (unsigned char)((b + left) & hmask(k));
                 S.hn[k] = (unsigned char)(S.hn[k] - left);
                 S.cnt[k] -= left;
                 rf = true;
