@@ -235,41 +235,88 @@ __global__ void __launch_bounds__(NT) k_free_levels(const u64 *__restrict__ old_
 // x + 2^s <= y, repeat — and it never crosses a root boundary (the roots are the binary digits of
 // the arena, largest first, so each root start is a multiple of twice its size and every later
 // root is smaller).  So the merge that k_free_levels does level by level (27 dependent levels at
-// config 4) is computed in one pass of independent steps: old blocks in address order (radix sort
-// of the per-order lists), merged with the freed blocks, coalesced into maximal runs (the fits
-// path's kernels), each run decomposed, the result grouped by order (stable one-pass sort).
+// config 4) is computed in one pass of independent steps: the free set, kept in address order
+// beside the per-order lists (bq: start << 6 | order, maintained by both phases), merged with the
+// freed blocks, coalesced into maximal runs (the fits path's kernels), each run decomposed, the
+// result grouped by order (stable one-pass sort) for the alloc phase.
 __device__ __forceinline__ int bud_step(u64 x, u64 y) {   // order of the greedy block at x in [x, y)
     const int a = x ? __ffsll((long long)x) - 1 : 63;
     const int b = 63 - __clzll(y - x);
     return a < b ? a : b;
 }
-// old per-order lists -> (start key, index) for the address sort
-__global__ void k_bud_keys(const u64 *__restrict__ list, const DevCtr *ctr, u32 *__restrict__ key,
-                           u32 *__restrict__ val) {
+// merge of the address-ordered free set (packed start << 6 | order) with the freed blocks
+// (start, end), both sorted by start (disjoint), into (start, end) arrays (merge path)
+constexpr int QSH = 6;
+__global__ void __launch_bounds__(256) k_bud_merge(const u64 *__restrict__ q, const DevCtr *ctr,
+                                                   const u64 *__restrict__ bs, const u64 *__restrict__ be,
+                                                   const u64 *nb_dev, u64 *__restrict__ os, u64 *__restrict__ oe,
+                                                   u64 *total) {
     PDL_ENTRY();
-    const u64 n = ctr->bud_total;
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        key[i] = (u32)list[i];
-        val[i] = (u32)i;
+    const u64 na = ctr->bud_qn, nb = *nb_dev, n = na + nb;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *total = n;
+    constexpr int IPT = 8;
+    const u64 nchunks = (n + IPT - 1) / IPT;
+    for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += (u64)gridDim.x * blockDim.x) {
+        const u64 diag = c * IPT;
+        u64 lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+        while (lo < hi) {
+            const u64 mid = (lo + hi) >> 1;
+            if ((q[mid] >> QSH) <= bs[diag - mid - 1]) lo = mid + 1; else hi = mid;
+        }
+        u64 i = lo, j = diag - lo;
+#pragma unroll
+        for (int k = 0; k < IPT; k++) {
+            const u64 o = diag + k;
+            if (o >= n) break;
+            const u64 qa = i < na ? q[i] : 0;
+            const bool ta = (j >= nb) || (i < na && (qa >> QSH) <= bs[j]);
+            if (ta) { os[o] = qa >> QSH; oe[o] = (qa >> QSH) + (1ull << (qa & 63)); i++; }
+            else { os[o] = bs[j]; oe[o] = be[j]; j++; }
+        }
     }
 }
-// sorted indices -> (start, end) in address order
-__global__ void k_bud_unpack(const u64 *__restrict__ list, const u32 *__restrict__ idx, const DevCtr *ctr, int K,
-                             u64 *__restrict__ os, u64 *__restrict__ oe) {
+// after an alloc phase: the surviving blocks of the address-ordered set (each order lost a prefix:
+// keep iff start >= the order's first surviving start), then the leftovers inserted in place
+__global__ void k_bud_qflags(const u64 *__restrict__ q, const DevCtr *ctr, u32 *__restrict__ flags) {
     PDL_ENTRY();
-    __shared__ u64 off[42];
-    if (threadIdx.x <= (unsigned)K + 1) off[threadIdx.x] = ctr->bud_off[threadIdx.x];
+    const u64 n = ctr->bud_qn;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 v = q[i];
+        flags[i] = (v >> QSH) >= ctr->bud_thr[v & 63] ? 1u : 0u;
+    }
+}
+__global__ void k_bud_qwrite(const u64 *__restrict__ q, const u32 *__restrict__ flags, const u32 *__restrict__ pos,
+                             const u64 *kept_dev, int K, u64 *__restrict__ out, DevCtr *ctr) {
+    PDL_ENTRY();
+    __shared__ u64 lv[48];
+    __shared__ int nl;
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int t = 0; t <= K; t++)
+            if (ctr->bud_left[t] != FAIL) lv[c++] = (ctr->bud_left[t] << QSH) | (u64)t;
+        nl = c;
+    }
     __syncthreads();
-    const u64 n = ctr->bud_total;
+    const u64 n = ctr->bud_qn, kept = *kept_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        const u32 p = idx[i];
-        int lo = 0, hi = K;                 // order t: off[t] <= p < off[t + 1]
-        while (lo < hi) { const int m = (lo + hi + 1) >> 1; if (off[m] <= p) lo = m; else hi = m - 1; }
-        const u64 a = list[p];
-        os[i] = a;
-        oe[i] = a + (1ull << lo);
+        if (!flags[i]) continue;
+        const u64 v = q[i];
+        u64 d = 0;
+        for (int c = 0; c < nl; c++) d += (lv[c] >> QSH) < (v >> QSH) ? 1 : 0;
+        out[pos[i] + d] = v;
     }
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)nl) {
+        const u64 v = lv[threadIdx.x], st = v >> QSH;
+        u64 lo = 0, hi = n;                  // kept blocks below it: pos at the first start >= st
+        while (lo < hi) { const u64 m = (lo + hi) >> 1; if ((q[m] >> QSH) < st) lo = m + 1; else hi = m; }
+        const u64 kb = lo < n ? pos[lo] : kept;
+        u64 d = 0;
+        for (int c = 0; c < nl; c++) d += (lv[c] >> QSH) < st ? 1 : 0;
+        out[kb + d] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->bud_qn = kept + (u64)nl;
 }
+
 // blocks of each maximal run's greedy decomposition
 __global__ void k_bud_count(const u64 *__restrict__ rs, const u64 *__restrict__ re, const u64 *R_dev,
                             u32 *__restrict__ cnt) {
@@ -286,7 +333,7 @@ __global__ void k_bud_count(const u64 *__restrict__ rs, const u64 *__restrict__ 
 // write the decomposition in address order: start (units) and the order as the sort key
 __global__ void k_bud_write(const u64 *__restrict__ rs, const u64 *__restrict__ re, const u64 *R_dev,
                             const u32 *__restrict__ pos, u64 *__restrict__ ostart, u32 *__restrict__ okey,
-                            u32 *__restrict__ oval, u64 cap, DevCtr *ctr) {
+                            u32 *__restrict__ oval, u64 *__restrict__ oq, u64 cap, DevCtr *ctr) {
     PDL_ENTRY();
     const u64 R = *R_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += (u64)gridDim.x * blockDim.x) {
@@ -295,7 +342,7 @@ __global__ void k_bud_write(const u64 *__restrict__ rs, const u64 *__restrict__ 
         u64 o = pos[i];
         while (x < y) {
             const int t = bud_step(x, y);
-            if (o < cap) { ostart[o] = x; okey[o] = (u32)t; oval[o] = (u32)o; }
+            if (o < cap) { ostart[o] = x; okey[o] = (u32)t; oval[o] = (u32)o; oq[o] = (x << QSH) | (u64)t; }
             else atomicOr(&ctr->error_flags, (u64)ERR_CAP_FREE);
             x += 1ull << t;
             o++;
@@ -321,7 +368,7 @@ __global__ void k_bud_offsets(const u32 *__restrict__ key, const u64 *n_dev, int
     }
     __syncthreads();
     if (t <= K) ctr->bud_cnt[t] = ctr->bud_off[t + 1] - ctr->bud_off[t];
-    if (t == 0) ctr->bud_total = n;
+    if (t == 0) { ctr->bud_total = n; ctr->bud_qn = n; }
 }
 
 // freed (start, end) -> sort key = order, payload = index
@@ -500,6 +547,14 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         __syncthreads();
     }
     __syncthreads();
+    // for the address-ordered set (k_bud_qflags / k_bud_qwrite): per order the first surviving
+    // start (the first nd blocks were consumed) and the leftover
+    if (threadIdx.x <= (unsigned)K) {
+        const int t = threadIdx.x;
+        const u64 n_t = ooff[t + 1] - ooff[t], nd = doff[t + 1] - doff[t];
+        ctr->bud_thr[t] = nd == 0 ? 0ull : (nd < n_t ? old_list[ooff[t] + nd] : FAIL);
+        ctr->bud_left[t] = s_left[t];
+    }
     // ---- new per-order lists: surviving batch-start blocks, or the one leftover ----
     __shared__ u64 noff[42];
     if (threadIdx.x == 0) {

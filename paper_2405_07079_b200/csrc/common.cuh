@@ -38,6 +38,10 @@ struct DevCtr {
     u64 bud_cnt[48];
     u64 bud_off[49];
     u64 bud_total;
+    // buddy free set in address order (buddy.cuh parallel form): its length, and from the last
+    // alloc phase per order the first surviving start (consumed blocks are a prefix) and leftover
+    u64 bud_qn;
+    u64 bud_thr[48], bud_left[48];
     u64 eng[32];        // alloc engine diagnostics (engine_tlsf.cuh)
     u64 lifo_clock;     // SEGFIT_LIFO logical push clock (fits.cuh)
     u64 req_n;          // request count of a graph-launched batch (heap.cu graph path)

@@ -42,7 +42,7 @@ struct Layout {
     u64 o_ctr, o_stats, o_tbl, o_fs0, o_fs1, o_fe0, o_fe1, o_kA, o_kB, o_vA, o_vB, o_flags, o_pos,
         o_hist, o_tsum, o_vs, o_ve, o_vsc, o_vec, o_ms, o_me, o_r, o_c, o_out, o_off, o_child,
         o_sib, o_cs, o_bm, o_slot, bm_w0, bm_w1, bm_w2, bm_bytes, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
-        o_promo, o_fr, o_froff, o_reqoff, o_ft0, o_ft1, o_vt, o_mt, o_lnext, total;
+        o_promo, o_bq0, o_bq1, o_fr, o_froff, o_reqoff, o_ft0, o_ft1, o_vt, o_mt, o_lnext, total;
     // HEAP_HYBRID: pool geometry and arrays, then the TLSF heap's own workspace at o_sub
     pool::Geom geo;
     u64 o_pctr, o_bits, o_sbcnt, o_sbpre, o_tsz, o_tout, o_toff, o_tidx, o_coff, o_sstats, o_sub, sub_total;
@@ -260,6 +260,7 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.o_bufA = take(L.bud_cap * 8);
         L.o_bufB = take(L.bud_cap * 8);
         L.o_promo = take(L.bud_cap * 8);
+        if (policy == HEAP_BUDDY) { L.o_bq0 = take(L.cap_f * 8); L.o_bq1 = take(L.cap_f * 8); }
         L.o_fr = take(max_batch * 8);
         L.o_froff = take(64 * 4);
         L.o_reqoff = take(64 * 4);
@@ -288,6 +289,7 @@ struct heap {
     DevCtr *ctr;
     heap_stats_t *dstats;
     u64 *tbl, *fs[2], *fe[2];
+    u64 *bq[2] = {nullptr, nullptr};   // BUDDY: the free set in address order (start << 6 | order)
     u32 *kA, *kB, *vA, *vB, *flags, *pos, *hist, *tsum;
     u64 *vs, *ve, *vsc, *vec, *ms, *me, *r, *out;
     u32 *c, *off, *child, *sib, *bm, *slot;
@@ -402,6 +404,11 @@ __global__ void k_init(DevCtr *ctr, u64 *tbl, u64 tcap, u64 *fs, u64 *fe, u64 A_
             }
             ctr->bud_off[K + 1] = o;
             ctr->bud_total = o;
+            // the same roots in address order (largest first) for the parallel free phase (fe = bq)
+            u64 q = 0;
+            for (int t = K; t >= 0; t--)
+                if ((A_u >> t) & 1) fe[q++] = (addr[t] << buddy::QSH) | (u64)t;
+            ctr->bud_qn = q;
         }
     }
 }
@@ -753,6 +760,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->dtm = at<u32>(w, L.o_dtm); h->dsrc = at<u32>(w, L.o_dsrc); h->baddr = at<u64>(w, L.o_baddr);
         h->btm = at<u32>(w, L.o_btm); h->bsrc = at<u32>(w, L.o_bsrc);
         h->bufA = at<u64>(w, L.o_bufA); h->bufB = at<u64>(w, L.o_bufB); h->promo = at<u64>(w, L.o_promo);
+        if (L.o_bq0) { h->bq[0] = at<u64>(w, L.o_bq0); h->bq[1] = at<u64>(w, L.o_bq1); }
         h->fr = at<u64>(w, L.o_fr); h->froff = at<u32>(w, L.o_froff); h->reqoff = at<u32>(w, L.o_reqoff);
     }
     if (L.partial) {
@@ -764,8 +772,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     h->prof_mask = 0;
     h->tag = HEAP_TAG_MISC;
     cudaStream_t st = (cudaStream_t)s;
-    LAUNCH(h, k_init, h->G, 256, 0, st, h->ctr, h->tbl, L.tcap, h->fs[0], h->fe[0], L.A_u,
-           policy == HEAP_BUDDY ? 1 : (policy == HEAP_FIB_BUDDY ? 2 : 0), L.K);
+    LAUNCH(h, k_init, h->G, 256, 0, st, h->ctr, h->tbl, L.tcap, h->fs[0], policy == HEAP_BUDDY ? h->bq[0] : h->fe[0],
+           L.A_u, policy == HEAP_BUDDY ? 1 : (policy == HEAP_FIB_BUDDY ? 2 : 0), L.K);
     if (policy == HEAP_FIB_BUDDY) LAUNCH(h, fib::k_init_lists, 1, 1, 0, st, h->ctr, h->fs[0], h->fgeom);
     if (policy == HEAP_FIRST_FIT || policy == HEAP_NEXT_FIT) {
         u64 offs[fits::FF_MAX_LEVELS] = {0};
@@ -875,12 +883,8 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
         if (!fibp && !h->bud_levels) {
             // parallel form (buddy.cuh): old blocks in address order, merged with the freed ones,
             // coalesced into maximal runs, each run's greedy decomposition grouped by order
-            const int abits = ilog2(L.A_u - 1 > 0 ? L.A_u - 1 : 1) + 1;
-            LAUNCH(h, buddy::k_bud_keys, h->G, 256, 0, s, h->fs[cur], C, h->kA, h->vA);
-            const int r1 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->bud_total, abits, s);
-            LAUNCH(h, buddy::k_bud_unpack, h->G, 256, 0, s, h->fs[cur], r1 ? h->vB : h->vA, C, L.K, h->bufA, h->bufB);
-            LAUNCH(h, prims::k_merge, h->G, prims::NT, 0, s, h->bufA, h->bufB, &C->bud_total, h->vsc, h->vec, &C->nv,
-                   h->ms, h->me, &C->M, (const u32 *)nullptr, (const u32 *)nullptr, (u32 *)nullptr);
+            // the free set is kept in address order too (bq, maintained by both phases)
+            LAUNCH(h, buddy::k_bud_merge, h->G, 256, 0, s, h->bq[cur], C, h->vsc, h->vec, &C->nv, h->ms, h->me, &C->M);
             LAUNCH(h, fits::k_coal_flags, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags);
             scan(h, h->flags, h->pos, &C->M, &C->tmp[2], s);
             LAUNCH(h, fits::k_coal_write, h->G, 256, 0, s, h->ms, h->me, &C->M, h->flags, h->pos, h->bufA, h->bufB,
@@ -888,7 +892,7 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
             LAUNCH(h, buddy::k_bud_count, h->G, 256, 0, s, h->bufA, h->bufB, &C->tmp[2], h->flags);
             scan(h, h->flags, h->pos, &C->tmp[2], &C->tmp[3], s);
             LAUNCH(h, buddy::k_bud_write, h->G, 256, 0, s, h->bufA, h->bufB, &C->tmp[2], h->pos, h->promo, h->kA,
-                   h->vA, L.cap_f, C);
+                   h->vA, h->bq[nxt], L.cap_f, C);
             const int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[3], 8, s);
             LAUNCH(h, buddy::k_bud_lists, h->G, 256, 0, s, r2 ? h->vB : h->vA, &C->tmp[3], h->promo, h->fs[nxt]);
             LAUNCH(h, buddy::k_bud_offsets, 1, 64, 0, s, r2 ? h->kB : h->kA, &C->tmp[3], L.K, C);
@@ -942,6 +946,12 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kB, &C->tmp[0], L.K + 2, h->reqoff);
         LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, buddy::ALLOC_SMEM, s, h->vB, h->reqoff, h->fs[cur], h->fs[nxt], h->dtm,
                h->dsrc, nullptr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
+        if (!h->bud_levels) {   // the address-ordered free set: survivors compacted, leftovers inserted
+            LAUNCH(h, buddy::k_bud_qflags, h->G, 256, 0, s, h->bq[cur], C, h->flags);
+            scan(h, h->flags, h->pos, &C->bud_qn, &C->tmp[2], s);
+            LAUNCH(h, buddy::k_bud_qwrite, h->G, 256, 0, s, h->bq[cur], h->flags, h->pos, &C->tmp[2], L.K,
+                   h->bq[nxt], C);
+        }
         LAUNCH(h, buddy::k_alloc_r, h->G, 256, 0, s, h->kA, n, n_in, L.K, h->r);
         TAG(h, HEAP_TAG_FINISH);
         LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, n_in, h->alog2, (u64 *)d_out,
