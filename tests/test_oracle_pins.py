@@ -717,6 +717,53 @@ def test_buddy_roots_closed_form():
         assert st["largest_free"] == 1 << bits[0] and st["high_water_end"] == 0 and st["n_free"] == len(bits)
 
 
+def _greedy_runs(fp, A, align):
+    """Maximal free runs of `fp` (byte pairs), each decomposed greedily: at x the largest 2^s units
+    with x % 2^s == 0 and x + 2^s <= the run's end."""
+    runs = []
+    for s_, z in (tuple(int(v) for v in p) for p in fp):
+        if runs and runs[-1][1] == s_:
+            runs[-1][1] = s_ + z
+        else:
+            runs.append([s_, s_ + z])
+    out = []
+    for x, y in runs:
+        x //= align
+        y //= align
+        while x < y:
+            s_ = (x & -x).bit_length() - 1 if x else 63
+            s_ = min(s_, (y - x).bit_length() - 1)
+            out.append((x * align, (1 << s_) * align))
+            x += 1 << s_
+    return out
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_buddy_free_set_is_greedy_decomposition_of_runs(seed):
+    """The lemma behind the GPU's parallel buddy free phase (buddy.cuh k_bud_*): after
+    any sequence of batches the buddy free set (Oracle-L's one-by-one merges) equals
+    the greedy decomposition of its maximal free runs into maximal aligned power-of-two blocks —
+    including arenas that are not a power of two (the greedy never crosses a root boundary).
+    Checked after every batch of random traces on several arena shapes."""
+    rng = np.random.default_rng(seed)
+    for A_u in (1 << 12, (1 << 12) + (1 << 9) + 7, 3000, 1 << 10):
+        align = 16
+        o = OracleL(A_u * align, align, tg.BUDDY)
+        live = []
+        for _ in range(40):
+            nf = int(rng.integers(0, len(live) + 1)) if live else 0
+            idx = rng.permutation(len(live))[:nf]
+            frees = np.array([live[i] for i in idx], dtype=np.uint64)
+            live = [v for i, v in enumerate(live) if i not in set(idx.tolist())]
+            o.free_batch(frees)
+            sizes = (1 << rng.integers(0, 8, size=int(rng.integers(1, 40)))) * align
+            out = o.alloc_batch(sizes.astype(np.uint64))
+            live += [int(v) for v in out if v != (1 << 64) - 1]
+            fp, _ = o.export()
+            got = [tuple(int(v) for v in p) for p in fp]
+            assert got == _greedy_runs(fp, A_u, align), (A_u, seed)
+
+
 def test_size_statistics_closed_forms():
     """largest_free and high_water_end (heap_stats_t) on hand-worked sequences, for both oracles:
     a fresh heap's largest block is the arena; after allocations of r_0, r_1, ... the high-water
