@@ -1,4 +1,4 @@
-"""Dev: per-level cycles / sizes of buddy::k_free_levels (BUDDY_TIMING builds) on config 4."""
+"""Dev: k_alloc_levels phase clocks (BUDDY_TIMING build) on config 4."""
 import os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
@@ -17,4 +17,5 @@ for i, (f, s, first) in enumerate(bs):
     idm[first:first + len(s)] = h.alloc_batch(torch.from_numpy(s.view(np.int64)).cuda())
 c = h.debug_counters()
 d = [(a - b) / (nb - 4) for a, b in zip(c, prev)]
-print(" ".join(f"{t}:{d[t]:.0f}" for t in range(27)), " total", sum(d[:27]))
+print("alloc levels cycles/batch: bottom-up %.0f  top-down %.0f  lists %.0f" % (d[20], d[21], d[22]))
+print("bottom-up per level:", " ".join(f"{t}:{d[t]:.0f}" for t in range(20)))
