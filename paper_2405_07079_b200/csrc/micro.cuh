@@ -326,6 +326,58 @@ __global__ void __launch_bounds__(MT, 1) k_micro_alloc(const u64 *__restrict__ s
         // pe[] becomes the piece sizes during the engine (carves shrink them), restored after
         for (u32 j = lane; j < F; j += 32) pe[j] -= ps[j];
         __syncwarp();
+        if ((POL == P_FF || POL == P_NF) && F <= 128) {
+            // small free array, first / next fit: piece lane + 32 q in registers of its lane
+            // (q < 4); four independent ballots per request, the winning lane carves in place —
+            // no shared-memory round trip on the chain
+            u32 z[4], st[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const u32 j = lane + 32 * q;
+                z[q] = j < F ? pe[j] : 0u;
+                st[q] = j < F ? ps[j] : 0u;
+            }
+            u32 rn = n ? rr[0] : 0u;
+            for (u32 i = 0; i < (u32)n; i++) {
+                const u32 r = rn;
+                rn = i + 1 < (u32)n ? rr[i + 1] : 0u;      // the next request, off the chain
+                u32 f = NONE;
+                if (r != 0) {
+                    u32 bq[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) bq[q] = __ballot_sync(FULLMASK, z[q] >= r && lane + 32 * q >= f0);
+                    const u32 any = bq[0] | bq[1] | bq[2] | bq[3];
+                    if (any) {
+                        const int q = bq[0] ? 0 : bq[1] ? 1 : bq[2] ? 2 : 3;
+                        f = 32 * q + __ffs(bq[q]) - 1;
+                    } else if (POL == P_NF && f0 > 0) {  // wrap: first fit from piece 0
+#pragma unroll
+                        for (int q = 0; q < 4; q++) bq[q] = __ballot_sync(FULLMASK, z[q] >= r);
+                        if (bq[0] | bq[1] | bq[2] | bq[3]) {
+                            const int q = bq[0] ? 0 : bq[1] ? 1 : bq[2] ? 2 : 3;
+                            f = 32 * q + __ffs(bq[q]) - 1;
+                        }
+                    }
+                }
+                if (f == NONE) {
+                    if (lane == 0) res[i] = NONE;
+                } else {
+                    if ((f & 31) == lane) {
+                        const int q = (int)(f >> 5);
+#pragma unroll
+                        for (int k = 0; k < 4; k++)
+                            if (k == q) { res[i] = st[k]; st[k] += r; z[k] -= r; }
+                    }
+                    if (POL == P_NF) { f0 = f; moved = true; }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const u32 j = lane + 32 * q;
+                if (j < F) { ps[j] = st[q]; pe[j] = z[q]; }
+            }
+            __syncwarp();
+        } else
         for (u32 i = 0; i < (u32)n; i++) {
             const u32 r = rr[i];
             u32 f = NONE;

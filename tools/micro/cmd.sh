@@ -1,3 +1,2 @@
-HEAP_DEV_LIB=libheap_t_bt.so timeout 300 python tools/micro/buddy_probe.py > gpurun_out/buddy_probe.txt 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "buddy or BUDDY or config4 or p5 or p9 or edge or extremes" > gpurun_out/pytest_bud.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_bud.log
-for i in 1 2; do timeout 600 python tools/micro/per_config.py 4 2>&1 | cut -c1-120; done > gpurun_out/per_config.txt
+mkdir -p gpurun_out/prof
+ncu --set full --clock-control none --import-source on -k regex:k_micro_alloc -s 12 -c 1 -o gpurun_out/prof/micro_alloc python tools/micro/micro_probe.py 1 > gpurun_out/prof/ma.log 2>&1
