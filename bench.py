@@ -542,31 +542,26 @@ def run_config(cfg, nbatches, dev, flush, warmup=3):
     outs, t_ms, ops = [], 0.0, 0
     staged = [(torch.from_numpy(f.astype(np.int64)).to(dev), torch.from_numpy(s.view(np.int64)).to(dev), first)
               for f, s, first in batches]
-    timing = "graph"
     # warm-up batches run eagerly; the timed window is captured as ONE CUDA graph (the library launches
     # directly under capture) and replayed once, so small batches are timed without host issue gaps
     for bi, (fd, sd, first) in enumerate(staged[:warmup]):
         h.free_batch(idmap[fd] if len(fd) else fd)
         h.alloc_batch(sd, out=idmap[first:first + len(sd)])
     torch.cuda.synchronize()
-    try:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for fd, sd, first in staged[warmup:]:
-                h.free_batch(idmap[fd] if len(fd) else fd)
-                h.alloc_batch(sd, out=idmap[first:first + len(sd)])
-        flush.fill_(1)
-        torch.cuda.synchronize()
-        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        g.replay()
-        e.record()
-        torch.cuda.synchronize()
-        t_ms = a.elapsed_time(e)
-        del g
-    except Exception:                      # capture unsupported: per-batch timing with host gaps
-        timing = "eager"
-        raise
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for fd, sd, first in staged[warmup:]:
+            h.free_batch(idmap[fd] if len(fd) else fd)
+            h.alloc_batch(sd, out=idmap[first:first + len(sd)])
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    t_ms = a.elapsed_time(e)
+    del g
     for bi, (fd, sd, first) in enumerate(staged):
         outs.append(idmap[first:first + len(sd)].cpu().numpy())
         if bi >= warmup:
@@ -582,7 +577,7 @@ def run_config(cfg, nbatches, dev, flush, warmup=3):
     return {"policy": tg.POLICY_NAME.get(cfg.policy), "batches": f"{warmup}..{len(batches) - 1} timed of {len(batches)}",
             "device_ops_s": dev_v, "ms_per_batch": t_ms / max(len(batches) - warmup, 1),
             "timing": ("the timed batches captured as one CUDA graph and replayed once (device time, no host "
-                       "gaps, no L2 flush between batches)") if timing == "graph" else "per-batch events",
+                       "gaps, no L2 flush between batches)"),
             "oracle_ops_s": orc["value"], "vs_oracle": dev_v / orc["value"] if orc["value"] else None,
             "parity_ok": orc["mismatch"] is None and st["error_flags"] == 0, "mismatch": orc["mismatch"],
             "payload_roofline": {"achieved": pay, "peak": peak, "unit": "GB/s", "frac": pay / peak,
@@ -596,11 +591,16 @@ def _engine_chain(dc, n_alloc, policy):
     if policy not in (tg.TLSF, tg.SEGFIT) or not dc or dc[0] == 0:
         return None
     ch = dc[0]
-    return {"allocs": n_alloc, "chunks": ch, "committed_per_chunk": n_alloc / ch,
-            "rounds_per_chunk": dc[3] / ch,
-            "cycles_per_chunk": {"speculation": dc[5] / ch, "dirty_check": dc[6] / ch,
-                                 "class_updates": dc[7] / ch, "arrivals": dc[8] / ch, "stores": dc[11] / ch},
-            "overflow_inserts": dc[15], "overflow_extractions": dc[9]}
+    out = {"allocs": n_alloc, "chunks": ch, "committed_per_chunk": n_alloc / ch,
+           "rounds_per_chunk": dc[3] / ch, "overflow_inserts": dc[15], "overflow_extractions": dc[9]}
+    if dc[5]:   # phase clocks exist only in an ENGINE_TIMING build (off in production: 0.4 % cost)
+        out["cycles_per_chunk"] = {"speculation": dc[5] / ch, "dirty_check": dc[6] / ch,
+                                   "class_update_pops": dc[16] / ch, "refill_csr": dc[17] / ch,
+                                   "refill_overflow": dc[18] / ch, "arrivals": dc[8] / ch, "stores": dc[11] / ch}
+    else:
+        out["cycles_per_chunk"] = ("ENGINE_TIMING build only: tools/engine_probe.py, "
+                                   "profiles/r02_engine_study.md")
+    return out
 
 
 def _payload_roofline(ops_per_s):

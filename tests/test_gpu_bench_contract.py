@@ -44,3 +44,20 @@ def test_reference_arm_line():
     d = _run(["--impl", "reference", "--config", "3", "--steps", "2", "--warmup", "3"])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_per_config_side_line():
+    """bench.py's per-config side measurement (configs 1-4 beside the headline): the timed batches
+    captured as one CUDA graph with the library launching directly under capture, replayed once,
+    every returned offset compared with Oracle-L afterwards.  Config 1 (the single-launch small-heap
+    path) and config 4 (binary buddies, ~40 launches per batch) on a few batches."""
+    sys.path.insert(0, ROOT)
+    import torch
+    import bench
+    import tracegen as tg
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(1 << 20, dtype=torch.int32, device=dev)
+    for cid, nb in ((1, 0), (4, 6)):
+        r = bench.run_config(tg.CONFIGS[cid], nb, dev, flush)
+        assert r["parity_ok"], (cid, r["mismatch"])
+        assert r["device_ops_s"] > 0 and r["oracle_ops_s"] > 0 and r["timing"].startswith("the timed batches")

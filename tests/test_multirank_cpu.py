@@ -76,11 +76,14 @@ def test_bench_line_helpers():
     assert abs(pr["bytes_per_op"] - 73.6) < 1e-9
     assert abs(pr["achieved"] - 0.0736) < 1e-12
     assert abs(pr["frac"] - pr["achieved"] / pr["peak"]) < 1e-15
-    dc = [0] * 16
-    dc[0], dc[3], dc[5], dc[6], dc[7], dc[8], dc[11], dc[9], dc[15] = 10, 10, 2000, 1000, 3000, 2500, 100, 7, 9
+    dc = [0] * 32
+    dc[0], dc[3], dc[5], dc[6], dc[8], dc[11], dc[9], dc[15] = 10, 10, 2000, 1000, 2500, 100, 7, 9
+    dc[16], dc[17], dc[18] = 350, 850, 2300
     ec = bench._engine_chain(dc, 190, tg.TLSF)
     assert ec["chunks"] == 10 and ec["committed_per_chunk"] == 19.0 and ec["rounds_per_chunk"] == 1.0
-    assert ec["cycles_per_chunk"]["class_updates"] == 300.0
+    assert ec["cycles_per_chunk"]["refill_overflow"] == 230.0 and ec["cycles_per_chunk"]["dirty_check"] == 100.0
     assert ec["overflow_extractions"] == 7 and ec["overflow_inserts"] == 9
+    dc[5] = 0                                # a production build: no phase clocks
+    assert isinstance(bench._engine_chain(dc, 190, tg.TLSF)["cycles_per_chunk"], str)
     assert bench._engine_chain(dc, 190, tg.BUDDY) is None
-    assert bench._engine_chain([0] * 16, 190, tg.TLSF) is None
+    assert bench._engine_chain([0] * 32, 190, tg.TLSF) is None
