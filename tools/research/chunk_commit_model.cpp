@@ -38,6 +38,7 @@ typedef std::set<std::pair<u64, u64>> CS;   // (class, start)
 int main(int argc, char **argv) {
     int nb = argc > 1 ? atoi(argv[1]) : 8;
     int first_b = argc > 2 ? atoi(argv[2]) : 1;
+    const int FIX = argc > 3 ? atoi(argv[3]) : 0;   // mismatching requests a chunk may fix in place
     const u64 A = 1ull << 32, B = 1 << 20, seed = 2405070790ull + 5000;
     tg_t *t = tg_create(0, seed, B, 2, 5, 100000000ull, 0, 4, 12, 0);
     std::vector<u64> fids(B), sz(B), off;
@@ -120,13 +121,15 @@ int main(int argc, char **argv) {
                     if (end > ns && icls(end - ns) == it->first) carved[key] = ns;
                     else removed.insert(*it);
                 }
-                // true replay, stop at the first mismatch
+                // true replay, stop at the first mismatch (FIX > 0: at the (FIX+1)-th; an upper
+                // bound for fixing a dirty request in place when the later ones stay valid)
                 size_t j = 0;
+                int fixes = 0;
                 for (; j < cand.size(); j++) {
                     u64 i = cand[j];
                     auto it = C.lower_bound({c[i], 0});
                     u64 tv = it == C.end() ? ~1ull : it->second;
-                    if (tv != spec[j] && j > 0) break;
+                    if (tv != spec[j] && j > 0 && fixes++ >= FIX) break;
                     if (it != C.end()) {
                         u64 st = it->second, s = Fr[st];
                         C.erase(it); Fr.erase(st);
