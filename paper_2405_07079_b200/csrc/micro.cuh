@@ -24,6 +24,9 @@ namespace micro {
 
 constexpr int MT = 512;                     // threads per CTA
 constexpr u32 MICRO_F = 4160;               // pieces (max_live + 1 <= MICRO_F)
+// (The engine below costs O(F) per request — brute force — and the first-fit scan O(F / 32) in the
+// worst case: the general path's indexes (max tree, blocked sorted list, class caches) win for
+// larger free arrays, so the single-launch path stops at a few thousand pieces.)
 constexpr u32 MICRO_N = 4096;               // requests per batch
 constexpr u32 NONE = 0xFFFFFFFFu;
 enum { P_FF = 0, P_NF = 1, P_BF = 2, P_CLS = 3 };
@@ -227,9 +230,12 @@ __global__ void __launch_bounds__(MT, 1) k_micro_free(const u64 *__restrict__ of
     __syncthreads();
     u32 Fn;
     {
-        const u32 c = tid < nw ? (u32)__popc(hb[tid]) : 0u;      // nw <= 258 < MT
-        const u32 ex = cta_scan(c, sm, &Fn);
-        if (tid < nw) wp[tid] = ex;
+        // two words per thread (nw <= (MICRO_F + MICRO_N) / 32 + 1 = 673 <= 2 MT)
+        const u32 c0 = 2 * tid < nw ? (u32)__popc(hb[2 * tid]) : 0u;
+        const u32 c1 = 2 * tid + 1 < nw ? (u32)__popc(hb[2 * tid + 1]) : 0u;
+        const u32 ex = cta_scan(c0 + c1, sm, &Fn);
+        if (2 * tid < nw) wp[2 * tid] = ex;
+        if (2 * tid + 1 < nw) wp[2 * tid + 1] = ex + c0;
     }
     __syncthreads();
     if (Fn > cap_f) {
@@ -425,10 +431,12 @@ __global__ void __launch_bounds__(MT, 1) k_micro_alloc(const u64 *__restrict__ s
     __syncthreads();
     u32 Fn;
     {
-        const u32 nw = (F + 31) / 32;
-        const u32 c = tid < nw ? (u32)__popc(sb[tid]) : 0u;   // nw <= 130 < MT
-        const u32 ex = cta_scan(c, sm, &Fn);
-        if (tid < nw) sp[tid] = ex;
+        const u32 nw = (F + 31) / 32;                         // <= 544 <= 2 MT: two words per thread
+        const u32 c0 = 2 * tid < nw ? (u32)__popc(sb[2 * tid]) : 0u;
+        const u32 c1 = 2 * tid + 1 < nw ? (u32)__popc(sb[2 * tid + 1]) : 0u;
+        const u32 ex = cta_scan(c0 + c1, sm, &Fn);
+        if (2 * tid < nw) sp[2 * tid] = ex;
+        if (2 * tid + 1 < nw) sp[2 * tid + 1] = ex + c0;
     }
     __syncthreads();
     for (u32 j = tid; j < F; j += MT)

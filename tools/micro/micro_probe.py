@@ -5,8 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import tracegen as tg
 from paper_2405_07079_b200 import Heap
 cfg = tg.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 1]
-bs = list(tg.Trace(cfg))[:40]
-h = Heap(cfg.arena_bytes, cfg.align, cfg.policy, cfg.max_live, 1000)
+bs = list(tg.Trace(cfg, total_ops=(cfg.batch * 40 if cfg.model == 0 else None)))[:40]
+h = Heap(cfg.arena_bytes, cfg.align, cfg.policy, cfg.max_live, max(cfg.batch, 1000))
 idm = torch.full((sum(len(b[1]) for b in bs) + 1,), -1, dtype=torch.int64, device="cuda")
 prev = h.debug_counters()
 names = {16: "f.load", 17: "f.classify", 18: "f.sort", 19: "f.lookup", 20: "f.compact", 21: "f.merge+write",
