@@ -88,11 +88,11 @@ __global__ void __launch_bounds__(256) k_free_lookup(const u32 *__restrict__ key
     PDL_ENTRY();
     __shared__ u64 sm[33];
     const u64 nk = *nk_dev, F = F_dev ? *F_dev : 0;
-    const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
+    const u32 lane = lane_id(), g = lane / table::TILE_LANES, sub = lane % table::TILE_LANES;
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
     u64 c_ok = 0, c_dbl = 0, c_inv = 0, c_units = 0;
-    for (u64 base = gw * 4; base < nk; base += nwarps * 4) {
+    for (u64 base = gw * table::KPW; base < nk; base += nwarps * table::KPW) {
         u64 idx = base + g;
         bool in = idx < nk;
         u32 key = in ? keys[idx] : 0;
@@ -257,11 +257,11 @@ __global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r,
     PDL_ENTRY();
     __shared__ u64 sm[33];
     if (n_in) n = *n_in;
-    const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
+    const u32 lane = lane_id(), g = lane / table::TILE_LANES, sub = lane % table::TILE_LANES;
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
     u64 c_ok = 0, c_fail = 0, c_units = 0, c_used = 0, c_tomb = 0, c_full = 0, hw = 0;
-    for (u64 base = gw * 4; base < n; base += nwarps * 4) {
+    for (u64 base = gw * table::KPW; base < n; base += nwarps * table::KPW) {
         u64 i = base + g;
         bool in = i < n;
         u64 o = in ? out_u[i] : HEAP_NULL_U64;

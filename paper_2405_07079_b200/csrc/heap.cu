@@ -467,9 +467,9 @@ __global__ void k_rb_insert(DevCtr *ctr, u64 *tbl, u64 tmask, u64 max_lines, con
     PDL_ENTRY();
     if (!ctr->tmp[4]) return;
     const u64 n = ctr->tmp[5];
-    const u32 g = lane_id() >> 3;
+    const u32 g = lane_id() / table::TILE_LANES;
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
-    for (u64 base = gw * 4; base < n; base += nw * 4) {
+    for (u64 base = gw * table::KPW; base < n; base += nw * table::KPW) {
         u64 i = base + g;
         bool in = i < n;
         u64 v = in ? scratch[i] : 0;

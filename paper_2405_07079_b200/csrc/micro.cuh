@@ -140,13 +140,13 @@ __global__ void __launch_bounds__(MT, 1) k_micro_free(const u64 *__restrict__ of
             }
     }
     MCLK(18)
-    // 3. table lookup + delete for the first copy of each key (8-lane tiles, 4 keys per warp),
+    // 3. table lookup + delete for the first copy of each key (2-lane tiles, table::KPW keys per warp),
     //    the copies classified from it: live -> 1 ok + copies-1 double; start of a free block ->
     //    all double; otherwise all invalid.  ve[q] = size of the freed block at key q (0: none).
     {
         u64 ok = 0, dbl = 0, inv = 0, units = 0;
-        const u32 g = lane >> 3, sub = lane & 7;
-        for (u32 base = warp * 4; base < ((nk + 3) & ~3u); base += (MT / 32) * 4) {
+        const u32 g = lane / table::TILE_LANES, sub = lane % table::TILE_LANES;
+        for (u32 base = warp * table::KPW; base < ((nk + table::KPW - 1) & ~(u32)(table::KPW - 1)); base += (MT / 32) * table::KPW) {
             const u32 q = base + g;
             const bool in = q < nk;
             const u32 key = in ? vs[q] : 0;
@@ -448,11 +448,11 @@ __global__ void __launch_bounds__(MT, 1) k_micro_alloc(const u64 *__restrict__ s
         }
     __syncthreads();
     MCLK(24)
-    // results, block-table inserts (8-lane tiles), counters
+    // results, block-table inserts (2-lane tiles), counters
     {
         u64 ok = 0, fail = 0, units = 0, used = 0, tomb = 0, full = 0, hw = 0;
-        const u32 g = lane >> 3, sub = lane & 7;
-        for (u32 base = warp * 4; base < (((u32)n + 3) & ~3u); base += (MT / 32) * 4) {
+        const u32 g = lane / table::TILE_LANES, sub = lane % table::TILE_LANES;
+        for (u32 base = warp * table::KPW; base < (((u32)n + table::KPW - 1) & ~(u32)(table::KPW - 1)); base += (MT / 32) * table::KPW) {
             const u32 i = base + g;
             const bool in = i < n;
             const u32 o = in ? res[i] : NONE;
@@ -512,9 +512,9 @@ __global__ void __launch_bounds__(MT, 1) k_micro_alloc(const u64 *__restrict__ s
     __syncthreads();
     const u32 nl = s_cnt;
     {
-        const u32 g = lane >> 3;
+        const u32 g = lane / table::TILE_LANES;
         u64 full = 0;
-        for (u32 base = warp * 4; base < ((nl + 3) & ~3u); base += (MT / 32) * 4) {
+        for (u32 base = warp * table::KPW; base < ((nl + table::KPW - 1) & ~(u32)(table::KPW - 1)); base += (MT / 32) * table::KPW) {
             const u32 i = base + g;
             const bool in = i < nl;
             const u64 v = in ? scratch[i] : 0;

@@ -105,7 +105,7 @@ __device__ __forceinline__ bool bsearch_free(const u64 *a, u64 n, u64 key) {
     return lo < n && a[lo] == key;
 }
 
-// Read-only resolution of every sorted key (one 8-lane tile per key, as table::lookup).
+// Read-only resolution of every sorted key (one table tile per key, as table::lookup).
 // kind[i]: K_INSIDE (own[i] = the live block's start, endu[i] = its end), K_DOUBLE (start of a
 // free block), K_INVALID (free memory that is not a block start).
 __global__ void __launch_bounds__(256) k_resolve(const u32 *__restrict__ keys, const u64 *nk_dev,
@@ -115,10 +115,10 @@ __global__ void __launch_bounds__(256) k_resolve(const u32 *__restrict__ keys, c
                                                  u64 *__restrict__ endu, DevCtr *ctr) {
     PDL_ENTRY();
     const u64 nk = *nk_dev, F = *F_dev;
-    const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
+    const u32 lane = lane_id(), g = lane / table::TILE_LANES, sub = lane % table::TILE_LANES;
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
-    for (u64 base = gw * 4; base < nk; base += nwarps * 4) {
+    for (u64 base = gw * table::KPW; base < nk; base += nwarps * table::KPW) {
         const u64 idx = base + g;
         const bool in = idx < nk;
         const u32 u = in ? keys[idx] : 0;
@@ -154,11 +154,11 @@ __global__ void __launch_bounds__(256) k_apply(const u32 *__restrict__ keys, con
     PDL_ENTRY();
     __shared__ u64 sm[33];
     const u64 nk = *nk_dev;
-    const u32 lane = lane_id(), g = lane >> 3, sub = lane & 7;
+    const u32 lane = lane_id(), g = lane / table::TILE_LANES, sub = lane % table::TILE_LANES;
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
     u64 c_ok = 0, c_dbl = 0, c_inv = 0, c_units = 0, c_whole = 0;
-    for (u64 base = gw * 4; base < nk; base += nwarps * 4) {
+    for (u64 base = gw * table::KPW; base < nk; base += nwarps * table::KPW) {
         const u64 idx = base + g;
         const bool in = idx < nk;
         const u32 k = in ? kind[idx] : K_INVALID;

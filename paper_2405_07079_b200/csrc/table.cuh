@@ -4,8 +4,11 @@
 // B200 design (differs from the paper's chained 6-word entries):
 //   * one 8-byte slot per live block: (key << 32) | (size_units - 1), key = offset / align;
 //     free-list links and prev_adj are not needed because free blocks live in sorted arrays;
-//   * linear probing over whole 128-byte lines (16 slots): a probe is one coalesced line
-//     read by an 8-lane tile (16 B per lane), match/empty found with one warp ballot;
+//   * linear probing over 32-byte sectors (4 slots): a probe is one sector read by a 2-lane tile
+//     (16 B per lane), match/empty found with one warp ballot, 16 keys per warp.  Round 1 probed
+//     whole 128-byte lines with 8-lane tiles; the sector probe cut config 5's lookup kernel from
+//     41 to 25 us (ncu) but not its DRAM bytes (~126 B per free either way: a random access fills a
+//     128-byte L2 line from HBM);
 //   * delete writes a TOMBSTONE; insert reuses the first EMPTY-or-TOMBSTONE slot of the first
 //     line that has one (CAS); lookup stops at the first line containing an EMPTY slot, which
 //     is sound because slots only become EMPTY again in a full rebuild.
@@ -17,8 +20,9 @@ namespace table {
 
 constexpr u64 EMPTY = 0xFFFFFFFFFFFFFFFFull;
 constexpr u64 TOMB = 0xFFFFFFFFFFFFFFFEull;
-constexpr int TILE_LANES = 8;   // lanes per key (4 keys per warp)
-constexpr int LINE = 16;        // slots per 128-byte line
+constexpr int TILE_LANES = 2;   // lanes per key
+constexpr int KPW = 32 / TILE_LANES;   // keys per warp
+constexpr int LINE = 4;         // slots per probed 32-byte sector (2 per lane)
 
 __device__ __forceinline__ u64 pack(u64 key, u64 size_units) { return (key << 32) | (size_units - 1); }
 __device__ __forceinline__ bool is_live(u64 s) { return s < TOMB; }
@@ -36,8 +40,8 @@ __device__ __forceinline__ u64 home_line(u64 key, u64 mask) {
 // inactive group pass active = false.  Returns the live slot value found (EMPTY if the key is
 // absent) on every lane of the group.
 __device__ u64 lookup(u64 *__restrict__ slots, u64 mask, u64 key, bool active, u64 repl, u64 max_lines) {
-    const u32 lane = lane_id(), sub = lane & (TILE_LANES - 1), g = lane >> 3;
-    const u32 gmask = 0xFFu << (g * 8);
+    const u32 lane = lane_id(), sub = lane & (TILE_LANES - 1), g = lane / TILE_LANES;
+    const u32 gmask = ((1u << TILE_LANES) - 1u) << (g * TILE_LANES);
     u64 line = active ? home_line(key, mask) : 0;
     u64 result = EMPTY;
     bool done = !active;
@@ -81,8 +85,8 @@ __device__ u64 lookup(u64 *__restrict__ slots, u64 mask, u64 key, bool active, u
 // other lanes; 2 on lane sub==0 if no slot was found within max_lines (table full).
 __device__ int insert(u64 *__restrict__ slots, u64 mask, u64 key, u64 size_units, bool active,
                       u64 max_lines) {
-    const u32 lane = lane_id(), sub = lane & (TILE_LANES - 1), g = lane >> 3;
-    const u32 gmask = 0xFFu << (g * 8);
+    const u32 lane = lane_id(), sub = lane & (TILE_LANES - 1), g = lane / TILE_LANES;
+    const u32 gmask = ((1u << TILE_LANES) - 1u) << (g * TILE_LANES);
     const u64 nv = active ? pack(key, size_units) : 0;
     u64 line = active ? home_line(key, mask) : 0;
     bool done = !active;
