@@ -111,6 +111,12 @@ struct Smem {
 #ifdef SMEM_PAD
     u32 pad_[SMEM_PAD];           // experiment: shared memory taken from the L1 carveout
 #endif
+    // two-warp engine (non-LIFO): warp 1 applies the arrivals of a chunk while warp 0 updates the
+    // classes that lost members; classes touched by both (etag == ctag) stay on warp 0
+    u32 etag[MAX_NC];             // chunk tag of the last chunk that popped / carved class k
+    u32 dg[32], dnk[32];          // per lane: its arrival group (dropper mask, 0 if not a leader), class
+    u32 ctag, eng_done, broken1;
+    u64 w1_visits, w1_inserts;
     u64 dkey[32];                 // the chunk's droppers in time order: (drop class << 32 | f) ...
     u32 dlane[32];                // ... and their lanes (the dirty check reads them as broadcasts)
 };
@@ -222,14 +228,11 @@ __device__ __forceinline__ u32 first_ge(const Smem &S, u32 sw, u32 c, int NC) {
     return (w2 << 5) + __ffs(S.cw[w2]) - 1;
 }
 
-__device__ __forceinline__ void set_bit(Smem &S, u32 k) {
-    atomicOr(&S.cw[k >> 5], 1u << (k & 31));
-    atomicOr(&S.sw, 1u << (k >> 5));
-}
-__device__ __forceinline__ void clear_bit(Smem &S, u32 k) {
-    u32 old = atomicAnd(&S.cw[k >> 5], ~(1u << (k & 31)));
-    if ((old & ~(1u << (k & 31))) == 0) atomicAnd(&S.sw, ~(1u << (k >> 5)));
-}
+// The first-level summary is not maintained here: each chunk recomputes it from the second-level
+// words with one ballot, so the arrivals warp and the class-update warp can set and clear bits of
+// the same word concurrently (atomics on cw only).
+__device__ __forceinline__ void set_bit(Smem &S, u32 k) { atomicOr(&S.cw[k >> 5], 1u << (k & 31)); }
+__device__ __forceinline__ void clear_bit(Smem &S, u32 k) { atomicAnd(&S.cw[k >> 5], ~(1u << (k & 31))); }
 
 struct Csr {
     const uint4 *r4;   // class-sorted {f, batch-start start, end - 1, 0} (one 16-byte record per member)
@@ -406,8 +409,38 @@ __device__ void arrive_lifo(Smem &S, const Lifo &lf, u32 k, u32 f, u32 s, u32 e1
     S.hn[k] = (unsigned char)(n + 1);
 }
 
+__device__ __forceinline__ void bar_sync_64(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void bar_arrive_64(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+
+// Warp 1 of the two-warp engine: per chunk, waits for warp 0's hand-off (named barrier 1), applies
+// the arrivals of every group whose class warp 0 is not updating in the same chunk, and signals
+// completion (barrier 2).  Classes are disjoint between the two warps within a chunk, the
+// availability words are updated with atomics, and new overflow slots are numbered atomically.
+__device__ void arrivals_worker(Smem &S, Heap hp) {
+    const u32 lane = lane_id();
+    for (;;) {
+        bar_sync_64(1);
+        if (S.eng_done) break;
+        const u32 tag = S.ctag, g = S.dg[lane], k = S.dnk[lane];
+        if (g && S.etag[k] != tag) {
+            u32 mm = g;
+            while (mm) {
+                const u32 d = __ffs(mm) - 1;
+                mm &= mm - 1;
+                arrive(S, hp, k, S.res_f[d], (u32)(S.res_s[d] + S.ch_r[d]), S.res_e[d]);
+            }
+        }
+        if (hp.broken) S.broken1 = 1;
+        bar_arrive_64(2);
+    }
+    const u64 v = warp_sum64(hp.visits), ins = warp_sum64(hp.inserts);
+    if (lane == 0) { S.w1_visits = v; S.w1_inserts = ins; }
+    __syncwarp();
+    bar_arrive_64(3);                            // its counters are in
+}
+
 template <bool LIFO>
-__global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict__ off,
+__global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict__ off,
                                                   u64 *__restrict__ fs, const u64 *__restrict__ fe,
                                                   const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
                                                   u64 *__restrict__ out_u, u32 *bm, u64 w0, u64 w1, u64 w2,
@@ -425,7 +458,14 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     const u32 lane = lane_id();
     const u64 nslots = (u64)NC;
     Heap hp{bm, bm + nslots * w0, bm + nslots * (w0 + w1), w0, w1, w2, S.slot, &S.nslot, S.ow_i, S.ow_v, 0, false};
-    if (lane == 0) S.nslot = 0;
+    const bool two = !LIFO && blockDim.x == 64;   // warp 1 applies arrivals (arrivals_worker)
+    if (threadIdx.x >= 32) {
+        bar_sync_64(4);                           // warp 0 has built the class state
+        if (two) arrivals_worker(S, hp);
+        return;
+    }
+    if (lane == 0) { S.nslot = 0; S.eng_done = 0; S.broken1 = 0; S.w1_visits = 0; S.w1_inserts = 0; }
+    for (int k = lane; k < MAX_NC; k += 32) S.etag[k] = NONE;
     // ---- init: CSR ranges, head caches, bitmaps ----
     for (int k = lane; k < NC; k += 32) {
         u32 b = off[k], e = off[k + 1];
@@ -458,6 +498,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         if (lane == 0) S.sw = swl;
     }
     __syncwarp();
+    if (blockDim.x == 64) bar_arrive_64(4);      // releases warp 1 (named barriers: warp-specialised)
     u64 rb_base = 0, rb_end = 0;
     u32 keep = 0;          // wilderness mode: candidates carried over from the previous chunk
     u64 resume = 0;        // ... and where its gather stopped
@@ -469,11 +510,11 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
     while (pos < n) {
         n_iter++;
         // watchdogs: the engine must terminate even if an invariant broke (reported as error)
-        if (__any_sync(FULLMASK, hp.broken) || n_iter > n + 64) {
-            if (lane == 0 && stats) stats[2] = hp.broken ? 4 : 3;
+        if (__any_sync(FULLMASK, hp.broken) || S.broken1 || n_iter > n + 64) {
+            if (lane == 0 && stats) stats[2] = (hp.broken || S.broken1) ? 4 : 3;
             break;
         }
-        const u32 sw = S.sw;
+        const u32 sw = __ballot_sync(FULLMASK, S.cw[lane] != 0u);   // NC <= 32 * 32
         u64 i = NIL64, ri = 0, scan_end = 0;
         u32 ci = NONE, limit = 0;
         bool act = false;
@@ -569,7 +610,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             n_rounds++;
             if (round > (u32)NC + 2) {
                 if (lane == 0 && stats) stats[2] = 2;
-                return;
+                goto engine_end;
             }
             const bool part = act && k != NONE;
             peers = (round == 0 && have_pm) ? pm_fin : __match_any_sync(FULLMASK, part ? k : (0x40000000u | lane));
@@ -741,7 +782,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
 #endif
         if (commit == 0) {               // cannot happen (lane 0 is never dirty); never hang
             if (lane == 0 && stats) stats[2] = 1;
-            return;
+            goto engine_end;
         }
         const bool cm = act && lane < commit;
         t_dirty += ENG_CLK() - t0;
@@ -765,6 +806,21 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         t_store += ENG_CLK() - t0;
         const u32 leftm = __ballot_sync(FULLMASK, cm && part && mynk != SAME);
         const u32 staym = __ballot_sync(FULLMASK, cm && part && mynk == SAME && last_on_block);
+        // arrival groups (the first committed dropper of each remainder class leads its group)
+        const bool cdrop = cm && dropper;
+        const u32 g = samecls & (commit >= 32 ? FULLMASK : ((1u << commit) - 1u));   // committed ones
+        const u32 mygrp = (cdrop && (g & lanemask_lt()) == 0) ? g : 0u;
+        const u32 ctag = (u32)n_iter;
+        if (two) {
+            // hand the arrivals to warp 1: the classes this warp updates are tagged first, and
+            // warp 1 applies only the groups of untagged classes
+            if (cm && part && rank == 0 && ((leftm | staym) & peers)) S.etag[k] = ctag;
+            S.dg[lane] = mygrp;
+            S.dnk[lane] = mynk;
+            if (lane == 0) S.ctag = ctag;
+            __syncwarp();
+            bar_arrive_64(1);
+        }
         bool rf = false;                         // this leader's class lost members: refill
         if (cm && part && rank == 0) {
             const u32 left = __popc(leftm & peers);
@@ -807,9 +863,8 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         t_cls += ENG_CLK() - t0;
         t0 = ENG_CLK();
         // ---- remainders join their new classes (grouped by class, time order) ----
-        const bool cdrop = cm && dropper;
-        const u32 g = samecls & (commit >= 32 ? FULLMASK : ((1u << commit) - 1u));   // committed ones
-        if (cdrop && (g & lanemask_lt()) == 0) {
+        // (two-warp engine: only the groups of classes this warp updated; warp 1 does the rest)
+        if (mygrp && (!two || S.etag[mynk] == ctag)) {
             u32 mm = g;
             while (mm) {
                 const u32 d = __ffs(mm) - 1;
@@ -820,6 +875,7 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
             }
         }
         __syncwarp();
+        if (two) bar_sync_64(2);                 // warp 1's arrivals are in
         t_arr += ENG_CLK() - t0;
         if (!wmode) {
             pos += commit;
@@ -838,10 +894,18 @@ __global__ void __launch_bounds__(32, 1) k_engine(Csr csr, const u32 *__restrict
         }
         __syncwarp();
     }
+engine_end:
+    if (two) {                                   // release warp 1 and wait for its counters
+        if (lane == 0) S.eng_done = 1;
+        __syncwarp();
+        bar_arrive_64(1);
+        bar_sync_64(3);
+    }
     if (slot_map)
         for (int k = lane; k < NC; k += 32) slot_map[k] = S.slot[k];   // for k_bitheap_clear
     if (stats) {
         u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits, nr = n_refill, ins = hp.inserts;
+        if (two && lane == 0) { vis += S.w1_visits; ins += S.w1_inserts; }
         u64 tmax = (u64)t_refill;
         for (int o = 16; o > 0; o >>= 1) {
             nr += __shfl_xor_sync(FULLMASK, nr, o);

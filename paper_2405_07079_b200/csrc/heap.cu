@@ -280,6 +280,7 @@ struct heap {
     int bf_flat;             // BEST_FIT: the flat one-array engine instead of the blocked one (env HEAP_BF_FLAT=1)
     int micro;               // small heap: each batch is one single-CTA launch (micro.cuh); env HEAP_MICRO=0 disables
     int pdl;                 // programmatic dependent launches (env HEAP_PDL=0 disables)
+    int eng_warps;           // TLSF/SEGFIT engine: 2 = arrivals on a second warp (default), 1 = one warp (HEAP_ENGINE_WARPS=1)
     int bud_levels;          // BUDDY free phase: the level-by-level kernel instead of the parallel form (env HEAP_BUDDY_LEVELS=1)
     Layout L;
     void *ws;
@@ -617,6 +618,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         h->wild_split = (ws && ws[0] == '0') ? 0 : 1;
         const char *bf = getenv("HEAP_BF_FLAT");
         h->bf_flat = (bf && bf[0] == '1') ? 1 : 0;
+        const char *ew = getenv("HEAP_ENGINE_WARPS");
+        h->eng_warps = (ew && ew[0] == '1') ? 1 : 2;
         const char *pd = getenv("HEAP_PDL");
         h->pdl = (pd && pd[0] == '0') ? 0 : 1;
         const char *bl = getenv("HEAP_BUDDY_LEVELS");
@@ -1014,7 +1017,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         TAG(h, HEAP_TAG_ENGINE);
         {
             tlsfw::Csr csr{h->cs};
-            LAUNCH(h, tlsfw::k_engine<false>, 1, 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
+            LAUNCH(h, tlsfw::k_engine<false>, 1, h->eng_warps * 32, sizeof(tlsfw::Smem), s, csr, h->off, h->fs[cur], h->fe[cur], h->r,
                    h->c, n, h->out, h->bm, L.bm_w0, L.bm_w1, L.bm_w2, h->slot, L.NC, L.L, C->eng, tlsfw::Lifo{}, n_in,
                    (const u32 *)C->wild);
         }

@@ -152,6 +152,18 @@ def test_wild_split_both_paths(case, split, monkeypatch):
         assert used > 0
 
 
+@pytest.mark.parametrize("warps", ["1", "2"])
+@pytest.mark.parametrize("case", WILD_CASES[1:4], ids=lambda c: f"p{c[0]}-A{c[1]}-B{c[3]}")
+def test_engine_one_and_two_warps(case, warps, monkeypatch):
+    """The TLSF/SEGFIT engine with its arrivals applied by a second warp concurrently with the class
+    updates (default) and with one warp doing both (HEAP_ENGINE_WARPS=1): both bit-exact with
+    Oracle-L, state compared after every batch."""
+    monkeypatch.setenv("HEAP_ENGINE_WARPS", warps)
+    pol, arena, align, batch, ops, sizes, rho = case
+    cfg = tg.custom(pol, arena, align, batch, rho=rho, total_ops=ops, sizes=sizes, idx=85 + pol)
+    run_parity(cfg, max_live=max(1 << 15, 8 * batch), max_batch=batch, every_batch_state=True)
+
+
 BF_CASES = [
     # (arena, batch, ops, sizes, rho): blocked engine (chunk pool) and, for the 20000-request
     # batches, the flat global-memory fallback
