@@ -116,6 +116,13 @@ struct Smem {
     u32 etag[MAX_NC];             // chunk tag of the last chunk that popped / carved class k
     u32 dg[32], dnk[32];          // per lane: its arrival group (dropper mask, 0 if not a leader), class
     u32 ctag, eng_done, broken1;
+    // warp 1 also gathers the next chunk's candidates (wilderness mode): carried-over candidates
+    // of this chunk first, then requests from g_scan with search class <= g_mx
+    u64 nx_i[32], nx_r[32];
+    u32 nx_c[32];
+    u32 nx_n, g_need, g_commit, g_limit;
+    int g_mx;
+    u64 nx_scan, g_scan;
     u64 w1_visits, w1_inserts;
     u64 dkey[32];                 // the chunk's droppers in time order: (drop class << 32 | f) ...
     u32 dlane[32];                // ... and their lanes (the dirty check reads them as broadcasts)
@@ -412,12 +419,63 @@ __device__ void arrive_lifo(Smem &S, const Lifo &lf, u32 k, u32 f, u32 s, u32 e1
 __device__ __forceinline__ void bar_sync_64(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void bar_arrive_64(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
 
+// Candidates of the next chunk (wilderness mode): the uncommitted candidates [commit, limit) of the
+// current chunk first (time order), then requests from `sc` whose search class is at most Mx
+// (requests above Mx are WILD or fail — written here, they never enter a chunk; a stale, higher Mx
+// only admits candidates the engine then marks itself).  Stages requests through rbuf/cbuf.
+// Returns the candidate count; *scan_end = where the scan stopped.
+__device__ u32 gather_next(Smem &S, const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
+                           u64 *__restrict__ out_u, u64 &rb_base, u64 &rb_end, int Mx, u32 commit, u32 limit,
+                           u64 sc, u64 *di, u64 *dr, u32 *dc, u64 *scan_end) {
+    const u32 lane = lane_id();
+    u32 ncand = limit > commit ? limit - commit : 0u;
+    {
+        u64 a = 0, b = 0;
+        u32 c = 0;
+        if (lane < ncand) { a = S.ch_i[commit + lane]; b = S.ch_r[commit + lane]; c = S.ch_c[commit + lane]; }
+        __syncwarp();
+        if (lane < ncand) { di[lane] = a; dr[lane] = b; dc[lane] = c; }
+    }
+    while (ncand < 32 && sc < n) {
+        if (sc < rb_base || sc + 32 > rb_end) {
+            __syncwarp();
+            rb_base = sc;
+            rb_end = sc + RB < n ? sc + RB : n;
+            for (u64 j = lane; j < rb_end - rb_base; j += 32) {
+                S.rbuf[j] = R[rb_base + j];
+                S.cbuf[j] = C[rb_base + j];
+            }
+            __syncwarp();
+        }
+        const u64 j = sc + lane;
+        const bool v = j < n;
+        const u64 rj = v ? S.rbuf[j - rb_base] : 0;
+        const u32 cj = v ? S.cbuf[j - rb_base] : NONE;
+        const bool cand = v && rj != 0 && (int)cj <= Mx;
+        const u32 cmask = __ballot_sync(FULLMASK, cand);
+        const u32 take = min((u32)__popc(cmask), 32u - ncand);
+        const u32 rk = __popc(cmask & lanemask_lt());
+        if (cand && rk < take) { di[ncand + rk] = j; dr[ncand + rk] = rj; dc[ncand + rk] = cj; }
+        u64 nsc = sc + 32 < n ? sc + 32 : n;               // scanning stops at the first one not taken
+        const u32 firstout = __ballot_sync(FULLMASK, cand && rk == take);
+        if (firstout) nsc = sc + __ffs(firstout) - 1;
+        if (v && !cand && j < nsc) out_u[j] = rj != 0 ? WILD : HEAP_NULL_U64;
+        ncand += take;
+        sc = nsc;
+    }
+    __syncwarp();
+    *scan_end = sc;
+    return ncand;
+}
+
 // Warp 1 of the two-warp engine: per chunk, waits for warp 0's hand-off (named barrier 1), applies
 // the arrivals of every group whose class warp 0 is not updating in the same chunk, and signals
 // completion (barrier 2).  Classes are disjoint between the two warps within a chunk, the
 // availability words are updated with atomics, and new overflow slots are numbered atomically.
-__device__ void arrivals_worker(Smem &S, Heap hp) {
+__device__ void arrivals_worker(Smem &S, Heap hp, const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
+                                u64 *__restrict__ out_u) {
     const u32 lane = lane_id();
+    u64 rb_base = 0, rb_end = 0;                  // this warp's view of the request staging buffer
     for (;;) {
         bar_sync_64(1);
         if (S.eng_done) break;
@@ -431,6 +489,13 @@ __device__ void arrivals_worker(Smem &S, Heap hp) {
             }
         }
         if (hp.broken) S.broken1 = 1;
+        if (S.g_need) {                           // the next chunk's candidates
+            u64 se = 0;
+            const u32 nc = gather_next(S, R, C, n, out_u, rb_base, rb_end, S.g_mx, S.g_commit, S.g_limit, S.g_scan,
+                                       S.nx_i, S.nx_r, S.nx_c, &se);
+            if (lane == 0) { S.nx_n = nc; S.nx_scan = se; }
+        }
+        __syncwarp();
         bar_arrive_64(2);
     }
     const u64 v = warp_sum64(hp.visits), ins = warp_sum64(hp.inserts);
@@ -461,7 +526,7 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
     const bool two = !LIFO && blockDim.x == 64;   // warp 1 applies arrivals (arrivals_worker)
     if (threadIdx.x >= 32) {
         bar_sync_64(4);                           // warp 0 has built the class state
-        if (two) arrivals_worker(S, hp);
+        if (two) arrivals_worker(S, hp, R, C, n_in ? *n_in : n, out_u);
         return;
     }
     if (lane == 0) { S.nslot = 0; S.eng_done = 0; S.broken1 = 0; S.w1_visits = 0; S.w1_inserts = 0; }
@@ -502,13 +567,17 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
     u64 rb_base = 0, rb_end = 0;
     u32 keep = 0;          // wilderness mode: candidates carried over from the previous chunk
     u64 resume = 0;        // ... and where its gather stopped
+    bool prefetched = false;   // two-warp wilderness mode: warp 1 gathered this chunk's candidates
+    int mx_chunk = 0;          // Mx at this chunk's start (the next gather's bound: never below the truth)
     u64 n_iter = 0, n_retarget = 0, n_rounds = 0, n_qsteps = 0, n_refill = 0;
     long long t_refill = 0;
     long long t_spec = 0, t_dirty = 0, t_cls = 0, t_arr = 0, t_store = 0, t0;
     long long t_pop = 0, t_rcsr = 0, t_rovf = 0;   // class-update sub-phases (warp-level)
+    long long t_gather = 0;                        // candidate gather / request staging
     u64 pos = 0;
     while (pos < n) {
         n_iter++;
+        const long long tg0 = ENG_CLK();
         // watchdogs: the engine must terminate even if an invariant broke (reported as error)
         if (__any_sync(FULLMASK, hp.broken) || S.broken1 || n_iter > n + 64) {
             if (lane == 0 && stats) stats[2] = (hp.broken || S.broken1) ? 4 : 3;
@@ -543,8 +612,20 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
                 const u32 w = 31 - __clz(sw);
                 Mx = (int)(w * 32 + 31 - __clz(S.cw[w]));
             }
+            mx_chunk = Mx;
             u32 ncand = keep;                        // ch_*[0, keep) already hold candidates
             u64 sc = keep ? resume : pos;
+            if (prefetched) {                        // gathered by warp 1 during the last chunk
+                ncand = S.nx_n;
+                sc = S.nx_scan;
+                if (ncand == 0) { pos = sc; continue; }
+                act = lane < ncand;
+                if (act) { i = S.nx_i[lane]; ri = S.nx_r[lane]; ci = S.nx_c[lane]; }
+                S.ch_i[lane] = i;                    // this chunk's candidates, for the next carry-over
+                S.ch_c[lane] = ci;
+                limit = ncand;
+                scan_end = sc;
+            } else
             while (ncand < 32 && sc < n) {
                 if (sc < rb_base || sc + 32 > rb_end) {   // a retried chunk can start below
                     __syncwarp();
@@ -574,17 +655,20 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
                 ncand += take;
                 sc = nsc;
             }
-            __syncwarp();
-            if (ncand == 0) { pos = sc; continue; }
-            act = lane < ncand;
-            if (act) { i = S.ch_i[lane]; ri = S.ch_r[lane]; ci = S.ch_c[lane]; }
-            limit = ncand;
-            scan_end = sc;
+            if (!prefetched) {
+                __syncwarp();
+                if (ncand == 0) { pos = sc; continue; }
+                act = lane < ncand;
+                if (act) { i = S.ch_i[lane]; ri = S.ch_r[lane]; ci = S.ch_c[lane]; }
+                limit = ncand;
+                scan_end = sc;
+            }
         }
         __syncwarp();
         S.ch_r[lane] = ri;
         __syncwarp();
         t0 = ENG_CLK();
+        t_gather += t0 - tg0;
         const bool fail0 = act && (ri == 0 || ci >= (u32)NC);
         u32 k = (act && !fail0) ? first_ge(S, sw, ci, NC) : NONE;
         // light pre-rounds (count model): a lane ranked at or past its class's member count is
@@ -817,7 +901,14 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
             if (cm && part && rank == 0 && ((leftm | staym) & peers)) S.etag[k] = ctag;
             S.dg[lane] = mygrp;
             S.dnk[lane] = mynk;
-            if (lane == 0) S.ctag = ctag;
+            if (lane == 0) {
+                S.ctag = ctag;
+                S.g_need = wmode ? 1u : 0u;          // warp 1 gathers the next chunk's candidates
+                S.g_commit = commit;
+                S.g_limit = limit;
+                S.g_scan = scan_end;
+                S.g_mx = mx_chunk;
+            }
             __syncwarp();
             bar_arrive_64(1);
         }
@@ -879,6 +970,9 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
         t_arr += ENG_CLK() - t0;
         if (!wmode) {
             pos += commit;
+        } else if (two) {                            // warp 1 has gathered the next candidates
+            prefetched = true;
+            pos = S.nx_n ? S.nx_i[0] : S.nx_scan;
         } else if (commit < limit) {                 // carry the uncommitted candidates over
             keep = limit - commit;
             u64 ci_ = 0, cr_ = 0;
@@ -923,7 +1017,7 @@ engine_end:
             stats[0] += n_iter; stats[1] += t; stats[3] += n_rounds; stats[4] += q;
             stats[5] += t_spec; stats[6] += t_dirty; stats[7] += t_cls; stats[8] += t_arr; stats[9] += dl; stats[10] += vis; stats[11] += t_store;
             stats[12] += nr; stats[13] += tmax; stats[15] += ins;
-            stats[16] += t_pop; stats[17] += t_rcsr; stats[18] += t_rovf;
+            stats[16] += t_pop; stats[17] += t_rcsr; stats[18] += t_rovf; stats[19] += t_gather;
         }
     }
 }

@@ -35,4 +35,4 @@ for bi, (f, s, first) in enumerate(tg.Trace(cfg, total_ops=cfg.batch * nb)):
     print(f"b{bi} na={na} F={st['n_free']} step={dt*1e3:.1f}ms engine={eng:.1f}ms chunks={d[0]} "
           f"commit={na/max(d[0],1):.1f} rounds/chunk={d[3]/max(d[0],1):.2f} qsteps/round={d[4]/max(d[3],1):.2f} "
           f"reaims={d[1]} cyc/chunk spec={d[5]/max(d[0],1):.0f} dirty={d[6]/max(d[0],1):.0f} "
-          f"cls={d[7]/max(d[0],1):.0f}(store {d[11]/max(d[0],1):.0f} refills {d[12]} maxlane_refill_cyc/chunk {d[13]/max(d[0],1):.0f}) arr={d[8]/max(d[0],1):.0f} delmin={d[9]} visits={d[10]} ovf_inserts={d[15]} cls_split pop={d[16]/max(d[0],1):.0f} rcsr={d[17]/max(d[0],1):.0f} rovf={d[18]/max(d[0],1):.0f} fail={c[2]}", flush=True)
+          f"cls={d[7]/max(d[0],1):.0f}(store {d[11]/max(d[0],1):.0f} refills {d[12]} maxlane_refill_cyc/chunk {d[13]/max(d[0],1):.0f}) arr={d[8]/max(d[0],1):.0f} delmin={d[9]} visits={d[10]} ovf_inserts={d[15]} cls_split pop={d[16]/max(d[0],1):.0f} rcsr={d[17]/max(d[0],1):.0f} rovf={d[18]/max(d[0],1):.0f} gather={d[19]/max(d[0],1):.0f} fail={c[2]}", flush=True)
