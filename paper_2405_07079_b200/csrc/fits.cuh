@@ -598,13 +598,8 @@ __device__ __forceinline__ void bf_pos_remove(BfSmem &S, u32 i) {
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
-                                                  const u64 *__restrict__ r, u64 n, const u64 *n_in,
-                                                  u64 *__restrict__ out_u) {
-    PDL_ENTRY();
-    extern __shared__ __align__(16) unsigned char bf_raw[];
-    BfSmem &S = *reinterpret_cast<BfSmem *>(bf_raw);
-    if (n_in) n = *n_in;
+__device__ void bf_blocked(BfSmem &S, u64 *gkeys, const u64 *F_dev, int FB, u64 *fs, const u64 *__restrict__ r, u64 n,
+                           u64 *__restrict__ out_u) {
     const u32 lane = lane_id();
     const u64 nb = *F_dev;
     const u64 nc0_ = (nb + BF_FILL - 1) / BF_FILL;
@@ -697,6 +692,267 @@ __global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, 
         }
         __syncwarp();
     }
+}
+
+__global__ void __launch_bounds__(32) k_bf_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
+                                                  const u64 *__restrict__ r, u64 n, const u64 *n_in,
+                                                  u64 *__restrict__ out_u) {
+    PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char bf_raw[];
+    if (n_in) n = *n_in;
+    bf_blocked(*reinterpret_cast<BfSmem *>(bf_raw), gkeys, F_dev, FB, fs, r, n, out_u);
+}
+
+// ------------------------------------------------------ BEST FIT, class-indexed ----
+// The same key order (size << FB | f ascending = (size, address), Alg. 3 with reading C3) kept as a
+// doubly linked list of chunks of <= 32 keys in shared memory, with a TLSF-style class index over
+// it (the two-level class of the size, used here only as an index): per class its
+// member count and the chunk holding its smallest key, and a two-level bitmap of the nonempty
+// classes.  The smallest key >= (r << FB) is either in r's own class or the smallest key of the
+// first nonempty class above it (every size in a higher class exceeds r), so a search is one ffs on
+// the bitmap (first nonempty class >= cls(r)), one chunk load at that class's start chunk and one
+// ballot — a walk to the next chunk only when the class's members below r fill the rest of the
+// chunk.  No 32-ary search over chunk maxima, no position array to shift when a chunk splits or
+// empties.  Piece starts are kept in shared memory (u32 units) for the batch.  Results are those of
+// bf_blocked and bf_flat (same keys, same order).  Chunk budget: as bf_blocked (fill 24, splits
+// 32 -> 16 + 16, at most nc0/2 + n/16 splits); heaps beyond it, beyond BC_FS pieces or with unit
+// addresses >= 2^32 run bf_blocked.
+#ifndef BF_TIMING
+#define BF_TIMING 0   // phase clocks of k_bf_cls_engine into ctr->eng[0..5] (tools/micro/bf_probe.py)
+#endif
+constexpr u32 BC_CH = 512, BC_FILL = 24, BC_FS = 12288, BC_NC = 928;
+constexpr unsigned short BC_NIL = 0xFFFF;
+struct BcSmem {
+    u64 K[BC_CH * 32];                         // chunk c holds K[c*32 .. c*32 + cnt[c]), ascending
+    u32 fsm[BC_FS];                            // piece starts (units)
+    u32 ccnt[BC_NC];                           // members per class
+    unsigned short cch[BC_NC];                 // chunk holding the class's smallest key (ccnt > 0)
+    unsigned short nxt[BC_CH], prv[BC_CH], fl[BC_CH];
+    unsigned char cnt[BC_CH];
+    u32 cw[32];                                // nonempty classes, one bit per class
+};
+constexpr size_t BF_ENGINE_SMEM = sizeof(BcSmem) > sizeof(BfSmem) ? sizeof(BcSmem) : sizeof(BfSmem);
+
+__device__ __forceinline__ u32 bc_cls(u64 key, int FB) { return cls_insert(key >> FB, 5); }
+
+// first nonempty class >= c (NIL32 if none); sw = one bit per nonzero bitmap word
+__device__ __forceinline__ u32 bc_first_ge(const BcSmem &S, u32 sw, u32 c) {
+    if (c >= BC_NC) return NIL32;
+    const u32 w = c >> 5;
+    const u32 m = S.cw[w] & (0xFFFFFFFFu << (c & 31));
+    if (m) return (w << 5) + __ffs(m) - 1;
+    const u32 sm = (w >= 31) ? 0u : (sw & (0xFFFFFFFFu << (w + 1)));
+    if (!sm) return NIL32;
+    const u32 w2 = __ffs(sm) - 1;
+    return (w2 << 5) + __ffs(S.cw[w2]) - 1;
+}
+
+// the first key >= t: chunk c (BC_NIL: none), slot j, chunk count m, each lane's key v of chunk c.
+// kt = cls(t): keys of classes below kt are < t, so the walk starts at the first nonempty class >= kt.
+__device__ __forceinline__ void bc_find(const BcSmem &S, u32 sw, u32 kt, u64 t, u32 &c, u32 &j, u32 &m, u64 &v) {
+    const u32 lane = lane_id();
+    const u32 k1 = bc_first_ge(S, sw, kt);
+    c = (k1 == NIL32) ? (u32)BC_NIL : (u32)S.cch[k1];
+    j = 0;
+    m = 0;
+    v = 0;
+    while (c != BC_NIL) {
+        m = S.cnt[c];
+        v = lane < m ? S.K[c * 32 + lane] : 0ull;
+        const u32 b = __ballot_sync(FULLMASK, lane < m && v >= t);
+        if (b) { j = __ffs(b) - 1; return; }
+        c = S.nxt[c];
+    }
+}
+
+__global__ void __launch_bounds__(32) k_bf_cls_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
+                                                      const u64 *__restrict__ r, u64 n, const u64 *n_in,
+                                                      u64 *__restrict__ out_u, int cls_ok, u64 *dbg) {
+    PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char bf_raw[];
+    if (n_in) n = *n_in;
+    const u32 lane = lane_id();
+    const u64 F = *F_dev;
+    const u64 nc0 = (F + BC_FILL - 1) / BC_FILL;
+#if BF_TIMING
+    long long tq = clock64(), tph[6] = {0, 0, 0, 0, 0, 0};
+#define BF_T(k) do { const long long _t = clock64(); tph[k] += _t - tq; tq = _t; } while (0)
+#else
+#define BF_T(k) do { } while (0)
+#endif
+    if (!cls_ok || F > BC_FS || nc0 + (nc0 + 1) / 2 + (n + 15) / 16 + 2 > BC_CH) {
+        bf_blocked(*reinterpret_cast<BfSmem *>(bf_raw), gkeys, F_dev, FB, fs, r, n, out_u);
+        return;
+    }
+    BcSmem &S = *reinterpret_cast<BcSmem *>(bf_raw);
+    const u64 fmask = (1ull << FB) - 1;
+    // ---- build: chunks of BC_FILL keys in order, class starts and counts, bitmap ----
+    for (u32 k = lane; k < BC_NC; k += 32) S.ccnt[k] = 0;
+    for (u64 x = lane; x < F; x += 32) {
+        S.K[(x / BC_FILL) * 32 + x % BC_FILL] = gkeys[x];
+        S.fsm[x] = (u32)fs[x];
+    }
+    for (u32 c = lane; c < (u32)nc0; c += 32) {
+        S.cnt[c] = (unsigned char)min((u64)BC_FILL, F - (u64)c * BC_FILL);
+        S.nxt[c] = (unsigned short)(c + 1 < nc0 ? c + 1 : BC_NIL);
+        S.prv[c] = (unsigned short)(c ? c - 1 : BC_NIL);
+    }
+    for (u32 c = (u32)nc0 + lane; c < BC_CH; c += 32) S.fl[BC_CH - 1 - c] = (unsigned short)c;   // lowest id popped first
+    u32 nfl = BC_CH - (u32)nc0;
+    __syncwarp();
+    for (u64 x = lane; x < F; x += 32) {                 // class starts: chunk of the first key, start index
+        const u32 k = bc_cls(gkeys[x], FB);
+        if (x == 0 || bc_cls(gkeys[x - 1], FB) != k) { S.cch[k] = (unsigned short)(x / BC_FILL); S.ccnt[k] = (u32)x; }
+    }
+    __syncwarp();
+    for (u64 x = lane; x < F; x += 32) {                 // class ends: count
+        const u32 k = bc_cls(gkeys[x], FB);
+        if (x + 1 == F || bc_cls(gkeys[x + 1], FB) != k) S.ccnt[k] = (u32)x - S.ccnt[k] + 1;
+    }
+    __syncwarp();
+    for (u32 w = 0; w < 32; w++) {
+        const u32 k = w * 32 + lane;
+        const u32 b = __ballot_sync(FULLMASK, k < BC_NC && S.ccnt[k] > 0);
+        if (lane == 0) S.cw[w] = b;
+    }
+    __syncwarp();
+    u32 sw = __ballot_sync(FULLMASK, S.cw[lane] != 0u);
+    u32 tail = nc0 ? (u32)nc0 - 1 : (u32)BC_NIL;      // last chunk (the list's head is never needed)
+    BF_T(0);
+    // ---- requests in order ----
+    for (u64 i0 = 0; i0 < n; i0 += 32) {
+        const u64 il = i0 + lane;
+        const u64 rl = il < n ? r[il] : 0ull;
+        const u32 kl = rl ? cls_insert(rl, 5) : 0u;      // r <= A_u < 2^32
+        const u32 nj = (n - i0) < 32 ? (u32)(n - i0) : 32u;
+        for (u32 jj = 0; jj < nj; jj++) {
+            const u64 ri = __shfl_sync(FULLMASK, rl, jj);
+            const u32 kr = __shfl_sync(FULLMASK, kl, jj);
+            const u64 i = i0 + jj;
+            if (ri == 0) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+            u32 c, j, m;
+            u64 v;
+            bc_find(S, sw, kr, ri << FB, c, j, m, v);
+            if (c == BC_NIL) { if (lane == 0) out_u[i] = HEAP_NULL_U64; continue; }
+            BF_T(1);
+            const u64 key = __shfl_sync(FULLMASK, v, j);
+            const u64 pv = __shfl_sync(FULLMASK, v, j ? j - 1 : 0);
+            const u64 z = key >> FB;
+            const u32 f = (u32)(key & fmask);
+            const u32 k = cls_insert(z, 5);
+            const u32 s0 = S.fsm[f];
+            const bool first = S.cch[k] == c && (j == 0 || bc_cls(pv, FB) != k);
+            const u32 cc = S.ccnt[k] - 1;
+            const u32 cn = S.nxt[c], cp = S.prv[c];
+            const u32 cwk = S.cw[k >> 5];
+            __syncwarp();
+            // ---- delete slot j of chunk c ----
+            const u32 m1 = m - 1;
+            if (lane > j && lane < m) S.K[c * 32 + lane - 1] = v;
+            if (lane == 0) {
+                S.cnt[c] = (unsigned char)m1;
+                S.ccnt[k] = cc;
+                if (cc == 0) S.cw[k >> 5] = cwk & ~(1u << (k & 31));
+                else if (first) S.cch[k] = (unsigned short)((j < m1) ? c : cn);
+                if (m1 == 0) {                               // chunk emptied: unlink, free
+                    if (cp != BC_NIL) S.nxt[cp] = (unsigned short)cn;
+                    if (cn != BC_NIL) S.prv[cn] = (unsigned short)cp;
+                    S.fl[nfl] = (unsigned short)c;
+                }
+            }
+            if (cc == 0 && (cwk & ~(1u << (k & 31))) == 0u) sw &= ~(1u << (k >> 5));
+            if (m1 == 0) {
+                if (cn == BC_NIL) tail = cp;
+                nfl++;
+            }
+            __syncwarp();
+            BF_T(2);
+            // ---- the remainder (z - r, f) joins its class ----
+            const u64 z2 = z - ri;
+            if (z2) {
+                const u64 x = (z2 << FB) | f;
+                const u32 k2 = cls_insert(z2, 5);
+                u32 c2, j2, m2;
+                u64 v2;
+                bc_find(S, sw, k2, x, c2, j2, m2, v2);
+                BF_T(3);
+                if (c2 == BC_NIL) {                          // above every key: append to the tail chunk
+                    if (tail == BC_NIL) {                    // the list is empty: a fresh chunk
+                        c2 = S.fl[--nfl];
+                        __syncwarp();
+                        if (lane == 0) { S.nxt[c2] = BC_NIL; S.prv[c2] = BC_NIL; S.cnt[c2] = 0; }
+                        tail = c2;
+                        m2 = 0;
+                        v2 = 0;
+                    } else {
+                        c2 = tail;
+                        m2 = S.cnt[c2];
+                        v2 = lane < m2 ? S.K[c2 * 32 + lane] : 0ull;
+                    }
+                    j2 = m2;
+                }
+                if (m2 == 32) {                              // split: upper half to a new chunk after c2
+                    const u32 cN = S.fl[--nfl];
+                    const u32 c2n = S.nxt[c2];
+                    const u64 pl = __shfl_sync(FULLMASK, v2, lane ? lane - 1 : 0);
+                    __syncwarp();
+                    if (lane >= 16) {
+                        S.K[cN * 32 + lane - 16] = v2;
+                        const u32 kv = bc_cls(v2, FB);
+                        if (kv != bc_cls(pl, FB)) S.cch[kv] = (unsigned short)cN;   // class starts that moved
+                    }
+                    if (lane == 0) {
+                        S.cnt[c2] = 16;
+                        S.cnt[cN] = 16;
+                        S.nxt[cN] = (unsigned short)c2n;
+                        S.prv[cN] = (unsigned short)c2;
+                        S.nxt[c2] = (unsigned short)cN;
+                        if (c2n != BC_NIL) S.prv[c2n] = (unsigned short)cN;
+                    }
+                    if (c2n == BC_NIL) tail = cN;
+                    const u64 hi = __shfl_sync(FULLMASK, v2, (lane + 16) & 31);
+                    if (j2 > 16) { c2 = cN; j2 -= 16; v2 = hi; }
+                    m2 = 16;
+                    __syncwarp();
+                }
+                // is x the smallest member of class k2?  (its predecessor in key order is of a lower class)
+                u64 pk;
+                bool haspk = true;
+                if (j2 > 0) pk = __shfl_sync(FULLMASK, v2, j2 - 1);
+                else {
+                    const u32 p = S.prv[c2];
+                    if (p == BC_NIL) { haspk = false; pk = 0; }
+                    else pk = S.K[p * 32 + S.cnt[p] - 1];
+                }
+                const bool first2 = !haspk || bc_cls(pk, FB) != k2;
+                const u32 cc2 = S.ccnt[k2];
+                const u32 cwk2 = S.cw[k2 >> 5];
+                __syncwarp();
+                if (lane >= j2 && lane < m2) S.K[c2 * 32 + lane + 1] = v2;
+                if (lane == 0) {
+                    S.K[c2 * 32 + j2] = x;
+                    S.cnt[c2] = (unsigned char)(m2 + 1);
+                    S.ccnt[k2] = cc2 + 1;
+                    if (cc2 == 0) S.cw[k2 >> 5] = cwk2 | (1u << (k2 & 31));
+                    if (first2) S.cch[k2] = (unsigned short)c2;
+                }
+                sw |= 1u << (k2 >> 5);
+                BF_T(4);
+            }
+            if (lane == 0) {
+                out_u[i] = s0;
+                S.fsm[f] = s0 + (u32)ri;
+            }
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    for (u64 x = lane; x < F; x += 32) fs[x] = S.fsm[x];
+#if BF_TIMING
+    BF_T(5);
+    if (lane == 0) for (int k = 0; k < 6; k++) dbg[k] += (u64)tph[k];
+#endif
+#undef BF_T
 }
 
 // the flat engine with the array in shared memory (small heaps) or global memory

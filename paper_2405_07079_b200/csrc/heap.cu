@@ -617,7 +617,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         const char *ws = getenv("HEAP_WILD_SPLIT");
         h->wild_split = (ws && ws[0] == '0') ? 0 : 1;
         const char *bf = getenv("HEAP_BF_FLAT");
-        h->bf_flat = (bf && bf[0] == '1') ? 1 : 0;
+        h->bf_flat = (bf && bf[0] == '1') ? 1 : (bf && bf[0] == '2') ? 2 : 0;
         const char *ew = getenv("HEAP_ENGINE_WARPS");
         h->eng_warps = (ew && ew[0] == '1') ? 1 : 2;
         const char *pd = getenv("HEAP_PDL");
@@ -661,6 +661,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
                              (int)micro::ALLOC_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(fits::k_bf_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(fits::BfSmem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(fits::k_bf_cls_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)fits::BF_ENGINE_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_free_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)buddy::FREE_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_alloc_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1054,9 +1056,12 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
             } else {
                 LAUNCH(h, fits::k_bf_engine_flat<false>, 1, 32, 0, s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in, h->out);
             }
-        } else {
+        } else if (h->bf_flat == 2) {   // ablation (HEAP_BF_FLAT=2): the blocked engine without the class index
             LAUNCH(h, fits::k_bf_engine, 1, 32, sizeof(fits::BfSmem), s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in,
                    h->out);
+        } else {
+            LAUNCH(h, fits::k_bf_cls_engine, 1, 32, fits::BF_ENGINE_SMEM, s, keys, &C->F, L.FB, h->fs[cur], h->r, n,
+                   n_in, h->out, L.A_u <= 0xFFFFFFFFull ? 1 : 0, C->eng);
         }
     }
     // compact the surviving pieces into the other buffer (address order is kept)

@@ -168,18 +168,19 @@ BF_CASES = [
     # (arena, batch, ops, sizes, rho): blocked engine (chunk pool) and, for the 20000-request
     # batches, the flat global-memory fallback
     (1 << 16, 24, 1500, (4, 10), (1, 2)),
+    (1 << 14, 64, 4000, (4, 10), (1, 3)),               # the heap fills: the key list empties and refills
     (1 << 24, 3000, 40000, (4, 14), (2, 5)),
     (256 << 20, 4096, 120000, (4, 20), (1, 2)),        # config-2 shaped
     (1 << 26, 20000, 200000, (4, 12), (1, 2)),        # fallback: too many requests for the pool
 ]
 
 
-@pytest.mark.parametrize("flat", [False, True], ids=["blocked", "flat"])
+@pytest.mark.parametrize("engine", ["0", "2", "1"], ids=["classes", "blocked", "flat"])
 @pytest.mark.parametrize("case", BF_CASES, ids=lambda c: f"A{c[0]}-B{c[1]}")
-def test_best_fit_engines(case, flat, monkeypatch):
-    """BEST_FIT's blocked (chunked) and flat engines (fits.cuh k_bf_engine, bf_flat), both
-    bit-exact with Oracle-L."""
-    monkeypatch.setenv("HEAP_BF_FLAT", "1" if flat else "0")
+def test_best_fit_engines(case, engine, monkeypatch):
+    """BEST_FIT's class-indexed, blocked (chunked) and flat engines (fits.cuh k_bf_cls_engine,
+    k_bf_engine, bf_flat), each bit-exact with Oracle-L."""
+    monkeypatch.setenv("HEAP_BF_FLAT", engine)
     arena, batch, ops, sizes, rho = case
     cfg = tg.custom(tg.BEST_FIT, arena, 16, batch, rho=rho, total_ops=ops, sizes=sizes, idx=90)
     run_parity(cfg, max_live=max(1 << 15, 8 * batch), max_batch=batch, every_batch_state=batch < 100)
