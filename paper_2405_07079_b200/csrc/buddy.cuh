@@ -41,18 +41,22 @@ constexpr u64 FAIL = 0xFFFFFFFFFFFFFFFFull;
 // CTA-wide copy global -> shared with 8 independent loads per thread in flight (a plain
 // strided loop would serialise one global round trip per element)
 template <typename TS, typename TD>
-__device__ __forceinline__ void cta_copy(TD *dst, const TS *src, u64 n) {
-    for (u64 base = 0; base < n; base += 8 * NT) {
+__device__ __forceinline__ void cta_copy(TD *dst, const TS *src, u64 n64) {
+    const u32 n = (u32)n64, wb = threadIdx.x & ~31u;
+    for (u32 base = 0; base < n; base += 8 * NT) {
+        // warp-uniform step count: warps past the end skip the unrolled steps instead of running
+        // them predicated off (the kernel is issue-bound on its one SM)
+        const u32 kw = base + wb < n ? min(8u, (n - base - wb + NT - 1) / NT) : 0u;
         TS v[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            u64 i = base + (u64)k * NT + threadIdx.x;
-            v[k] = i < n ? src[i] : (TS)0;
+        for (u32 k = 0; k < 8; k++) {
+            const u32 i = base + k * NT + threadIdx.x;
+            if (k < kw) v[k] = i < n ? src[i] : (TS)0;
         }
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            u64 i = base + (u64)k * NT + threadIdx.x;
-            if (i < n) dst[i] = (TD)v[k];
+        for (u32 k = 0; k < 8; k++) {
+            const u32 i = base + k * NT + threadIdx.x;
+            if (k < kw && i < n) dst[i] = (TD)v[k];
         }
     }
 }
@@ -422,6 +426,7 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
                                                      u32 *btm, u32 *bsrc, u64 *__restrict__ out_u, int K,
                                                      DevCtr *ctr) {
     PDL_ENTRY();
+    extern __shared__ __align__(16) u32 astage_td[];   // the staging area, reused by the top-down
     __shared__ u64 ooff[41];
     __shared__ u64 doff[42], boff[42];
     __shared__ u32 ro[42];
@@ -465,27 +470,28 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
             cta_copy(st, btm, nb);
             cta_copy(ss, bsrc, nb);
             __syncthreads();
-            const u64 per = (nd + NT - 1) / NT;
-            const u64 diag = (u64)threadIdx.x * per;
-            if (diag < nd) {
-                u64 lo = diag > nb ? diag - nb : 0, hi = diag < nr ? diag : nr;
+            const u32 nd_ = (u32)nd, nr_ = (u32)nr, nb_ = (u32)nb, nt_ = (u32)n_t, nbor_ = (u32)nbor;
+            const u32 per = (nd_ + NT - 1) / NT;
+            const u32 diag = threadIdx.x * per;
+            if (diag < nd_) {
+                u32 lo = diag > nb_ ? diag - nb_ : 0, hi = diag < nr_ ? diag : nr_;
                 while (lo < hi) {
-                    const u64 mid = (lo + hi) >> 1;
+                    const u32 mid = (lo + hi) >> 1;
                     if (sr[mid] <= st[diag - mid - 1]) lo = mid + 1; else hi = mid;
                 }
-                u64 i = lo, j = diag - lo;
-                for (u64 k = 0; k < per && diag + k < nd; k++) {
-                    const u64 o = diag + k;
-                    const bool ta = (j >= nb) || (i < nr && sr[i] <= st[j]);
+                u32 i = lo, j = diag - lo;
+                const u32 oe = min(diag + per, nd_);
+                for (u32 o = diag; o < oe; o++) {
+                    const bool ta = (j >= nb_) || (i < nr_ && sr[i] <= st[j]);
                     ot[o] = ta ? sr[i] : st[j];
                     os[o] = ta ? sr[i] : ss[j];
                     if (ta) i++; else j++;
                 }
             }
             __syncthreads();
-            for (u64 o = threadIdx.x; o < nd; o += NT) { Dt[o] = ot[o]; Ds[o] = os[o]; }
+            for (u32 o = threadIdx.x; o < nd_; o += NT) { Dt[o] = ot[o]; Ds[o] = os[o]; }
             // borrow j carries the time of demand n_t + 2j (btm / bsrc were staged: free to rewrite)
-            for (u64 jb = threadIdx.x; jb < nbor; jb += NT) { btm[jb] = ot[n_t + 2 * jb]; bsrc[jb] = (u32)jb | BORROW; }
+            for (u32 jb = threadIdx.x; jb < nbor_; jb += NT) { btm[jb] = ot[nt_ + 2 * jb]; bsrc[jb] = jb | BORROW; }
             __syncthreads();
         } else if (nr + 2 * nb <= (u64)ALLOC_CAP) {
             // small level: staged inputs, the merge writes the demands and the borrows directly
@@ -495,26 +501,27 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
             cta_copy(st, btm, nb);
             cta_copy(ss, bsrc, nb);
             __syncthreads();
-            const u64 per = (nd + NT - 1) / NT;
-            const u64 diag = (u64)threadIdx.x * per;
-            if (diag < nd) {
-                u64 lo = diag > nb ? diag - nb : 0, hi = diag < nr ? diag : nr;
+            const u32 nd_ = (u32)nd, nr_ = (u32)nr, nb_ = (u32)nb, nt_ = (u32)n_t, nbor_ = (u32)nbor;
+            const u32 per = (nd_ + NT - 1) / NT;
+            const u32 diag = threadIdx.x * per;
+            if (diag < nd_) {
+                u32 lo = diag > nb_ ? diag - nb_ : 0, hi = diag < nr_ ? diag : nr_;
                 while (lo < hi) {
-                    const u64 mid = (lo + hi) >> 1;
+                    const u32 mid = (lo + hi) >> 1;
                     if (sr[mid] <= st[diag - mid - 1]) lo = mid + 1; else hi = mid;
                 }
-                u64 i = lo, j = diag - lo;
-                for (u64 k = 0; k < per && diag + k < nd; k++) {
-                    const u64 o = diag + k;
-                    const bool ta = (j >= nb) || (i < nr && sr[i] <= st[j]);
+                u32 i = lo, j = diag - lo;
+                const u32 oe = min(diag + per, nd_);
+                for (u32 o = diag; o < oe; o++) {
+                    const bool ta = (j >= nb_) || (i < nr_ && sr[i] <= st[j]);
                     const u32 tm = ta ? sr[i] : st[j];
                     const u32 sc = ta ? sr[i] : ss[j];
                     if (ta) i++; else j++;
                     Dt[o] = tm;
                     Ds[o] = sc;
-                    if (o >= n_t && !((o - n_t) & 1)) {
-                        const u64 bj = (o - n_t) >> 1;
-                        if (bj < nbor) { btm[bj] = tm; bsrc[bj] = (u32)bj | BORROW; }
+                    if (o >= nt_ && !((o - nt_) & 1)) {
+                        const u32 bj = (o - nt_) >> 1;
+                        if (bj < nbor_) { btm[bj] = tm; bsrc[bj] = bj | BORROW; }
                     }
                 }
             }
@@ -541,58 +548,78 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         bacc += nbor;
         nb = nbor;
     }
-    if (threadIdx.x == 0) { doff[K + 1] = dacc; boff[K + 1] = bacc; }
+    if (threadIdx.x == 0) { doff[K + 1] = dacc; boff[K + 1] = bacc; ctr->bud_nd = dacc; }
     __syncthreads();
 #if BUDDY_TIMING
     if (threadIdx.x == 0) { const long long t1 = clock64(); ctr->eng[20] += t1 - tb0; tb0 = t1; }
 #endif
     // ---- top-down ----
+    // Borrow addresses of adjacent orders live in shared memory (ping-pong, the staging area is free
+    // now) when the largest order's borrows fit; a level's own loads (its demands' sources and
+    // resident blocks) do not depend on the level above, so they are issued before the barrier that
+    // publishes the level above's borrow addresses: per level one barrier and shared-memory
+    // latency instead of a global round trip.
     __shared__ u64 s_left[41], s_cnt[41];
+    u64 maxb = 0;
+    for (int t = 0; t <= K; t++) maxb = max(maxb, boff[t + 1] - boff[t]);
+    const bool bsm = 2 * maxb * sizeof(u64) <= ALLOC_SMEM;
+    u64 *sbuf = reinterpret_cast<u64 *>(astage_td);
     for (int t = K; t >= 0; t--) {
         const u64 n_t = ooff[t + 1] - ooff[t];
         const u64 nd = doff[t + 1] - doff[t];
+#if BUDDY_TIMING == 3
+        if (threadIdx.x == 0) { const long long t1 = clock64(); ctr->eng[t < 20 ? t : 19] += t1 - tb0; tb0 = t1; ctr->eng[23 + (t < 8 ? t : 7)] += nd; }
+#endif
         if (nd == 0) {                      // no demand: the level keeps its blocks, nothing moves
             if (threadIdx.x == 0) { s_left[t] = FAIL; s_cnt[t] = n_t; }
             continue;
         }
         const u64 *blk = old_list + ooff[t];
         const u32 *Ds = dsrc + doff[t];
-        const u64 *bad = baddr + boff[t];   // borrows of order t (served by t+1)
         const u64 nbor = boff[t + 1] - boff[t];
-        u64 *bad_lo = (t > 0) ? baddr + boff[t - 1] : nullptr;   // borrows of order t-1
-        // the last borrow's address (the leftover test below), loaded with the level's own loads
-        const u64 last_bad = (threadIdx.x == 0 && nbor > 0) ? bad[nbor - 1] : FAIL;
-        for (u64 base = 0; base < nd; base += 8 * NT) {    // 8 independent element chains per thread
+        const u64 *bad = bsm ? sbuf + (t & 1) * maxb : baddr + boff[t];     // borrows of order t (served by t+1)
+        u64 *bad_lo = (t > 0) ? (bsm ? sbuf + ((t - 1) & 1) * maxb : baddr + boff[t - 1]) : nullptr;   // of t-1
+        const u32 nd_ = (u32)nd, nt_ = (u32)n_t, nbor_ = (u32)nbor, wb = threadIdx.x & ~31u;
+        const u64 dbase = doff[t];
+        for (u32 base = 0; base < nd_; base += 8 * NT) {    // 8 independent elements per thread
+            const u32 kw = base + wb < nd_ ? min(8u, (nd_ - base - wb + NT - 1) / NT) : 0u;   // warp-uniform
             u64 a[8];
             u32 s[8];
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const u64 p = base + (u64)k * NT + threadIdx.x;
-                s[k] = p < nd ? Ds[p] : 0u;
-                if (p >= nd) a[k] = FAIL;
-                else if (p < n_t) a[k] = blk[p];
-                else {
-                    const u64 xx = p - n_t, j = xx >> 1;
-                    const u64 bj = j < nbor ? bad[j] : FAIL;
+            for (u32 k = 0; k < 8; k++) {                  // level-local loads
+                const u32 p = base + k * NT + threadIdx.x;
+                if (k < kw) {
+                    s[k] = p < nd_ ? Ds[p] : 0u;
+                    a[k] = (p < nd_ && p < nt_) ? blk[p] : FAIL;
+                }
+            }
+            if (base == 0) __syncthreads();                // the level above has written bad[]
+#pragma unroll
+            for (u32 k = 0; k < 8; k++) {
+                const u32 p = base + k * NT + threadIdx.x;
+                if (k < kw && p < nd_ && p >= nt_) {
+                    const u32 xx = p - nt_, j = xx >> 1;
+                    const u64 bj = j < nbor_ ? bad[j] : FAIL;
                     a[k] = (bj != FAIL) ? bj + ((xx & 1) ? (1ull << t) : 0) : FAIL;
                 }
             }
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const u64 p = base + (u64)k * NT + threadIdx.x;
-                if (p >= nd) continue;
+            for (u32 k = 0; k < 8; k++) {
+                const u32 p = base + k * NT + threadIdx.x;
+                if (k >= kw || p >= nd_) continue;
                 if (s[k] & BORROW) bad_lo[s[k] & ~BORROW] = a[k];
+                else if (daddr) daddr[dbase + p] = a[k];   // in demand order (coalesced); k_bud_scatter
                 else out_u[s[k]] = a[k];
             }
         }
         if (threadIdx.x == 0) {
+            const u64 last_bad = nbor > 0 ? bad[nbor - 1] : FAIL;
             u64 x = nd > n_t ? nd - n_t : 0;
             u64 left = FAIL;
             if ((x & 1) && nbor > 0 && last_bad != FAIL) left = last_bad + (1ull << t);
             s_left[t] = left;
             s_cnt[t] = (nd < n_t ? n_t - nd : 0) + (left != FAIL ? 1 : 0);
         }
-        __syncthreads();
     }
     __syncthreads();
 #if BUDDY_TIMING
@@ -633,6 +660,19 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
 #if BUDDY_TIMING
     if (threadIdx.x == 0) { const long long t1 = clock64(); ctr->eng[22] += t1 - tb0; }
 #endif
+}
+
+// The request demands' addresses, written by k_alloc_levels in demand order (one CTA: its stores
+// are coalesced), scattered to request order by the whole grid — one CTA issuing ~n scattered
+// 8-byte stores (one L2 transaction each) is what bounded the top-down pass.
+__global__ void k_bud_scatter(const u32 *__restrict__ dsrc, const u64 *__restrict__ daddr, const DevCtr *ctr,
+                              u64 *__restrict__ out_u) {
+    PDL_ENTRY();
+    const u64 nd = ctr->bud_nd;
+    for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g < nd; g += (u64)gridDim.x * blockDim.x) {
+        const u32 sc = dsrc[g];
+        if (!(sc & BORROW)) out_u[sc] = daddr[g];
+    }
 }
 
 // buddy results: order -> units = 2^k; reuse fits::k_alloc_finish by materialising r

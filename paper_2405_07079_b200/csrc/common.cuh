@@ -58,6 +58,7 @@ struct DevCtr {
     u32 sc_tile, sc_done, sc_epoch, sc_pad;   // single-pass scan: tile counter, CTAs done, epoch
     u32 os_gh[8][256];  // digit histograms of the current sort (zeroed again by the last CTA)
     u32 os_gbase[8][256];   // their exclusive scans: first output position of each digit
+    u64 bud_nd;         // buddy alloc: total demands of the last batch's levels (k_bud_scatter)
 };
 
 enum { ERR_CAP_LIVE = 1, ERR_TABLE_FULL = 2, ERR_CAP_FREE = 4, ERR_ENGINE = 8, ERR_LIVEMAP = 16 };

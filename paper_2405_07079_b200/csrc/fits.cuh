@@ -765,12 +765,8 @@ __device__ __forceinline__ void bc_find(const BcSmem &S, u32 sw, u32 kt, u64 t, 
     }
 }
 
-__global__ void __launch_bounds__(32) k_bf_cls_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
-                                                      const u64 *__restrict__ r, u64 n, const u64 *n_in,
-                                                      u64 *__restrict__ out_u, int cls_ok, u64 *dbg) {
-    PDL_ENTRY();
-    extern __shared__ __align__(16) unsigned char bf_raw[];
-    if (n_in) n = *n_in;
+__device__ void bf_classes(unsigned char *bf_raw, u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
+                           const u64 *__restrict__ r, u64 n, u64 *__restrict__ out_u, int cls_ok, u64 *dbg) {
     const u32 lane = lane_id();
     const u64 F = *F_dev;
     const u64 nc0 = (F + BC_FILL - 1) / BC_FILL;
@@ -950,9 +946,216 @@ __global__ void __launch_bounds__(32) k_bf_cls_engine(u64 *gkeys, const u64 *F_d
     for (u64 x = lane; x < F; x += 32) fs[x] = S.fsm[x];
 #if BF_TIMING
     BF_T(5);
-    if (lane == 0) for (int k = 0; k < 6; k++) dbg[k] += (u64)tph[k];
+    if (lane == 0) for (int k = 0; k < 6; k++) dbg[16 + k] += (u64)tph[k];
 #endif
 #undef BF_T
+}
+
+__global__ void __launch_bounds__(32) k_bf_cls_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
+                                                      const u64 *__restrict__ r, u64 n, const u64 *n_in,
+                                                      u64 *__restrict__ out_u, int cls_ok, u64 *dbg) {
+    PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char bf_raw[];
+    if (n_in) n = *n_in;
+    bf_classes(bf_raw, gkeys, F_dev, FB, fs, r, n, out_u, cls_ok, dbg);
+}
+
+// ------------------------------------------------- BEST FIT, speculative chunks ----
+// One warp serves the requests in chunks of up to 32 (lane = request order) against the
+// chunk-start key array A (sorted (size, address) keys in shared memory, as bf_flat):
+//   * each lane finds p = the first key >= (r << FB) by binary search; lanes with the same p are
+//     ranked in time order and take A[p + rank] (q);
+//   * lane i is *dirty* if an earlier lane of another group took an index in [p_i, q_i] (its
+//     choice is then not the smallest untaken key), or an earlier lane's remainder x_j (the carved
+//     piece's new key) lies in [r_i << FB, A[q_i]) (a better fit appeared).  Up to the first dirty
+//     lane the choices are exactly the sequential best fit (Alg. 3, reading C3): at request i the
+//     free set is A minus the earlier choices plus their remainders, the first untaken index
+//     >= p_i is q_i, and no remainder lies below A[q_i] and at or above the request;
+//   * the committed prefix writes its results, and A is rebuilt into the other buffer: the
+//     taken keys removed, the remainders (sorted in the warp) merged in — each lane moves one
+//     contiguous segment, the remainders' slots come from their ranks.
+// Lane 0 is never dirty, so every chunk commits at least one request.  Measured commit rate on
+// config 2: ~17-19 requests per 32-request chunk (tools/research/bestfit_chunk_model.cpp).
+constexpr u32 BS_N = 8192, BS_RB = 512;
+struct BsSmem {
+    u64 A[2][BS_N];
+    u32 fsm[BS_N];
+    u64 rb[BS_RB];
+    u64 dx[32], sX[32];
+    u32 dq[32], dp[32], sR[32];
+    u32 rmb[BS_N / 32 + 4];            // removed-index bitmap of the chunk (zero between chunks)
+};
+constexpr size_t BF_ENGINE_SMEM2 = sizeof(BsSmem) > BF_ENGINE_SMEM ? sizeof(BsSmem) : BF_ENGINE_SMEM;
+
+// #(A[i] < t) over a sorted A[0, N): fixed power-of-two steps (the same trip count on every lane,
+// so several searches of one thread interleave instead of diverging)
+template <typename T>
+__device__ __forceinline__ u32 bs_lower_bound(const T *A, u32 N, T t) {
+    u32 lo = 0;
+    for (u32 step = N ? 1u << (31 - __clz(N)) : 0u; step; step >>= 1)
+        if (lo + step <= N && A[lo + step - 1] < t) lo += step;
+    return lo;
+}
+template <typename T>
+__device__ __forceinline__ T warp_sort_asc(T v) {       // bitonic sort of one value per lane
+    const u32 lane = lane_id();
+#pragma unroll
+    for (u32 k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            const T o = __shfl_xor_sync(FULLMASK, v, j);
+            const bool up = ((lane & k) == 0);
+            const bool lower = (lane & j) == 0;
+            v = (lower == up) ? (v < o ? v : o) : (v < o ? o : v);
+        }
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(32) k_bf_spec_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
+                                                       const u64 *__restrict__ r, u64 n, const u64 *n_in,
+                                                       u64 *__restrict__ out_u, int cls_ok, u64 *dbg) {
+    PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char bf_raw[];
+    if (n_in) n = *n_in;
+    const u32 lane = lane_id();
+    const u64 F = *F_dev;
+    if (!cls_ok || F > BS_N) {
+        bf_classes(bf_raw, gkeys, F_dev, FB, fs, r, n, out_u, cls_ok, dbg);
+        return;
+    }
+    BsSmem &S = *reinterpret_cast<BsSmem *>(bf_raw);
+    const u64 fmask = (1ull << FB) - 1;
+    for (u32 x = lane; x < (u32)F; x += 32) {
+        S.A[0][x] = gkeys[x];
+        S.fsm[x] = (u32)fs[x];
+    }
+    for (u32 x = lane; x < BS_N / 32 + 4; x += 32) S.rmb[x] = 0u;
+    u32 N = (u32)F, cur = 0;
+    u64 rb0 = 0, rb1 = 0;             // staged request window [rb0, rb1)
+    u64 pos = 0, n_chunks = 0;
+#if BF_TIMING
+    long long tq = clock64(), tph[6] = {0, 0, 0, 0, 0, 0};
+#define BS_T(k) do { const long long _t = clock64(); tph[k] += _t - tq; tq = _t; } while (0)
+#else
+#define BS_T(k) do { } while (0)
+#endif
+    __syncwarp();
+    while (pos < n) {
+        n_chunks++;
+        if (pos + 32 > rb1 && rb1 < n) {                 // stage the next requests
+            __syncwarp();
+            rb0 = pos;
+            rb1 = pos + BS_RB < n ? pos + BS_RB : n;
+            for (u64 j = lane; j < rb1 - rb0; j += 32) S.rb[j] = r[rb0 + j];
+            __syncwarp();
+        }
+        const u32 limit = (n - pos) < 32 ? (u32)(n - pos) : 32u;
+        const bool act = lane < limit;
+        const u64 ri = act ? S.rb[pos + lane - rb0] : 0ull;
+        const bool valid = act && ri != 0;
+        const u64 t = ri << FB;
+        const u64 *A = S.A[cur];
+        const u32 p = valid ? bs_lower_bound<u64>(A, N, t) : 0u;
+        const u32 peers = __match_any_sync(FULLMASK, valid ? p : (0x80000000u | lane));
+        const u32 q = p + (u32)__popc(peers & lanemask_lt());
+        const bool has = valid && q < N;
+        const u64 K = has ? A[q] : ~0ull;
+        const u64 z = K >> FB;
+        const u64 rem = (has && z > ri) ? (((z - ri) << FB) | (K & fmask)) : ~0ull;
+        BS_T(0);
+        S.dq[lane] = has ? q : 0xFFFFFFFFu;
+        S.dp[lane] = p;
+        S.dx[lane] = rem;
+        __syncwarp();
+        bool bad = false;
+#pragma unroll
+        for (u32 j = 0; j < 31; j++) {                   // earlier lanes (independent broadcast loads)
+            const u32 qj = S.dq[j], pj = S.dp[j];
+            const u64 xj = S.dx[j];
+            const bool e = j < lane && valid;
+            bad |= e && qj != 0xFFFFFFFFu && pj != p && qj >= p && qj <= q;
+            bad |= e && xj != ~0ull && xj >= t && xj < K;
+        }
+        const u32 badm = __ballot_sync(FULLMASK, bad && act);
+        const u32 commit = badm ? (u32)(__ffs(badm) - 1) : limit;
+        const bool cm = lane < commit;
+        const u64 i = pos + lane;
+        BS_T(1);
+        if (cm) {
+            if (!has) out_u[i] = HEAP_NULL_U64;
+            else {
+                const u32 f = (u32)(K & fmask);
+                const u32 s0 = S.fsm[f];
+                out_u[i] = s0;
+                S.fsm[f] = s0 + (u32)ri;
+            }
+        }
+        const bool rmv = cm && has, ins = cm && rem != ~0ull;
+        const u32 nr = __popc(__ballot_sync(FULLMASK, rmv)), nx = __popc(__ballot_sync(FULLMASK, ins));
+        if (nr) {
+            // the removed indices and the remainders, sorted in the warp
+            const u32 sr = warp_sort_asc<u32>(rmv ? q : 0xFFFFFFFFu);
+            const u64 sx = warp_sort_asc<u64>(ins ? rem : ~0ull);
+            S.sR[lane] = sr;
+            S.sX[lane] = sx;
+            __syncwarp();
+            BS_T(2);
+            u64 *B = S.A[cur ^ 1];
+            // survivors, 4 tiles of 32 consecutive keys in flight: key e moves to
+            // e - #(removed indices < e) + #(remainders < key); removed indices come from a bitmap
+            if (rmv) atomicOr(&S.rmb[q >> 5], 1u << (q & 31));
+            __syncwarp();
+            BS_T(2);
+            u32 before = 0;
+            for (u32 base = 0; base < N; base += 128) {
+                u64 a[4];
+                u32 w[4], xc[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const u32 e = base + k * 32 + lane;
+                    a[k] = e < N ? A[e] : ~0ull;
+                    w[k] = S.rmb[(base >> 5) + k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; k++) xc[k] = 0;
+#pragma unroll
+                for (u32 step = 16; step; step >>= 1) {      // #remainders below the key (4 searches interleaved)
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        if (xc[k] + step <= nx && S.sX[xc[k] + step - 1] < a[k]) xc[k] += step;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const u32 e = base + k * 32 + lane;
+                    const bool rm = (w[k] >> lane) & 1u;
+                    if (e < N && !rm) B[e - before - __popc(w[k] & lanemask_lt()) + xc[k]] = a[k];
+                    before += __popc(w[k]);
+                }
+            }
+            __syncwarp();
+            if (rmv) S.rmb[q >> 5] = 0u;
+            BS_T(3);
+            // remainders: rank k plus the survivors below
+            if (lane < nx) {
+                const u32 lb = bs_lower_bound<u64>(A, N, sx);
+                const u32 lo = bs_lower_bound<u32>(S.sR, nr, lb);   // #(removed indices < lb)
+                B[lane + lb - lo] = sx;
+            }
+            N = N - nr + nx;
+            cur ^= 1;
+            __syncwarp();
+            BS_T(4);
+        }
+        pos += commit;
+    }
+    __syncwarp();
+    for (u32 x = lane; x < (u32)F; x += 32) fs[x] = S.fsm[x];
+    if (dbg && lane == 0) { dbg[8] += n_chunks; dbg[9] += n; }
+#if BF_TIMING
+    if (lane == 0) for (int k = 0; k < 5; k++) dbg[16 + k] += (u64)tph[k];
+#endif
+#undef BS_T
 }
 
 // the flat engine with the array in shared memory (small heaps) or global memory

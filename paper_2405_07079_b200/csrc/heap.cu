@@ -41,7 +41,7 @@ struct Layout {
     // offsets
     u64 o_ctr, o_stats, o_tbl, o_fs0, o_fs1, o_fe0, o_fe1, o_kA, o_kB, o_vA, o_vB, o_flags, o_pos,
         o_hist, o_tsum, o_vs, o_ve, o_vsc, o_vec, o_ms, o_me, o_r, o_c, o_out, o_off, o_child,
-        o_sib, o_cs, o_bm, o_slot, bm_w0, bm_w1, bm_w2, bm_bytes, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_btm, o_bsrc, o_bufA, o_bufB,
+        o_sib, o_cs, o_bm, o_slot, bm_w0, bm_w1, bm_w2, bm_bytes, o_tree, o_lvl, o_bk0, o_bk1, o_dtm, o_dsrc, o_baddr, o_daddr, o_btm, o_bsrc, o_bufA, o_bufB,
         o_promo, o_bq0, o_bq1, o_fr, o_froff, o_reqoff, o_ft0, o_ft1, o_vt, o_mt, o_lnext, total;
     // HEAP_HYBRID: pool geometry and arrays, then the TLSF heap's own workspace at o_sub
     pool::Geom geo;
@@ -255,6 +255,7 @@ bool make_layout(u64 arena, u64 align, int policy, u64 max_live, u64 max_batch, 
         L.o_dtm = take(L.dpool * 4);
         L.o_dsrc = take(L.dpool * 4);
         L.o_baddr = take(L.bpool * 8);
+        L.o_daddr = take(L.dpool * 8);
         L.o_btm = take(L.bpool * 4);
         L.o_bsrc = take(L.bpool * 4);
         L.o_bufA = take(L.bud_cap * 8);
@@ -299,7 +300,7 @@ struct heap {
     u64 *tree, *lvl;
     u64 *bk[2];
     u32 *dtm, *dsrc, *btm, *bsrc, *froff, *reqoff;
-    u64 *baddr, *bufA, *bufB, *promo, *fr;
+    u64 *baddr, *daddr, *bufA, *bufB, *promo, *fr;
     fib::Geom *fgeom;                         // HEAP_FIB_BUDDY
     u64 *flo, *fbufL, *fscr;
     u32 *frem;
@@ -617,7 +618,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         const char *ws = getenv("HEAP_WILD_SPLIT");
         h->wild_split = (ws && ws[0] == '0') ? 0 : 1;
         const char *bf = getenv("HEAP_BF_FLAT");
-        h->bf_flat = (bf && bf[0] == '1') ? 1 : (bf && bf[0] == '2') ? 2 : 0;
+        h->bf_flat = (bf && bf[0] >= '1' && bf[0] <= '3') ? bf[0] - '0' : 0;
         const char *ew = getenv("HEAP_ENGINE_WARPS");
         h->eng_warps = (ew && ew[0] == '1') ? 1 : 2;
         const char *pd = getenv("HEAP_PDL");
@@ -663,6 +664,8 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
                              (int)sizeof(fits::BfSmem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(fits::k_bf_cls_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)fits::BF_ENGINE_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+    if (cudaFuncSetAttribute(fits::k_bf_spec_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)fits::BF_ENGINE_SMEM2) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_free_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)buddy::FREE_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(buddy::k_alloc_levels, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -762,7 +765,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
                                  (int)fib::eng_smem(fib::MAXC - 3)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     }
     if (policy == HEAP_BUDDY || policy == HEAP_FIB_BUDDY) {
-        h->dtm = at<u32>(w, L.o_dtm); h->dsrc = at<u32>(w, L.o_dsrc); h->baddr = at<u64>(w, L.o_baddr);
+        h->dtm = at<u32>(w, L.o_dtm); h->dsrc = at<u32>(w, L.o_dsrc); h->baddr = at<u64>(w, L.o_baddr); h->daddr = at<u64>(w, L.o_daddr);
         h->btm = at<u32>(w, L.o_btm); h->bsrc = at<u32>(w, L.o_bsrc);
         h->bufA = at<u64>(w, L.o_bufA); h->bufB = at<u64>(w, L.o_bufB); h->promo = at<u64>(w, L.o_promo);
         if (L.o_bq0) { h->bq[0] = at<u64>(w, L.o_bq0); h->bq[1] = at<u64>(w, L.o_bq1); }
@@ -950,7 +953,8 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s);   // 1 pass: result in kB/vB
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kB, &C->tmp[0], L.K + 2, h->reqoff);
         LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, buddy::ALLOC_SMEM, s, h->vB, h->reqoff, h->fs[cur], h->fs[nxt], h->dtm,
-               h->dsrc, nullptr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
+               h->dsrc, h->daddr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
+        LAUNCH(h, buddy::k_bud_scatter, h->G, 256, 0, s, h->dsrc, h->daddr, C, h->out);
         if (!h->bud_levels) {   // the address-ordered free set: survivors compacted, leftovers inserted
             LAUNCH(h, buddy::k_bud_qflags, h->G, 256, 0, s, h->bq[cur], C, h->flags);
             scan(h, h->flags, h->pos, &C->bud_qn, &C->tmp[2], s);
@@ -1059,8 +1063,11 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         } else if (h->bf_flat == 2) {   // ablation (HEAP_BF_FLAT=2): the blocked engine without the class index
             LAUNCH(h, fits::k_bf_engine, 1, 32, sizeof(fits::BfSmem), s, keys, &C->F, L.FB, h->fs[cur], h->r, n, n_in,
                    h->out);
-        } else {
+        } else if (h->bf_flat == 3) {   // ablation (HEAP_BF_FLAT=3): one request at a time on the class index
             LAUNCH(h, fits::k_bf_cls_engine, 1, 32, fits::BF_ENGINE_SMEM, s, keys, &C->F, L.FB, h->fs[cur], h->r, n,
+                   n_in, h->out, L.A_u <= 0xFFFFFFFFull ? 1 : 0, C->eng);
+        } else {
+            LAUNCH(h, fits::k_bf_spec_engine, 1, 32, fits::BF_ENGINE_SMEM2, s, keys, &C->F, L.FB, h->fs[cur], h->r, n,
                    n_in, h->out, L.A_u <= 0xFFFFFFFFull ? 1 : 0, C->eng);
         }
     }

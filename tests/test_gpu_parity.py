@@ -175,11 +175,11 @@ BF_CASES = [
 ]
 
 
-@pytest.mark.parametrize("engine", ["0", "2", "1"], ids=["classes", "blocked", "flat"])
+@pytest.mark.parametrize("engine", ["0", "3", "2", "1"], ids=["spec", "classes", "blocked", "flat"])
 @pytest.mark.parametrize("case", BF_CASES, ids=lambda c: f"A{c[0]}-B{c[1]}")
 def test_best_fit_engines(case, engine, monkeypatch):
-    """BEST_FIT's class-indexed, blocked (chunked) and flat engines (fits.cuh k_bf_cls_engine,
-    k_bf_engine, bf_flat), each bit-exact with Oracle-L."""
+    """BEST_FIT's speculative-chunk, class-indexed, blocked (chunked) and flat engines (fits.cuh
+    k_bf_spec_engine, k_bf_cls_engine, k_bf_engine, bf_flat), each bit-exact with Oracle-L."""
     monkeypatch.setenv("HEAP_BF_FLAT", engine)
     arena, batch, ops, sizes, rho = case
     cfg = tg.custom(tg.BEST_FIT, arena, 16, batch, rho=rho, total_ops=ops, sizes=sizes, idx=90)

@@ -23,5 +23,7 @@ d = [(a - b) for a, b in zip(c, prev)]
 k = nb - nb // 2
 names = ["build", "search", "delete", "rsearch", "insert", "writeback"]
 print(f"batches {nb//2}..{nb-1}: {na/k:.0f} allocs/batch, n_free now {st.get('n_free')}")
-print("cycles/batch: " + "  ".join(f"{n} {d[j]/k:.0f}" for j, n in enumerate(names)))
-print("cycles/request: " + "  ".join(f"{n} {d[j]/na:.0f}" for j, n in enumerate(names[1:5], 1)))
+print("cycles/batch: " + "  ".join(f"{n} {d[16 + j]/k:.0f}" for j, n in enumerate(names)))
+print("cycles/request: " + "  ".join(f"{n} {d[16 + j]/na:.0f}" for j, n in enumerate(names[1:5], 1)))
+if d[9]:
+    print(f"speculative chunks: {d[8]/k:.0f}/batch, {d[9]/max(d[8],1):.1f} requests per chunk")

@@ -1,7 +1,7 @@
 """Top CUDA source lines by executed warp instructions from an ncu report (dev tool): python tools/ncu_inst_lines.py <rep>."""
 import collections, csv, subprocess, sys
 rep=sys.argv[1]
-out = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","cuda,sass","-k","k_engine"],capture_output=True,text=True).stdout
+out = subprocess.run(["ncu","-i",rep,"--page","source","--csv","--print-source","cuda,sass","-k",(sys.argv[2] if len(sys.argv)>2 else "k_engine")],capture_output=True,text=True).stdout
 rows=list(csv.reader(out.splitlines()))
 hdr=None; cur=None; agg=collections.Counter(); src={}; fn=None
 for r in rows:
