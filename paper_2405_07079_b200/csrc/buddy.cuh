@@ -46,7 +46,8 @@ __device__ __forceinline__ void cta_copy(TD *dst, const TS *src, u64 n64) {
     for (u32 base = 0; base < n; base += 8 * NT) {
         // warp-uniform step count: warps past the end skip the unrolled steps instead of running
         // them predicated off (the kernel is issue-bound on its one SM)
-        const u32 kw = base + wb < n ? min(8u, (n - base - wb + NT - 1) / NT) : 0u;
+        if (base + wb >= n) break;                  // warp-uniform: nothing left for this warp
+        const u32 kw = min(8u, (n - base - wb + NT - 1) / NT);
         TS v[8];
 #pragma unroll
         for (u32 k = 0; k < 8; k++) {
@@ -560,8 +561,14 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
     // publishes the level above's borrow addresses: per level one barrier and shared-memory
     // latency instead of a global round trip.
     __shared__ u64 s_left[41], s_cnt[41];
-    u64 maxb = 0;
-    for (int t = 0; t <= K; t++) maxb = max(maxb, boff[t + 1] - boff[t]);
+    __shared__ u64 s_maxb;
+    if (threadIdx.x == 0) {
+        u64 m = 0;
+        for (int t = 0; t <= K; t++) m = max(m, boff[t + 1] - boff[t]);
+        s_maxb = m;
+    }
+    __syncthreads();
+    const u64 maxb = s_maxb;
     const bool bsm = 2 * maxb * sizeof(u64) <= ALLOC_SMEM;
     u64 *sbuf = reinterpret_cast<u64 *>(astage_td);
     for (int t = K; t >= 0; t--) {
@@ -585,15 +592,18 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
             const u32 kw = base + wb < nd_ ? min(8u, (nd_ - base - wb + NT - 1) / NT) : 0u;   // warp-uniform
             u64 a[8];
             u32 s[8];
+            if (kw) {
 #pragma unroll
-            for (u32 k = 0; k < 8; k++) {                  // level-local loads
-                const u32 p = base + k * NT + threadIdx.x;
-                if (k < kw) {
-                    s[k] = p < nd_ ? Ds[p] : 0u;
-                    a[k] = (p < nd_ && p < nt_) ? blk[p] : FAIL;
+                for (u32 k = 0; k < 8; k++) {              // level-local loads
+                    const u32 p = base + k * NT + threadIdx.x;
+                    if (k < kw) {
+                        s[k] = p < nd_ ? Ds[p] : 0u;
+                        a[k] = (p < nd_ && p < nt_) ? blk[p] : FAIL;
+                    }
                 }
             }
             if (base == 0) __syncthreads();                // the level above has written bad[]
+            if (!kw) continue;                             // idle warp: nothing of this level
 #pragma unroll
             for (u32 k = 0; k < 8; k++) {
                 const u32 p = base + k * NT + threadIdx.x;

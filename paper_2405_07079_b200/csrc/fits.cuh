@@ -972,8 +972,9 @@ __global__ void __launch_bounds__(32) k_bf_cls_engine(u64 *gkeys, const u64 *F_d
 //     free set is A minus the earlier choices plus their remainders, the first untaken index
 //     >= p_i is q_i, and no remainder lies below A[q_i] and at or above the request;
 //   * the committed prefix writes its results, and A is rebuilt into the other buffer: the
-//     taken keys removed, the remainders (sorted in the warp) merged in — each lane moves one
-//     contiguous segment, the remainders' slots come from their ranks.
+//     taken keys removed (a bitmap over indices), the remainders merged in (each one's insertion
+//     point in A by binary search, a bitmap over insertion points; its rank among the remainders
+//     by ballots), every key moved by popcounts over the two bitmaps, 4 tiles of 32 in flight.
 // Lane 0 is never dirty, so every chunk commits at least one request.  Measured commit rate on
 // config 2: ~17-19 requests per 32-request chunk (tools/research/bestfit_chunk_model.cpp).
 constexpr u32 BS_N = 8192, BS_RB = 512;
@@ -982,8 +983,9 @@ struct BsSmem {
     u32 fsm[BS_N];
     u64 rb[BS_RB];
     u64 dx[32], sX[32];
-    u32 dq[32], dp[32], sR[32];
+    uint2 dqp[32];                     // per lane: (p, q or NONE)
     u32 rmb[BS_N / 32 + 4];            // removed-index bitmap of the chunk (zero between chunks)
+    u32 lbm[BS_N / 32 + 4];            // remainders' insertion points (zero between chunks)
 };
 constexpr size_t BF_ENGINE_SMEM2 = sizeof(BsSmem) > BF_ENGINE_SMEM ? sizeof(BsSmem) : BF_ENGINE_SMEM;
 
@@ -996,22 +998,6 @@ __device__ __forceinline__ u32 bs_lower_bound(const T *A, u32 N, T t) {
         if (lo + step <= N && A[lo + step - 1] < t) lo += step;
     return lo;
 }
-template <typename T>
-__device__ __forceinline__ T warp_sort_asc(T v) {       // bitonic sort of one value per lane
-    const u32 lane = lane_id();
-#pragma unroll
-    for (u32 k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-        for (u32 j = k >> 1; j > 0; j >>= 1) {
-            const T o = __shfl_xor_sync(FULLMASK, v, j);
-            const bool up = ((lane & k) == 0);
-            const bool lower = (lane & j) == 0;
-            v = (lower == up) ? (v < o ? v : o) : (v < o ? o : v);
-        }
-    }
-    return v;
-}
-
 __global__ void __launch_bounds__(32) k_bf_spec_engine(u64 *gkeys, const u64 *F_dev, int FB, u64 *fs,
                                                        const u64 *__restrict__ r, u64 n, const u64 *n_in,
                                                        u64 *__restrict__ out_u, int cls_ok, u64 *dbg) {
@@ -1030,7 +1016,7 @@ __global__ void __launch_bounds__(32) k_bf_spec_engine(u64 *gkeys, const u64 *F_
         S.A[0][x] = gkeys[x];
         S.fsm[x] = (u32)fs[x];
     }
-    for (u32 x = lane; x < BS_N / 32 + 4; x += 32) S.rmb[x] = 0u;
+    for (u32 x = lane; x < BS_N / 32 + 4; x += 32) { S.rmb[x] = 0u; S.lbm[x] = 0u; }
     u32 N = (u32)F, cur = 0;
     u64 rb0 = 0, rb1 = 0;             // staged request window [rb0, rb1)
     u64 pos = 0, n_chunks = 0;
@@ -1064,17 +1050,16 @@ __global__ void __launch_bounds__(32) k_bf_spec_engine(u64 *gkeys, const u64 *F_
         const u64 z = K >> FB;
         const u64 rem = (has && z > ri) ? (((z - ri) << FB) | (K & fmask)) : ~0ull;
         BS_T(0);
-        S.dq[lane] = has ? q : 0xFFFFFFFFu;
-        S.dp[lane] = p;
+        S.dqp[lane] = make_uint2(p, has ? q : 0xFFFFFFFFu);
         S.dx[lane] = rem;
         __syncwarp();
         bool bad = false;
 #pragma unroll
         for (u32 j = 0; j < 31; j++) {                   // earlier lanes (independent broadcast loads)
-            const u32 qj = S.dq[j], pj = S.dp[j];
+            const uint2 pq = S.dqp[j];
             const u64 xj = S.dx[j];
             const bool e = j < lane && valid;
-            bad |= e && qj != 0xFFFFFFFFu && pj != p && qj >= p && qj <= q;
+            bad |= e && pq.y != 0xFFFFFFFFu && pq.x != p && pq.y >= p && pq.y <= q;
             bad |= e && xj != ~0ull && xj >= t && xj < K;
         }
         const u32 badm = __ballot_sync(FULLMASK, bad && act);
@@ -1094,36 +1079,57 @@ __global__ void __launch_bounds__(32) k_bf_spec_engine(u64 *gkeys, const u64 *F_
         const bool rmv = cm && has, ins = cm && rem != ~0ull;
         const u32 nr = __popc(__ballot_sync(FULLMASK, rmv)), nx = __popc(__ballot_sync(FULLMASK, ins));
         if (nr) {
-            // the removed indices and the remainders, sorted in the warp
-            const u32 sr = warp_sort_asc<u32>(rmv ? q : 0xFFFFFFFFu);
-            const u64 sx = warp_sort_asc<u64>(ins ? rem : ~0ull);
-            S.sR[lane] = sr;
-            S.sX[lane] = sx;
-            __syncwarp();
-            BS_T(2);
             u64 *B = S.A[cur ^ 1];
-            // survivors, 4 tiles of 32 consecutive keys in flight: key e moves to
-            // e - #(removed indices < e) + #(remainders < key); removed indices come from a bitmap
+            // each remainder's insertion point in A (#keys below it), its rank among the remainders
+            // and #removed indices below its insertion point (one ballot pair per remainder)
+            const u32 lb = ins ? bs_lower_bound<u64>(A, N, rem) : 0u;
+            const u32 insm = __ballot_sync(FULLMASK, ins);
+            u32 rank = 0, rcnt = 0;
+            for (u32 mm = insm; mm; mm &= mm - 1) {
+                const u32 k = __ffs(mm) - 1;
+                const u32 lbk = __shfl_sync(FULLMASK, lb, k);
+                const u64 xk = __shfl_sync(FULLMASK, rem, k);
+                const u32 r1 = __popc(__ballot_sync(FULLMASK, rmv && q < lbk));
+                const u32 r2 = __popc(__ballot_sync(FULLMASK, ins && rem < xk));
+                if (lane == k) { rcnt = r1; rank = r2; }
+            }
+            // one bit per insertion point; two remainders between the same neighbours (rare) make
+            // the survivors count the remainders below them by binary search instead
+            const u32 dupm = __match_any_sync(FULLMASK, ins ? lb : (0x80000000u | lane));
+            const bool dup = __any_sync(FULLMASK, ins && __popc(dupm) > 1);
             if (rmv) atomicOr(&S.rmb[q >> 5], 1u << (q & 31));
+            if (ins) {
+                S.sX[rank] = rem;
+                if (!dup) atomicOr(&S.lbm[lb >> 5], 1u << (lb & 31));
+            }
             __syncwarp();
             BS_T(2);
-            u32 before = 0;
+            // survivors, 4 tiles of 32 consecutive keys in flight: key e moves to
+            // e - #(removed indices < e) + #(remainders whose insertion point is <= e)
+            const u32 lmle = lanemask_lt() | (1u << lane);
+            u32 before = 0, xbefore = 0;
             for (u32 base = 0; base < N; base += 128) {
                 u64 a[4];
-                u32 w[4], xc[4];
+                u32 w[4], v[4], xc[4];
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
                     const u32 e = base + k * 32 + lane;
                     a[k] = e < N ? A[e] : ~0ull;
                     w[k] = S.rmb[(base >> 5) + k];
+                    v[k] = dup ? 0u : S.lbm[(base >> 5) + k];
                 }
+                if (dup) {
 #pragma unroll
-                for (int k = 0; k < 4; k++) xc[k] = 0;
+                    for (int k = 0; k < 4; k++) xc[k] = 0;
 #pragma unroll
-                for (u32 step = 16; step; step >>= 1) {      // #remainders below the key (4 searches interleaved)
+                    for (u32 step = 16; step; step >>= 1) {
 #pragma unroll
-                    for (int k = 0; k < 4; k++)
-                        if (xc[k] + step <= nx && S.sX[xc[k] + step - 1] < a[k]) xc[k] += step;
+                        for (int k = 0; k < 4; k++)
+                            if (xc[k] + step <= nx && S.sX[xc[k] + step - 1] < a[k]) xc[k] += step;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) { xc[k] = xbefore + __popc(v[k] & lmle); xbefore += __popc(v[k]); }
                 }
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
@@ -1133,15 +1139,11 @@ __global__ void __launch_bounds__(32) k_bf_spec_engine(u64 *gkeys, const u64 *F_
                     before += __popc(w[k]);
                 }
             }
+            BS_T(3);
+            if (ins) B[rank + lb - rcnt] = rem;       // rank among the remainders + survivors below
             __syncwarp();
             if (rmv) S.rmb[q >> 5] = 0u;
-            BS_T(3);
-            // remainders: rank k plus the survivors below
-            if (lane < nx) {
-                const u32 lb = bs_lower_bound<u64>(A, N, sx);
-                const u32 lo = bs_lower_bound<u32>(S.sR, nr, lb);   // #(removed indices < lb)
-                B[lane + lb - lo] = sx;
-            }
+            if (ins) S.lbm[lb >> 5] = 0u;
             N = N - nr + nx;
             cur ^= 1;
             __syncwarp();

@@ -1164,6 +1164,9 @@ __global__ void k_set_req_n(DevCtr *ctr, u64 n) {
 
 static bool use_graph(heap *h, cudaStream_t s) {
     if (!h->graphs || h->prof_mask || (h->sub && h->sub->prof_mask) || (h->sub2 && h->sub2->prof_mask)) return false;
+    // a single-launch (micro) batch is already one launch: the graph's count-setting kernel and
+    // staging copies would only add nodes (measured: config 1, 4 of the 7 nodes per batch)
+    if (h->micro && !getenv("HEAP_MICRO_GRAPH")) return false;
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return false;
     return true;
