@@ -174,6 +174,15 @@ int heap_destroy(heap_t *h);
 /* Free a batch of n offsets (bytes).  0 <= n <= max_batch. */
 int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_stream_t s);
 
+/* The same batch by handle: offset i is d_table[d_idx[i]] (device arrays; d_table holds
+ * table_len offsets, e.g. the results of earlier heap_alloc_batch calls, HEAP_NULL allowed; an
+ * index >= table_len frees nothing and counts as a null free).  Identical to heap_free_batch on the
+ * gathered offsets (Alg. 2); a single-launch heap reads them inside its free
+ * kernel, other heaps gather them first (one extra launch).  0 <= n <= max_batch;
+ * HEAP_EINVAL on a null heap or null arrays with n > 0. */
+int heap_free_batch_handles(heap_t *h, const uint64_t *d_table, uint64_t table_len, const uint64_t *d_idx,
+                            uint64_t n, heap_stream_t s);
+
 /* Allocate a batch of n requests: d_sizes[i] bytes -> d_out_offsets[i] (byte offset into the
  * arena, or HEAP_NULL).  0 <= n <= max_batch.  d_out_offsets must not alias d_sizes. */
 int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out_offsets, uint64_t n,

@@ -280,6 +280,8 @@ struct heap {
     int wild_split;          // TLSF/SEGFIT wilderness split (engine_tlsf.cuh); env HEAP_WILD_SPLIT=0 disables
     int bf_flat;             // BEST_FIT: the flat one-array engine instead of the blocked one (env HEAP_BF_FLAT=1)
     int micro;               // small heap: each batch is one single-CTA launch (micro.cuh); env HEAP_MICRO=0 disables
+    const u64 *hidx = nullptr;   // heap_free_batch_handles on a micro heap: the handle indices (else null)
+    u64 hlen = 0;
     int pdl;                 // programmatic dependent launches (env HEAP_PDL=0 disables)
     int eng_warps;           // TLSF/SEGFIT engine: 2 = arrivals on a second warp (default), 1 = one warp (HEAP_ENGINE_WARPS=1)
     int bud_levels;          // BUDDY free phase: the level-by-level kernel instead of the parallel form (env HEAP_BUDDY_LEVELS=1)
@@ -831,7 +833,7 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
         TAG(h, HEAP_TAG_MICRO);
         LAUNCH(h, micro::k_micro_free, 1, micro::MT, micro::FREE_SMEM, s, (const u64 *)d_offsets, n, n_in, h->alog2,
                L.A_u, h->fs[cur], h->fe[cur], h->fs[nxt], h->fe[nxt], h->tbl, L.tcap - 1, L.tcap / table::LINE,
-               L.cap_f, C);
+               L.cap_f, C, h->hidx, h->hlen);
         h->cur = nxt;
         if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
         return HEAP_OK;
@@ -1278,6 +1280,18 @@ static int hybrid_alloc(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint6
     return HEAP_OK;
 }
 
+// offsets by handle: d_table[d_idx[i]] (an index >= table_len frees nothing).  A single-launch
+// (micro) heap reads them inside its free kernel; other heaps gather them into the graph staging
+// buffer of the alloc side (unused during a free batch) and run the plain free batch on it.
+__global__ void k_gather_handles(const u64 *__restrict__ table, u64 tlen, const u64 *__restrict__ idx, u64 n,
+                                 u64 *__restrict__ out) {
+    PDL_ENTRY();
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 x = idx[i];
+        out[i] = x < tlen ? table[x] : HEAP_NULL_U64;
+    }
+}
+
 extern "C" {
 
 int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_stream_t sp) {
@@ -1285,6 +1299,25 @@ int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_strea
     if (n == 0) return HEAP_OK;
     if (use_graph(h, (cudaStream_t)sp)) return graph_batch(h, 0, d_offsets, nullptr, n, (cudaStream_t)sp);
     return batch_free(h, d_offsets, n, nullptr, (cudaStream_t)sp);
+}
+
+int heap_free_batch_handles(heap_t *h, const uint64_t *d_table, uint64_t table_len, const uint64_t *d_idx,
+                            uint64_t n, heap_stream_t sp) {
+    if (!h || n > h->max_batch || (n && (!d_table || !d_idx))) return HEAP_EINVAL;
+    if (n == 0) return HEAP_OK;
+    cudaStream_t s = (cudaStream_t)sp;
+    if (h->micro) {
+        h->hidx = (const u64 *)d_idx;
+        h->hlen = table_len;
+        const int rc = batch_free(h, d_table, n, nullptr, s);
+        h->hidx = nullptr;
+        h->hlen = 0;
+        return rc;
+    }
+    LAUNCH(h, k_gather_handles, h->G, 256, 0, s, (const u64 *)d_table, (u64)table_len, (const u64 *)d_idx, (u64)n,
+           (u64 *)h->gout);
+    if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+    return heap_free_batch(h, (const uint64_t *)h->gout, n, sp);
 }
 
 int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, heap_stream_t sp) {

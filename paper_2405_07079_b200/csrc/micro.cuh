@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(MT, 1) k_micro_free(const u64 *__restrict__ of
                                                       u64 A_u, const u64 *__restrict__ fs_in,
                                                       const u64 *__restrict__ fe_in, u64 *__restrict__ fs_out,
                                                       u64 *__restrict__ fe_out, u64 *__restrict__ tbl, u64 tmask,
-                                                      u64 max_lines, u64 cap_f, DevCtr *ctr) {
+                                                      u64 max_lines, u64 cap_f, DevCtr *ctr,
+                                                      const u64 *__restrict__ hidx, u64 hlen) {
     PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char dyn[];
     u32 *ps = reinterpret_cast<u32 *>(dyn);          // free array (units), F entries
@@ -80,8 +81,14 @@ __global__ void __launch_bounds__(MT, 1) k_micro_free(const u64 *__restrict__ of
         return;
     }
     if (tid == 0) { c_null = 0; c_inv = 0; c_ok = 0; c_dbl = 0; c_units = 0; s_nk = 0; }
+    // handles (heap_free_batch_handles): offset i is offs[hidx[i]] (an index >= hlen frees nothing)
+    auto off_at = [&](u32 i) -> u64 {
+        if (!hidx) return offs[i];
+        const u64 x = hidx[i];
+        return x < hlen ? offs[x] : HEAP_NULL_U64;
+    };
     // the first MT offsets are loaded together with the free array (one memory round trip)
-    const u64 o_first = tid < n ? offs[tid] : HEAP_NULL_U64;
+    const u64 o_first = tid < n ? off_at(tid) : HEAP_NULL_U64;
     for (u32 i = tid; i < F; i += MT) { ps[i] = (u32)fs_in[i]; pe[i] = (u32)fe_in[i]; }
     __syncthreads();
     MCLK(16)
@@ -93,7 +100,7 @@ __global__ void __launch_bounds__(MT, 1) k_micro_free(const u64 *__restrict__ of
         bool cand = false;
         u32 key = 0;
         if (i < n) {
-            const u64 o = base == 0 ? o_first : offs[i];
+            const u64 o = base == 0 ? o_first : off_at(i);
             if (o == HEAP_NULL_U64) nnull++;
             else if ((o & amask) || (o >> alog2) >= A_u) ninv++;
             else { cand = true; key = (u32)(o >> alog2); }

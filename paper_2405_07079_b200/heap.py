@@ -61,6 +61,13 @@ def heap_free_batch(h, offsets: torch.Tensor, stream=None) -> None:
                                                    _stream_handle(stream)))
 
 
+def heap_free_batch_handles(h, table: torch.Tensor, idx: torch.Tensor, stream=None) -> None:
+    n = idx.numel()
+    check("heap_free_batch_handles",
+          lib().heap_free_batch_handles(h, _dev_ptr(table, "table") if n else None, table.numel(),
+                                        _dev_ptr(idx, "idx") if n else None, n, _stream_handle(stream)))
+
+
 def heap_alloc_batch(h, sizes: torch.Tensor, out_offsets: torch.Tensor, stream=None) -> None:
     n = sizes.numel()
     if out_offsets.numel() < n:
@@ -202,6 +209,12 @@ class Heap:
     def free_batch(self, offsets: torch.Tensor) -> None:
         with torch.cuda.device(self.device):
             heap_free_batch(self._h, offsets, self._stream())
+
+    def free_batch_handles(self, table: torch.Tensor, idx: torch.Tensor) -> None:
+        """Free the offsets table[idx[i]] (int64 tensors; an index >= table.numel() frees nothing):
+        a caller keeping its blocks in a handle table frees them without a separate gather."""
+        with torch.cuda.device(self.device):
+            heap_free_batch_handles(self._h, table, idx, self._stream())
 
     def alloc_batch(self, sizes: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """Serve a batch of sizes (bytes) in request order; returns the offsets (HEAP_NULL as -1).

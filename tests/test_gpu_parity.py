@@ -596,3 +596,34 @@ def test_arena_extremes_all_policies(pol):
         compare_state(g, o, f"p{pol} {arena} free all")
         assert np.array_equal(g.alloc_batch(sizes[::-1].copy()), o.alloc_batch(sizes[::-1].copy())), (pol, arena)
         compare_state(g, o, f"p{pol} {arena} realloc")
+
+
+@pytest.mark.parametrize("micro", ["1", "0"], ids=["single_launch", "general"])
+@pytest.mark.parametrize("policy", [tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.BUDDY])
+def test_free_batch_handles(policy, micro, monkeypatch):
+    """heap_free_batch_handles frees table[idx[i]] exactly as heap_free_batch frees the gathered
+    offsets: a handle table on the device (the alloc results written into it), frees by index,
+    including indices past the table (no-op nulls), repeated and HEAP_NULL entries; every batch
+    against Oracle-L on the gathered offsets."""
+    from paper_2405_07079_b200 import Heap
+    monkeypatch.setenv("HEAP_MICRO", micro)
+    kind, sizes = (1, (4, 10)) if policy == tg.BUDDY else (0, (4, 12))
+    cfg = tg.custom(policy, 1 << 20, 16, 128, total_ops=6000, sizes=sizes, size_kind=kind, idx=93)
+    h = Heap(cfg.arena_bytes, cfg.align, policy, 1 << 12, 256)
+    o = OracleL(cfg.arena_bytes, cfg.align, policy)
+    table = torch.full((8192,), -1, dtype=torch.int64, device="cuda")
+    rng = np.random.default_rng(7)
+    for bi, (fids, sz, first) in enumerate(tg.Trace(cfg)):
+        idx = fids.astype(np.int64)
+        if bi % 3 == 2 and len(idx):          # an index past the table and a repeated handle
+            idx = np.concatenate([idx, [table.numel() + 5, idx[0]]])
+            rng.shuffle(idx)
+        offs = np.where(idx < table.numel(), table.cpu().numpy()[np.minimum(idx, table.numel() - 1)], -1)
+        h.free_batch_handles(table, torch.from_numpy(idx).cuda())
+        o.free_batch(offs.view(np.uint64))
+        got = h.alloc_batch(torch.from_numpy(sz.view(np.int64)).cuda(), out=table[first:first + len(sz)])
+        want = o.alloc_batch(sz)
+        assert np.array_equal(got.cpu().numpy().view(np.uint64), want), (policy, micro, bi)
+    st, ost = h.stats(), o.stats()
+    for k in COUNTERS:
+        assert st[k] == ost[k], (k, st[k], ost[k])
