@@ -304,9 +304,9 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     def run_device(h, idmap, outbuf, b, stream_stats=True):
         fids, sizes, first = b
-        h.free_batch_handles(idmap, fids)        # offsets idmap[fids], looked up by the library
         na = sizes.numel()
-        h.alloc_batch(sizes, out=idmap[first:first + na])
+        # heap_step: frees by handle (offsets idmap[fids], looked up by the library), then the allocs
+        h.step(idmap, sizes, idx=fids, out=idmap[first:first + na])
         if world > 1 and stream_stats:
             if gloo:      # CPU tests / one-GPU dev mode: NCCL cannot put two ranks on one GPU
                 heap_stats_async(h.handle, stats_dev)
@@ -545,15 +545,14 @@ def run_config(cfg, nbatches, dev, flush, warmup=3):
     # frees by handle (heap_free_batch_handles): the id -> offset lookup happens inside the library's
     # free (fused into the kernel on single-launch heaps), as the oracle's host-side lookup sits
     # outside its own timing
+    # (heap_step: the free batch then the alloc batch in one call — one launch on a single-launch heap)
     for bi, (fd, sd, first) in enumerate(staged[:warmup]):
-        h.free_batch_handles(idmap, fd)
-        h.alloc_batch(sd, out=idmap[first:first + len(sd)])
+        h.step(idmap, sd, idx=fd, out=idmap[first:first + len(sd)])
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         for fd, sd, first in staged[warmup:]:
-            h.free_batch_handles(idmap, fd)
-            h.alloc_batch(sd, out=idmap[first:first + len(sd)])
+            h.step(idmap, sd, idx=fd, out=idmap[first:first + len(sd)])
     flush.fill_(1)
     torch.cuda.synchronize()
     a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

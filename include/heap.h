@@ -183,6 +183,16 @@ int heap_free_batch(heap_t *h, const uint64_t *d_offsets, uint64_t n, heap_strea
 int heap_free_batch_handles(heap_t *h, const uint64_t *d_table, uint64_t table_len, const uint64_t *d_idx,
                             uint64_t n, heap_stream_t s);
 
+/* One canonical batch (BASELINE north_star: the frees, then the allocs in request order) in one
+ * call: heap_free_batch(d_offsets, nf) — or, when d_idx is not NULL, heap_free_batch_handles(
+ * d_offsets as the table of table_len handles, d_idx, nf) — followed by heap_alloc_batch(d_sizes,
+ * d_out, na), with exactly their results.  A single-launch heap runs both phases in ONE kernel
+ * (micro.cuh k_micro_step); other heaps issue the two batches.  d_out may alias the handle table:
+ * the frees are read before any result is written.  0 <= nf, na <= max_batch; HEAP_EINVAL on a
+ * null heap or null arrays with a nonzero count. */
+int heap_step(heap_t *h, const uint64_t *d_offsets, const uint64_t *d_idx, uint64_t table_len, uint64_t nf,
+              const uint64_t *d_sizes, uint64_t *d_out_offsets, uint64_t na, heap_stream_t s);
+
 /* Allocate a batch of n requests: d_sizes[i] bytes -> d_out_offsets[i] (byte offset into the
  * arena, or HEAP_NULL).  0 <= n <= max_batch.  d_out_offsets must not alias d_sizes. */
 int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out_offsets, uint64_t n,

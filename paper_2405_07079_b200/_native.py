@@ -58,7 +58,7 @@ class HeapStats(ctypes.Structure):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
-EXPORTS = ("heap_workspace_bytes", "heap_create", "heap_destroy", "heap_free_batch", "heap_free_batch_handles",
+EXPORTS = ("heap_workspace_bytes", "heap_create", "heap_destroy", "heap_free_batch", "heap_free_batch_handles", "heap_step",
            "heap_alloc_batch", "heap_stats_async", "heap_stats", "heap_export",
            "heap_launch_count", "heap_set_graphs", "heap_profile_enable", "heap_profile_read", "heap_tag_name",
            "heap_debug_counters", "heap_stats_allgather", "heap_nccl_unique_id", "heap_nccl_comm_init",
@@ -86,6 +86,8 @@ def lib():
         L.heap_free_batch.argtypes = [vp, vp, u64, vp]
         L.heap_free_batch_handles.restype = i32
         L.heap_free_batch_handles.argtypes = [vp, vp, u64, vp, u64, vp]
+        L.heap_step.restype = i32
+        L.heap_step.argtypes = [vp, vp, vp, u64, u64, vp, vp, u64, vp]
         L.heap_alloc_batch.restype = i32
         L.heap_alloc_batch.argtypes = [vp, vp, vp, u64, vp]
         L.heap_stats_async.restype = i32

@@ -640,6 +640,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     h->sms = sms;
     h->G = sms * 4;
+    if (const char *gg = getenv("HEAP_GRID")) { const int g = atoi(gg); if (g > 0) h->G = g; }   // dev knob: grid of the grid-stride kernels
     if (cudaFuncSetAttribute(tlsfw::k_engine<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(tlsfw::Smem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(tlsfw::k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -661,7 +662,15 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         cudaFuncSetAttribute(micro::k_micro_alloc<micro::P_BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)micro::ALLOC_SMEM) != cudaSuccess ||
         cudaFuncSetAttribute(micro::k_micro_alloc<micro::P_CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)micro::ALLOC_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
+                             (int)micro::ALLOC_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(micro::k_micro_step<micro::P_FF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::STEP_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(micro::k_micro_step<micro::P_NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::STEP_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(micro::k_micro_step<micro::P_BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::STEP_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(micro::k_micro_step<micro::P_CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)micro::STEP_SMEM) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(fits::k_bf_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(fits::BfSmem)) != cudaSuccess) { delete h; return HEAP_ECUDA; }
     if (cudaFuncSetAttribute(fits::k_bf_cls_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1318,6 +1327,39 @@ int heap_free_batch_handles(heap_t *h, const uint64_t *d_table, uint64_t table_l
            (u64 *)h->gout);
     if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
     return heap_free_batch(h, (const uint64_t *)h->gout, n, sp);
+}
+
+int heap_step(heap_t *h, const uint64_t *d_offsets, const uint64_t *d_idx, uint64_t table_len, uint64_t nf,
+              const uint64_t *d_sizes, uint64_t *d_out, uint64_t na, heap_stream_t sp) {
+    if (!h || nf > h->max_batch || na > h->max_batch || (nf && !d_offsets) || (na && (!d_sizes || !d_out)))
+        return HEAP_EINVAL;
+    if (h->micro && (nf || na)) {          // one launch: the free batch, then the alloc batch
+        const Layout &L = h->L;
+        const int cur = h->cur, nxt = cur ^ 1;
+        DevCtr *C = h->ctr;
+        cudaStream_t s = (cudaStream_t)sp;
+        TAG(h, HEAP_TAG_MICRO);
+#define MICRO_STEP(P)                                                                                            \
+    LAUNCH(h, micro::k_micro_step<P>, 1, micro::MT, micro::STEP_SMEM, s, (const u64 *)d_offsets, (u64)nf,          \
+           (const u64 *)d_idx, (u64)(d_idx ? table_len : 0), (const u64 *)d_sizes, (u64)na, (u64 *)d_out, h->alog2, \
+           L.A_u, L.L, h->fs[cur], h->fe[cur], h->fs[nxt], h->fe[nxt], h->tbl, L.tcap - 1, L.tcap / table::LINE,   \
+           L.tcap, L.cap_f, h->ms, C, h->max_live)
+        switch (h->policy) {
+            case HEAP_FIRST_FIT: MICRO_STEP(micro::P_FF); break;
+            case HEAP_NEXT_FIT: MICRO_STEP(micro::P_NF); break;
+            case HEAP_BEST_FIT: MICRO_STEP(micro::P_BF); break;
+            default: MICRO_STEP(micro::P_CLS); break;
+        }
+#undef MICRO_STEP
+        h->cur = cur ^ (nf ? 1 : 0) ^ (na ? 1 : 0);
+        if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
+        return HEAP_OK;
+    }
+    int rc = HEAP_OK;
+    if (nf) rc = d_idx ? heap_free_batch_handles(h, d_offsets, table_len, d_idx, nf, sp)
+                       : heap_free_batch(h, d_offsets, nf, sp);
+    if (rc != HEAP_OK) return rc;
+    return na ? heap_alloc_batch(h, d_sizes, d_out, na, sp) : HEAP_OK;
 }
 
 int heap_alloc_batch(heap_t *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_t n, heap_stream_t sp) {

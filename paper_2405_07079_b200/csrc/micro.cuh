@@ -53,13 +53,12 @@ constexpr size_t ALLOC_SMEM = (size_t)MICRO_N * 8 + (size_t)MICRO_F * 8 + (MICRO
 __device__ __forceinline__ u32 cta_scan(u32 v, u32 *sm, u32 *total) { return block_excl_scan<MT>(v, sm, total); }
 
 // ------------------------------------------------------------------------------ free ----
-__global__ void __launch_bounds__(MT, 1) k_micro_free(const u64 *__restrict__ offs, u64 n, const u64 *n_in, int alog2,
-                                                      u64 A_u, const u64 *__restrict__ fs_in,
-                                                      const u64 *__restrict__ fe_in, u64 *__restrict__ fs_out,
-                                                      u64 *__restrict__ fe_out, u64 *__restrict__ tbl, u64 tmask,
-                                                      u64 max_lines, u64 cap_f, DevCtr *ctr,
-                                                      const u64 *__restrict__ hidx, u64 hlen) {
-    PDL_ENTRY();
+#define MICRO_FREE_PARAMS                                                                                    \
+    const u64 *__restrict__ offs, u64 n, const u64 *n_in, int alog2, u64 A_u, const u64 *__restrict__ fs_in,      \
+        const u64 *__restrict__ fe_in, u64 *__restrict__ fs_out, u64 *__restrict__ fe_out, u64 *__restrict__ tbl, \
+        u64 tmask, u64 max_lines, u64 cap_f, DevCtr *ctr, const u64 *__restrict__ hidx, u64 hlen
+#define MICRO_FREE_ARGS offs, n, n_in, alog2, A_u, fs_in, fe_in, fs_out, fe_out, tbl, tmask, max_lines, cap_f, ctr, hidx, hlen
+__device__ __forceinline__ void micro_free_body(MICRO_FREE_PARAMS) {
     extern __shared__ __align__(16) unsigned char dyn[];
     u32 *ps = reinterpret_cast<u32 *>(dyn);          // free array (units), F entries
     u32 *pe = ps + MICRO_F;
@@ -287,14 +286,14 @@ __device__ __forceinline__ u32 pkey(u32 z, u32 r, u32 cs, u32 j, u32 f0, int L) 
     return z;                                        // BEST_FIT
 }
 
+#define MICRO_ALLOC_PARAMS                                                                                    \
+    const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2, u64 A_u, int L, const u64 *__restrict__ fs_in, \
+        const u64 *__restrict__ fe_in, u64 *__restrict__ fs_out, u64 *__restrict__ fe_out, u64 *__restrict__ out_bytes, \
+        u64 *__restrict__ tbl, u64 tmask, u64 max_lines, u64 tcap, u64 *__restrict__ scratch, DevCtr *ctr, u64 max_live
+#define MICRO_ALLOC_ARGS sizes, n, n_in, alog2, A_u, L, fs_in, fe_in, fs_out, fe_out, out_bytes, tbl, tmask, max_lines, tcap, \
+    scratch, ctr, max_live
 template <int POL>
-__global__ void __launch_bounds__(MT, 1) k_micro_alloc(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2,
-                                                       u64 A_u, int L, const u64 *__restrict__ fs_in,
-                                                       const u64 *__restrict__ fe_in, u64 *__restrict__ fs_out,
-                                                       u64 *__restrict__ fe_out, u64 *__restrict__ out_bytes,
-                                                       u64 *__restrict__ tbl, u64 tmask, u64 max_lines, u64 tcap,
-                                                       u64 *__restrict__ scratch, DevCtr *ctr, u64 max_live) {
-    PDL_ENTRY();
+__device__ __forceinline__ void micro_alloc_body(MICRO_ALLOC_PARAMS) {
     extern __shared__ __align__(16) unsigned char dyn[];
     u32 *rr = reinterpret_cast<u32 *>(dyn);          // request units (0: fails)
     u32 *res = rr + MICRO_N;                         // result (unit offset) or NONE
@@ -533,5 +532,38 @@ __global__ void __launch_bounds__(MT, 1) k_micro_alloc(const u64 *__restrict__ s
     }
     if (tid == 0) { ctr->tbl_used = nl; ctr->tbl_tombs = 0; }
 }
+
+__global__ void __launch_bounds__(MT, 1) k_micro_free(MICRO_FREE_PARAMS) {
+    PDL_ENTRY();
+    micro_free_body(MICRO_FREE_ARGS);
+}
+
+template <int POL>
+__global__ void __launch_bounds__(MT, 1) k_micro_alloc(MICRO_ALLOC_PARAMS) {
+    PDL_ENTRY();
+    micro_alloc_body<POL>(MICRO_ALLOC_ARGS);
+}
+
+// heap_step on a single-launch heap: the free batch then the alloc batch in ONE launch (the
+// canonical batch order; the alloc phase reads the state the free phase wrote, made visible to the
+// CTA by the barrier between them).  Dynamic shared memory: max(FREE_SMEM, ALLOC_SMEM).
+template <int POL>
+__global__ void __launch_bounds__(MT, 1) k_micro_step(const u64 *__restrict__ offs, u64 nf, const u64 *__restrict__ hidx,
+                                                      u64 hlen, const u64 *__restrict__ sizes, u64 na,
+                                                      u64 *__restrict__ out_bytes, int alog2, u64 A_u, int L,
+                                                      u64 *fs0, u64 *fe0, u64 *fs1, u64 *fe1, u64 *__restrict__ tbl,
+                                                      u64 tmask, u64 max_lines, u64 tcap, u64 cap_f,
+                                                      u64 *__restrict__ scratch, DevCtr *ctr, u64 max_live) {
+    PDL_ENTRY();
+    if (nf) micro_free_body(offs, nf, nullptr, alog2, A_u, fs0, fe0, fs1, fe1, tbl, tmask, max_lines, cap_f, ctr, hidx, hlen);
+    __syncthreads();
+    if (na) {
+        if (nf) micro_alloc_body<POL>(sizes, na, nullptr, alog2, A_u, L, fs1, fe1, fs0, fe0, out_bytes, tbl, tmask,
+                                      max_lines, tcap, scratch, ctr, max_live);
+        else micro_alloc_body<POL>(sizes, na, nullptr, alog2, A_u, L, fs0, fe0, fs1, fe1, out_bytes, tbl, tmask,
+                                   max_lines, tcap, scratch, ctr, max_live);
+    }
+}
+constexpr size_t STEP_SMEM = FREE_SMEM > ALLOC_SMEM ? FREE_SMEM : ALLOC_SMEM;
 
 }  // namespace micro

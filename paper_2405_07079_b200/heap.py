@@ -68,6 +68,18 @@ def heap_free_batch_handles(h, table: torch.Tensor, idx: torch.Tensor, stream=No
                                         _dev_ptr(idx, "idx") if n else None, n, _stream_handle(stream)))
 
 
+def heap_step(h, offsets: torch.Tensor, idx: torch.Tensor | None, sizes: torch.Tensor, out_offsets: torch.Tensor,
+              stream=None) -> None:
+    nf = idx.numel() if idx is not None else offsets.numel()
+    na = sizes.numel()
+    if out_offsets.numel() < na:
+        raise ValueError("out_offsets too small")
+    check("heap_step", lib().heap_step(
+        h, _dev_ptr(offsets, "offsets") if nf else None, _dev_ptr(idx, "idx") if (idx is not None and nf) else None,
+        offsets.numel(), nf, _dev_ptr(sizes, "sizes") if na else None,
+        _dev_ptr(out_offsets, "out_offsets") if na else None, na, _stream_handle(stream)))
+
+
 def heap_alloc_batch(h, sizes: torch.Tensor, out_offsets: torch.Tensor, stream=None) -> None:
     n = sizes.numel()
     if out_offsets.numel() < n:
@@ -215,6 +227,17 @@ class Heap:
         a caller keeping its blocks in a handle table frees them without a separate gather."""
         with torch.cuda.device(self.device):
             heap_free_batch_handles(self._h, table, idx, self._stream())
+
+    def step(self, offsets: torch.Tensor, sizes: torch.Tensor, idx: torch.Tensor | None = None,
+             out: torch.Tensor | None = None) -> torch.Tensor:
+        """One canonical batch: free `offsets` (or, with `idx`, the handles offsets[idx]), then
+        allocate `sizes`; returns the offsets as alloc_batch does (`out` may be a slice of the
+        handle table)."""
+        n = sizes.numel()
+        with torch.cuda.device(self.device):
+            dst = self._out[:n] if out is None else out[:n]
+            heap_step(self._h, offsets, idx, sizes, dst, self._stream())
+            return dst.clone() if out is None else dst
 
     def alloc_batch(self, sizes: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """Serve a batch of sizes (bytes) in request order; returns the offsets (HEAP_NULL as -1).

@@ -48,6 +48,7 @@ def test_workspace_bytes_and_argument_checks():
     assert L.heap_create(1 << 20, 24, 4, 1024, 1024, None, 0, None, ctypes.byref(h)) == -1
     assert L.heap_free_batch(None, None, 0, None) == -1
     assert L.heap_free_batch_handles(None, None, 0, None, 0, None) == -1
+    assert L.heap_step(None, None, None, 0, 0, None, None, 0, None) == -1
     assert L.heap_strerror(-3) == b"metadata capacity exceeded in a batch"
 
 

@@ -598,13 +598,15 @@ def test_arena_extremes_all_policies(pol):
         compare_state(g, o, f"p{pol} {arena} realloc")
 
 
+@pytest.mark.parametrize("mode", ["handles", "step", "step_offsets"])
 @pytest.mark.parametrize("micro", ["1", "0"], ids=["single_launch", "general"])
 @pytest.mark.parametrize("policy", [tg.FIRST_FIT, tg.BEST_FIT, tg.TLSF, tg.BUDDY])
-def test_free_batch_handles(policy, micro, monkeypatch):
+def test_free_batch_handles(policy, micro, mode, monkeypatch):
     """heap_free_batch_handles frees table[idx[i]] exactly as heap_free_batch frees the gathered
-    offsets: a handle table on the device (the alloc results written into it), frees by index,
-    including indices past the table (no-op nulls), repeated and HEAP_NULL entries; every batch
-    against Oracle-L on the gathered offsets."""
+    offsets, and heap_step (free batch + alloc batch in one call: one kernel on a single-launch
+    heap) equals the two calls: a handle table on the device (the alloc results written into it),
+    frees by index, including indices past the table (no-op nulls), repeated and HEAP_NULL
+    entries, batches without frees or allocs; every batch against Oracle-L."""
     from paper_2405_07079_b200 import Heap
     monkeypatch.setenv("HEAP_MICRO", micro)
     kind, sizes = (1, (4, 10)) if policy == tg.BUDDY else (0, (4, 12))
@@ -619,9 +621,20 @@ def test_free_batch_handles(policy, micro, monkeypatch):
             idx = np.concatenate([idx, [table.numel() + 5, idx[0]]])
             rng.shuffle(idx)
         offs = np.where(idx < table.numel(), table.cpu().numpy()[np.minimum(idx, table.numel() - 1)], -1)
-        h.free_batch_handles(table, torch.from_numpy(idx).cuda())
+        if bi % 7 == 3:                       # a batch without allocs, then one without frees
+            sz = sz[:0]
+        if bi % 7 == 4:
+            idx, offs = idx[:0], offs[:0]
+        sd = torch.from_numpy(sz.view(np.int64)).cuda()
+        dst = table[first:first + len(sz)]
+        if mode == "handles":
+            h.free_batch_handles(table, torch.from_numpy(idx).cuda())
+            got = h.alloc_batch(sd, out=dst)
+        elif mode == "step":
+            got = h.step(table, sd, idx=torch.from_numpy(idx).cuda(), out=dst)
+        else:
+            got = h.step(torch.from_numpy(offs.astype(np.int64)).cuda(), sd, out=dst)
         o.free_batch(offs.view(np.uint64))
-        got = h.alloc_batch(torch.from_numpy(sz.view(np.int64)).cuda(), out=table[first:first + len(sz)])
         want = o.alloc_batch(sz)
         assert np.array_equal(got.cpu().numpy().view(np.uint64), want), (policy, micro, bi)
     st, ost = h.stats(), o.stats()
