@@ -157,8 +157,10 @@ size_t heap_workspace_bytes(uint64_t arena_bytes, uint64_t align, int policy,
  * host handle (the only memory the library owns).
  * Environment (read here; for ablation and for testing both paths — results are identical either
  * way): HEAP_WILD_SPLIT=0 turns off the TLSF/SEGFIT wilderness split (the alloc engine then
- * carries the top class's single member like any other piece); HEAP_BF_FLAT=1 runs BEST_FIT on
- * one flat sorted key array instead of the blocked chunk list; HEAP_MICRO=0 keeps small heaps
+ * carries the top class's single member like any other piece); HEAP_BF_FLAT=1 / 2 / 3 runs
+ * BEST_FIT one request at a time on one flat sorted key array / the blocked chunk list / the
+ * class-indexed chunk list instead of the speculative 32-request chunks; HEAP_ENGINE_WARPS=1 runs
+ * the TLSF/SEGFIT engine on one warp instead of two; HEAP_MICRO=0 keeps small heaps
  * (FIRST/NEXT/BEST fit, SEGFIT, TLSF with max_live_blocks + 1 <= 4160, arena_bytes / align < 2^32,
  * max_batch <= 4096) off the single-launch path (one 512-thread CTA per batch, micro.cuh);
  * HEAP_BUDDY_LEVELS=1 runs the binary-buddy free phase level by level instead of in parallel
