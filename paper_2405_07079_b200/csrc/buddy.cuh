@@ -43,6 +43,10 @@ constexpr u64 FAIL = 0xFFFFFFFFFFFFFFFFull;
 template <typename TS, typename TD>
 __device__ __forceinline__ void cta_copy(TD *dst, const TS *src, u64 n64) {
     const u32 n = (u32)n64, wb = threadIdx.x & ~31u;
+    if (n <= NT) {                                   // one element per thread at most (most levels)
+        if (threadIdx.x < n) dst[threadIdx.x] = (TD)src[threadIdx.x];
+        return;
+    }
     for (u32 base = 0; base < n; base += 8 * NT) {
         // warp-uniform step count: warps past the end skip the unrolled steps instead of running
         // them predicated off (the kernel is issue-bound on its one SM)
@@ -588,6 +592,26 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         u64 *bad_lo = (t > 0) ? (bsm ? sbuf + ((t - 1) & 1) * maxb : baddr + boff[t - 1]) : nullptr;   // of t-1
         const u32 nd_ = (u32)nd, nt_ = (u32)n_t, nbor_ = (u32)nbor, wb = threadIdx.x & ~31u;
         const u64 dbase = doff[t];
+        if (nd_ <= NT) {                                   // one demand per thread at most (most levels)
+            const u32 p = threadIdx.x;
+            u32 sc = 0;
+            u64 a = FAIL;
+            if (p < nd_) {
+                sc = Ds[p];
+                if (p < nt_) a = blk[p];
+            }
+            __syncthreads();                               // the level above has written bad[]
+            if (p < nd_) {
+                if (p >= nt_) {
+                    const u32 xx = p - nt_, j = xx >> 1;
+                    const u64 bj = j < nbor_ ? bad[j] : FAIL;
+                    a = (bj != FAIL) ? bj + ((xx & 1) ? (1ull << t) : 0) : FAIL;
+                }
+                if (sc & BORROW) bad_lo[sc & ~BORROW] = a;
+                else if (daddr) daddr[dbase + p] = a;
+                else out_u[sc] = a;
+            }
+        } else
         for (u32 base = 0; base < nd_; base += 8 * NT) {    // 8 independent elements per thread
             const u32 kw = base + wb < nd_ ? min(8u, (nd_ - base - wb + NT - 1) / NT) : 0u;   // warp-uniform
             u64 a[8];
