@@ -362,25 +362,22 @@ __global__ void k_bud_write(const u64 *__restrict__ rs, const u64 *__restrict__ 
     }
 }
 // order-grouped (stable: address order inside an order) -> the new per-order lists
+// (block 0 also writes the per-order offsets and counts: the keys were just sorted by one 8-bit
+// onesweep pass, whose digit-histogram scan is still in ctr->os_gbase[0] — the first position with
+// order >= t is its entry t)
 __global__ void k_bud_lists(const u32 *__restrict__ idx, const u64 *n_dev, const u64 *__restrict__ start,
-                            u64 *__restrict__ out) {
+                            u64 *__restrict__ out, int K, DevCtr *ctr) {
     PDL_ENTRY();
     const u64 n = *n_dev;
     for (u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (u64)gridDim.x * blockDim.x)
         out[p] = start[idx[p]];
-}
-__global__ void k_bud_offsets(const u32 *__restrict__ key, const u64 *n_dev, int K, DevCtr *ctr) {
-    PDL_ENTRY();
-    const u64 n = *n_dev;
-    const int t = threadIdx.x;
-    if (t <= K + 1) {
-        u64 lo = 0, hi = n;                 // first position with order >= t
-        while (lo < hi) { const u64 m = (lo + hi) >> 1; if (key[m] < (u32)t) lo = m + 1; else hi = m; }
-        ctr->bud_off[t] = lo;
+    if (blockIdx.x == 0) {
+        const int t = threadIdx.x;
+        if (t <= K + 1) ctr->bud_off[t] = (t <= K) ? (u64)ctr->os_gbase[0][t] : n;
+        __syncthreads();
+        if (t <= K) ctr->bud_cnt[t] = ctr->bud_off[t + 1] - ctr->bud_off[t];
+        if (t == 0) { ctr->bud_total = n; ctr->bud_qn = n; }
     }
-    __syncthreads();
-    if (t <= K) ctr->bud_cnt[t] = ctr->bud_off[t + 1] - ctr->bud_off[t];
-    if (t == 0) { ctr->bud_total = n; ctr->bud_qn = n; }
 }
 
 // freed (start, end) -> sort key = order, payload = index
@@ -436,7 +433,11 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
     __shared__ u64 doff[42], boff[42];
     __shared__ u32 ro[42];
     if (threadIdx.x <= (unsigned)K + 1) ooff[threadIdx.x] = ctr->bud_off[threadIdx.x];
-    if (threadIdx.x <= (unsigned)K + 2) ro[threadIdx.x] = req_off[threadIdx.x];
+    // request offsets by order: req_off, or (nullptr) the digit-histogram scan of the one-pass order
+    // sort that just ran (ctr->os_gbase[0]) with the request count in ctr->tmp[0]
+    if (threadIdx.x <= (unsigned)K + 2)
+        ro[threadIdx.x] = req_off ? req_off[threadIdx.x]
+                                  : (threadIdx.x <= (unsigned)K + 1 ? ctr->os_gbase[0][threadIdx.x] : (u32)ctr->tmp[0]);
     __syncthreads();
     // requests of the fail bucket
     for (u64 i = ro[K + 1] + threadIdx.x; i < ro[K + 2]; i += NT) out_u[req[i]] = FAIL;

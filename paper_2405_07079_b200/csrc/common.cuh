@@ -33,6 +33,7 @@ struct DevCtr {
     u64 n_hist;         // radix histogram length (256 * tiles)
     u64 nsort;          // element count for a sort
     u64 tmp[8];
+    u64 rb_n;           // table rebuild: live slots collected (k_rb_clear -> k_rb_insert)
     // buddy: per-order counts of the current per-order free lists and their offsets (binary
     // buddies use K + 1 <= 33 orders, Fibonacci buddies K + 1 <= 46 classes: fib::MAXC = 48)
     u64 bud_cnt[48];

@@ -67,6 +67,16 @@ __global__ void k_compact(const T *__restrict__ in, const u32 *__restrict__ flag
         if (flags[i]) out[pos[i]] = in[i];
 }
 
+// two arrays compacted by the same flags / positions in one launch
+template <typename T>
+__global__ void k_compact2(const T *__restrict__ a, const T *__restrict__ b, const u32 *__restrict__ flags,
+                           const u32 *__restrict__ pos, const u64 *n_dev, T *__restrict__ oa, T *__restrict__ ob) {
+    PDL_ENTRY();
+    const u64 n = *n_dev;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        if (flags[i]) { const u32 p = pos[i]; oa[p] = a[i]; ob[p] = b[i]; }
+}
+
 __device__ __forceinline__ bool bsearch_u64(const u64 *a, u64 n, u64 key) {
     u64 lo = 0, hi = n;
     while (lo < hi) {
@@ -253,7 +263,9 @@ __global__ void k_piece_flags(const u64 *__restrict__ fs, const u64 *__restrict_
 __global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r, const u64 *__restrict__ out_u,
                                                       u64 n, const u64 *n_in, int alog2, u64 *__restrict__ out_bytes,
                                                       u64 *__restrict__ slots, u64 tmask, u64 max_lines,
-                                                      DevCtr *ctr, u64 max_live) {
+                                                      DevCtr *ctr, u64 max_live,
+                                                      const u32 *__restrict__ order = nullptr) {
+    // order != nullptr (binary buddies): the request's units are 2^order[i] (r unused)
     PDL_ENTRY();
     __shared__ u64 sm[33];
     if (n_in) n = *n_in;
@@ -266,7 +278,7 @@ __global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r,
         bool in = i < n;
         u64 o = in ? out_u[i] : HEAP_NULL_U64;
         bool ok = in && o != HEAP_NULL_U64;
-        u64 ri = ok ? r[i] : 0;
+        u64 ri = ok ? (order ? (1ull << order[i]) : r[i]) : 0;
         int rc = table::insert(slots, tmask, o, ri, ok, max_lines);
         if (rc == 1) c_used++;
         if (rc == -1) c_tomb++;

@@ -448,29 +448,30 @@ __global__ void k_set_F(DevCtr *ctr) {
 }
 
 // ---- table rebuild (tombstone purge), each kernel a no-op unless the flag is set ----
-__global__ void k_rb_check(DevCtr *ctr, u64 thresh) {
+// k_rb_collect decides (every CTA reads the same tbl_used; block 0 records the flag for the other
+// two kernels) and counts the live slots into tmp[5] (zero between rebuilds); k_rb_clear moves the
+// count to rb_n and re-zeroes tmp[5]; k_rb_insert re-inserts rb_n slots.
+__global__ void k_rb_collect(DevCtr *ctr, const u64 *tbl, u64 tcap, u64 *scratch, u64 thresh) {
     PDL_ENTRY();
-    ctr->tmp[4] = (ctr->tbl_used > thresh) ? 1 : 0;
-    ctr->tmp[5] = 0;
-}
-__global__ void k_rb_collect(DevCtr *ctr, const u64 *tbl, u64 tcap, u64 *scratch) {
-    PDL_ENTRY();
-    if (!ctr->tmp[4]) return;
+    const bool rb = ctr->tbl_used > thresh;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->tmp[4] = rb ? 1 : 0;
+    if (!rb) return;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x) {
         u64 v = tbl[i];
         if (table::is_live(v)) scratch[atomicAdd(&ctr->tmp[5], 1ull)] = v;
     }
 }
-__global__ void k_rb_clear(const DevCtr *ctr, u64 *tbl, u64 tcap) {
+__global__ void k_rb_clear(DevCtr *ctr, u64 *tbl, u64 tcap) {
     PDL_ENTRY();
     if (!ctr->tmp[4]) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctr->rb_n = ctr->tmp[5]; ctr->tmp[5] = 0; }
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tcap; i += (u64)gridDim.x * blockDim.x)
         tbl[i] = table::EMPTY;
 }
 __global__ void k_rb_insert(DevCtr *ctr, u64 *tbl, u64 tmask, u64 max_lines, const u64 *scratch) {
     PDL_ENTRY();
     if (!ctr->tmp[4]) return;
-    const u64 n = ctr->tmp[5];
+    const u64 n = ctr->rb_n;
     const u32 g = lane_id() / table::TILE_LANES;
     const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((u64)gridDim.x * blockDim.x) >> 5;
     for (u64 base = gw * table::KPW; base < n; base += nw * table::KPW) {
@@ -486,8 +487,7 @@ __global__ void k_rb_insert(DevCtr *ctr, u64 *tbl, u64 tmask, u64 max_lines, con
 void maybe_rebuild(heap *h, cudaStream_t s) {
     u64 thresh = h->L.tcap / 4 * 3;
     TAG(h, HEAP_TAG_REBUILD);
-    LAUNCH(h, k_rb_check, 1, 1, 0, s, h->ctr, thresh);
-    LAUNCH(h, k_rb_collect, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap, h->ms);
+    LAUNCH(h, k_rb_collect, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap, h->ms, thresh);
     LAUNCH(h, k_rb_clear, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap);
     LAUNCH(h, k_rb_insert, h->G, 256, 0, s, h->ctr, h->tbl, h->L.tcap - 1, h->L.tcap / table::LINE, h->ms);
 }
@@ -876,8 +876,7 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
     TAG(h, HEAP_TAG_SCAN);
     scan(h, h->flags, h->pos, &C->nk, &C->nv, s);
     TAG(h, HEAP_TAG_COMPACT);
-    LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->vs, h->flags, h->pos, &C->nk, h->vsc);
-    LAUNCH(h, fits::k_compact<u64>, h->G, 256, 0, s, h->ve, h->flags, h->pos, &C->nk, h->vec);
+    LAUNCH(h, fits::k_compact2<u64>, h->G, 256, 0, s, h->vs, h->ve, h->flags, h->pos, &C->nk, h->vsc, h->vec);
     if (!bud) {
         // 4. merge path with the free array, 5. coalesce maximal runs
         const bool lifo = h->policy == HEAP_SEGFIT_LIFO;
@@ -913,8 +912,7 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
             LAUNCH(h, buddy::k_bud_write, h->G, 256, 0, s, h->bufA, h->bufB, &C->tmp[2], h->pos, h->promo, h->kA,
                    h->vA, h->bq[nxt], L.cap_f, C);
             const int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[3], 8, s);
-            LAUNCH(h, buddy::k_bud_lists, h->G, 256, 0, s, r2 ? h->vB : h->vA, &C->tmp[3], h->promo, h->fs[nxt]);
-            LAUNCH(h, buddy::k_bud_offsets, 1, 64, 0, s, r2 ? h->kB : h->kA, &C->tmp[3], L.K, C);
+            LAUNCH(h, buddy::k_bud_lists, h->G, 256, 0, s, r2 ? h->vB : h->vA, &C->tmp[3], h->promo, h->fs[nxt], L.K, C);
             h->cur = nxt;
             if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
             return HEAP_OK;
@@ -952,7 +950,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         LAUNCH(h, fib::k_alloc_commit, 1, 1, 0, s, C, h->fgeom, noff);
         TAG(h, HEAP_TAG_FINISH);
         LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, n_in, h->alog2, (u64 *)d_out,
-               h->tbl, L.tcap - 1, L.tcap / table::LINE, C, h->max_live);
+               h->tbl, L.tcap - 1, L.tcap / table::LINE, C, h->max_live, (const u32 *)nullptr);
         h->cur = nxt;
         maybe_rebuild(h, s);
         if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
@@ -962,8 +960,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         TAG(h, HEAP_TAG_BUDDY_ALLOC);
         LAUNCH(h, buddy::k_alloc_orders, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, L.A_u, L.K, h->kA, h->vA, &C->tmp[0]);
         radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s);   // 1 pass: result in kB/vB
-        LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, h->kB, &C->tmp[0], L.K + 2, h->reqoff);
-        LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, buddy::ALLOC_SMEM, s, h->vB, h->reqoff, h->fs[cur], h->fs[nxt], h->dtm,
+        LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, buddy::ALLOC_SMEM, s, h->vB, (const u32 *)nullptr, h->fs[cur], h->fs[nxt], h->dtm,
                h->dsrc, h->daddr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
         LAUNCH(h, buddy::k_bud_scatter, h->G, 256, 0, s, h->dsrc, h->daddr, C, h->out);
         if (!h->bud_levels) {   // the address-ordered free set: survivors compacted, leftovers inserted
@@ -972,10 +969,9 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
             LAUNCH(h, buddy::k_bud_qwrite, h->G, 256, 0, s, h->bq[cur], h->flags, h->pos, &C->tmp[2], L.K,
                    h->bq[nxt], C);
         }
-        LAUNCH(h, buddy::k_alloc_r, h->G, 256, 0, s, h->kA, n, n_in, L.K, h->r);
-        TAG(h, HEAP_TAG_FINISH);
+        TAG(h, HEAP_TAG_FINISH);   // (units 2^order read from the order keys: no k_alloc_r pass)
         LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, n_in, h->alog2, (u64 *)d_out,
-               h->tbl, L.tcap - 1, L.tcap / table::LINE, C, h->max_live);
+               h->tbl, L.tcap - 1, L.tcap / table::LINE, C, h->max_live, (const u32 *)h->kA);
         h->cur = nxt;
         maybe_rebuild(h, s);
         if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
@@ -1092,7 +1088,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
     LAUNCH(h, k_set_F, 1, 1, 0, s, C);
     TAG(h, HEAP_TAG_FINISH);
     LAUNCH(h, fits::k_alloc_finish, h->G, 256, 0, s, h->r, h->out, n, n_in, h->alog2, (u64 *)d_out, h->tbl, L.tcap - 1,
-           L.tcap / table::LINE, C, h->max_live);
+           L.tcap / table::LINE, C, h->max_live, (const u32 *)nullptr);
     if (L.partial) LAUNCH(h, partial::k_set_bits, h->G, 256, 0, s, h->out, n, n_in, L.lbm);
     h->cur = nxt;
     maybe_rebuild(h, s);
