@@ -159,8 +159,9 @@ size_t heap_workspace_bytes(uint64_t arena_bytes, uint64_t align, int policy,
  * way): HEAP_WILD_SPLIT=0 turns off the TLSF/SEGFIT wilderness split (the alloc engine then
  * carries the top class's single member like any other piece); HEAP_BF_FLAT=1 / 2 / 3 runs
  * BEST_FIT one request at a time on one flat sorted key array / the blocked chunk list / the
- * class-indexed chunk list instead of the speculative 32-request chunks; HEAP_ENGINE_WARPS=1 runs
- * the TLSF/SEGFIT engine on one warp instead of two; HEAP_MICRO=0 keeps small heaps
+ * class-indexed chunk list instead of the speculative 32-request chunks; HEAP_ENGINE_WARPS=1 / 3
+ * runs the TLSF/SEGFIT engine on one warp / three warps (warp 1 also refilling the classes without
+ * arrivals, warp 2 gathering candidates) instead of two; HEAP_MICRO=0 keeps small heaps
  * (FIRST/NEXT/BEST fit, SEGFIT, TLSF with max_live_blocks + 1 <= 4160, arena_bytes / align < 2^32,
  * max_batch <= 4096) off the single-launch path (one 512-thread CTA per batch, micro.cuh);
  * HEAP_BUDDY_LEVELS=1 runs the binary-buddy free phase level by level instead of in parallel

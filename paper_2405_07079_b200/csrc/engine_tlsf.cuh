@@ -114,7 +114,11 @@ struct Smem {
     // two-warp engine (non-LIFO): warp 1 applies the arrivals of a chunk while warp 0 updates the
     // classes that lost members; classes touched by both (etag == ctag) stay on warp 0
     u32 etag[MAX_NC];             // chunk tag of the last chunk that popped / carved class k
+    u32 atag[MAX_NC];             // three-warp engine: chunk tag of the last chunk with an arrival into class k
     u32 dg[32], dnk[32];          // per lane: its arrival group (dropper mask, 0 if not a leader), class
+    u32 rk[32];                   // three-warp engine, per lane: a class that lost members and has no
+                                  // arrival in the chunk (warp 1 refills it), else NONE
+    u64 w1_delmin;
     u32 ctag, eng_done, broken1;
     // warp 1 also gathers the next chunk's candidates (wilderness mode): carried-over candidates
     // of this chunk first, then requests from g_scan with search class <= g_mx
@@ -416,8 +420,8 @@ __device__ void arrive_lifo(Smem &S, const Lifo &lf, u32 k, u32 f, u32 s, u32 e1
     S.hn[k] = (unsigned char)(n + 1);
 }
 
-__device__ __forceinline__ void bar_sync_64(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void bar_arrive_64(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // Candidates of the next chunk (wilderness mode): the uncommitted candidates [commit, limit) of the
 // current chunk first (time order), then requests from `sc` whose search class is at most Mx
@@ -468,44 +472,63 @@ __device__ u32 gather_next(Smem &S, const u64 *__restrict__ R, const u32 *__rest
     return ncand;
 }
 
-// Warp 1 of the two-warp engine: per chunk, waits for warp 0's hand-off (named barrier 1), applies
-// the arrivals of every group whose class warp 0 is not updating in the same chunk, and signals
-// completion (barrier 2).  Classes are disjoint between the two warps within a chunk, the
-// availability words are updated with atomics, and new overflow slots are numbered atomically.
-__device__ void arrivals_worker(Smem &S, Heap hp, const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
-                                u64 *__restrict__ out_u) {
+// Helper warps of the multi-warp engine (nthr = 64 or 96 threads).  Per chunk each waits for warp
+// 0's hand-off (named barrier 1), does its share and signals completion (barrier 2):
+//   * warp 1 applies the arrival groups of every class warp 0 does not pop / carve in the chunk
+//     (classes are disjoint between the warps within a chunk, the availability words are updated
+//     with atomics, new overflow slots are numbered atomically); with three warps it also refills
+//     the classes that lost members and see no arrival in the chunk (CSR part, then overflow part,
+//     converged as on warp 0);
+//   * the next chunk's candidate gather (wilderness mode) runs on warp 1 with two warps, on warp 2
+//     with three — it reads only the request staging, so it overlaps everything else.
+__device__ void helper_worker(Smem &S, Heap hp, const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
+                              u64 *__restrict__ out_u, const Csr csr, const u64 *__restrict__ fs,
+                              const u64 *__restrict__ fe, const int nthr, const int wid) {
     const u32 lane = lane_id();
     u64 rb_base = 0, rb_end = 0;                  // this warp's view of the request staging buffer
+    u64 delmin = 0;
+    const bool arr = wid == 1, refills = wid == 1 && nthr == 96, gath = (wid == 1 && nthr == 64) || wid == 2;
     for (;;) {
-        bar_sync_64(1);
+        bar_sync_n(1, nthr);
         if (S.eng_done) break;
-        const u32 tag = S.ctag, g = S.dg[lane], k = S.dnk[lane];
-        if (g && S.etag[k] != tag) {
-            u32 mm = g;
-            while (mm) {
-                const u32 d = __ffs(mm) - 1;
-                mm &= mm - 1;
-                arrive(S, hp, k, S.res_f[d], (u32)(S.res_s[d] + S.ch_r[d]), S.res_e[d]);
+        if (arr) {
+            const u32 tag = S.ctag, g = S.dg[lane], k = S.dnk[lane];
+            if (g && S.etag[k] != tag) {
+                u32 mm = g;
+                while (mm) {
+                    const u32 d = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    arrive(S, hp, k, S.res_f[d], (u32)(S.res_s[d] + S.ch_r[d]), S.res_e[d]);
+                }
             }
         }
-        if (hp.broken) S.broken1 = 1;
-        if (S.g_need) {                           // the next chunk's candidates
+        if (refills) {
+            const u32 rk = S.rk[lane];
+            __syncwarp();
+            const bool rf2 = rk != NONE && refill_csr(S, csr, rk);
+            __syncwarp();
+            if (rf2) refill_ovf(S, hp, fs, fe, rk, delmin);
+        }
+        if (arr && hp.broken) S.broken1 = 1;
+        if (gath && S.g_need) {                   // the next chunk's candidates
             u64 se = 0;
             const u32 nc = gather_next(S, R, C, n, out_u, rb_base, rb_end, S.g_mx, S.g_commit, S.g_limit, S.g_scan,
                                        S.nx_i, S.nx_r, S.nx_c, &se);
             if (lane == 0) { S.nx_n = nc; S.nx_scan = se; }
         }
         __syncwarp();
-        bar_arrive_64(2);
+        bar_arrive_n(2, nthr);
     }
-    const u64 v = warp_sum64(hp.visits), ins = warp_sum64(hp.inserts);
-    if (lane == 0) { S.w1_visits = v; S.w1_inserts = ins; }
+    if (arr) {
+        const u64 v = warp_sum64(hp.visits), ins = warp_sum64(hp.inserts), dm = warp_sum64(delmin);
+        if (lane == 0) { S.w1_visits = v; S.w1_inserts = ins; S.w1_delmin = dm; }
+    }
     __syncwarp();
-    bar_arrive_64(3);                            // its counters are in
+    bar_arrive_n(3, nthr);                       // its counters are in
 }
 
 template <bool LIFO>
-__global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict__ off,
+__global__ void __launch_bounds__(96, 1) k_engine(Csr csr, const u32 *__restrict__ off,
                                                   u64 *__restrict__ fs, const u64 *__restrict__ fe,
                                                   const u64 *__restrict__ R, const u32 *__restrict__ C, u64 n,
                                                   u64 *__restrict__ out_u, u32 *bm, u64 w0, u64 w1, u64 w2,
@@ -523,14 +546,16 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
     const u32 lane = lane_id();
     const u64 nslots = (u64)NC;
     Heap hp{bm, bm + nslots * w0, bm + nslots * (w0 + w1), w0, w1, w2, S.slot, &S.nslot, S.ow_i, S.ow_v, 0, false};
-    const bool two = !LIFO && blockDim.x == 64;   // warp 1 applies arrivals (arrivals_worker)
+    const int nthr = blockDim.x;
+    const bool two = !LIFO && nthr >= 64;        // helper warps (helper_worker)
+    const bool three = two && nthr == 96;        // warp 1 also refills classes without arrivals, warp 2 gathers
     if (threadIdx.x >= 32) {
-        bar_sync_64(4);                           // warp 0 has built the class state
-        if (two) arrivals_worker(S, hp, R, C, n_in ? *n_in : n, out_u);
+        bar_sync_n(4, nthr);                      // warp 0 has built the class state
+        if (two) helper_worker(S, hp, R, C, n_in ? *n_in : n, out_u, csr, fs, fe, nthr, threadIdx.x >> 5);
         return;
     }
-    if (lane == 0) { S.nslot = 0; S.eng_done = 0; S.broken1 = 0; S.w1_visits = 0; S.w1_inserts = 0; }
-    for (int k = lane; k < MAX_NC; k += 32) S.etag[k] = NONE;
+    if (lane == 0) { S.nslot = 0; S.eng_done = 0; S.broken1 = 0; S.w1_visits = 0; S.w1_inserts = 0; S.w1_delmin = 0; }
+    for (int k = lane; k < MAX_NC; k += 32) { S.etag[k] = NONE; S.atag[k] = NONE; }
     // ---- init: CSR ranges, head caches, bitmaps ----
     for (int k = lane; k < NC; k += 32) {
         u32 b = off[k], e = off[k + 1];
@@ -563,7 +588,7 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
         if (lane == 0) S.sw = swl;
     }
     __syncwarp();
-    if (blockDim.x == 64) bar_arrive_64(4);      // releases warp 1 (named barriers: warp-specialised)
+    if (nthr >= 64) bar_arrive_n(4, nthr);       // releases the helper warps (named barriers: warp-specialised)
     u64 rb_base = 0, rb_end = 0;
     u32 keep = 0;          // wilderness mode: candidates carried over from the previous chunk
     u64 resume = 0;        // ... and where its gather stopped
@@ -895,22 +920,29 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
         const u32 g = samecls & (commit >= 32 ? FULLMASK : ((1u << commit) - 1u));   // committed ones
         const u32 mygrp = (cdrop && (g & lanemask_lt()) == 0) ? g : 0u;
         const u32 ctag = (u32)n_iter;
-        if (two) {
-            // hand the arrivals to warp 1: the classes this warp updates are tagged first, and
-            // warp 1 applies only the groups of untagged classes
-            if (cm && part && rank == 0 && ((leftm | staym) & peers)) S.etag[k] = ctag;
+        auto handoff = [&](u32 rkv) {
+            S.rk[lane] = rkv;
             S.dg[lane] = mygrp;
             S.dnk[lane] = mynk;
             if (lane == 0) {
                 S.ctag = ctag;
-                S.g_need = wmode ? 1u : 0u;          // warp 1 gathers the next chunk's candidates
+                S.g_need = wmode ? 1u : 0u;          // a helper gathers the next chunk's candidates
                 S.g_commit = commit;
                 S.g_limit = limit;
                 S.g_scan = scan_end;
                 S.g_mx = mx_chunk;
             }
             __syncwarp();
-            bar_arrive_64(1);
+            bar_arrive_n(1, nthr);
+        };
+        if (two) {
+            // the classes this warp updates are tagged first (warp 1 applies only the arrival groups
+            // of untagged classes); with three warps the classes with arrivals too (a class that
+            // lost members and has none is refilled by warp 1), and the hand-off waits for the pops
+            if (cm && part && rank == 0 && ((leftm | staym) & peers)) S.etag[k] = ctag;
+            if (three && mygrp) S.atag[mynk] = ctag;
+            __syncwarp();
+            if (!three) handoff(NONE);
         }
         bool rf = false;                         // this leader's class lost members: refill
         if (cm && part && rank == 0) {
@@ -934,13 +966,18 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
                 rf = true;
             }
         }
+        bool rfw = rf;                           // refilled by this warp
+        if (three) {
+            rfw = rf && S.atag[k] == ctag;
+            handoff((rf && !rfw) ? k : NONE);
+        }
         if constexpr (LIFO) {
             if (rf) refill_lifo(S, lf, csr, fs, fe, k, n_delmin);
         } else {
             // the leaders' refills run converged: every CSR part, then every overflow part
             __syncwarp();
             const long long ta = ENG_CLK();
-            const bool rf2 = rf && refill_csr(S, csr, k);
+            const bool rf2 = rfw && refill_csr(S, csr, k);
             __syncwarp();
             const long long tb = ENG_CLK();
             if (rf2) refill_ovf(S, hp, fs, fe, k, n_delmin);
@@ -966,7 +1003,7 @@ __global__ void __launch_bounds__(64, 1) k_engine(Csr csr, const u32 *__restrict
             }
         }
         __syncwarp();
-        if (two) bar_sync_64(2);                 // warp 1's arrivals are in
+        if (two) bar_sync_n(2, nthr);            // the helpers' arrivals, refills and gather are in
         t_arr += ENG_CLK() - t0;
         if (!wmode) {
             pos += commit;
@@ -992,14 +1029,14 @@ engine_end:
     if (two) {                                   // release warp 1 and wait for its counters
         if (lane == 0) S.eng_done = 1;
         __syncwarp();
-        bar_arrive_64(1);
-        bar_sync_64(3);
+        bar_arrive_n(1, nthr);
+        bar_sync_n(3, nthr);
     }
     if (slot_map)
         for (int k = lane; k < NC; k += 32) slot_map[k] = S.slot[k];   // for k_bitheap_clear
     if (stats) {
         u64 t = n_retarget, q = n_qsteps, dl = n_delmin, vis = hp.visits, nr = n_refill, ins = hp.inserts;
-        if (two && lane == 0) { vis += S.w1_visits; ins += S.w1_inserts; }
+        if (two && lane == 0) { vis += S.w1_visits; ins += S.w1_inserts; dl += S.w1_delmin; }
         u64 tmax = (u64)t_refill;
         for (int o = 16; o > 0; o >>= 1) {
             nr += __shfl_xor_sync(FULLMASK, nr, o);

@@ -622,7 +622,7 @@ int heap_create(uint64_t arena_bytes, uint64_t align, int policy, uint64_t max_l
         const char *bf = getenv("HEAP_BF_FLAT");
         h->bf_flat = (bf && bf[0] >= '1' && bf[0] <= '3') ? bf[0] - '0' : 0;
         const char *ew = getenv("HEAP_ENGINE_WARPS");
-        h->eng_warps = (ew && ew[0] == '1') ? 1 : 2;
+        h->eng_warps = (ew && (ew[0] == '1' || ew[0] == '3')) ? ew[0] - '0' : 2;
         const char *pd = getenv("HEAP_PDL");
         h->pdl = (pd && pd[0] == '0') ? 0 : 1;
         const char *bl = getenv("HEAP_BUDDY_LEVELS");
