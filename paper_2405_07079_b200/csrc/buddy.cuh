@@ -465,7 +465,17 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         // direct requests: time = request index, src = request index; merged by time with the
         // borrows from t-1 (btm, bsrc); staged in shared memory when the level fits, and then the
         // merge itself writes the borrows to t+1: borrow j carries the time of demand n_t + 2j
-        if (nd >= 2048 && 3 * nr + 4 * nb <= (u64)ALLOC_CAP) {
+        if (nb == 0 || nr == 0) {
+            // one stream only (level 0 has no borrows, the levels above the largest request order
+            // have no requests): the demands are that stream, no merge.  Requests: time = src =
+            // request index; borrows from t-1: (btm, bsrc), read before this level rewrites them
+            const u32 nd_ = (u32)nd, nt_ = (u32)n_t, nbor_ = (u32)nbor;
+            const u32 *tin = nb == 0 ? rq : btm, *sin = nb == 0 ? rq : bsrc;
+            for (u32 o = threadIdx.x; o < nd_; o += NT) { Dt[o] = tin[o]; Ds[o] = sin[o]; }
+            __syncthreads();                       // (btm may be rewritten below: read Dt instead)
+            for (u32 jb = threadIdx.x; jb < nbor_; jb += NT) { btm[jb] = Dt[nt_ + 2 * jb]; bsrc[jb] = jb | BORROW; }
+            __syncthreads();
+        } else if (nd >= 2048 && 3 * nr + 4 * nb <= (u64)ALLOC_CAP) {
             // large level: inputs and the merged demands both in shared memory — the merge-path
             // threads own contiguous output chunks, so their stores are staged and written out
             // coalesced (level 0 of config 4: 31.6k -> 12.0k cycles)
