@@ -686,15 +686,15 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
         noff[K + 1] = o;
     }
     __syncthreads();
-    for (int t = 0; t <= K; t++) {
+    // the surviving batch-start blocks of each order are copied by the whole grid (k_bud_scatter);
+    // this CTA records what to copy and writes the single leftovers
+    if (threadIdx.x <= (unsigned)K) {
+        const int t = threadIdx.x;
         const u64 n_t = ooff[t + 1] - ooff[t];
         const u64 nd = doff[t + 1] - doff[t];
-        const u64 *blk = old_list + ooff[t];
-        if (nd < n_t) {
-            for (u64 p = nd + threadIdx.x; p < n_t; p += NT) new_list[noff[t] + (p - nd)] = blk[p];
-        } else if (s_left[t] != FAIL && threadIdx.x == 0) {
-            new_list[noff[t]] = s_left[t];
-        }
+        ctr->bud_csrc[t] = ooff[t] + nd;
+        ctr->bud_ccnt[t] = nd < n_t ? n_t - nd : 0;
+        if (nd >= n_t && s_left[t] != FAIL) new_list[noff[t]] = s_left[t];
     }
     __syncthreads();
     if (threadIdx.x <= (unsigned)K + 1) {
@@ -711,12 +711,28 @@ __global__ void __launch_bounds__(NT) k_alloc_levels(const u32 *__restrict__ req
 // are coalesced), scattered to request order by the whole grid — one CTA issuing ~n scattered
 // 8-byte stores (one L2 transaction each) is what bounded the top-down pass.
 __global__ void k_bud_scatter(const u32 *__restrict__ dsrc, const u64 *__restrict__ daddr, const DevCtr *ctr,
-                              u64 *__restrict__ out_u) {
+                              u64 *__restrict__ out_u, const u64 *__restrict__ old_list, u64 *__restrict__ new_list,
+                              int K) {
     PDL_ENTRY();
     const u64 nd = ctr->bud_nd;
     for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g < nd; g += (u64)gridDim.x * blockDim.x) {
         const u32 sc = dsrc[g];
         if (!(sc & BORROW)) out_u[sc] = daddr[g];
+    }
+    // ... and the surviving batch-start blocks of every order into the new per-order lists
+    __shared__ u64 pre[50];
+    if (threadIdx.x == 0) {
+        u64 a = 0;
+        for (int t = 0; t <= K; t++) { pre[t] = a; a += ctr->bud_ccnt[t]; }
+        pre[K + 1] = a;
+    }
+    __syncthreads();
+    const u64 tot = pre[K + 1];
+    for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g < tot; g += (u64)gridDim.x * blockDim.x) {
+        int lo = 0, hi = K + 1;                   // the order t with pre[t] <= g < pre[t+1]
+        while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (pre[mid] <= g) lo = mid; else hi = mid; }
+        const u64 q = g - pre[lo];
+        new_list[ctr->bud_off[lo] + q] = old_list[ctr->bud_csrc[lo] + q];
     }
 }
 

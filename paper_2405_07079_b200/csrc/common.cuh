@@ -43,6 +43,8 @@ struct DevCtr {
     // alloc phase per order the first surviving start (consumed blocks are a prefix) and leftover
     u64 bud_qn;
     u64 bud_thr[48], bud_left[48];
+    u64 bud_csrc[48], bud_ccnt[48];   // alloc phase: per order, the surviving batch-start blocks to copy
+                                      // (first index in the old list, count) — k_bud_scatter copies them
     u64 eng[32];        // alloc engine diagnostics (engine_tlsf.cuh)
     u64 lifo_clock;     // SEGFIT_LIFO logical push clock (fits.cuh)
     u64 req_n;          // request count of a graph-launched batch (heap.cu graph path)

@@ -962,7 +962,7 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s);   // 1 pass: result in kB/vB
         LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, buddy::ALLOC_SMEM, s, h->vB, (const u32 *)nullptr, h->fs[cur], h->fs[nxt], h->dtm,
                h->dsrc, h->daddr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
-        LAUNCH(h, buddy::k_bud_scatter, h->G, 256, 0, s, h->dsrc, h->daddr, C, h->out);
+        LAUNCH(h, buddy::k_bud_scatter, h->G, 256, 0, s, h->dsrc, h->daddr, C, h->out, h->fs[cur], h->fs[nxt], L.K);
         if (!h->bud_levels) {   // the address-ordered free set: survivors compacted, leftovers inserted
             LAUNCH(h, buddy::k_bud_qflags, h->G, 256, 0, s, h->bq[cur], C, h->flags);
             scan(h, h->flags, h->pos, &C->bud_qn, &C->tmp[2], s);
