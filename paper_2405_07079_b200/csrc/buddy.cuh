@@ -343,10 +343,16 @@ __global__ void k_bud_count(const u64 *__restrict__ rs, const u64 *__restrict__ 
     }
 }
 // write the decomposition in address order: start (units) and the order as the sort key
-__global__ void k_bud_write(const u64 *__restrict__ rs, const u64 *__restrict__ re, const u64 *R_dev,
-                            const u32 *__restrict__ pos, u64 *__restrict__ ostart, u32 *__restrict__ okey,
-                            u32 *__restrict__ oval, u64 *__restrict__ oq, u64 cap, DevCtr *ctr) {
+// (launched with prims::OS_NT threads: it also counts the order digits of what it writes — the
+// one-pass onesweep sort by order that follows needs no histogram launch)
+__global__ void __launch_bounds__(256) k_bud_write(const u64 *__restrict__ rs, const u64 *__restrict__ re,
+                                                   const u64 *R_dev, const u32 *__restrict__ pos,
+                                                   u64 *__restrict__ ostart, u32 *__restrict__ okey,
+                                                   u32 *__restrict__ oval, u64 *__restrict__ oq, u64 cap, DevCtr *ctr) {
     PDL_ENTRY();
+    __shared__ u32 hh[1][256];
+    hh[0][threadIdx.x] = 0;
+    __syncthreads();
     const u64 R = *R_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < R; i += (u64)gridDim.x * blockDim.x) {
         u64 x = rs[i];
@@ -354,12 +360,15 @@ __global__ void k_bud_write(const u64 *__restrict__ rs, const u64 *__restrict__ 
         u64 o = pos[i];
         while (x < y) {
             const int t = bud_step(x, y);
-            if (o < cap) { ostart[o] = x; okey[o] = (u32)t; oval[o] = (u32)o; oq[o] = (x << QSH) | (u64)t; }
-            else atomicOr(&ctr->error_flags, (u64)ERR_CAP_FREE);
+            if (o < cap) {
+                ostart[o] = x; okey[o] = (u32)t; oval[o] = (u32)o; oq[o] = (x << QSH) | (u64)t;
+                atomicAdd(&hh[0][t], 1u);
+            } else atomicOr(&ctr->error_flags, (u64)ERR_CAP_FREE);
             x += 1ull << t;
             o++;
         }
     }
+    prims::os_hist_finish(hh, 1, ctr);
 }
 // order-grouped (stable: address order inside an order) -> the new per-order lists
 // (block 0 also writes the per-order offsets and counts: the keys were just sorted by one 8-bit
@@ -400,9 +409,15 @@ __global__ void k_gather_u64(const u64 *__restrict__ src, const u32 *__restrict_
 
 // ------------------------------------------------------------------ alloc phase ----
 // r -> order key (K+1 = fail bucket)
-__global__ void k_alloc_orders(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2, u64 A_u, int K,
-                               u32 *__restrict__ key, u32 *__restrict__ val, u64 *n_dev) {
+// (launched with prims::OS_NT threads: it also counts the order digits — the one-pass onesweep sort
+// that follows needs no histogram launch)
+__global__ void __launch_bounds__(256) k_alloc_orders(const u64 *__restrict__ sizes, u64 n, const u64 *n_in, int alog2,
+                                                      u64 A_u, int K, u32 *__restrict__ key, u32 *__restrict__ val,
+                                                      u64 *n_dev, DevCtr *ctr) {
     PDL_ENTRY();
+    __shared__ u32 hh[1][256];
+    hh[0][threadIdx.x] = 0;
+    __syncthreads();
     if (n_in) n = *n_in;
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
     const u64 amask = (1ull << alog2) - 1;
@@ -416,7 +431,9 @@ __global__ void k_alloc_orders(const u64 *__restrict__ sizes, u64 n, const u64 *
         }
         key[i] = k;
         val[i] = (u32)i;
+        atomicAdd(&hh[0][k], 1u);
     }
+    prims::os_hist_finish(hh, 1, ctr);
 }
 
 // Bottom-up + top-down L6 in one CTA.

@@ -419,11 +419,13 @@ __global__ void k_init(DevCtr *ctr, u64 *tbl, u64 tcap, u64 *fs, u64 *fe, u64 A_
 
 // radix sort of *n_dev keys (ping-pong); returns the buffer index (0 = a, 1 = b) holding the result
 template <typename K, bool HV>
-int radix_sort(heap *h, K *ka, K *kb, u32 *va, u32 *vb, const u64 *n_dev, int bits, cudaStream_t s) {
-    // onesweep (prims.cuh): one histogram launch for every pass, then one launch per pass
+int radix_sort(heap *h, K *ka, K *kb, u32 *va, u32 *vb, const u64 *n_dev, int bits, cudaStream_t s,
+               bool hist_done = false) {
+    // onesweep (prims.cuh): one histogram launch for every pass (none when the keys' producer
+    // counted them: hist_done), then one launch per pass
     const int passes = (bits + 7) / 8;
     u64 *flags = reinterpret_cast<u64 *>(h->hist);
-    LAUNCH(h, prims::k_os_hist<K>, h->sms, prims::OS_NT, 0, s, ka, n_dev, passes, h->ctr);
+    if (!hist_done) LAUNCH(h, prims::k_os_hist<K>, h->sms, prims::OS_NT, 0, s, ka, n_dev, passes, h->ctr);
     K *kin = ka, *kout = kb;
     u32 *vin = va, *vout = vb;
     for (int p = 0; p < passes; p++) {
@@ -909,9 +911,9 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
                    L.bud_cap, C);
             LAUNCH(h, buddy::k_bud_count, h->G, 256, 0, s, h->bufA, h->bufB, &C->tmp[2], h->flags);
             scan(h, h->flags, h->pos, &C->tmp[2], &C->tmp[3], s);
-            LAUNCH(h, buddy::k_bud_write, h->G, 256, 0, s, h->bufA, h->bufB, &C->tmp[2], h->pos, h->promo, h->kA,
+            LAUNCH(h, buddy::k_bud_write, h->G, prims::OS_NT, 0, s, h->bufA, h->bufB, &C->tmp[2], h->pos, h->promo, h->kA,
                    h->vA, h->bq[nxt], L.cap_f, C);
-            const int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[3], 8, s);
+            const int r2 = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[3], 8, s, true);
             LAUNCH(h, buddy::k_bud_lists, h->G, 256, 0, s, r2 ? h->vB : h->vA, &C->tmp[3], h->promo, h->fs[nxt], L.K, C);
             h->cur = nxt;
             if (cudaGetLastError() != cudaSuccess) return HEAP_ECUDA;
@@ -958,8 +960,9 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
     }
     if (h->policy == HEAP_BUDDY) {
         TAG(h, HEAP_TAG_BUDDY_ALLOC);
-        LAUNCH(h, buddy::k_alloc_orders, h->G, 256, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, L.A_u, L.K, h->kA, h->vA, &C->tmp[0]);
-        radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s);   // 1 pass: result in kB/vB
+        LAUNCH(h, buddy::k_alloc_orders, h->G, prims::OS_NT, 0, s, (const u64 *)d_sizes, n, n_in, h->alog2, L.A_u, L.K,
+               h->kA, h->vA, &C->tmp[0], C);
+        radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->tmp[0], 8, s, true);   // 1 pass: result in kB/vB
         LAUNCH(h, buddy::k_alloc_levels, 1, buddy::NT, buddy::ALLOC_SMEM, s, h->vB, (const u32 *)nullptr, h->fs[cur], h->fs[nxt], h->dtm,
                h->dsrc, h->daddr, h->baddr, h->btm, h->bsrc, h->out, L.K, C);
         LAUNCH(h, buddy::k_bud_scatter, h->G, 256, 0, s, h->dsrc, h->daddr, C, h->out, h->fs[cur], h->fs[nxt], L.K);

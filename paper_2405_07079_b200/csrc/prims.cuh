@@ -69,6 +69,30 @@ __device__ __forceinline__ u32 lookback(u64 *flags, u64 stride, u64 t, u32 tag, 
     return prefix;
 }
 
+// The end of a histogram pass (OS_NT threads per CTA; h = this CTA's digit counts in shared
+// memory): the counts go to the global histograms, the last CTA turns them into digit start offsets
+// (os_gbase), re-zeroes them and resets the onesweep tile counters / bumps the epoch.  Shared by
+// k_os_hist and by producers that count their keys' digits while writing them (a fused histogram).
+__device__ __forceinline__ void os_hist_finish(u32 (*h)[256], int passes, DevCtr *ctr) {
+    __shared__ u32 s_last, sm[33];
+    __syncthreads();
+    for (int p = 0; p < passes; p++)
+        if (h[p][threadIdx.x]) atomicAdd(&ctr->os_gh[p][threadIdx.x], h[p][threadIdx.x]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(&ctr->os_done, 1u) == gridDim.x - 1) ? 1u : 0u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int p = 0; p < passes; p++) {
+        const u32 c = atomicExch(&ctr->os_gh[p][threadIdx.x], 0u);   // read and re-zero
+        u32 tot;
+        ctr->os_gbase[p][threadIdx.x] = block_excl_scan<OS_NT>(c, sm, &tot);
+    }
+    if (threadIdx.x < 8) ctr->os_tile[threadIdx.x] = 0;
+    if (threadIdx.x == 0) { ctr->os_epoch += 1; ctr->os_done = 0; }
+}
+
 template <typename K>
 __global__ void __launch_bounds__(OS_NT) k_os_hist(const K *__restrict__ keys, const u64 *n_dev, int passes,
                                                    DevCtr *ctr) {
