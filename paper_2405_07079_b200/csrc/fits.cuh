@@ -27,11 +27,16 @@
 namespace fits {
 
 // ------------------------------------------------------------------ free phase ----
-__global__ void k_free_classify(const u64 *__restrict__ offs, u64 n, const u64 *n_in, int alog2, u64 A_u,
-                                u32 *__restrict__ keys, u32 *__restrict__ flags, u64 *n_dev,
-                                DevCtr *ctr) {
+// (also counts the digits of the candidate keys for the address sort that follows — the compaction
+// in between keeps exactly the candidates — so that sort needs no histogram launch; prims::NT threads)
+__global__ void __launch_bounds__(256) k_free_classify(const u64 *__restrict__ offs, u64 n, const u64 *n_in, int alog2,
+                                                       u64 A_u, u32 *__restrict__ keys, u32 *__restrict__ flags,
+                                                       u64 *n_dev, DevCtr *ctr, int passes) {
     PDL_ENTRY();
     __shared__ u64 sm[33];
+    __shared__ u32 hh[4][256];
+    for (int p = 0; p < passes; p++) hh[p][threadIdx.x] = 0;
+    __syncthreads();
     if (n_in) n = *n_in;   // count on the device (a hybrid heap's TLSF share)
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
     u64 nnull = 0, ninv = 0;
@@ -45,7 +50,11 @@ __global__ void k_free_classify(const u64 *__restrict__ offs, u64 n, const u64 *
             u32 f = 0, key = 0;
             if (o == HEAP_NULL_U64) nnull++;
             else if ((o & amask) || (o >> alog2) >= A_u) ninv++;
-            else { f = 1; key = (u32)(o >> alog2); }
+            else {
+                f = 1;
+                key = (u32)(o >> alog2);
+                for (int p = 0; p < passes; p++) atomicAdd(&hh[p][(key >> (8 * p)) & 255u], 1u);
+            }
             flags[i] = f;
             keys[i] = key;
         }
@@ -56,6 +65,7 @@ __global__ void k_free_classify(const u64 *__restrict__ offs, u64 n, const u64 *
         if (a) atomicAdd(&ctr->frees_null, a);
         if (b) atomicAdd(&ctr->frees_invalid, b);
     }
+    prims::os_hist_finish(hh, passes, ctr);
 }
 
 template <typename T>

@@ -851,15 +851,16 @@ static int free_impl(heap *h, const uint64_t *d_offsets, uint64_t n, const u64 *
     }
     // 1. classify (null / unaligned / out of range) and compact the candidate keys
     TAG(h, HEAP_TAG_CLASSIFY);
-    LAUNCH(h, fits::k_free_classify, h->G, prims::NT, 0, s, (const u64 *)d_offsets, n, n_in, h->alog2, L.A_u, h->kA, h->flags, n_dev, C);
+    const int kbits = ilog2(L.A_u - 1 > 0 ? L.A_u - 1 : 1) + 1;   // address-sort key width (4 passes at most)
+    LAUNCH(h, fits::k_free_classify, h->G, prims::NT, 0, s, (const u64 *)d_offsets, n, n_in, h->alog2, L.A_u, h->kA,
+           h->flags, n_dev, C, (kbits + 7) / 8);
     TAG(h, HEAP_TAG_SCAN);
     scan(h, h->flags, h->pos, n_dev, &C->nk, s);
     TAG(h, HEAP_TAG_COMPACT);
     LAUNCH(h, fits::k_compact<u32>, h->G, 256, 0, s, h->kA, h->flags, h->pos, n_dev, h->kB);
     // 2. sort the keys (address order; duplicates become adjacent)
-    int kbits = ilog2(L.A_u - 1 > 0 ? L.A_u - 1 : 1) + 1;
-    TAG(h, HEAP_TAG_SORT);
-    int rb = radix_sort<u32, false>(h, h->kB, h->kA, nullptr, nullptr, &C->nk, kbits, s);
+    TAG(h, HEAP_TAG_SORT);   // (digits counted by k_free_classify)
+    int rb = radix_sort<u32, false>(h, h->kB, h->kA, nullptr, nullptr, &C->nk, kbits, s, true);
     u32 *keys = rb ? h->kA : h->kB;
     // 3. block-table lookup + delete; classify double / invalid
     TAG(h, HEAP_TAG_LOOKUP);
