@@ -329,14 +329,22 @@ __global__ void __launch_bounds__(256) k_alloc_finish(const u64 *__restrict__ r,
 // engine's shared-memory head cache or, past the cache, in k''s overflow bitmap over f (a block
 // is in one class at a time).  Class emptiness is kept in two-level bitmaps (one u32 word per
 // first level, 32 second-level classes = one word), searched with ffs.
-__global__ void k_cls_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev, int L,
-                           u32 *__restrict__ key, u32 *__restrict__ val) {
+// (prims::NT threads: also counts the key digits of the `passes` sort passes that follow)
+__global__ void __launch_bounds__(256) k_cls_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe,
+                                                  const u64 *F_dev, int L, u32 *__restrict__ key, u32 *__restrict__ val,
+                                                  DevCtr *ctr, int passes) {
     PDL_ENTRY();
+    __shared__ u32 hh[4][256];
+    for (int p = 0; p < passes; p++) hh[p][threadIdx.x] = 0;
+    __syncthreads();
     const u64 F = *F_dev;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x) {
-        key[i] = cls_insert(fe[i] - fs[i], L);
+        const u32 k = cls_insert(fe[i] - fs[i], L);
+        key[i] = k;
         val[i] = (u32)i;
+        for (int p = 0; p < passes; p++) atomicAdd(&hh[p][(k >> (8 * p)) & 255u], 1u);
     }
+    prims::os_hist_finish(hh, passes, ctr);
 }
 
 // off[k] = first position in the class-sorted order whose class >= k, for k = 0..NC
@@ -493,12 +501,21 @@ __global__ void __launch_bounds__(32) k_ff_engine(u64 *tree, const u64 *__restri
 // warp search finds the first key >= (r << FB): the smallest fitting block, lowest address on
 // ties (Alg. 3 with reading C3).  The carved piece moves down to its new rank (warp shift).
 // The array lives in shared memory when it fits, otherwise in global memory.
-__global__ void k_bf_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe, const u64 *F_dev, int FB,
-                          u64 *__restrict__ key) {
+// (prims::NT threads: also counts the key digits of the `passes` sort passes that follow)
+__global__ void __launch_bounds__(256) k_bf_keys(const u64 *__restrict__ fs, const u64 *__restrict__ fe,
+                                                 const u64 *F_dev, int FB, u64 *__restrict__ key, DevCtr *ctr,
+                                                 int passes) {
     PDL_ENTRY();
+    __shared__ u32 hh[8][256];
+    for (int p = 0; p < passes; p++) hh[p][threadIdx.x] = 0;
+    __syncthreads();
     const u64 F = *F_dev;
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x)
-        key[i] = ((fe[i] - fs[i]) << FB) | i;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < F; i += (u64)gridDim.x * blockDim.x) {
+        const u64 k = ((fe[i] - fs[i]) << FB) | i;
+        key[i] = k;
+        for (int p = 0; p < passes; p++) atomicAdd(&hh[p][(u32)(k >> (8 * p)) & 255u], 1u);
+    }
+    prims::os_hist_finish(hh, passes, ctr);
 }
 
 __device__ __forceinline__ u64 warp_lower_bound(const u64 *a, u64 lo, u64 hi, u64 target) {

@@ -1024,8 +1024,10 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
         LAUNCH(h, fits::k_clock_add, 1, 1, 0, s, C, n_in, (u64)n);
     } else if (cls) {
         TAG(h, HEAP_TAG_INDEX);
-        LAUNCH(h, fits::k_cls_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.L, h->kA, h->vA);
-        int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->F, ilog2((u64)L.NC) + 1, s);
+        const int cbits = ilog2((u64)L.NC) + 1;
+        LAUNCH(h, fits::k_cls_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.L, h->kA, h->vA, C,
+               (cbits + 7) / 8);
+        int rb = radix_sort<u32, true>(h, h->kA, h->kB, h->vA, h->vB, &C->F, cbits, s, true);
         u32 *sk = rb ? h->kB : h->kA, *sv = rb ? h->vB : h->vA;
         LAUNCH(h, fits::k_cls_off, h->G, 256, 0, s, sk, &C->F, L.NC, h->off);
         LAUNCH(h, tlsfw::k_csr_data, h->G, 256, 0, s, sv, h->fs[cur], h->fe[cur], &C->F, h->cs);
@@ -1058,9 +1060,9 @@ static int alloc_impl(heap *h, const uint64_t *d_sizes, uint64_t *d_out, uint64_
                h->policy == HEAP_NEXT_FIT ? &C->rover : (u64 *)nullptr);
     } else {   // BEST_FIT
         TAG(h, HEAP_TAG_INDEX);
-        LAUNCH(h, fits::k_bf_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.FB, h->bk[0]);
         int bits = 33 + L.FB;
-        int rb = radix_sort<u64, false>(h, h->bk[0], h->bk[1], nullptr, nullptr, &C->F, bits, s);
+        LAUNCH(h, fits::k_bf_keys, h->G, 256, 0, s, h->fs[cur], h->fe[cur], &C->F, L.FB, h->bk[0], C, (bits + 7) / 8);
+        int rb = radix_sort<u64, false>(h, h->bk[0], h->bk[1], nullptr, nullptr, &C->F, bits, s, true);
         u64 *keys = h->bk[rb];
         TAG(h, HEAP_TAG_ENGINE);
         if (h->bf_flat) {      // ablation (HEAP_BF_FLAT=1): the one-array engine
