@@ -326,7 +326,16 @@ __global__ void k_bud_qwrite(const u64 *__restrict__ q, const u32 *__restrict__ 
         for (int c = 0; c < nl; c++) d += (lv[c] >> QSH) < st ? 1 : 0;
         out[kb + d] = v;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->bud_qn = kept + (u64)nl;
+    // the new length is published by the last CTA to finish: every CTA reads the old one at its
+    // start, and a CTA scheduled after block 0 had finished would otherwise see the new length
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&ctr->bud_qdone, 1u) == gridDim.x - 1) {
+            ctr->bud_qn = kept + (u64)nl;
+            ctr->bud_qdone = 0;
+        }
+    }
 }
 
 // blocks of each maximal run's greedy decomposition

@@ -34,6 +34,7 @@ struct DevCtr {
     u64 nsort;          // element count for a sort
     u64 tmp[8];
     u64 rb_n;           // table rebuild: live slots collected (k_rb_clear -> k_rb_insert)
+    u32 bud_qdone, bud_pad;   // k_bud_qwrite: CTAs finished (the last one publishes bud_qn)
     // buddy: per-order counts of the current per-order free lists and their offsets (binary
     // buddies use K + 1 <= 33 orders, Fibonacci buddies K + 1 <= 46 classes: fib::MAXC = 48)
     u64 bud_cnt[48];
