@@ -30,6 +30,9 @@ constexpr u32 MICRO_F = 4160;               // pieces (max_live + 1 <= MICRO_F)
 constexpr u32 MICRO_N = 4096;               // requests per batch
 constexpr u32 NONE = 0xFFFFFFFFu;
 enum { P_FF = 0, P_NF = 1, P_BF = 2, P_CLS = 3 };
+#ifndef PAIR_FF
+#define PAIR_FF 1      // first fit on the register path: two requests per step (0: one)
+#endif
 
 constexpr size_t FREE_SMEM = (size_t)MICRO_F * 8 + (size_t)MICRO_N * 8 + ((MICRO_F + MICRO_N) / 32 + 64) * 8;
 constexpr size_t ALLOC_SMEM = (size_t)MICRO_N * 8 + (size_t)MICRO_F * 8 + (MICRO_F / 32 + 64) * 8;
@@ -350,6 +353,57 @@ __device__ __forceinline__ void micro_alloc_body(MICRO_ALLOC_PARAMS) {
                 st[q] = j < F ? ps[j] : 0u;
             }
             u32 rn = n ? rr[0] : 0u;
+            if (POL == P_FF && PAIR_FF) {
+                // first fit, two requests per step: both searches run on the state before the first
+                // one's carve (eight independent ballots).  Only the first request's piece fa changed
+                // (it shrank), so the second one's speculative choice fb stands unless fb == fa and fa
+                // no longer fits it — then it is the next fitting piece after fa in the same masks.
+                for (u32 i = 0; i < (u32)n; i += 2) {
+                    const u32 ra = rr[i], rb = i + 1 < (u32)n ? rr[i + 1] : 0u;
+                    u32 ba[4], bb[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        ba[q] = __ballot_sync(FULLMASK, ra != 0 && z[q] >= ra);
+                        bb[q] = __ballot_sync(FULLMASK, rb != 0 && z[q] >= rb);
+                    }
+                    const u32 fa = ba[0] ? __ffs(ba[0]) - 1 : ba[1] ? 32 + __ffs(ba[1]) - 1
+                                 : ba[2] ? 64 + __ffs(ba[2]) - 1 : ba[3] ? 96 + __ffs(ba[3]) - 1 : NONE;
+                    u32 fb = bb[0] ? __ffs(bb[0]) - 1 : bb[1] ? 32 + __ffs(bb[1]) - 1
+                           : bb[2] ? 64 + __ffs(bb[2]) - 1 : bb[3] ? 96 + __ffs(bb[3]) - 1 : NONE;
+                    u32 zsel = 0;                          // this lane's size of piece row fa >> 5, after a
+                    if (fa == NONE) {
+                        if (lane == 0) res[i] = NONE;
+                    } else {
+                        const int qa = (int)(fa >> 5);
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            if (k == qa && (fa & 31) == lane) { res[i] = st[k]; st[k] += ra; z[k] -= ra; }
+                            if (k == qa) zsel = z[k];
+                        }
+                    }
+                    if (i + 1 >= (u32)n) break;
+                    if (fb != NONE && fb == fa) {
+                        const u32 zf = __shfl_sync(FULLMASK, zsel, fa & 31);
+                        if (zf < rb) {                     // the next fitting piece after fa
+                            const int qa = (int)(fa >> 5);
+                            u32 m[4];
+#pragma unroll
+                            for (int k = 0; k < 4; k++)
+                                m[k] = k < qa ? 0u : k > qa ? bb[k] : (bb[k] & ~((2u << (fa & 31)) - 1u));
+                            fb = m[0] ? __ffs(m[0]) - 1 : m[1] ? 32 + __ffs(m[1]) - 1
+                               : m[2] ? 64 + __ffs(m[2]) - 1 : m[3] ? 96 + __ffs(m[3]) - 1 : NONE;
+                        }
+                    }
+                    if (fb == NONE) {
+                        if (lane == 0) res[i + 1] = NONE;
+                    } else if ((fb & 31) == lane) {
+                        const int qb = (int)(fb >> 5);
+#pragma unroll
+                        for (int k = 0; k < 4; k++)
+                            if (k == qb) { res[i + 1] = st[k]; st[k] += rb; z[k] -= rb; }
+                    }
+                }
+            } else
             for (u32 i = 0; i < (u32)n; i++) {
                 const u32 r = rn;
                 rn = i + 1 < (u32)n ? rr[i + 1] : 0u;      // the next request, off the chain
